@@ -1,0 +1,186 @@
+"""Generate golden vectors from the REFERENCE implementation itself.
+
+TEST INFRASTRUCTURE ONLY.  Run in the build container, where the read-only
+reference exists:
+
+    python oracle/make_golden.py            # writes tests/golden/*.npz
+
+It imports `pintswe` from /root/reference/pkg/src (never copies its source)
+and records, on seeded inputs, the outputs of the reference's own transforms
+(spharm.py:238-343), tendencies (dynamics.py:121-165), IMEX step
+(steppers.py:155-168) and Parareal/MGRIT engine (pint.py:355-430).  It also
+copies the reference's frozen run outputs (pkg/frontend/fixtures/*.csv,
+produced by `pintswe run-pint` on fixtures/manifest.json) as data.
+The GPU box never runs this script; the committed .npz files travel instead.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import shutil
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+
+
+def _state_arrays(s):
+    return np.stack([s.phi, s.xi, s.delta])
+
+
+def _random_state(grid, rng, phibar, scales=(1e3, 1e-5, 1e-6)):
+    """Random valid state (test_dynamics.py:23-31 scales), m = 0 rows real."""
+    from pintswe.dynamics import PrognosticState
+    out = []
+    for sc in scales:
+        c = rng.standard_normal(grid.n_modes) + 1j * rng.standard_normal(grid.n_modes)
+        c[: grid.M + 1] = c[: grid.M + 1].real
+        # smooth spectrum so the nonlinear terms stay tame
+        c *= sc * (grid.n_of + 1.0) ** -2.0
+        out.append(c)
+    out[1][0] = 0.0
+    out[2][0] = 0.0
+    out[0][0] += phibar * np.sqrt(2.0)
+    return PrognosticState(grid, out[0], out[1], out[2], phibar)
+
+
+def gen_sht(M, seed):
+    from pintswe.spharm import get_grid
+    g = get_grid(M)
+    rng = np.random.default_rng(seed)
+    nb = 3
+    c = rng.standard_normal((nb, g.n_modes)) + 1j * rng.standard_normal((nb, g.n_modes))
+    c[:, : M + 1] = c[:, : M + 1].real
+    grid_in = rng.standard_normal((nb, g.nlat, g.nlon))
+    out = dict(M=M, mu=g.mu, weights=g.weights, coeffs=c, grid_in=grid_in)
+    out["synthesis"] = np.stack([g.synthesis(x) for x in c])
+    out["analysis"] = np.stack([g.analysis(x) for x in grid_in])
+    out["pair"] = np.stack([g._synthesis_pair(c[0], c[1])])
+    u, v = g.uv_from_vortdiv(c[0], c[1])
+    out["u"], out["v"] = u, v
+    xi, de = g.vortdiv_from_uv(grid_in[0], grid_in[1])
+    out["vd_xi"], out["vd_delta"] = xi, de
+    gx, gy = g.grad_grid(c[2])
+    out["gx"], out["gy"] = gx, gy
+    return out
+
+
+def gen_tendencies(M, seed):
+    from pintswe import dynamics
+    from pintswe.spharm import get_grid
+    g = get_grid(M)
+    rng = np.random.default_rng(seed)
+    phibar = 9.80616 * 29400.0
+    s = _random_state(g, rng, phibar)
+    out = dict(M=M, phibar=phibar, state=_state_arrays(s))
+    for name in ("linear_gravity", "linear_coriolis", "nonlinear_advection",
+                 "nonlinear_rest", "full_rhs"):
+        t = getattr(dynamics, name)(s)
+        out[name] = np.stack([t.phi, t.xi, t.delta])
+    return out
+
+
+def gen_steps(M, seed):
+    """One and several IMEX steps on bumps and on a random state."""
+    from pintswe import scenarios, steppers
+    from pintswe.dynamics import ViscositySpec
+    from pintswe.spharm import get_grid
+    from pintswe.steppers import StepperConfig, StepperState
+    g = get_grid(M)
+    rng = np.random.default_rng(seed)
+    bumps = scenarios.gaussian_bumps(g)
+    rnd = _random_state(g, rng, bumps.phibar)
+    cases = {
+        "bumps_dt600_nu1e5": (bumps, StepperConfig(dt=600.0, viscosity=ViscositySpec(2, 1e5)), 1),
+        "bumps_dt240_nu0_x3": (bumps, StepperConfig(dt=240.0), 3),
+        "random_dt120_q4": (rnd, StepperConfig(dt=120.0, viscosity=ViscositySpec(4, 1e16)), 1),
+        "bumps_dt600_explicit": (bumps, StepperConfig(dt=600.0, coriolis_treatment="explicit"), 1),
+    }
+    out = dict(M=M, phibar=bumps.phibar)
+    for key, (s0, cfg, n) in cases.items():
+        s = StepperState(s0)
+        for _ in range(n):
+            s = steppers.advance(s, cfg)
+        out[key + "_in"] = _state_arrays(s0)
+        out[key + "_out"] = _state_arrays(s.current)
+        out[key + "_cfg"] = np.array([cfg.dt, cfg.viscosity.order_q, cfg.viscosity.coeff_nu,
+                                      1.0 if cfg.coriolis_treatment == "implicit" else 0.0, n])
+    return out
+
+
+def gen_window_step(M, dt, nu, window=32):
+    """Big-M step on bumps, stored only on the n <= window modes."""
+    from pintswe import scenarios, steppers
+    from pintswe.dynamics import ViscositySpec
+    from pintswe.spharm import get_grid
+    from pintswe.steppers import StepperConfig
+    g = get_grid(M)
+    s0 = scenarios.gaussian_bumps(g)
+    s1 = steppers.imex_step(s0, StepperConfig(dt=dt, viscosity=ViscositySpec(2, nu)))
+    sel = (g.n_of <= window)
+    return dict(M=M, dt=dt, nu=nu, window=window, sel=np.flatnonzero(sel),
+                out_window=_state_arrays(s1)[:, sel],
+                out_maxabs=np.array([np.abs(f).max() for f in (s1.phi, s1.xi, s1.delta)]))
+
+
+def gen_pint(name, fineM, coarseM, dt0, T, nlevels, cfactor, nrelax, iters, nu_f, nu_c,
+             cycle="F_then_V"):
+    from pintswe import pint, scenarios
+    from pintswe.dynamics import ViscositySpec
+    from pintswe.pint import LevelSpec, PintConfig, SweProblem
+    from pintswe.steppers import StepperConfig
+    levels = [LevelSpec(0, fineM, StepperConfig(dt=dt0, viscosity=ViscositySpec(2, nu_f)))]
+    for l in range(1, nlevels):
+        levels.append(LevelSpec(l, coarseM, StepperConfig(dt=dt0 * cfactor ** l,
+                                                          viscosity=ViscositySpec(2, nu_c))))
+    N0 = int(round(T / dt0))
+    pc = PintConfig(levels=tuple(levels), T=T, N0=N0, cfactor=cfactor, nrelax=nrelax,
+                    max_iters=iters, cycle=cycle)
+    prob = SweProblem(pc)
+    u0 = scenarios.gaussian_bumps(prob.grids[0])
+    fine = pint.fine_serial_cpoints(prob, pc, u0)
+    tr = pint.mgrit_run(prob, pc, u0)
+    snaps = np.stack([np.stack([_state_arrays(x) for x in snap]) for snap in tr.snapshots])
+    return dict(name=name, fineM=fineM, coarseM=coarseM, dt0=dt0, T=T, nlevels=nlevels,
+                cfactor=cfactor, nrelax=nrelax, iters=iters, nu_f=nu_f, nu_c=nu_c,
+                cycle=cycle, u0=_state_arrays(u0), phibar=u0.phibar,
+                fine=np.stack([_state_arrays(x) for x in fine]), snapshots=snaps)
+
+
+def main():
+    sys.path.insert(0, REF)
+    os.makedirs(OUT, exist_ok=True)
+    np.savez_compressed(os.path.join(OUT, "sht_M16.npz"), **gen_sht(16, 230609497))
+    np.savez_compressed(os.path.join(OUT, "sht_M32.npz"), **gen_sht(32, 230609498))
+    np.savez_compressed(os.path.join(OUT, "tend_M24.npz"), **gen_tendencies(24, 7))
+    np.savez_compressed(os.path.join(OUT, "step_M16.npz"), **gen_steps(16, 11))
+    np.savez_compressed(os.path.join(OUT, "step_M32.npz"), **gen_steps(32, 12))
+    np.savez_compressed(os.path.join(OUT, "step_window_M256.npz"),
+                        **gen_window_step(256, 60.0, 1e5))
+    # the frozen fixture run (manifest.json): Parareal, M16/M16, 4 iterations
+    np.savez_compressed(os.path.join(OUT, "pint_fixture_M16.npz"),
+                        **gen_pint("fixture", 16, 16, 600.0, 7200.0, 2, 2, 0, 4, 0.0, 1e5))
+    # a 3-level F_then_V MGRIT with relaxation, spatial coarsening
+    np.savez_compressed(os.path.join(OUT, "pint_mgrit3_M24.npz"),
+                        **gen_pint("mgrit3", 24, 16, 300.0, 9600.0, 3, 2, 1, 3, 0.0, 1e5))
+    # 2-level MGRIT with nrelax=1 (cfg2's level structure at small M)
+    np.savez_compressed(os.path.join(OUT, "pint_mgrit2_M32.npz"),
+                        **gen_pint("mgrit2", 32, 16, 240.0, 7680.0, 2, 2, 1, 3, 1e5, 1e5))
+    fx = os.path.join(OUT, "fixtures")
+    os.makedirs(fx, exist_ok=True)
+    src = "/root/reference/pkg/frontend/fixtures"
+    for name in ("errors.csv", "spectrum.csv", "manifest.json"):
+        shutil.copyfile(os.path.join(src, name), os.path.join(fx, name))
+    with open(os.path.join(OUT, "README.md"), "w") as fh:
+        fh.write("Golden vectors generated by `python oracle/make_golden.py` from the "
+                 "reference `pintswe` (imported read-only from /root/reference/pkg/src).\n"
+                 "`fixtures/` holds the reference's frozen run-pint outputs "
+                 "(pkg/frontend/fixtures) as data.\n")
+    print(json.dumps(sorted(os.listdir(OUT))))
+
+
+if __name__ == "__main__":
+    main()

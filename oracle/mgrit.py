@@ -1,0 +1,236 @@
+"""Oracle FAS-MGRIT / Parareal driver and error diagnostics.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Restates
+`/root/reference/pkg/src/pintswe/pint.py` (IMEX levels only; the SETTLS
+history policy is out of scope) and the parts of
+`diagnostics.py` that the frozen fixtures exercise:
+
+* level sizes / validation ........ pint.py:55-95
+* SweProblem protocol ............. pint.py:157-194
+* F- / C-relaxation sweeps ........ pint.py:223-263
+* residual, FAS restriction ....... pint.py:267-304
+* coarsest serial sweep ........... pint.py:306-320
+* recursive cycle ................. pint.py:322-337
+* initial guess, run, blow-up ..... pint.py:341-400
+* serial fine C-points ............ pint.py:421-430
+* spectral / l2 errors, KE spectrum diagnostics.py:46-118
+
+Slices are processed one state at a time (batch 1) so the control flow reads
+like the reference; the batched GPU engine is checked against this.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+from .sht import OracleSphere
+from .swe import OracleState, StepCfg, imex_step
+
+
+class PintBlowUp(RuntimeError):
+    def __init__(self, iteration, slice_index, trace):
+        super().__init__(f"blow-up at iteration {iteration}, slice {slice_index}")
+        self.iteration, self.slice_index, self.trace = iteration, slice_index, trace
+
+
+@dataclasses.dataclass(frozen=True)
+class Level:
+    M: int
+    cfg: StepCfg
+
+
+@dataclasses.dataclass(frozen=True)
+class PintCfg:
+    levels: tuple
+    T: float
+    N0: int
+    cfactor: int = 2
+    nrelax: int = 0
+    max_iters: int = 10
+    cycle: str = "F_then_V"
+
+    def points_on(self, level):                       # pint.py:89-90
+        return self.N0 // self.cfactor ** level
+
+
+class OracleProblem:
+    """Per-level sphere + stepper (pint.py:157-194), one state per call."""
+
+    def __init__(self, pcfg: PintCfg, spheres=None):
+        cache = {} if spheres is None else dict(spheres)
+        self.spheres = []
+        for lv in pcfg.levels:
+            if lv.M not in cache:
+                cache[lv.M] = OracleSphere(lv.M)
+            self.spheres.append(cache[lv.M])
+        self.cfgs = [lv.cfg for lv in pcfg.levels]
+        self.step_calls = 0
+
+    def step(self, level, value):
+        self.step_calls += 1
+        return imex_step(value, self.cfgs[level])
+
+    def restrict(self, level, value):
+        return value.to_truncation(self.spheres[level + 1])
+
+    def prolong(self, level, value):
+        return value.to_truncation(self.spheres[level - 1])
+
+
+@dataclasses.dataclass
+class Trace:
+    snapshots: list
+    blowup: dict = None
+
+
+class OracleMgrit:
+    """Same control flow as MgritEngine (pint.py:197-400)."""
+
+    def __init__(self, problem: OracleProblem, pcfg: PintCfg):
+        self.p, self.c, self.m, self.L = problem, pcfg, pcfg.cfactor, len(pcfg.levels)
+
+    def f_sweep(self, level, u, g):                   # pint.py:223-241
+        m = self.m
+        for i in range(1, len(u) // m + 1):
+            v = u[m * (i - 1)]
+            for j in range(m * (i - 1) + 1, m * i):
+                v = self.p.step(level, v)
+                if g is not None:
+                    v = v + g[j]
+                u[j] = v
+
+    def c_sweep(self, level, u, g):                   # pint.py:243-256
+        m = self.m
+        new = {}
+        for i in range(1, len(u) // m + 1):
+            v = self.p.step(level, u[m * i - 1])
+            new[m * i] = v if g is None else v + g[m * i]
+        for k, v in new.items():
+            u[k] = v
+
+    def relax(self, level, u, g):                     # pint.py:258-263
+        self.f_sweep(level, u, g)
+        for _ in range(self.c.nrelax):
+            self.c_sweep(level, u, g)
+            self.f_sweep(level, u, g)
+
+    def fas_restrict(self, level, u, g):              # pint.py:267-304
+        m = self.m
+        n = len(u) // m
+        ubar = [self.p.restrict(level, u[m * i]) for i in range(n + 1)]
+        res = [None]
+        for i in range(1, n + 1):
+            prop = self.p.step(level, u[m * i - 1])
+            if g is not None:
+                prop = prop + g[m * i]
+            res.append(prop - u[m * i])
+        gbar = [None]
+        for i in range(1, n + 1):
+            tau = ubar[i] - self.p.step(level + 1, ubar[i - 1])
+            gbar.append(self.p.restrict(level, res[i]) + tau)
+        return ubar, gbar
+
+    def coarsest(self, u, g):                         # pint.py:306-320
+        lv = self.L - 1
+        for j in range(1, len(u)):
+            v = self.p.step(lv, u[j - 1])
+            u[j] = v if g is None else v + g[j]
+
+    def cycle(self, level, u, g, kind):               # pint.py:322-337
+        if level == self.L - 1:
+            self.coarsest(u, g)
+            return
+        m = self.m
+        self.relax(level, u, g)
+        ubar, gbar = self.fas_restrict(level, u, g)
+        v = [x.copy() for x in ubar]
+        self.cycle(level + 1, v, gbar, kind)
+        for i in range(1, len(u) // m + 1):
+            u[m * i] = u[m * i] + self.p.prolong(level + 1, v[i] - ubar[i])
+        self.f_sweep(level, u, g)
+        if kind == "F_then_V" and level + 1 < self.L - 1:
+            self.cycle(level, u, g, "V")
+
+    def initial_guess(self, u0):                      # pint.py:341-353
+        n1 = self.c.points_on(1)
+        v = [self.p.restrict(0, u0)]
+        for j in range(1, n1 + 1):
+            v.append(self.p.step(1, v[j - 1]))
+        return [self.p.prolong(1, x) for x in v]
+
+    def run(self, u0: OracleState, iters=None) -> Trace:   # pint.py:355-394
+        m, n0, n1 = self.m, self.c.N0, self.c.points_on(1)
+        guess = self.initial_guess(u0)
+        trace = Trace(snapshots=[guess])
+        limit = 1e10 * max(float(u0.max_abs()[0]), 1e-300)
+        self.check(trace, 0, guess, limit)
+        u = [None] * (n0 + 1)
+        u[0] = u0.copy()
+        for i in range(1, n1 + 1):
+            u[m * i] = guess[i].copy()
+            for j in range(m * (i - 1) + 1, m * i):
+                u[j] = guess[i - 1].copy()
+        for k in range(1, (self.c.max_iters if iters is None else iters) + 1):
+            with np.errstate(over="ignore", invalid="ignore"):
+                self.cycle(0, u, None, self.c.cycle)
+            snap = [u[m * i].copy() for i in range(n1 + 1)]
+            trace.snapshots.append(snap)
+            self.check(trace, k, snap, limit)
+        return trace
+
+    @staticmethod
+    def check(trace, k, snap, limit):                 # pint.py:396-400
+        for i, v in enumerate(snap):
+            if not bool(v.is_finite()[0]) or float(v.max_abs()[0]) > limit:
+                trace.blowup = {"iteration": k, "slice": i}
+                raise PintBlowUp(k, i, trace)
+
+
+def fine_serial_cpoints(problem: OracleProblem, pcfg: PintCfg, u0):   # pint.py:421-430
+    out = [u0.copy()]
+    v = u0.copy()
+    for _ in range(pcfg.points_on(1)):
+        for _ in range(pcfg.cfactor):
+            v = problem.step(0, v)
+        out.append(v.copy())
+    return out
+
+
+# -- diagnostics ------------------------------------------------------------------
+
+
+def spectral_error(c, sph, cref, sph_ref, rnorm):      # diagnostics.py:46-65
+    sel = (sph.m_of <= rnorm) & (sph.n_of <= rnorm)
+    sel_r = (sph_ref.m_of <= rnorm) & (sph_ref.n_of <= rnorm)
+    w, wr = c[..., sel], cref[..., sel_r]
+    return float(np.abs(w - wr).max() / np.abs(wr).max())
+
+
+def l2_error(g, gref):                                 # diagnostics.py:68-75
+    den = np.sqrt(np.mean(gref ** 2))
+    return float(np.sqrt(np.mean((g - gref) ** 2)) / den)
+
+
+def phi_error_records(k, state, target_name, target, rnorms, include_l2=False):
+    """Rows (k, rnorm, target, value) (diagnostics.py:99-118)."""
+    common = state.sph if state.sph.M <= target.sph.M else target.sph
+    s, t = state.to_truncation(common), target.to_truncation(common)
+    rows = [(k, str(int(r)), target_name,
+             spectral_error(s.phi[0], common, t.phi[0], common, r)) for r in rnorms]
+    if include_l2:
+        rows.append((k, "l2", target_name,
+                     l2_error(common.synthesis(s.phi[0]), common.synthesis(t.phi[0]))))
+    return rows
+
+
+def ke_spectrum(state: OracleState):                   # diagnostics.py:78-87
+    sph = state.sph
+    a = sph.radius
+    mult = np.where(sph.m_of == 0, 1.0, 2.0)
+    power = mult * (np.abs(state.xi[0]) ** 2 + np.abs(state.delta[0]) ** 2)
+    per_n = np.bincount(sph.n_of, weights=power, minlength=sph.M + 1)
+    n = np.arange(1, sph.M + 1)
+    energy = 0.25 * a * a / (n * (n + 1.0)) * per_n[1:]
+    return n, 2.0 * np.pi * a / n, energy
