@@ -1,0 +1,106 @@
+/* swe_b200.h -- C ABI of the B200 fine-propagator library (libswe_b200.so).
+ *
+ * Drop-in boundary for the hot path of the reference `pintswe` package
+ * (/root/reference/pkg/src/pintswe).  The reference has no FFI: its engine
+ * talks to a duck-typed Python problem object (pint.py:10-13, SweProblem
+ * pint.py:157-194) backed by SphereGrid (spharm.py:146-343) and the IMEX
+ * stepper (steppers.py:155-168).  Every entry point below replaces one of
+ * those Python calls; the Python mirror in paper_2306_09497_b200/ binds them
+ * with ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers owned by the caller.
+ *  - Spectral data: complex128 interleaved (re, im), packed m-major layout of
+ *    spharm.py:149-173 (block m holds n = m..M), shape [batch][K] or, for
+ *    prognostic states, [batch][3][K] with fields (Phi total, xi, delta).
+ *  - Grid data: float64 [batch][nlat][nlon], latitudes north to south.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
+ *    stream-ordered and use the plan's workspace, so one plan must not be used
+ *    from two streams concurrently.
+ *  - Return codes: SWE_OK 0; SWE_ESHAPE 1 (ValueError in the reference);
+ *    SWE_ENOCONV 2 (ImplicitSolveError, steppers.py:113-118); SWE_ENONFINITE 3;
+ *    SWE_ECUDA 4; SWE_ENCCL 5.  swe_last_error() returns the message.
+ */
+#ifndef SWE_B200_H
+#define SWE_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWE_OK 0
+#define SWE_ESHAPE 1
+#define SWE_ENOCONV 2
+#define SWE_ENONFINITE 3
+#define SWE_ECUDA 4
+#define SWE_ENCCL 5
+
+typedef struct swe_plan swe_plan;
+
+/* Mirror of StepperConfig (steppers.py:31-50) for scheme="imex". */
+typedef struct {
+  double dt;               /* > 0 */
+  int visc_order;          /* ViscositySpec.order_q (even >= 2), dynamics.py:107-118 */
+  double visc_nu;          /* ViscositySpec.coeff_nu (>= 0) */
+  int coriolis_implicit;   /* 1: "implicit" (default), 0: "explicit" */
+  int include_nonlinear;   /* 1 (default) */
+  double implicit_tol;     /* 1e-12 */
+  int implicit_max_iter;   /* 200 */
+} swe_stepper_cfg;
+
+/* SphereGrid(Truncation.for_wavenumber(M), SphereGeometry(a, omega, g))
+ * -- spharm.py:154-202, get_grid spharm.py:346-349. */
+int swe_plan_create(int M, double radius_a, double omega, double gravity_g, int device,
+                    swe_plan **out);
+void swe_plan_destroy(swe_plan *plan);
+/* nlat, nlon, n_modes (spharm.py:61-72); all outputs nullable */
+int swe_plan_info(const swe_plan *plan, int *nlat, int *nlon, int *nmodes);
+/* Gaussian nodes mu (decreasing) and weights, HOST arrays of nlat (spharm.py:75-108) */
+int swe_plan_grid(const swe_plan *plan, double *mu, double *weights);
+/* bytes of device memory held by tables (+ current workspace) */
+long long swe_plan_bytes(const swe_plan *plan);
+
+/* SphereGrid.synthesis (spharm.py:249-257): spec [batch][K] -> grid [batch][nlat][nlon] */
+int swe_synthesis(swe_plan *plan, const double *spec, double *grid, int batch, void *stream);
+/* SphereGrid.analysis (spharm.py:238-247): grid -> spec */
+int swe_analysis(swe_plan *plan, const double *grid, double *spec, int batch, void *stream);
+/* SphereGrid.uv_from_vortdiv (spharm.py:296-313) */
+int swe_uv_from_vortdiv(swe_plan *plan, const double *xi, const double *delta, double *u,
+                        double *v, int batch, void *stream);
+/* SphereGrid.vortdiv_from_uv (spharm.py:315-343) */
+int swe_vortdiv_from_uv(swe_plan *plan, const double *u, const double *v, double *xi,
+                        double *delta, int batch, void *stream);
+
+/* Tendencies of a state batch (dynamics.py:121-165).  kind:
+ *   0 linear_gravity, 1 linear_coriolis, 2 nonlinear_advection + nonlinear_rest,
+ *   3 full_rhs.  state/out: [batch][3][K]; phibar: [batch] (device). */
+int swe_tendency(swe_plan *plan, int kind, const double *state, const double *phibar,
+                 double *out, int batch, void *stream);
+
+/* `nsteps` IMEX steps (steppers.py:155-168, advance :215-222) of every slice,
+ * in place on state [batch][3][K]; phibar [batch] (device).
+ * iters_out (HOST, nullable): [nsteps][batch][2] fixed-point iterations of the
+ * two Crank-Nicolson solves.  resid_out (HOST, nullable): [batch] residual of
+ * slices that hit implicit_max_iter (SWE_ENOCONV). */
+int swe_imex_step(swe_plan *plan, double *state, const double *phibar, int batch,
+                  const swe_stepper_cfg *cfg, int nsteps, int *iters_out, double *resid_out,
+                  void *stream);
+
+/* truncate_pad (spharm.py:352-368) of `nfields` packed arrays between plans
+ * (PrognosticState.to_truncation, dynamics.py:73-83). */
+int swe_truncate_pad(const swe_plan *src, const swe_plan *dst, const double *in, double *out,
+                     int nfields, void *stream);
+
+/* PrognosticState.max_abs / is_finite (dynamics.py:65-71) per state of
+ * [batch][3][K]; outputs are DEVICE arrays [batch]. */
+int swe_state_stats(const swe_plan *plan, const double *state, int batch, double *max_abs_out,
+                    int *finite_out, void *stream);
+
+/* Number of this library's kernels launched since load (evidence counter). */
+long long swe_kernel_launches(void);
+const char *swe_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

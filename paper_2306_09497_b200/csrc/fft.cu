@@ -1,0 +1,414 @@
+// Longitude FFT stage with fused grid products (see fft.cuh).
+//
+// Complex transforms of length N2 = I/2 run in place in shared memory, one
+// warp per row, as mixed-radix Cooley-Tukey:
+//   inverse (c2r): decimation in time; the input Z is written directly in
+//                  digit-reversed order by the spectral loader, output natural;
+//   forward (r2c): decimation in frequency; natural input, digit-reversed
+//                  output read back through the same permutation.
+// Every butterfly reads and writes the same R slots, so a lane needs only R
+// complex registers.  Radices 2,3,4,5,7,11,13 are unrolled (odd R uses the
+// conjugate-pair symmetric form); other primes run warp-cooperatively.
+#include "fft.cuh"
+
+namespace swe {
+
+namespace {
+
+SWE_DEV double2 cm(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+SWE_DEV double2 twd(const double2 *tw, int e, double dir) {
+  double2 w = __ldg(tw + e);
+  w.y *= dir;
+  return w;
+}
+
+// y_t = sum_q v_q exp(dir 2 pi i q t / R), optionally times exp(dir 2 pi i t kt / N2),
+// stored to dst[t*stride].  cr/sr hold cos/sin(2 pi e / R) for e = 0..(R-1)/2.
+template <int R>
+SWE_DEV void dft_store(double2 (&v)[R], double dir, const double *cr, const double *sr,
+                       double2 *dst, int stride, const double2 *tw, int kt) {
+  double2 y[R];
+  if constexpr (R == 2) {
+    y[0] = make_double2(v[0].x + v[1].x, v[0].y + v[1].y);
+    y[1] = make_double2(v[0].x - v[1].x, v[0].y - v[1].y);
+  } else if constexpr (R == 4) {
+    const double2 s02 = make_double2(v[0].x + v[2].x, v[0].y + v[2].y);
+    const double2 d02 = make_double2(v[0].x - v[2].x, v[0].y - v[2].y);
+    const double2 s13 = make_double2(v[1].x + v[3].x, v[1].y + v[3].y);
+    const double2 d13 = make_double2(v[1].x - v[3].x, v[1].y - v[3].y);
+    const double2 rot = make_double2(-dir * d13.y, dir * d13.x);  // i*dir*d13
+    y[0] = make_double2(s02.x + s13.x, s02.y + s13.y);
+    y[2] = make_double2(s02.x - s13.x, s02.y - s13.y);
+    y[1] = make_double2(d02.x + rot.x, d02.y + rot.y);
+    y[3] = make_double2(d02.x - rot.x, d02.y - rot.y);
+  } else {
+    constexpr int H = (R - 1) / 2;
+    y[0] = v[0];
+#pragma unroll
+    for (int q = 1; q <= H; ++q) {
+      const double2 p = v[q], m = v[R - q];
+      v[q] = make_double2(p.x + m.x, p.y + m.y);
+      v[R - q] = make_double2(p.x - m.x, p.y - m.y);
+      y[0].x += v[q].x;
+      y[0].y += v[q].y;
+    }
+#pragma unroll
+    for (int t = 1; t <= H; ++t) {
+      double re = v[0].x, im = v[0].y, sx = 0.0, sy = 0.0;
+#pragma unroll
+      for (int q = 1; q <= H; ++q) {
+        const int e = (q * t) % R;
+        const double c = e <= H ? cr[e] : cr[R - e];
+        const double s = e <= H ? sr[e] : -sr[R - e];
+        re += v[q].x * c;
+        im += v[q].y * c;
+        sx += v[R - q].x * s;
+        sy += v[R - q].y * s;
+      }
+      y[t] = make_double2(re - dir * sy, im + dir * sx);
+      y[R - t] = make_double2(re + dir * sy, im - dir * sx);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t) dst[t * stride] = (kt && t) ? cm(y[t], twd(tw, t * kt, dir)) : y[t];
+}
+
+// in-place stage of radix R over blocks of span L = Lp*R.
+// DIT: inputs twiddled by W_L^{qk}; DIF: outputs twiddled by W_L^{tk}.
+template <int R, bool DIT>
+SWE_DEV void stage_small(double2 *x, int N2, int Lp, double dir, const double2 *tw, int lane) {
+  constexpr int H = (R - 1) / 2;
+  double cr[H + 1], sr[H + 1];
+  if constexpr (R != 2 && R != 4) {
+#pragma unroll
+    for (int e = 0; e <= H; ++e) {
+      const double2 w = __ldg(tw + e * (N2 / R));
+      cr[e] = w.x;
+      sr[e] = w.y;
+    }
+  }
+  const int L = Lp * R, nbf = N2 / R, tws = N2 / L;
+  for (int bf = lane; bf < nbf; bf += 32) {
+    const int g = bf / Lp, k = bf - g * Lp, base = g * L + k;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      v[q] = x[base + q * Lp];
+      if (DIT && q && k) v[q] = cm(v[q], twd(tw, q * k * tws, dir));
+    }
+    dft_store<R>(v, dir, cr, sr, x + base, Lp, tw, DIT ? 0 : k * tws);
+  }
+  __syncwarp();
+}
+
+// any radix: one butterfly at a time, lanes split the R outputs (scr holds R inputs)
+template <bool DIT>
+SWE_DEV void stage_generic(double2 *x, double2 *scr, int N2, int Lp, int R, double dir,
+                           const double2 *tw, int lane) {
+  const int L = Lp * R, nbf = N2 / R, tws = N2 / L, rstep = N2 / R;
+  for (int bf = 0; bf < nbf; ++bf) {
+    const int g = bf / Lp, k = bf - g * Lp, base = g * L + k;
+    for (int q = lane; q < R; q += 32) {
+      double2 v = x[base + q * Lp];
+      if (DIT && q && k) v = cm(v, twd(tw, q * k * tws, dir));
+      scr[q] = v;
+    }
+    __syncwarp();
+    for (int t = lane; t < R; t += 32) {
+      double2 acc = make_double2(0.0, 0.0);
+      int e = 0;
+      for (int q = 0; q < R; ++q) {
+        const double2 z = cm(scr[q], twd(tw, e * rstep, dir));
+        acc.x += z.x;
+        acc.y += z.y;
+        e += t;
+        if (e >= R) e -= R;
+      }
+      if (!DIT && t && k) acc = cm(acc, twd(tw, t * k * tws, dir));
+      x[base + t * Lp] = acc;
+    }
+    __syncwarp();
+  }
+}
+
+template <bool DIT>
+SWE_DEV void run_stage(double2 *x, double2 *scr, int N2, int Lp, int R, double dir,
+                       const double2 *tw, int lane) {
+  switch (R) {
+    case 2: stage_small<2, DIT>(x, N2, Lp, dir, tw, lane); break;
+    case 3: stage_small<3, DIT>(x, N2, Lp, dir, tw, lane); break;
+    case 4: stage_small<4, DIT>(x, N2, Lp, dir, tw, lane); break;
+    case 5: stage_small<5, DIT>(x, N2, Lp, dir, tw, lane); break;
+    case 7: stage_small<7, DIT>(x, N2, Lp, dir, tw, lane); break;
+    case 11: stage_small<11, DIT>(x, N2, Lp, dir, tw, lane); break;
+    case 13: stage_small<13, DIT>(x, N2, Lp, dir, tw, lane); break;
+    default: stage_generic<DIT>(x, scr, N2, Lp, R, dir, tw, lane); break;
+  }
+}
+
+// inverse: digit-reversed input -> natural output (stages r_0 .. r_{S-1})
+SWE_DEV void warp_ifft(double2 *x, double2 *scr, const FftArgs &a, int lane) {
+  int Lp = 1;
+  for (int s = 0; s < a.nst; ++s) {
+    run_stage<true>(x, scr, a.N2, Lp, a.radix[s], 1.0, a.tw, lane);
+    Lp *= a.radix[s];
+  }
+}
+
+// forward: natural input -> digit-reversed output (stages r_{S-1} .. r_0)
+SWE_DEV void warp_fft(double2 *x, double2 *scr, const FftArgs &a, int lane) {
+  int L = a.N2;
+  for (int s = a.nst - 1; s >= 0; --s) {
+    const int R = a.radix[s];
+    run_stage<false>(x, scr, a.N2, L / R, R, -1.0, a.tw, lane);
+    L /= R;
+  }
+}
+
+struct Ctx {
+  double2 *rows, *scr;
+  int j, b0, nsl, tid, nthr, warp, lane, nw;
+};
+
+SWE_DEV double2 *row_of(const FftArgs &a, const Ctx &c, int f, int s) {
+  return c.rows + (size_t)(f * a.spb + s) * a.N2;
+}
+
+// Half spectrum X[0..M] (global [m][J][ld]) -> Z in digit-reversed order, where
+// IDFT_N2(Z)[r] = g[2r] + i g[2r+1] and g = irfft(X * I, n = I) (Im X[0] dropped):
+//   Z[k] = (X[k] + conj X[N2-k]) + i w^k (X[k] - conj X[N2-k]),  w = e^{2 pi i / I}
+SWE_DEV void load_half_z(const FftArgs &a, const Ctx &c, const double *src, int f) {
+  const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1;
+  const double2 *base = reinterpret_cast<const double2 *>(src + (size_t)c.j * a.ld) + c.b0;
+  const size_t mstride = (size_t)a.J * a.ld / 2;  // in double2
+  for (int idx = c.tid; idx < npair * c.nsl; idx += c.nthr) {
+    const int k = idx / c.nsl, s = idx - k * c.nsl;
+    double2 *x = row_of(a, c, f, s);
+    if (k == 0) {
+      const double x0 = __ldg(base + s).x;
+      x[__ldg(a.pos)] = make_double2(x0, x0);
+      continue;
+    }
+    const int k2 = N2 - k;
+    const double2 Xk = k <= M ? __ldg(base + (size_t)k * mstride + s) : make_double2(0.0, 0.0);
+    const double2 Xc = k2 <= M ? __ldg(base + (size_t)k2 * mstride + s) : make_double2(0.0, 0.0);
+    const double2 A = make_double2(Xk.x + Xc.x, Xk.y - Xc.y);
+    const double2 D = make_double2(Xk.x - Xc.x, Xk.y + Xc.y);
+    const double2 Bk = cm(D, __ldg(a.twh + k));
+    x[__ldg(a.pos + k)] = make_double2(A.x - Bk.y, A.y + Bk.x);
+    if (k2 != k) {
+      const double2 A2 = make_double2(Xc.x + Xk.x, Xc.y - Xk.y);
+      const double2 D2 = make_double2(Xc.x - Xk.x, Xc.y + Xk.y);
+      const double2 B2 = cm(D2, __ldg(a.twh + k2));
+      x[__ldg(a.pos + k2)] = make_double2(A2.x - B2.y, A2.y + B2.x);
+    }
+  }
+}
+
+SWE_DEV void load_grid(const FftArgs &a, const Ctx &c, const double *src, int f) {
+  for (int s = 0; s < c.nsl; ++s) {
+    const double *g = src + ((size_t)(c.b0 + s) * a.J + c.j) * a.I;
+    double *r = reinterpret_cast<double *>(row_of(a, c, f, s));
+    for (int n = c.tid; n < a.I; n += c.nthr) r[n] = __ldg(g + n);
+  }
+}
+
+SWE_DEV void store_grid(const FftArgs &a, const Ctx &c, double *dst, int f, double scale) {
+  for (int s = 0; s < c.nsl; ++s) {
+    double *g = dst + ((size_t)(c.b0 + s) * a.J + c.j) * a.I;
+    const double *r = reinterpret_cast<const double *>(row_of(a, c, f, s));
+    for (int n = c.tid; n < a.I; n += c.nthr) g[n] = r[n] * scale;
+  }
+}
+
+SWE_DEV double2 *warp_scr(const FftArgs &a, const Ctx &c) { return c.scr + (size_t)c.warp * a.rgen; }
+
+// inverse transforms of fields [f0, f0+nf) (rows loaded by load_half_z)
+SWE_DEV void c2r_fields(const FftArgs &a, const Ctx &c, int f0, int nf) {
+  for (int task = c.warp; task < nf * c.nsl; task += c.nw) {
+    const int f = f0 + task / c.nsl, s = task % c.nsl;
+    warp_ifft(row_of(a, c, f, s), warp_scr(a, c), a, c.lane);
+  }
+}
+
+// forward transforms of fields fld[o]; store fm[k] * scale[o] (k = 0..M) to a.out[o]
+//   fm[k] = (1/I) sum_n g[n] w^{-nk} = (Ge[k] + w^{-k} Go[k]) / I
+template <int NOUT>
+SWE_DEV void r2c_outputs(const FftArgs &a, const Ctx &c, const int (&fld)[NOUT],
+                         const double (&scale)[NOUT]) {
+  const int N2 = a.N2, M = a.M;
+  for (int task = c.warp; task < NOUT * c.nsl; task += c.nw) {
+    const int o = task / c.nsl, s = task % c.nsl;
+    double2 *x = row_of(a, c, fld[o], s);
+    warp_fft(x, warp_scr(a, c), a, c.lane);
+    const double h = 0.5 * scale[o];
+    double2 *dst = reinterpret_cast<double2 *>(a.out[o] + (size_t)c.j * a.ld) + c.b0 + s;
+    const size_t mstride = (size_t)a.J * a.ld / 2;
+    for (int k = c.lane; k <= M; k += 32) {
+      const double2 zk = x[__ldg(a.pos + k)];
+      const double2 z2 = x[__ldg(a.pos + (k == 0 ? 0 : N2 - k))];
+      const double2 zc = make_double2(z2.x, -z2.y);
+      const double2 S = make_double2(zk.x + zc.x, zk.y + zc.y);     // 2 Ge
+      const double2 D = make_double2(zk.y - zc.y, -(zk.x - zc.x));  // 2 Go
+      double2 w = __ldg(a.twh + k);
+      w.y = -w.y;
+      const double2 t = cm(w, D);
+      dst[(size_t)k * mstride] = make_double2((S.x + t.x) * h, (S.y + t.y) * h);
+    }
+  }
+}
+
+}  // namespace
+
+template <int OP>
+__global__ void __launch_bounds__(256) fft_kernel(const __grid_constant__ FftArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Ctx c;
+  c.j = blockIdx.x;
+  c.b0 = blockIdx.y * a.spb;
+  c.nsl = min(a.spb, a.nslices - c.b0);
+  c.tid = threadIdx.x;
+  c.nthr = blockDim.x;
+  c.warp = threadIdx.x >> 5;
+  c.lane = threadIdx.x & 31;
+  c.nw = blockDim.x >> 5;
+  c.rows = reinterpret_cast<double2 *>(smem_raw);
+  c.scr = c.rows + (size_t)fft_rows_per_slice(OP) * a.spb * a.N2;
+  const int j = c.j;
+  const double ia = a.inv_acos[j];
+  const int I = a.I;
+
+  auto pointwise = [&](auto fn) {
+    for (int idx = c.tid; idx < c.nsl * I; idx += c.nthr) {
+      const int s = idx / I, n = idx - s * I;
+      fn(s, n);
+    }
+  };
+  auto rd = [&](int f, int s) { return reinterpret_cast<double *>(row_of(a, c, f, s)); };
+
+  if constexpr (OP == FOP_SYNTH_GRID) {
+    load_half_z(a, c, a.in[0], 0);
+    __syncthreads();
+    c2r_fields(a, c, 0, 1);
+    __syncthreads();
+    store_grid(a, c, a.gout[0], 0, a.scale_mode ? ia : 1.0);
+  } else if constexpr (OP == FOP_SYNTH2_GRID) {
+    load_half_z(a, c, a.in[0], 0);
+    load_half_z(a, c, a.in[1], 1);
+    __syncthreads();
+    c2r_fields(a, c, 0, 2);
+    __syncthreads();
+    store_grid(a, c, a.gout[0], 0, ia);
+    store_grid(a, c, a.gout[1], 1, ia);
+  } else if constexpr (OP == FOP_ANALYSIS) {
+    load_grid(a, c, a.gin[0], 0);
+    __syncthreads();
+    const int f[1] = {0};
+    const double sc[1] = {a.wq[j] * a.inv_I};
+    r2c_outputs<1>(a, c, f, sc);
+  } else if constexpr (OP == FOP_VORTDIV) {
+    load_grid(a, c, a.gin[0], 0);
+    load_grid(a, c, a.gin[1], 1);
+    __syncthreads();
+    const double cs = a.coslat[j];
+    pointwise([&](int s, int n) {
+      rd(0, s)[n] *= cs;
+      rd(1, s)[n] *= cs;
+    });
+    __syncthreads();
+    const int f[2] = {0, 1};
+    const double w = a.wsin2[j] * a.inv_I * a.inv_a;
+    const double sc[2] = {w, w};
+    r2c_outputs<2>(a, c, f, sc);
+  } else if constexpr (OP == FOP_CORIOLIS) {
+    // linear_coriolis (dynamics.py:129-135): f*u, f*v, then vortdiv_from_uv
+    load_half_z(a, c, a.in[0], 0);
+    load_half_z(a, c, a.in[1], 1);
+    __syncthreads();
+    c2r_fields(a, c, 0, 2);
+    __syncthreads();
+    const double cs = a.coslat[j], fc = a.fcor[j];
+    pointwise([&](int s, int n) {
+      double *u = rd(0, s), *v = rd(1, s);
+      u[n] = (fc * (u[n] * ia)) * cs;
+      v[n] = (fc * (v[n] * ia)) * cs;
+    });
+    __syncthreads();
+    const int f[2] = {0, 1};
+    const double w = a.wsin2[j] * a.inv_I * a.inv_a;
+    const double sc[2] = {w, w};
+    r2c_outputs<2>(a, c, f, sc);
+  } else if constexpr (OP == FOP_NONLINEAR) {
+    // nonlinear_advection + nonlinear_rest (dynamics.py:142-160)
+    // in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi, 5 Phi', 6 delta (half spectra)
+    for (int f = 0; f < 4; ++f) load_half_z(a, c, a.in[f], f);
+    __syncthreads();
+    c2r_fields(a, c, 0, 4);
+    __syncthreads();
+    pointwise([&](int s, int n) {
+      double *r0 = rd(0, s), *r1 = rd(1, s), *r2 = rd(2, s), *r3 = rd(3, s);
+      const double u = r0[n] * ia, v = r1[n] * ia, gx = r2[n] * ia, gy = r3[n] * ia;
+      r0[n] = u;
+      r1[n] = v;
+      r2[n] = -(u * gx + v * gy);
+      r3[n] = 0.5 * (u * u + v * v);
+    });
+    load_half_z(a, c, a.in[4], 4);
+    __syncthreads();
+    c2r_fields(a, c, 4, 1);
+    __syncthreads();
+    const double cs = a.coslat[j];
+    pointwise([&](int s, int n) {
+      double *r0 = rd(0, s), *r1 = rd(1, s);
+      const double xi = rd(4, s)[n];
+      r0[n] = (xi * r0[n]) * cs;
+      r1[n] = (xi * r1[n]) * cs;
+    });
+    __syncthreads();
+    load_half_z(a, c, a.in[5], 4);
+    load_half_z(a, c, a.in[6], 5);
+    __syncthreads();
+    c2r_fields(a, c, 4, 2);
+    __syncthreads();
+    pointwise([&](int s, int n) { rd(2, s)[n] -= rd(4, s)[n] * rd(5, s)[n]; });
+    __syncthreads();
+    const int f[4] = {2, 3, 0, 1};
+    const double w = a.wq[j] * a.inv_I, wv = a.wsin2[j] * a.inv_I * a.inv_a;
+    const double sc[4] = {w, w, wv, wv};
+    r2c_outputs<4>(a, c, f, sc);
+  }
+}
+
+bool fft_small_radix(int R) {
+  return R == 2 || R == 3 || R == 4 || R == 5 || R == 7 || R == 11 || R == 13;
+}
+
+template <int OP>
+static int launch_op(const FftArgs &a, int smem, cudaStream_t st) {
+  static int attr = 0;
+  if (smem > attr) {
+    SWE_CUDA(cudaFuncSetAttribute(fft_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
+  }
+  dim3 grid(a.J, (a.nslices + a.spb - 1) / a.spb);
+  fft_kernel<OP><<<grid, a.nwarps * 32, smem, st>>>(a);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int fft_launch(int op, const FftArgs &a, int smem, cudaStream_t st) {
+  switch (op) {
+    case FOP_SYNTH_GRID: return launch_op<FOP_SYNTH_GRID>(a, smem, st);
+    case FOP_SYNTH2_GRID: return launch_op<FOP_SYNTH2_GRID>(a, smem, st);
+    case FOP_ANALYSIS: return launch_op<FOP_ANALYSIS>(a, smem, st);
+    case FOP_VORTDIV: return launch_op<FOP_VORTDIV>(a, smem, st);
+    case FOP_CORIOLIS: return launch_op<FOP_CORIOLIS>(a, smem, st);
+    case FOP_NONLINEAR: return launch_op<FOP_NONLINEAR>(a, smem, st);
+  }
+  set_error("unknown fft op %d", op);
+  return E_SHAPE;
+}
+
+}  // namespace swe

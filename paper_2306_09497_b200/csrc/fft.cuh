@@ -1,0 +1,52 @@
+// Longitude FFT stage with fused grid-space products.
+//
+// Reference: np.fft.irfft / rfft calls of SphereGrid (spharm.py:241, :257,
+// :267, :325-326) and the grid products of dynamics.py:129-160.  One CTA owns
+// one latitude row j and `spb` consecutive slices; every field of that row is
+// inverse-transformed into shared memory, combined pointwise, and
+// forward-transformed, so grid values never touch HBM.  The real transforms
+// of even length I are done as complex transforms of length N2 = I/2
+// (mixed-radix Stockham, one warp per row).
+#pragma once
+
+#include "common.cuh"
+
+namespace swe {
+
+constexpr int FFT_MAXST = 12;
+constexpr int FFT_MAXF = 8;
+
+enum FftOpKind {
+  FOP_SYNTH_GRID = 0,    // 1 half-spectrum  -> grid (scale: none | 1/(a cos))
+  FOP_SYNTH2_GRID = 1,   // 2 half-spectra   -> 2 grids (scale 1/(a cos)): winds
+  FOP_ANALYSIS = 2,      // grid             -> F (w/I)
+  FOP_VORTDIV = 3,       // 2 grids (u, v)   -> 2 F (u cos, v cos; w/((1-mu^2) I a))
+  FOP_CORIOLIS = 4,      // half(u), half(v) -> F(f u cos), F(f v cos)
+  FOP_NONLINEAR = 5,     // 7 half-spectra   -> F(tphi), F(ke), F(xi u cos), F(xi v cos)
+};
+
+struct FftArgs {
+  int M, J, I, N2, nst;
+  int radix[FFT_MAXST];
+  int ns[FFT_MAXST];
+  const double2 *tw;   // [N2]  e^{2 pi i e / N2}
+  const double2 *twh;  // [N2]  e^{2 pi i k / I}
+  const int *pos;      // [N2]  slot of natural index k in digit-reversed order
+  int rgen;            // largest non-unrolled radix (per-warp scratch, complex), 0 if none
+  int nslices, ld, spb, nwarps;
+  int scale_mode;      // FOP_SYNTH_GRID: 0 none, 1 times 1/(a cos)
+  const double *coslat, *inv_acos, *fcor, *wq, *wsin2;  // per latitude row [J]
+  double inv_I, inv_a;
+  const double *in[FFT_MAXF];   // half spectra [m][J][ld]
+  double *out[FFT_MAXF];        // F spectra    [m][J][ld]
+  const double *gin[2];         // grids [slice][J][I]
+  double *gout[2];
+};
+
+int fft_launch(int op, const FftArgs &a, int smem_bytes, cudaStream_t st);
+__host__ __device__ constexpr int fft_rows_per_slice(int op) {
+  return op == FOP_NONLINEAR ? 6 : ((op == FOP_SYNTH2_GRID || op == FOP_VORTDIV || op == FOP_CORIOLIS) ? 2 : 1);
+}
+bool fft_small_radix(int R);
+
+}  // namespace swe

@@ -1,0 +1,58 @@
+// Legendre-stage kernels: grouped, parity-folded FP64 DMMA GEMMs over order m.
+//
+// Reference: SphereGrid.synthesis / _synthesis_pair / analysis / vortdiv_from_uv
+// (/root/reference/pkg/src/pintswe/spharm.py:238-267, :315-343) loop over m and
+// run one skinny BLAS GEMM per order.  Here every order m is a group of one
+// batched launch, and the north/south symmetry P_mn(-mu) = (-1)^(n-m) P_mn(mu)
+// (H flips the other way) halves the flops: tables hold only the latitude
+// pairs p = 0..Jh-1 (north rows), with the modes of each m-block reordered as
+// [even n-m | odd n-m].
+#pragma once
+
+#include "common.cuh"
+
+namespace swe {
+
+// One additive term of a Legendre contraction.
+//  synthesis: out[E/O] += T(p, n) * f(src[mode][col])
+//  analysis : out[mode][col] += sum_p T(p, n) * f(F±[p][col])
+// with f(x) = sign * scale[mode] * (times_im ? i*m : 1) * x and, for the
+// (0,0) mode only, x.re -= phi0[slice] (phi_prime, dynamics.py:52-56).
+struct LegTerm {
+  const double *tab;    // P or H table, row stride Jp
+  const double *src;    // synthesis: spectral [K][ld]; analysis: grid spectra [m][J][ld]
+  const double *scale;  // per packed mode (synthesis only), nullable
+  const double *phi0;   // per slice, nullable (synthesis only)
+  double sign;
+  int times_im;
+  int flip;  // 0: P-like parity, 1: H-like (odd in mu for even n-m)
+};
+
+struct LegOut {
+  LegTerm t[2];
+  int nterms;
+  double *dst;  // synthesis: [m][J][ld] (north/south rows); analysis: [K][ld]
+};
+
+constexpr int LEG_MAXOUT = 8;
+
+struct LegArgs {
+  LegOut out[LEG_MAXOUT];
+  int nout;
+  int M, J, Jh, Jp, ld;
+  const int *offsets;  // [M+2] packed-mode block offsets
+  const int2 *items;   // (m, tile) work items, heaviest first
+  int nitems;
+};
+
+// Launch helpers (legendre.cu).  items/tiles are prepared by the plan.
+int leg_synth_launch(const LegArgs &a, int ncoltiles, cudaStream_t st);
+int leg_anal_launch(const LegArgs &a, int ncoltiles, cudaStream_t st);
+
+constexpr int SY_BM = 64;   // latitude pairs per CTA
+constexpr int SY_BN = 64;   // real columns per CTA
+constexpr int AN_BR = 16;   // modes per parity per CTA
+constexpr int AN_BN = 64;   // real columns per CTA
+constexpr int AN_KP = 16;   // latitude pairs per k-chunk (Jp is a multiple of this)
+
+}  // namespace swe

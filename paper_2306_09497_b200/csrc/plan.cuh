@@ -1,0 +1,58 @@
+// Transform plan: grid, Legendre tables, FFT factorisation, workspaces.
+//
+// Mirrors SphereGrid.__init__ (spharm.py:154-202): Gauss-Legendre nodes,
+// orthonormal P_mn and H_mn = (1-mu^2) dP/dmu tables, Laplacian eigenvalues,
+// w/(1-mu^2), f = 2 Omega mu.  HBM layout (doubles):
+//   P, H          [K rows][Jp]   row = offset[m] + (n-m even ? (n-m)/2 : ne(m) + (n-m-1)/2),
+//                                column = latitude pair p (north row), zero for p >= Jh
+//   spectral      [K][ld]        packed mode (m-major, n = m..M) x column 2*slice + re/im
+//   half / F      [M+1][J][ld]   order m x latitude row x column
+#pragma once
+
+#include <vector>
+
+#include "fft.cuh"
+#include "legendre.cuh"
+
+namespace swe {
+
+struct Work {
+  int cap = 0;         // slices the buffers were sized for
+  double *spec = nullptr;   // NSPEC spectral arrays [K][2*cap]
+  double *half = nullptr;   // NHALF half-spectrum arrays [M+1][J][2*cap]
+  double *fspec = nullptr;  // NF analysis-input arrays  [M+1][J][2*cap]
+  double *stats = nullptr;  // [cap][8]
+  int *flags = nullptr;     // [cap] active / converged flags, iteration counts
+  int *iters = nullptr;     // [cap]
+  int *counter = nullptr;   // device counter (active slices)
+  int *h_counter = nullptr; // pinned host mirror
+  double *phi0 = nullptr;   // [cap] phibar*sqrt(2)
+  double *phibar = nullptr; // [cap]
+};
+
+constexpr int NSPEC = 22;
+constexpr int NHALF = 7;
+constexpr int NF = 4;
+
+}  // namespace swe
+
+struct swe_plan {
+  int M, J, I, Jh, Jp, K, N2, device;
+  double a, omega, gravity;
+  std::vector<double> mu, w;  // host copies (decreasing mu)
+  // device tables
+  double *P = nullptr, *H = nullptr;
+  int *offsets = nullptr;
+  double *lap_eig = nullptr, *inv_lap = nullptr, *eps = nullptr;
+  double *coslat = nullptr, *inv_acos = nullptr, *fcor = nullptr, *wq = nullptr, *wsin2 = nullptr;
+  double2 *tw = nullptr, *twh = nullptr;
+  int *fft_pos = nullptr;
+  int rgen = 0;
+  int2 *synth_items = nullptr, *anal_items = nullptr;
+  int n_synth_items = 0, n_anal_items = 0;
+  int nst = 0;
+  int radix[swe::FFT_MAXST], ns[swe::FFT_MAXST];
+  std::vector<int> h_offsets;
+  swe::Work ws;
+  size_t table_bytes = 0;
+};

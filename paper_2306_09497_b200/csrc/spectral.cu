@@ -1,0 +1,413 @@
+// Per-mode (spectral-space) kernels: layout changes, Helmholtz/Crank-Nicolson
+// updates, Heun combinations, viscosity, convergence statistics.
+//
+// Reference: dynamics.py:52-63 (phi_prime, add_tendency), :121-126
+// (linear_gravity), :181-200 (viscosity), steppers.py:61-118 (Helmholtz solve,
+// Coriolis fixed point and its convergence test), :143-168 (CN / Heun).
+// Internal spectral layout: [K][ld] doubles, column 2*slice + re/im.
+#include "spectral.cuh"
+
+namespace swe {
+
+// ---- layout: boundary [B][F][K] complex <-> internal F x [K][B] complex ------
+__global__ void k_to_internal(const double2 *__restrict__ src, SpecPtrs dst, int B, int F, int K) {
+  __shared__ double2 tile[32][33];
+  const int f = blockIdx.z, k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int b = b0 + r, k = k0 + threadIdx.x;
+    if (b < B && k < K) tile[r][threadIdx.x] = src[((size_t)b * F + f) * K + k];
+  }
+  __syncthreads();
+  double2 *d = reinterpret_cast<double2 *>(dst.p[f]);
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int k = k0 + r, b = b0 + threadIdx.x;
+    if (b < B && k < K) d[(size_t)k * B + b] = tile[threadIdx.x][r];
+  }
+}
+
+__global__ void k_to_boundary(SpecPtrsC src, double2 *__restrict__ dst, int B, int F, int K) {
+  __shared__ double2 tile[32][33];
+  const int f = blockIdx.z, k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  const double2 *s = reinterpret_cast<const double2 *>(src.p[f]);
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int k = k0 + r, b = b0 + threadIdx.x;
+    if (b < B && k < K) tile[r][threadIdx.x] = s[(size_t)k * B + b];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int b = b0 + r, k = k0 + threadIdx.x;
+    if (b < B && k < K) dst[((size_t)b * F + f) * K + k] = tile[threadIdx.x][r];
+  }
+}
+
+int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, cudaStream_t st) {
+  dim3 grid((K + 31) / 32, (B + 31) / 32, F), blk(32, 8);
+  k_to_internal<<<grid, blk, 0, st>>>(reinterpret_cast<const double2 *>(src), dst, B, F, K);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, cudaStream_t st) {
+  dim3 grid((K + 31) / 32, (B + 31) / 32, F), blk(32, 8);
+  k_to_boundary<<<grid, blk, 0, st>>>(src, reinterpret_cast<double2 *>(dst), B, F, K);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+// ---- grid-stride helper over (k, b) complex elements -------------------------
+#define FOR_KB(K, B)                                                                  \
+  for (size_t _i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; _i < (size_t)(K) * (B); \
+       _i += (size_t)gridDim.x * blockDim.x)
+
+static inline int nblocks(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16); }
+
+SWE_DEV double2 ld2(const double *p, size_t i) { return reinterpret_cast<const double2 *>(p)[i]; }
+SWE_DEV void st2(double *p, size_t i, double2 v) { reinterpret_cast<double2 *>(p)[i] = v; }
+SWE_DEV double2 sc2(double s, double2 v) { return make_double2(s * v.x, s * v.y); }
+SWE_DEV double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
+// rhs = U + alpha * (L_G U + L_C U)   (steppers.py:143-152, dynamics.py:121-139)
+__global__ void k_lin_rhs(int K, int B, const double *U0, const double *U1, const double *U2,
+                          const double *lcx, const double *lcd, double alpha, const double *eps,
+                          const double *phibar, double *R0, double *R1, double *R2) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
+    const double2 ph = ld2(U0, _i), xi = ld2(U1, _i), de = ld2(U2, _i);
+    const double pb = phibar[b];
+    // lin.phi = -phibar*delta ; lin.xi = L_C.xi ; lin.delta = -lap(phi) + L_C.delta
+    const double2 lphi = make_double2(-pb * de.x, -pb * de.y);
+    const double2 lxi = lcx ? ld2(lcx, _i) : make_double2(0.0, 0.0);
+    double2 lde = sc2(eps[k], ph);
+    if (lcd) lde = add2(lde, ld2(lcd, _i));
+    st2(R0, _i, add2(ph, sc2(alpha, lphi)));
+    st2(R1, _i, add2(xi, sc2(alpha, lxi)));
+    st2(R2, _i, add2(de, sc2(alpha, lde)));
+  }
+}
+
+// T = L_G U (+ L_C U)   (dynamics.py:121-139)
+__global__ void k_lin_tend(int K, int B, const double *U0, const double *U2, const double *lcx,
+                           const double *lcd, const double *eps, const double *phibar, double *T0,
+                           double *T1, double *T2) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
+    const double2 ph = ld2(U0, _i), de = ld2(U2, _i);
+    const double pb = phibar[b];
+    st2(T0, _i, make_double2(-pb * de.x, -pb * de.y));
+    st2(T1, _i, lcx ? ld2(lcx, _i) : make_double2(0.0, 0.0));
+    double2 d = sc2(eps[k], ph);
+    if (lcd) d = add2(d, ld2(lcd, _i));
+    st2(T2, _i, d);
+  }
+}
+
+// u = helm(rhs + alpha*lc) (steppers.py:61-71, :96-99) for active slices, with the
+// per-slice convergence statistics of steppers.py:100-109 accumulated in stats:
+// stats[b*8 + f] = max|new_f|, stats[b*8 + 3 + f] = max|new_f - old_f|.
+__global__ void k_helm(int K, int B, const double *R0, const double *R1, const double *R2,
+                       const double *lcx, const double *lcd, double alpha, const double *eps,
+                       const double *phibar, double *U0, double *U1, double *U2,
+                       const int *active, double *stats) {
+  // block: 32 slices x 8 mode rows; grid.x over slice tiles, grid.y over modes
+  __shared__ double red[8][32][6];
+  const int b = blockIdx.x * 32 + threadIdx.x;
+  double mx[6] = {0, 0, 0, 0, 0, 0};
+  const bool act = (b < B) && (active == nullptr || active[b]);
+  if (act) {
+    const double pb = phibar[b];
+    for (int k = blockIdx.y * blockDim.y + threadIdx.y; k < K; k += gridDim.y * blockDim.y) {
+      const size_t i = (size_t)k * B + b;
+      const double2 rp = ld2(R0, i);
+      double2 rx = ld2(R1, i), rd = ld2(R2, i);
+      if (lcx) {
+        rx = add2(rx, sc2(alpha, ld2(lcx, i)));
+        rd = add2(rd, sc2(alpha, ld2(lcd, i)));
+      }
+      const double e = eps[k];
+      const double denom = 1.0 + alpha * alpha * pb * e;
+      const double apb = alpha * pb;
+      const double2 ph = make_double2((rp.x - apb * rd.x) / denom, (rp.y - apb * rd.y) / denom);
+      const double ae = alpha * e;
+      const double2 de = make_double2(rd.x + ae * ph.x, rd.y + ae * ph.y);
+      if (stats) {
+        const double2 o0 = ld2(U0, i), o1 = ld2(U1, i), o2 = ld2(U2, i);
+        mx[0] = fmax(mx[0], hypot(ph.x, ph.y));
+        mx[1] = fmax(mx[1], hypot(rx.x, rx.y));
+        mx[2] = fmax(mx[2], hypot(de.x, de.y));
+        mx[3] = fmax(mx[3], hypot(ph.x - o0.x, ph.y - o0.y));
+        mx[4] = fmax(mx[4], hypot(rx.x - o1.x, rx.y - o1.y));
+        mx[5] = fmax(mx[5], hypot(de.x - o2.x, de.y - o2.y));
+        // NaN must survive the max (np.max propagates it)
+        for (int q = 0; q < 3; ++q) {
+          const double2 nv = q == 0 ? ph : (q == 1 ? rx : de);
+          const double2 ov = q == 0 ? o0 : (q == 1 ? o1 : o2);
+          if (isnan(nv.x) || isnan(nv.y)) mx[q] = nan("");
+          if (isnan(nv.x - ov.x) || isnan(nv.y - ov.y)) mx[3 + q] = nan("");
+        }
+      }
+      st2(U0, i, ph);
+      st2(U1, i, rx);
+      st2(U2, i, de);
+    }
+  }
+  if (!stats) return;
+  for (int q = 0; q < 6; ++q) red[threadIdx.y][threadIdx.x][q] = mx[q];
+  __syncthreads();
+  if (threadIdx.y == 0 && act) {
+    for (int q = 0; q < 6; ++q) {
+      double v = red[0][threadIdx.x][q];
+      for (int r = 1; r < blockDim.y; ++r) {
+        const double w = red[r][threadIdx.x][q];
+        v = (isnan(w) || isnan(v)) ? nan("") : fmax(v, w);
+      }
+      atomic_max_nonneg(stats + (size_t)b * 8 + q, v);
+    }
+  }
+}
+
+// per-slice convergence decision (steppers.py:100-112); resets stats
+__global__ void k_decide(int B, double *stats, int *active, int *iters, int *counter, double tol) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double *s = stats + (size_t)b * 8;
+  if (active[b]) {
+    iters[b] += 1;
+    double overall = fmax(fmax(s[0], s[1]), s[2]);
+    if (isnan(s[0]) || isnan(s[1]) || isnan(s[2])) overall = nan("");
+    overall = (overall > 1e-300 || isnan(overall)) ? overall : 1e-300;
+    bool done = true;
+    for (int f = 0; f < 3; ++f) {
+      const double tiny = 1e-13 * overall;
+      const double scale = (s[f] >= tiny || isnan(s[f])) ? s[f] : tiny;
+      if (s[3 + f] > tol * scale) done = false;
+    }
+    if (done) active[b] = 0;
+    else atomicAdd(counter, 1);
+  }
+  for (int q = 0; q < 8; ++q) s[q] = 0.0;
+}
+
+__global__ void k_fill_int(int *p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// y = a + s*(x1 (+ x2)) for three fields (add_tendency, dynamics.py:58-63)
+__global__ void k_axpy3(int n, Ptr3C a, Ptr3C x1, Ptr3C x2, double s, Ptr3 y) {
+  FOR_KB(n, 1) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      double2 t = ld2(x1.p[f], _i);
+      if (x2.p[f]) t = add2(t, ld2(x2.p[f], _i));
+      st2(y.p[f], _i, add2(ld2(a.p[f], _i), sc2(s, t)));
+    }
+  }
+}
+
+// d = curl - lap(ke) (dynamics.py:151), optionally + L_C (explicit Coriolis)
+__global__ void k_tend_finish(int K, int B, double *kd, const double *ke, const double *lap,
+                              double *kx, const double *lcx, const double *lcd) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B);
+    const double2 ke2 = ld2(ke, _i);
+    const double l = lap[k];
+    double2 d = ld2(kd, _i);
+    d = make_double2(d.x - ke2.x * l, d.y - ke2.y * l);
+    if (lcd) {
+      d = add2(d, ld2(lcd, _i));
+      st2(kx, _i, add2(ld2(kx, _i), ld2(lcx, _i)));
+    }
+    st2(kd, _i, d);
+  }
+}
+
+// backward-Euler damping b(n) (dynamics.py:181-200), in place on three fields
+__global__ void k_visc(int K, int B, Ptr3 u, const double *nn1a2, double dtnu, double halfq) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B);
+    const double bh = 1.0 / (1.0 + dtnu * pow(nn1a2[k], halfq));
+#pragma unroll
+    for (int f = 0; f < 3; ++f) st2(u.p[f], _i, sc2(bh, ld2(u.p[f], _i)));
+  }
+}
+
+__global__ void k_copy3(int n, Ptr3C a, Ptr3 y) {
+  FOR_KB(n, 1) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) st2(y.p[f], _i, ld2(a.p[f], _i));
+  }
+}
+
+__global__ void k_phi0(int B, const double *phibar, double *pb, double *phi0) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) {
+    pb[b] = phibar[b];
+    phi0[b] = phibar[b] * 1.4142135623730951;  // SQRT2 (dynamics.py:20, :52-56)
+  }
+}
+
+// residual |u - alpha*(L_G + L_C) u - rhs| per slice (steppers.py:113-118)
+__global__ void k_resid(int K, int B, Ptr3C u, Ptr3C rhs, const double *lcx, const double *lcd,
+                        double alpha, const double *eps, const double *phibar, double *res) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
+    const double2 ph = ld2(u.p[0], _i), xi = ld2(u.p[1], _i), de = ld2(u.p[2], _i);
+    const double pb = phibar[b];
+    const double2 lph = make_double2(-pb * de.x, -pb * de.y);
+    const double2 lxi = ld2(lcx, _i);
+    const double2 lde = add2(sc2(eps[k], ph), ld2(lcd, _i));
+    double r = 0.0;
+    const double2 v[3] = {ph, xi, de}, l[3] = {lph, lxi, lde};
+    for (int f = 0; f < 3; ++f) {
+      const double2 rr = ld2(rhs.p[f], _i);
+      r = fmax(r, hypot(v[f].x - alpha * l[f].x - rr.x, v[f].y - alpha * l[f].y - rr.y));
+    }
+    atomic_max_nonneg(res + b, r);
+  }
+}
+
+// boundary-layout state stats: max|c| over 3 fields and finiteness (dynamics.py:65-71)
+__global__ void k_state_stats(const double2 *__restrict__ s, int B, int K, double *maxabs,
+                              int *finite) {
+  const int b = blockIdx.y;
+  double mx = 0.0;
+  int fin = 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * K; i += gridDim.x * blockDim.x) {
+    const double2 v = s[(size_t)b * 3 * K + i];
+    if (!isfinite(v.x) || !isfinite(v.y)) fin = 0;
+    const double h = hypot(v.x, v.y);
+    mx = (isnan(h) || isnan(mx)) ? nan("") : fmax(mx, h);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double w = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (isnan(w) || isnan(mx)) ? nan("") : fmax(mx, w);
+    fin &= __shfl_xor_sync(0xffffffffu, fin, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(maxabs + b, mx);
+    if (!fin) atomicAnd(finite + b, 0);
+  }
+}
+
+// truncate_pad (spharm.py:352-368): [nb][Ks] -> [nb][Kd]
+__global__ void k_truncate(const double2 *__restrict__ src, double2 *__restrict__ dst, int nb,
+                           int Ms, int Md, const int *offs_s, const int *offs_d) {
+  const int Kd = (Md + 1) * (Md + 2) / 2, Ks = (Ms + 1) * (Ms + 2) / 2;
+  const int mm = min(Ms, Md);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)nb * Kd;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / Kd), k = (int)(i - (size_t)b * Kd);
+    // locate (m, n) of destination mode k
+    int lo = 0, hi = Md;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (offs_d[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    const int m = lo, n = m + (k - offs_d[m]);
+    double2 v = make_double2(0.0, 0.0);
+    if (m <= mm && n <= mm) v = src[(size_t)b * Ks + offs_s[m] + (n - m)];
+    dst[i] = v;
+  }
+}
+
+// ---- host wrappers -----------------------------------------------------------
+int lin_rhs(int K, int B, const double *const U[3], const double *lcx, const double *lcd,
+            double alpha, const double *eps, const double *phibar, double *const R[3],
+            cudaStream_t st) {
+  k_lin_rhs<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, U[0], U[1], U[2], lcx, lcd, alpha, eps,
+                                                    phibar, R[0], R[1], R[2]);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int lin_tend(int K, int B, const double *U0, const double *U2, const double *lcx,
+             const double *lcd, const double *eps, const double *phibar, double *const T[3],
+             cudaStream_t st) {
+  k_lin_tend<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, U0, U2, lcx, lcd, eps, phibar, T[0],
+                                                     T[1], T[2]);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int helm(int K, int B, const double *const R[3], const double *lcx, const double *lcd,
+         double alpha, const double *eps, const double *phibar, double *const U[3],
+         const int *active, double *stats, cudaStream_t st) {
+  const int ybl = std::max(1, std::min((K + 7) / 8, (148 * 8) / ((B + 31) / 32)));
+  dim3 grid((B + 31) / 32, ybl), blk(32, 8);
+  k_helm<<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0], U[1],
+                                U[2], active, stats);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int decide(int B, double *stats, int *active, int *iters, int *counter, double tol,
+           cudaStream_t st) {
+  k_decide<<<(B + 127) / 128, 128, 0, st>>>(B, stats, active, iters, counter, tol);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int fill_int(int *p, int n, int v, cudaStream_t st) {
+  k_fill_int<<<(n + 255) / 256, 256, 0, st>>>(p, n, v);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int axpy3(size_t n, Ptr3C a, Ptr3C x1, Ptr3C x2, double s, Ptr3 y, cudaStream_t st) {
+  k_axpy3<<<nblocks(n), 256, 0, st>>>((int)n, a, x1, x2, s, y);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int tend_finish(int K, int B, double *kd, const double *ke, const double *lap, double *kx,
+                const double *lcx, const double *lcd, cudaStream_t st) {
+  k_tend_finish<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, kd, ke, lap, kx, lcx, lcd);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int visc(int K, int B, Ptr3 u, const double *nn1a2, double dtnu, double halfq, cudaStream_t st) {
+  k_visc<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, u, nn1a2, dtnu, halfq);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int copy3(size_t n, Ptr3C a, Ptr3 y, cudaStream_t st) {
+  k_copy3<<<nblocks(n), 256, 0, st>>>((int)n, a, y);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int set_phibar(int B, const double *phibar, double *pb, double *phi0, cudaStream_t st) {
+  k_phi0<<<(B + 127) / 128, 128, 0, st>>>(B, phibar, pb, phi0);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int resid(int K, int B, Ptr3C u, Ptr3C rhs, const double *lcx, const double *lcd, double alpha,
+          const double *eps, const double *phibar, double *res, cudaStream_t st) {
+  k_resid<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, u, rhs, lcx, lcd, alpha, eps, phibar, res);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int state_stats(const double *s, int B, int K, double *maxabs, int *finite, cudaStream_t st) {
+  SWE_CUDA(cudaMemsetAsync(maxabs, 0, sizeof(double) * B, st));
+  k_fill_int<<<(B + 255) / 256, 256, 0, st>>>(finite, B, 1);
+  dim3 grid(std::max(1, std::min(64, (3 * K + 255) / 256)), B);
+  k_state_stats<<<grid, 256, 0, st>>>(reinterpret_cast<const double2 *>(s), B, K, maxabs, finite);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int truncate_pad(const double *src, double *dst, int nb, int Ms, int Md, const int *offs_s,
+                 const int *offs_d, cudaStream_t st) {
+  const size_t n = (size_t)nb * (Md + 1) * (Md + 2) / 2;
+  k_truncate<<<nblocks(n), 256, 0, st>>>(reinterpret_cast<const double2 *>(src),
+                                        reinterpret_cast<double2 *>(dst), nb, Ms, Md, offs_s,
+                                        offs_d);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+}  // namespace swe

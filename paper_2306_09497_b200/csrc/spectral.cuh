@@ -1,0 +1,49 @@
+// Spectral-space kernels (declarations); see spectral.cu.
+#pragma once
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace swe {
+
+struct SpecPtrs {
+  double *p[8];
+};
+struct SpecPtrsC {
+  const double *p[8];
+};
+struct Ptr3 {
+  double *p[3];
+};
+struct Ptr3C {
+  const double *p[3];
+};
+
+int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, cudaStream_t st);
+int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, cudaStream_t st);
+int lin_rhs(int K, int B, const double *const U[3], const double *lcx, const double *lcd,
+            double alpha, const double *eps, const double *phibar, double *const R[3],
+            cudaStream_t st);
+int lin_tend(int K, int B, const double *U0, const double *U2, const double *lcx,
+             const double *lcd, const double *eps, const double *phibar, double *const T[3],
+             cudaStream_t st);
+int helm(int K, int B, const double *const R[3], const double *lcx, const double *lcd,
+         double alpha, const double *eps, const double *phibar, double *const U[3],
+         const int *active, double *stats, cudaStream_t st);
+int decide(int B, double *stats, int *active, int *iters, int *counter, double tol,
+           cudaStream_t st);
+int fill_int(int *p, int n, int v, cudaStream_t st);
+int axpy3(size_t n, Ptr3C a, Ptr3C x1, Ptr3C x2, double s, Ptr3 y, cudaStream_t st);
+int tend_finish(int K, int B, double *kd, const double *ke, const double *lap, double *kx,
+                const double *lcx, const double *lcd, cudaStream_t st);
+int visc(int K, int B, Ptr3 u, const double *nn1a2, double dtnu, double halfq, cudaStream_t st);
+int copy3(size_t n, Ptr3C a, Ptr3 y, cudaStream_t st);
+int set_phibar(int B, const double *phibar, double *pb, double *phi0, cudaStream_t st);
+int resid(int K, int B, Ptr3C u, Ptr3C rhs, const double *lcx, const double *lcd, double alpha,
+          const double *eps, const double *phibar, double *res, cudaStream_t st);
+int state_stats(const double *s, int B, int K, double *maxabs, int *finite, cudaStream_t st);
+int truncate_pad(const double *src, double *dst, int nb, int Ms, int Md, const int *offs_s,
+                 const int *offs_d, cudaStream_t st);
+
+}  // namespace swe

@@ -1,0 +1,593 @@
+// Host orchestration of the batched fine propagator and the C ABI.
+//
+// Reference call graph (steppers.py:155-168):
+//   imex_step: CN_half(dt/4) -> Heun on N = N_A + N_R -> CN_half(dt/4) -> viscosity
+//   CN_half:   rhs = U + a (L_G + L_C) U ; (I - a L) U = rhs by Helmholtz + Coriolis
+//              fixed point (steppers.py:74-118)
+// Here one call advances `batch` slices in lockstep; the fixed point freezes
+// each slice at its own convergence iteration (per-slice semantics kept).
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/swe_b200.h"
+#include "plan.cuh"
+#include "spectral.cuh"
+
+namespace swe {
+
+long long g_launches = 0;
+const char *last_error();
+int plan_create(int M, double a, double omega, double gravity, int device, swe_plan **out);
+void plan_destroy(swe_plan *pl);
+int work_reserve(swe_plan *pl, int B);
+
+namespace {
+
+struct Run {
+  swe_plan *pl;
+  int B;
+  size_t ld;
+  cudaStream_t st;
+  double *spec(int i) const { return pl->ws.spec + (size_t)i * pl->K * ld; }
+  double *half(int i) const { return pl->ws.half + (size_t)i * (pl->M + 1) * pl->J * ld; }
+  double *fsp(int i) const { return pl->ws.fspec + (size_t)i * (pl->M + 1) * pl->J * ld; }
+};
+
+LegArgs leg_args(const Run &r) {
+  LegArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = r.pl->M;
+  a.J = r.pl->J;
+  a.Jh = r.pl->Jh;
+  a.Jp = r.pl->Jp;
+  a.ld = (int)r.ld;
+  a.offsets = r.pl->offsets;
+  return a;
+}
+
+LegTerm term(const double *tab, const double *src, double sign = 1.0, int times_im = 0,
+             const double *scale = nullptr, const double *phi0 = nullptr) {
+  LegTerm t;
+  t.tab = tab;
+  t.src = src;
+  t.scale = scale;
+  t.phi0 = phi0;
+  t.sign = sign;
+  t.times_im = times_im;
+  t.flip = 0;
+  return t;
+}
+
+void set_out(LegArgs &a, int i, double *dst, LegTerm t0, const LegTerm *t1, const double *H) {
+  a.out[i].dst = dst;
+  a.out[i].t[0] = t0;
+  a.out[i].t[0].flip = (t0.tab == H);
+  a.out[i].nterms = 1;
+  if (t1) {
+    a.out[i].t[1] = *t1;
+    a.out[i].t[1].flip = (t1->tab == H);
+    a.out[i].nterms = 2;
+  }
+}
+
+int synth(const Run &r, LegArgs &a) {
+  a.items = r.pl->synth_items;
+  a.nitems = r.pl->n_synth_items;
+  return leg_synth_launch(a, (int)((r.ld + SY_BN - 1) / SY_BN), r.st);
+}
+
+int anal(const Run &r, LegArgs &a) {
+  a.items = r.pl->anal_items;
+  a.nitems = r.pl->n_anal_items;
+  return leg_anal_launch(a, (int)((r.ld + AN_BN - 1) / AN_BN), r.st);
+}
+
+int fft_tasks_per_slice(int op) {
+  switch (op) {
+    case FOP_NONLINEAR: return 4;
+    case FOP_SYNTH2_GRID: case FOP_VORTDIV: case FOP_CORIOLIS: return 2;
+    default: return 1;
+  }
+}
+
+int fft(const Run &r, int op, FftArgs &a) {
+  swe_plan *pl = r.pl;
+  a.M = pl->M;
+  a.J = pl->J;
+  a.I = pl->I;
+  a.N2 = pl->N2;
+  a.nst = pl->nst;
+  for (int s = 0; s < pl->nst; ++s) {
+    a.radix[s] = pl->radix[s];
+    a.ns[s] = pl->ns[s];
+  }
+  a.tw = pl->tw;
+  a.twh = pl->twh;
+  a.pos = pl->fft_pos;
+  a.rgen = pl->rgen;
+  a.nslices = r.B;
+  a.ld = (int)r.ld;
+  a.coslat = pl->coslat;
+  a.inv_acos = pl->inv_acos;
+  a.fcor = pl->fcor;
+  a.wq = pl->wq;
+  a.wsin2 = pl->wsin2;
+  a.inv_I = 1.0 / pl->I;
+  a.inv_a = 1.0 / pl->a;
+  const int rows = fft_rows_per_slice(op);
+  const size_t rowb = (size_t)pl->N2 * sizeof(double2);
+  const size_t scrb = (size_t)pl->rgen * sizeof(double2);
+  const size_t limit = 227 * 1024;
+  int spb = std::min(2, r.B), nw = 1;
+  size_t smem = 0;
+  for (; spb >= 1; --spb) {
+    nw = std::min(8, fft_tasks_per_slice(op) * spb);
+    smem = rows * spb * rowb + nw * scrb;
+    if (smem <= limit) break;
+  }
+  if (spb < 1) {
+    set_error("FFT row buffers for M=%d do not fit in shared memory", pl->M);
+    return E_SHAPE;
+  }
+  a.spb = spb;
+  a.nwarps = nw;
+  return fft_launch(op, a, (int)smem, r.st);
+}
+
+// L_C(xi, delta) = (0, -div(fV), curl(fV))  (dynamics.py:129-135)
+int eval_coriolis(const Run &r, const double *xi, const double *de, double *oxi, double *ode) {
+  swe_plan *pl = r.pl;
+  const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
+  int rc;
+  {
+    LegArgs a = leg_args(r);
+    a.nout = 2;
+    // u = P (i m chi) + H (-psi), v = P (i m psi) + H chi   (spharm.py:296-313)
+    LegTerm hu = term(H, xi, -1.0, 0, il), hv = term(H, de, 1.0, 0, il);
+    set_out(a, 0, r.half(0), term(P, de, 1.0, 1, il), &hu, H);
+    set_out(a, 1, r.half(1), term(P, xi, 1.0, 1, il), &hv, H);
+    if ((rc = synth(r, a))) return rc;
+  }
+  {
+    FftArgs f;
+    memset(&f, 0, sizeof(f));
+    f.in[0] = r.half(0);
+    f.in[1] = r.half(1);
+    f.out[0] = r.fsp(0);
+    f.out[1] = r.fsp(1);
+    if ((rc = fft(r, FOP_CORIOLIS, f))) return rc;
+  }
+  {
+    LegArgs a = leg_args(r);
+    a.nout = 2;
+    // xi_t = -div = -(i m P'A - H'B) ; delta_t = curl = i m P'B + H'A   (spharm.py:336-343)
+    LegTerm hx = term(H, r.fsp(1), 1.0), hd = term(H, r.fsp(0), 1.0);
+    set_out(a, 0, oxi, term(P, r.fsp(0), -1.0, 1), &hx, H);
+    set_out(a, 1, ode, term(P, r.fsp(1), 1.0, 1), &hd, H);
+    if ((rc = anal(r, a))) return rc;
+  }
+  return OK;
+}
+
+// N = N_A + N_R (dynamics.py:142-160) into k[3]; ke uses scratch spectral array `tmp`
+int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], double *tmp) {
+  swe_plan *pl = r.pl;
+  const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
+  int rc;
+  {
+    LegArgs a = leg_args(r);
+    a.nout = 7;
+    LegTerm hu = term(H, U[1], -1.0, 0, il), hv = term(H, U[2], 1.0, 0, il);
+    set_out(a, 0, r.half(0), term(P, U[2], 1.0, 1, il), &hu, H);          // u
+    set_out(a, 1, r.half(1), term(P, U[1], 1.0, 1, il), &hv, H);          // v
+    set_out(a, 2, r.half(2), term(P, U[0], 1.0, 1), nullptr, H);          // d_lambda Phi
+    set_out(a, 3, r.half(3), term(H, U[0], 1.0), nullptr, H);             // H Phi
+    set_out(a, 4, r.half(4), term(P, U[1]), nullptr, H);                  // xi
+    set_out(a, 5, r.half(5), term(P, U[0], 1.0, 0, nullptr, pl->ws.phi0), nullptr, H);  // Phi'
+    set_out(a, 6, r.half(6), term(P, U[2]), nullptr, H);                  // delta
+    if ((rc = synth(r, a))) return rc;
+  }
+  {
+    FftArgs f;
+    memset(&f, 0, sizeof(f));
+    for (int i = 0; i < 7; ++i) f.in[i] = r.half(i);
+    for (int i = 0; i < 4; ++i) f.out[i] = r.fsp(i);
+    if ((rc = fft(r, FOP_NONLINEAR, f))) return rc;
+  }
+  {
+    LegArgs a = leg_args(r);
+    a.nout = 4;
+    LegTerm hx = term(H, r.fsp(3), 1.0), hd = term(H, r.fsp(2), 1.0);
+    set_out(a, 0, k[0], term(P, r.fsp(0)), nullptr, H);          // -(V.grad Phi) - Phi' delta
+    set_out(a, 1, tmp, term(P, r.fsp(1)), nullptr, H);           // ke
+    set_out(a, 2, k[1], term(P, r.fsp(2), -1.0, 1), &hx, H);     // -div(xi V)
+    set_out(a, 3, k[2], term(P, r.fsp(3), 1.0, 1), &hd, H);      // curl(xi V)
+    if ((rc = anal(r, a))) return rc;
+  }
+  return OK;
+}
+
+// explicit tendency (steppers.py:127-140)
+int explicit_tendency(const Run &r, const swe_stepper_cfg &cfg, const double *const U[3],
+                      double *const k[3], double *tmp, double *lcx, double *lcd) {
+  int rc;
+  const size_t n = (size_t)r.pl->K * r.B;
+  const bool expl = !cfg.coriolis_implicit;
+  if (cfg.include_nonlinear) {
+    if ((rc = eval_nonlinear(r, U, k, tmp))) return rc;
+    if (expl && (rc = eval_coriolis(r, U[1], U[2], lcx, lcd))) return rc;
+    return tend_finish(r.pl->K, r.B, k[2], tmp, r.pl->lap_eig, k[1], expl ? lcx : nullptr,
+                       expl ? lcd : nullptr, r.st);
+  }
+  for (int f = 0; f < 3; ++f) SWE_CUDA(cudaMemsetAsync(k[f], 0, n * 16, r.st));
+  if (expl) {
+    if ((rc = eval_coriolis(r, U[1], U[2], k[1], k[2]))) return rc;
+  }
+  return OK;
+}
+
+struct Bufs {
+  double *U[3], *R[3], *LC[2], *US[3], *K1[3], *MID[3], *K2[3], *TMP;
+};
+
+Bufs bufs(const Run &r) {
+  Bufs b;
+  for (int f = 0; f < 3; ++f) {
+    b.U[f] = r.spec(f);
+    b.R[f] = r.spec(3 + f);
+    b.US[f] = r.spec(8 + f);
+    b.K1[f] = r.spec(11 + f);
+    b.MID[f] = r.spec(14 + f);
+    b.K2[f] = r.spec(17 + f);
+  }
+  b.LC[0] = r.spec(6);
+  b.LC[1] = r.spec(7);
+  b.TMP = r.spec(20);
+  return b;
+}
+
+// (I - a L) dst = (I + a L) src   (steppers.py:143-152, :74-118)
+int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *const src[3],
+            double *const dst[3], double alpha, int *iters_host, double *resid_host) {
+  swe_plan *pl = r.pl;
+  const int K = pl->K, B = r.B;
+  const bool impl = cfg.coriolis_implicit != 0;
+  int rc;
+  if (impl && (rc = eval_coriolis(r, src[1], src[2], b.LC[0], b.LC[1]))) return rc;
+  const double *Uc[3] = {src[0], src[1], src[2]};
+  if ((rc = lin_rhs(K, B, Uc, impl ? b.LC[0] : nullptr, impl ? b.LC[1] : nullptr, alpha, pl->eps,
+                    pl->ws.phibar, b.R, r.st)))
+    return rc;
+  const double *Rc[3] = {b.R[0], b.R[1], b.R[2]};
+  if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, pl->ws.phibar, dst, nullptr, nullptr,
+                 r.st)))
+    return rc;
+  if (!impl || pl->omega == 0.0) {
+    if (iters_host)
+      for (int i = 0; i < B; ++i) iters_host[2 * i] = 0;
+    return OK;
+  }
+  Work &w = pl->ws;
+  if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
+  SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * 8 * B, r.st));
+  int active = B;
+  for (int it = 0; it < cfg.implicit_max_iter && active > 0; ++it) {
+    if ((rc = eval_coriolis(r, dst[1], dst[2], b.LC[0], b.LC[1]))) return rc;
+    if ((rc = helm(K, B, Rc, b.LC[0], b.LC[1], alpha, pl->eps, w.phibar, dst, w.flags, w.stats,
+                   r.st)))
+      return rc;
+    SWE_CUDA(cudaMemsetAsync(w.counter, 0, sizeof(int), r.st));
+    if ((rc = decide(B, w.stats, w.flags, w.iters, w.counter, cfg.implicit_tol, r.st))) return rc;
+    SWE_CUDA(cudaMemcpyAsync(w.h_counter, w.counter, sizeof(int), cudaMemcpyDeviceToHost, r.st));
+    SWE_CUDA(cudaStreamSynchronize(r.st));
+    active = *w.h_counter;
+  }
+  if (iters_host) {
+    std::vector<int> it(B);
+    SWE_CUDA(cudaMemcpyAsync(it.data(), w.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, r.st));
+    SWE_CUDA(cudaStreamSynchronize(r.st));
+    for (int i = 0; i < B; ++i) iters_host[2 * i] = it[i];
+  }
+  if (active > 0) {
+    // residual of the unconverged slices (steppers.py:113-118)
+    if ((rc = eval_coriolis(r, dst[1], dst[2], b.LC[0], b.LC[1]))) return rc;
+    SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * B, r.st));
+    Ptr3C u = {{dst[0], dst[1], dst[2]}}, rr = {{b.R[0], b.R[1], b.R[2]}};
+    if ((rc = resid(K, B, u, rr, b.LC[0], b.LC[1], alpha, pl->eps, w.phibar, w.stats, r.st)))
+      return rc;
+    std::vector<double> res(B);
+    std::vector<int> fl(B);
+    SWE_CUDA(cudaMemcpyAsync(res.data(), w.stats, sizeof(double) * B, cudaMemcpyDeviceToHost, r.st));
+    SWE_CUDA(cudaMemcpyAsync(fl.data(), w.flags, sizeof(int) * B, cudaMemcpyDeviceToHost, r.st));
+    SWE_CUDA(cudaStreamSynchronize(r.st));
+    double worst = 0.0;
+    for (int i = 0; i < B; ++i) {
+      if (!fl[i]) res[i] = 0.0;
+      worst = std::max(worst, res[i]);
+      if (resid_host) resid_host[i] = res[i];
+    }
+    set_error("Coriolis iteration did not converge; residual %.3e", worst);
+    return E_NOCONV;
+  }
+  return OK;
+}
+
+int imex_internal(const Run &r, const swe_stepper_cfg &cfg, int *iters_host, double *resid_host) {
+  swe_plan *pl = r.pl;
+  const Bufs b = bufs(r);
+  const double dt = cfg.dt;
+  const size_t n = (size_t)pl->K * r.B;
+  int rc;
+  std::vector<int> it2(iters_host ? 2 * r.B : 0);
+  // U* = CN_half(U)
+  if ((rc = cn_half(r, cfg, b, b.U, b.US, dt / 4.0, iters_host ? it2.data() : nullptr,
+                    resid_host)))
+    return rc;
+  // Heun on the explicit part (steppers.py:162-166)
+  const double *USc[3] = {b.US[0], b.US[1], b.US[2]};
+  if ((rc = explicit_tendency(r, cfg, USc, b.K1, b.TMP, b.LC[0], b.LC[1]))) return rc;
+  Ptr3C us = {{b.US[0], b.US[1], b.US[2]}}, k1 = {{b.K1[0], b.K1[1], b.K1[2]}};
+  Ptr3C k2 = {{b.K2[0], b.K2[1], b.K2[2]}}, none = {{nullptr, nullptr, nullptr}};
+  Ptr3 mid = {{b.MID[0], b.MID[1], b.MID[2]}};
+  if ((rc = axpy3(n, us, k1, none, dt, mid, r.st))) return rc;
+  const double *MIDc[3] = {b.MID[0], b.MID[1], b.MID[2]};
+  if ((rc = explicit_tendency(r, cfg, MIDc, b.K2, b.TMP, b.LC[0], b.LC[1]))) return rc;
+  if ((rc = axpy3(n, us, k1, k2, 0.5 * dt, mid, r.st))) return rc;
+  // U_new = CN_half(U_exp)
+  if ((rc = cn_half(r, cfg, b, b.MID, b.U, dt / 4.0, iters_host ? it2.data() + 1 : nullptr,
+                    resid_host)))
+    return rc;
+  if (iters_host) memcpy(iters_host, it2.data(), sizeof(int) * 2 * r.B);
+  // viscosity (dynamics.py:191-200); nu = 0 is a copy
+  if (cfg.visc_nu != 0.0) {
+    Ptr3 u = {{b.U[0], b.U[1], b.U[2]}};
+    if ((rc = visc(pl->K, r.B, u, pl->eps, dt * cfg.visc_nu, cfg.visc_order / 2.0, r.st))) return rc;
+  }
+  return OK;
+}
+
+int check_cfg(const swe_stepper_cfg *cfg) {
+  if (!cfg || !(cfg->dt > 0)) {
+    set_error("dt must be positive");
+    return E_SHAPE;
+  }
+  if (cfg->visc_order < 2 || cfg->visc_order % 2 || cfg->visc_nu < 0) {
+    set_error("viscosity order must be an even integer >= 2 and coefficient >= 0");
+    return E_SHAPE;
+  }
+  if (cfg->implicit_max_iter < 0) {
+    set_error("implicit_max_iter must be >= 0");
+    return E_SHAPE;
+  }
+  return OK;
+}
+
+Run make_run(swe_plan *pl, int B, void *stream) {
+  Run r;
+  r.pl = pl;
+  r.B = B;
+  r.ld = 2 * (size_t)B;
+  r.st = (cudaStream_t)stream;
+  return r;
+}
+
+int prepare(swe_plan *pl, int B, const double *phibar, cudaStream_t st) {
+  int rc;
+  if (B < 1) {
+    set_error("batch must be >= 1");
+    return E_SHAPE;
+  }
+  SWE_CUDA(cudaSetDevice(pl->device));
+  if ((rc = work_reserve(pl, B))) return rc;
+  if (phibar && (rc = set_phibar(B, phibar, pl->ws.phibar, pl->ws.phi0, st))) return rc;
+  return OK;
+}
+
+}  // namespace
+}  // namespace swe
+
+using namespace swe;
+
+extern "C" {
+
+int swe_plan_create(int M, double radius_a, double omega, double gravity_g, int device,
+                    swe_plan **out) {
+  if (!out) {
+    set_error("out is NULL");
+    return E_SHAPE;
+  }
+  return plan_create(M, radius_a, omega, gravity_g, device, out);
+}
+
+void swe_plan_destroy(swe_plan *plan) { plan_destroy(plan); }
+
+int swe_plan_info(const swe_plan *pl, int *nlat, int *nlon, int *nmodes) {
+  if (!pl) return E_SHAPE;
+  if (nlat) *nlat = pl->J;
+  if (nlon) *nlon = pl->I;
+  if (nmodes) *nmodes = pl->K;
+  return OK;
+}
+
+int swe_plan_grid(const swe_plan *pl, double *mu, double *weights) {
+  if (!pl) return E_SHAPE;
+  if (mu) memcpy(mu, pl->mu.data(), sizeof(double) * pl->J);
+  if (weights) memcpy(weights, pl->w.data(), sizeof(double) * pl->J);
+  return OK;
+}
+
+long long swe_plan_bytes(const swe_plan *pl) {
+  if (!pl) return 0;
+  const size_t ld = 2 * (size_t)pl->ws.cap;
+  return (long long)(pl->table_bytes + 8 * ld * ((size_t)NSPEC * pl->K +
+                                               (size_t)(NHALF + NF) * (pl->M + 1) * pl->J));
+}
+
+int swe_synthesis(swe_plan *pl, const double *spec, double *grid, int batch, void *stream) {
+  int rc;
+  if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  SpecPtrs d = {{r.spec(0)}};
+  if ((rc = to_internal(spec, d, batch, 1, pl->K, r.st))) return rc;
+  LegArgs a = leg_args(r);
+  a.nout = 1;
+  set_out(a, 0, r.half(0), term(pl->P, r.spec(0)), nullptr, pl->H);
+  if ((rc = synth(r, a))) return rc;
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.in[0] = r.half(0);
+  f.gout[0] = grid;
+  f.scale_mode = 0;
+  return fft(r, FOP_SYNTH_GRID, f);
+}
+
+int swe_analysis(swe_plan *pl, const double *grid, double *spec, int batch, void *stream) {
+  int rc;
+  if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.gin[0] = grid;
+  f.out[0] = r.fsp(0);
+  if ((rc = fft(r, FOP_ANALYSIS, f))) return rc;
+  LegArgs a = leg_args(r);
+  a.nout = 1;
+  set_out(a, 0, r.spec(0), term(pl->P, r.fsp(0)), nullptr, pl->H);
+  if ((rc = anal(r, a))) return rc;
+  SpecPtrsC s = {{r.spec(0)}};
+  return to_boundary(s, spec, batch, 1, pl->K, r.st);
+}
+
+int swe_uv_from_vortdiv(swe_plan *pl, const double *xi, const double *delta, double *u, double *v,
+                        int batch, void *stream) {
+  int rc;
+  if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  SpecPtrs d0 = {{r.spec(0)}}, d1 = {{r.spec(1)}};
+  if ((rc = to_internal(xi, d0, batch, 1, pl->K, r.st))) return rc;
+  if ((rc = to_internal(delta, d1, batch, 1, pl->K, r.st))) return rc;
+  const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
+  LegArgs a = leg_args(r);
+  a.nout = 2;
+  LegTerm hu = term(H, r.spec(0), -1.0, 0, il), hv = term(H, r.spec(1), 1.0, 0, il);
+  set_out(a, 0, r.half(0), term(P, r.spec(1), 1.0, 1, il), &hu, H);
+  set_out(a, 1, r.half(1), term(P, r.spec(0), 1.0, 1, il), &hv, H);
+  if ((rc = synth(r, a))) return rc;
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.in[0] = r.half(0);
+  f.in[1] = r.half(1);
+  f.gout[0] = u;
+  f.gout[1] = v;
+  return fft(r, FOP_SYNTH2_GRID, f);
+}
+
+int swe_vortdiv_from_uv(swe_plan *pl, const double *u, const double *v, double *xi, double *delta,
+                        int batch, void *stream) {
+  int rc;
+  if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.gin[0] = u;
+  f.gin[1] = v;
+  f.out[0] = r.fsp(0);
+  f.out[1] = r.fsp(1);
+  if ((rc = fft(r, FOP_VORTDIV, f))) return rc;
+  const double *P = pl->P, *H = pl->H;
+  LegArgs a = leg_args(r);
+  a.nout = 2;
+  // xi = i m P'B + H'A ; delta = i m P'A - H'B   (spharm.py:336-343)
+  LegTerm hx = term(H, r.fsp(0), 1.0), hd = term(H, r.fsp(1), -1.0);
+  set_out(a, 0, r.spec(0), term(P, r.fsp(1), 1.0, 1), &hx, H);
+  set_out(a, 1, r.spec(1), term(P, r.fsp(0), 1.0, 1), &hd, H);
+  if ((rc = anal(r, a))) return rc;
+  SpecPtrsC s0 = {{r.spec(0)}}, s1 = {{r.spec(1)}};
+  if ((rc = to_boundary(s0, xi, batch, 1, pl->K, r.st))) return rc;
+  return to_boundary(s1, delta, batch, 1, pl->K, r.st);
+}
+
+int swe_tendency(swe_plan *pl, int kind, const double *state, const double *phibar, double *out,
+                 int batch, void *stream) {
+  int rc;
+  if (kind < 0 || kind > 3) {
+    set_error("unknown tendency kind %d", kind);
+    return E_SHAPE;
+  }
+  if ((rc = prepare(pl, batch, phibar, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  const Bufs b = bufs(r);
+  const int K = pl->K;
+  SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
+  if ((rc = to_internal(state, d, batch, 3, K, r.st))) return rc;
+  const size_t n = (size_t)K * batch;
+  for (int f = 0; f < 3; ++f) SWE_CUDA(cudaMemsetAsync(b.K1[f], 0, n * 16, r.st));
+  const double *Uc[3] = {b.U[0], b.U[1], b.U[2]};
+  const bool cor = (kind == 1 || kind == 3);
+  if (cor && (rc = eval_coriolis(r, b.U[1], b.U[2], b.LC[0], b.LC[1]))) return rc;
+  if (kind == 1) {
+    SWE_CUDA(cudaMemcpyAsync(b.K1[1], b.LC[0], n * 16, cudaMemcpyDeviceToDevice, r.st));
+    SWE_CUDA(cudaMemcpyAsync(b.K1[2], b.LC[1], n * 16, cudaMemcpyDeviceToDevice, r.st));
+  } else if (kind == 0 || kind == 3) {
+    if ((rc = lin_tend(K, batch, b.U[0], b.U[2], cor ? b.LC[0] : nullptr, cor ? b.LC[1] : nullptr,
+                       pl->eps, pl->ws.phibar, b.K1, r.st)))
+      return rc;
+  }
+  if (kind == 2 || kind == 3) {
+    if ((rc = eval_nonlinear(r, Uc, b.K2, b.TMP))) return rc;
+    if ((rc = tend_finish(K, batch, b.K2[2], b.TMP, pl->lap_eig, b.K2[1], nullptr, nullptr, r.st)))
+      return rc;
+    Ptr3C k1c = {{b.K1[0], b.K1[1], b.K1[2]}}, k2c = {{b.K2[0], b.K2[1], b.K2[2]}},
+          none = {{nullptr, nullptr, nullptr}};
+    Ptr3 k1 = {{b.K1[0], b.K1[1], b.K1[2]}};
+    if ((rc = axpy3(n, k1c, k2c, none, 1.0, k1, r.st))) return rc;
+  }
+  SpecPtrsC s = {{b.K1[0], b.K1[1], b.K1[2]}};
+  return to_boundary(s, out, batch, 3, K, r.st);
+}
+
+int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
+                  const swe_stepper_cfg *cfg, int nsteps, int *iters_out, double *resid_out,
+                  void *stream) {
+  int rc;
+  if ((rc = check_cfg(cfg))) return rc;
+  if (!phibar) {
+    set_error("phibar is NULL");
+    return E_SHAPE;
+  }
+  if ((rc = prepare(pl, batch, phibar, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  const Bufs b = bufs(r);
+  SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
+  if ((rc = to_internal(state, d, batch, 3, pl->K, r.st))) return rc;
+  for (int s = 0; s < nsteps; ++s) {
+    rc = imex_internal(r, *cfg, iters_out ? iters_out + (size_t)s * 2 * batch : nullptr, resid_out);
+    if (rc) return rc;
+  }
+  SpecPtrsC s = {{b.U[0], b.U[1], b.U[2]}};
+  return to_boundary(s, state, batch, 3, pl->K, r.st);
+}
+
+int swe_truncate_pad(const swe_plan *src, const swe_plan *dst, const double *in, double *out,
+                     int nfields, void *stream) {
+  if (!src || !dst) return E_SHAPE;
+  if (src->a != dst->a || src->omega != dst->omega || src->gravity != dst->gravity) {
+    set_error("truncate_pad requires matching geometries");
+    return E_SHAPE;
+  }
+  return truncate_pad(in, out, nfields, src->M, dst->M, src->offsets, dst->offsets,
+                      (cudaStream_t)stream);
+}
+
+int swe_state_stats(const swe_plan *pl, const double *state, int batch, double *max_abs_out,
+                    int *finite_out, void *stream) {
+  if (!pl || batch < 1) return E_SHAPE;
+  return state_stats(state, batch, pl->K, max_abs_out, finite_out, (cudaStream_t)stream);
+}
+
+long long swe_kernel_launches(void) { return g_launches; }
+const char *swe_last_error(void) { return last_error(); }
+
+}  // extern "C"
