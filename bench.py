@@ -1,0 +1,341 @@
+"""Benchmark: batched fine IMEX propagator of cfg2 (M=256, dt=60 s, nu=1e5).
+
+One bench step = one F-relaxation sweep step of cfg2's fine level: every one of
+the 64 time slices owned by a GPU advances one IMEX step (steppers.py:155-168)
+in a single batched call.  value = fine slice-steps/s over all ranks (weak
+scaling: 64 slices per GPU, no data-path collective).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port under oracle/, the reference being pure Python/numpy that cannot
+travel to the GPU box) on the host cores: one process per core, each advancing
+its own slice, on the same M/dt/nu.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine SWE steps/s (fp64, M=256) at 1/2/4/8 B200; % FP64-TC / HBM roofline"
+UNIT = "fine slice-steps/s"
+M, DT, NU = 256, 60.0, 1.0e5
+SLICES_PER_GPU = 64
+
+
+def workload(slices):
+    return {"workload": f"cfg2 fine level: gaussian_bumps M={M} dt={DT:g}s nu={NU:g} IMEX, "
+                        f"{slices} time slices per GPU advanced one fine step per bench step",
+            "M": M, "dt": DT, "nu": NU, "slices_per_gpu": slices, "parallelism": "slices"}
+
+
+# --------------------------------------------------------------------------- CPU legs
+_SPH = None
+_STATES = None
+
+
+def _cpu_worker_step(i):
+    from oracle.swe import StepCfg, imex_step
+    s = _STATES.slice(i)
+    t0 = time.perf_counter()
+    imex_step(s, StepCfg(dt=DT, visc_nu=NU))
+    return time.perf_counter() - t0
+
+
+def _cpu_setup(nproc):
+    global _SPH, _STATES
+    from oracle.sht import OracleSphere
+    from oracle.swe import OracleState, gaussian_bumps
+    if _SPH is None:
+        _SPH = OracleSphere(M)
+    base = gaussian_bumps(_SPH, batch=nproc)
+    rng = np.random.default_rng(0)
+    for b in range(nproc):
+        base.xi[b] += 1e-9 * rng.standard_normal(_SPH.n_modes) * (_SPH.n_of + 1.0) ** -2
+    base.xi[:, : M + 1] = base.xi[:, : M + 1].real
+    _STATES = base
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_steps(nsteps, nproc):
+    """Oracle IMEX steps, one process per core, each on its own slice.
+    Returns (elapsed seconds of the timed steps, slice-steps done)."""
+    import multiprocessing as mp
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    _cpu_setup(nproc)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(nproc) as pool:
+        pool.map(_cpu_worker_step, range(nproc))          # warm the workers
+        t0 = time.perf_counter()
+        for _ in range(nsteps):
+            pool.map(_cpu_worker_step, range(nproc))
+        el = time.perf_counter() - t0
+    return el, nsteps * nproc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    nproc = min(cpu_cores(), 16)
+    el_w, _ = cpu_steps(args.warmup, nproc) if args.warmup else (0.0, 0)
+    el, done = cpu_steps(args.steps, nproc)
+    v = done / el
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (gaussian_bumps + per-slice perturbation)",
+            "config": workload(nproc), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nproc, "kind": "port",
+                             "sample": f"{nproc} slices (one per process) x 1 IMEX step per bench "
+                                       f"step, numpy oracle port of steppers.imex_step at M={M}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU leg
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={device}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for ln in fh:
+                parts = [x.strip() for x in ln.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def fp64_peak_tflops(torch, dev):
+    """cuBLAS DGEMM 8192^3, best of 5 (burst) -- the FP64 denominator
+    (MEASURED_PEAKS.json has no fp64 entry)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def make_states(grid, n, seed):
+    """Gaussian bumps + a per-slice vorticity/divergence perturbation."""
+    import torch
+    from paper_2306_09497_b200 import scenarios
+    s = scenarios.gaussian_bumps(grid, batch=n)
+    rng = np.random.default_rng(seed)
+    pert = rng.standard_normal((n, grid.n_modes)) + 1j * rng.standard_normal((n, grid.n_modes))
+    pert[:, : M + 1] = pert[:, : M + 1].real
+    pert *= (grid.n_of + 1.0) ** -2
+    pt = torch.from_numpy(pert).to(s.data.device)
+    s.data[:, 1] += 1e-9 * pt
+    s.data[:, 2] += 1e-10 * pt
+    return s
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2306_09497_b200 import _lib, dynamics, spharm, steppers
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    B = args.slices
+    grid = spharm.get_grid(M)
+    cfg = steppers.StepperConfig(dt=DT, viscosity=dynamics.ViscositySpec(2, NU))
+    state = make_states(grid, B, seed=rank)
+    peak64 = fp64_peak_tflops(torch, dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > L2
+
+    for _ in range(args.warmup):
+        steppers.imex_steps_inplace(state, cfg, 1)
+    barrier()
+
+    iters = np.zeros((1, B, 2), dtype=np.int32)
+    its = []
+    clocks = Clocks(local)
+    n_launch0 = _lib.kernel_launches()
+    _lib.profile(True)
+    total_ms = 0.0
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record()
+        steppers.imex_steps_inplace(state, cfg, 1, iters)
+        e_ev.record()
+        e_ev.synchronize()
+        total_ms += s_ev.elapsed_time(e_ev)
+        its.append(iters.copy())
+    barrier()
+    _lib.profile(False)
+    prof = _lib.profile_read()
+    launches = _lib.kernel_launches() - n_launch0
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t[0])
+    value = world * B * args.steps / (total_ms * 1e-3)
+
+    # e2e through the public API with pinned host buffers (H2D + step + D2H per step)
+    host_in = state.data.cpu().pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    pb = state.phibar_t.clone()
+    barrier()
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record()
+        d = host_in.to(dev, non_blocking=True)
+        st = dynamics.PrognosticState(grid, d, pb)
+        steppers.imex_steps_inplace(st, cfg, 1)
+        host_out.copy_(st.data, non_blocking=True)
+        e_ev.record()
+        e_ev.synchronize()
+        e2e_ms += s_ev.elapsed_time(e_ev)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * args.steps / (float(t[0]) * 1e-3)
+    nbytes = host_in.numel() * host_in.element_size()
+
+    # roofline of the dominant kernel class (device time share inside the step)
+    leg_ms = prof["legendre_synthesis"][0] + prof["legendre_analysis"][0]
+    leg_flops = prof["legendre_synthesis"][1] + prof["legendre_analysis"][1]
+    fft_ms, fft_bytes = prof["fft_grid"][0], prof["fft_grid"][1]
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    share = {k: round(v[0] / max(total_ms, 1e-9), 4) for k, v in prof.items()}
+    if leg_ms >= fft_ms:
+        ach = leg_flops / (leg_ms * 1e-3) / 1e12
+        roof = {"kernel": "leg_synth_kernel + leg_anal_kernel (FP64 DMMA, parity-folded)",
+                "bound": "tensor", "achieved": ach, "peak": peak64, "unit": "TFLOP/s",
+                "frac": ach / peak64, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured live in bench.py (burst)",
+                "work_per_unit": "2*J*K flops per slice per Legendre term (folded)"}
+    else:
+        ach = fft_bytes / (fft_ms * 1e-3) / 1e9
+        roof = {"kernel": "fft_kernel (FFT + grid products)", "bound": "hbm", "achieved": ach,
+                "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    it_arr = np.concatenate(its)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (gaussian_bumps + per-slice perturbation)",
+            "config": dict(workload(B), l2="256 MB buffer written between timed steps",
+                           avg_fixed_point_iters=float(it_arr.mean())),
+            "roofline": roof,
+            "kernel_time_share": share,
+            "legendre_tflops": leg_flops / max(leg_ms, 1e-9) / 1e9,
+            "fft_stage_gbs": fft_bytes / max(fft_ms, 1e-9) / 1e6,
+            "fp64_peak_tflops_measured": peak64,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": nbytes},
+            "gpu_launches": launches, "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        nproc = min(cpu_cores(), 16)
+        el, done = cpu_steps(1, nproc)
+        line["cpu_baseline"] = {"value": done / el, "unit": UNIT, "cores": nproc, "kind": "port",
+                                "sample": f"{nproc} slices x 1 IMEX step (one process per core) "
+                                          f"of the numpy oracle port at M={M}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--slices", type=int, default=SLICES_PER_GPU)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

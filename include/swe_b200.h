@@ -98,6 +98,17 @@ int swe_state_stats(const swe_plan *plan, const double *state, int batch, double
 
 /* Number of this library's kernels launched since load (evidence counter). */
 long long swe_kernel_launches(void);
+/* Live per-launch profiling with CUDA events on the launching stream.
+ * swe_profile(1) clears and starts recording, swe_profile(0) stops.
+ * swe_profile_read fills, per kernel class [4] = {Legendre synthesis GEMM,
+ * Legendre analysis GEMM, FFT + grid products, spectral elementwise}, the summed
+ * device milliseconds, algorithmic work (flops for the GEMMs, bytes for the
+ * FFT stage) and launch counts (all outputs HOST, nullable). */
+int swe_profile(int enable);
+/* Tuning switches.  "fft_path": 0 auto, 1 warp-per-row FFT kernel, 2 lane=row
+ * FFT kernel (falls back to 1 where its radix/size limits do not hold). */
+int swe_set_option(const char *key, int value);
+int swe_profile_read(double *ms_out, double *work_out, long long *count_out);
 const char *swe_last_error(void);
 
 #ifdef __cplusplus

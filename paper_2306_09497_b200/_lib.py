@@ -19,7 +19,8 @@ EXPORTS = (
     "swe_plan_create", "swe_plan_destroy", "swe_plan_info", "swe_plan_grid", "swe_plan_bytes",
     "swe_synthesis", "swe_analysis", "swe_uv_from_vortdiv", "swe_vortdiv_from_uv",
     "swe_tendency", "swe_imex_step", "swe_truncate_pad", "swe_state_stats",
-    "swe_kernel_launches", "swe_last_error",
+    "swe_kernel_launches", "swe_last_error", "swe_profile", "swe_profile_read",
+    "swe_set_option",
 )
 
 
@@ -66,6 +67,9 @@ def load(path: str = LIB_PATH):
         "swe_state_stats": (I, [P, P, I, P, P, P]),
         "swe_kernel_launches": (ctypes.c_longlong, []),
         "swe_last_error": (ctypes.c_char_p, []),
+        "swe_profile": (I, [I]),
+        "swe_profile_read": (I, [P, P, P]),
+        "swe_set_option": (I, [ctypes.c_char_p, I]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)
@@ -94,3 +98,27 @@ def check(rc: int, what: str = ""):
 
 def kernel_launches() -> int:
     return int(load().swe_kernel_launches())
+
+
+def set_option(key: str, value: int):
+    """Tuning switch (e.g. fft_path: 0 auto, 1 warp-per-row, 2 lane=row)."""
+    check(load().swe_set_option(key.encode(), int(value)), "swe_set_option")
+
+
+KERNEL_CLASSES =("legendre_synthesis", "legendre_analysis", "fft_grid", "spectral")
+
+
+def profile(enable: bool):
+    check(load().swe_profile(1 if enable else 0), "swe_profile")
+
+
+def profile_read():
+    """{class: (device ms, algorithmic work, launches)} since profile(True)."""
+    import numpy as np
+    ms = np.zeros(4)
+    work = np.zeros(4)
+    cnt = np.zeros(4, dtype=np.int64)
+    check(load().swe_profile_read(ms.ctypes.data_as(ctypes.c_void_p),
+                                  work.ctypes.data_as(ctypes.c_void_p),
+                                  cnt.ctypes.data_as(ctypes.c_void_p)), "swe_profile_read")
+    return {k: (float(ms[i]), float(work[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}

@@ -10,74 +10,18 @@
 // complex registers.  Radices 2,3,4,5,7,11,13 are unrolled (odd R uses the
 // conjugate-pair symmetric form); other primes run warp-cooperatively.
 #include "fft.cuh"
+#include "fft_core.cuh"
 
 namespace swe {
 
 namespace {
 
-SWE_DEV double2 cm(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-SWE_DEV double2 twd(const double2 *tw, int e, double dir) {
-  double2 w = __ldg(tw + e);
-  w.y *= dir;
-  return w;
-}
-
-// y_t = sum_q v_q exp(dir 2 pi i q t / R), optionally times exp(dir 2 pi i t kt / N2),
-// stored to dst[t*stride].  cr/sr hold cos/sin(2 pi e / R) for e = 0..(R-1)/2.
-template <int R>
-SWE_DEV void dft_store(double2 (&v)[R], double dir, const double *cr, const double *sr,
-                       double2 *dst, int stride, const double2 *tw, int kt) {
-  double2 y[R];
-  if constexpr (R == 2) {
-    y[0] = make_double2(v[0].x + v[1].x, v[0].y + v[1].y);
-    y[1] = make_double2(v[0].x - v[1].x, v[0].y - v[1].y);
-  } else if constexpr (R == 4) {
-    const double2 s02 = make_double2(v[0].x + v[2].x, v[0].y + v[2].y);
-    const double2 d02 = make_double2(v[0].x - v[2].x, v[0].y - v[2].y);
-    const double2 s13 = make_double2(v[1].x + v[3].x, v[1].y + v[3].y);
-    const double2 d13 = make_double2(v[1].x - v[3].x, v[1].y - v[3].y);
-    const double2 rot = make_double2(-dir * d13.y, dir * d13.x);  // i*dir*d13
-    y[0] = make_double2(s02.x + s13.x, s02.y + s13.y);
-    y[2] = make_double2(s02.x - s13.x, s02.y - s13.y);
-    y[1] = make_double2(d02.x + rot.x, d02.y + rot.y);
-    y[3] = make_double2(d02.x - rot.x, d02.y - rot.y);
-  } else {
-    constexpr int H = (R - 1) / 2;
-    y[0] = v[0];
-#pragma unroll
-    for (int q = 1; q <= H; ++q) {
-      const double2 p = v[q], m = v[R - q];
-      v[q] = make_double2(p.x + m.x, p.y + m.y);
-      v[R - q] = make_double2(p.x - m.x, p.y - m.y);
-      y[0].x += v[q].x;
-      y[0].y += v[q].y;
-    }
-#pragma unroll
-    for (int t = 1; t <= H; ++t) {
-      double re = v[0].x, im = v[0].y, sx = 0.0, sy = 0.0;
-#pragma unroll
-      for (int q = 1; q <= H; ++q) {
-        const int e = (q * t) % R;
-        const double c = e <= H ? cr[e] : cr[R - e];
-        const double s = e <= H ? sr[e] : -sr[R - e];
-        re += v[q].x * c;
-        im += v[q].y * c;
-        sx += v[R - q].x * s;
-        sy += v[R - q].y * s;
-      }
-      y[t] = make_double2(re - dir * sy, im + dir * sx);
-      y[R - t] = make_double2(re + dir * sy, im - dir * sx);
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < R; ++t) dst[t * stride] = (kt && t) ? cm(y[t], twd(tw, t * kt, dir)) : y[t];
-}
+using namespace fftcore;
 
 // in-place stage of radix R over blocks of span L = Lp*R.
-// DIT: inputs twiddled by W_L^{qk}; DIF: outputs twiddled by W_L^{tk}.
-template <int R, bool DIT>
+// MODE 0 (DIT): inputs twiddled by W_L^{qk}; 1 (DIF): outputs twiddled by W_L^{tk};
+// 2 (prime-factor / Good-Thomas): no twiddles.
+template <int R, int MODE>
 SWE_DEV void stage_small(double2 *x, int N2, int Lp, double dir, const double2 *tw, int lane) {
   constexpr int H = (R - 1) / 2;
   double cr[H + 1], sr[H + 1];
@@ -96,15 +40,15 @@ SWE_DEV void stage_small(double2 *x, int N2, int Lp, double dir, const double2 *
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       v[q] = x[base + q * Lp];
-      if (DIT && q && k) v[q] = cm(v[q], twd(tw, q * k * tws, dir));
+      if (MODE == 0 && q && k) v[q] = cm(v[q], twd(tw, q * k * tws, dir));
     }
-    dft_store<R>(v, dir, cr, sr, x + base, Lp, tw, DIT ? 0 : k * tws);
+    dft_store<R>(v, dir, cr, sr, x + base, Lp, tw, MODE == 1 ? k * tws : 0);
   }
   __syncwarp();
 }
 
 // any radix: one butterfly at a time, lanes split the R outputs (scr holds R inputs)
-template <bool DIT>
+template <int MODE>
 SWE_DEV void stage_generic(double2 *x, double2 *scr, int N2, int Lp, int R, double dir,
                            const double2 *tw, int lane) {
   const int L = Lp * R, nbf = N2 / R, tws = N2 / L, rstep = N2 / R;
@@ -112,7 +56,7 @@ SWE_DEV void stage_generic(double2 *x, double2 *scr, int N2, int Lp, int R, doub
     const int g = bf / Lp, k = bf - g * Lp, base = g * L + k;
     for (int q = lane; q < R; q += 32) {
       double2 v = x[base + q * Lp];
-      if (DIT && q && k) v = cm(v, twd(tw, q * k * tws, dir));
+      if (MODE == 0 && q && k) v = cm(v, twd(tw, q * k * tws, dir));
       scr[q] = v;
     }
     __syncwarp();
@@ -126,43 +70,54 @@ SWE_DEV void stage_generic(double2 *x, double2 *scr, int N2, int Lp, int R, doub
         e += t;
         if (e >= R) e -= R;
       }
-      if (!DIT && t && k) acc = cm(acc, twd(tw, t * k * tws, dir));
+      if (MODE == 1 && t && k) acc = cm(acc, twd(tw, t * k * tws, dir));
       x[base + t * Lp] = acc;
     }
     __syncwarp();
   }
 }
 
-template <bool DIT>
+template <int MODE>
 SWE_DEV void run_stage(double2 *x, double2 *scr, int N2, int Lp, int R, double dir,
                        const double2 *tw, int lane) {
   switch (R) {
-    case 2: stage_small<2, DIT>(x, N2, Lp, dir, tw, lane); break;
-    case 3: stage_small<3, DIT>(x, N2, Lp, dir, tw, lane); break;
-    case 4: stage_small<4, DIT>(x, N2, Lp, dir, tw, lane); break;
-    case 5: stage_small<5, DIT>(x, N2, Lp, dir, tw, lane); break;
-    case 7: stage_small<7, DIT>(x, N2, Lp, dir, tw, lane); break;
-    case 11: stage_small<11, DIT>(x, N2, Lp, dir, tw, lane); break;
-    case 13: stage_small<13, DIT>(x, N2, Lp, dir, tw, lane); break;
-    default: stage_generic<DIT>(x, scr, N2, Lp, R, dir, tw, lane); break;
+    case 2: stage_small<2, MODE>(x, N2, Lp, dir, tw, lane); break;
+    case 3: stage_small<3, MODE>(x, N2, Lp, dir, tw, lane); break;
+    case 4: stage_small<4, MODE>(x, N2, Lp, dir, tw, lane); break;
+    case 5: stage_small<5, MODE>(x, N2, Lp, dir, tw, lane); break;
+    case 7: stage_small<7, MODE>(x, N2, Lp, dir, tw, lane); break;
+    case 11: stage_small<11, MODE>(x, N2, Lp, dir, tw, lane); break;
+    case 13: stage_small<13, MODE>(x, N2, Lp, dir, tw, lane); break;
+    default: stage_generic<MODE>(x, scr, N2, Lp, R, dir, tw, lane); break;
   }
 }
 
-// inverse: digit-reversed input -> natural output (stages r_0 .. r_{S-1})
+// inverse: spectral order pos_z in -> grid order pos_g out.  Cooley-Tukey:
+// digit-reversed -> natural (DIT, stages r_0 .. r_{S-1}); prime-factor:
+// Ruritanian -> CRT (twiddle-free stages along each axis).
 SWE_DEV void warp_ifft(double2 *x, double2 *scr, const FftArgs &a, int lane) {
   int Lp = 1;
   for (int s = 0; s < a.nst; ++s) {
-    run_stage<true>(x, scr, a.N2, Lp, a.radix[s], 1.0, a.tw, lane);
+    if (a.pfa) run_stage<2>(x, scr, a.N2, Lp, a.radix[s], 1.0, a.tw, lane);
+    else run_stage<0>(x, scr, a.N2, Lp, a.radix[s], 1.0, a.tw, lane);
     Lp *= a.radix[s];
   }
 }
 
-// forward: natural input -> digit-reversed output (stages r_{S-1} .. r_0)
+// forward: grid order pos_g in -> spectral order pos_z out (DIF r_{S-1} .. r_0, or PFA)
 SWE_DEV void warp_fft(double2 *x, double2 *scr, const FftArgs &a, int lane) {
+  if (a.pfa) {
+    int Lp = 1;
+    for (int s = 0; s < a.nst; ++s) {
+      run_stage<2>(x, scr, a.N2, Lp, a.radix[s], -1.0, a.tw, lane);
+      Lp *= a.radix[s];
+    }
+    return;
+  }
   int L = a.N2;
   for (int s = a.nst - 1; s >= 0; --s) {
     const int R = a.radix[s];
-    run_stage<false>(x, scr, a.N2, L / R, R, -1.0, a.tw, lane);
+    run_stage<1>(x, scr, a.N2, L / R, R, -1.0, a.tw, lane);
     L /= R;
   }
 }
@@ -188,7 +143,7 @@ SWE_DEV void load_half_z(const FftArgs &a, const Ctx &c, const double *src, int 
     double2 *x = row_of(a, c, f, s);
     if (k == 0) {
       const double x0 = __ldg(base + s).x;
-      x[__ldg(a.pos)] = make_double2(x0, x0);
+      x[__ldg(a.pos_z)] = make_double2(x0, x0);
       continue;
     }
     const int k2 = N2 - k;
@@ -197,12 +152,12 @@ SWE_DEV void load_half_z(const FftArgs &a, const Ctx &c, const double *src, int 
     const double2 A = make_double2(Xk.x + Xc.x, Xk.y - Xc.y);
     const double2 D = make_double2(Xk.x - Xc.x, Xk.y + Xc.y);
     const double2 Bk = cm(D, __ldg(a.twh + k));
-    x[__ldg(a.pos + k)] = make_double2(A.x - Bk.y, A.y + Bk.x);
+    x[__ldg(a.pos_z + k)] = make_double2(A.x - Bk.y, A.y + Bk.x);
     if (k2 != k) {
       const double2 A2 = make_double2(Xc.x + Xk.x, Xc.y - Xk.y);
       const double2 D2 = make_double2(Xc.x - Xk.x, Xc.y + Xk.y);
       const double2 B2 = cm(D2, __ldg(a.twh + k2));
-      x[__ldg(a.pos + k2)] = make_double2(A2.x - B2.y, A2.y + B2.x);
+      x[__ldg(a.pos_z + k2)] = make_double2(A2.x - B2.y, A2.y + B2.x);
     }
   }
 }
@@ -211,7 +166,8 @@ SWE_DEV void load_grid(const FftArgs &a, const Ctx &c, const double *src, int f)
   for (int s = 0; s < c.nsl; ++s) {
     const double *g = src + ((size_t)(c.b0 + s) * a.J + c.j) * a.I;
     double *r = reinterpret_cast<double *>(row_of(a, c, f, s));
-    for (int n = c.tid; n < a.I; n += c.nthr) r[n] = __ldg(g + n);
+    // grid sample n is component n&1 of transform slot pos_g[n/2]
+    for (int n = c.tid; n < a.I; n += c.nthr) r[2 * __ldg(a.pos_g + (n >> 1)) + (n & 1)] = __ldg(g + n);
   }
 }
 
@@ -219,7 +175,7 @@ SWE_DEV void store_grid(const FftArgs &a, const Ctx &c, double *dst, int f, doub
   for (int s = 0; s < c.nsl; ++s) {
     double *g = dst + ((size_t)(c.b0 + s) * a.J + c.j) * a.I;
     const double *r = reinterpret_cast<const double *>(row_of(a, c, f, s));
-    for (int n = c.tid; n < a.I; n += c.nthr) g[n] = r[n] * scale;
+    for (int n = c.tid; n < a.I; n += c.nthr) g[n] = r[2 * __ldg(a.pos_g + (n >> 1)) + (n & 1)] * scale;
   }
 }
 
@@ -247,8 +203,8 @@ SWE_DEV void r2c_outputs(const FftArgs &a, const Ctx &c, const int (&fld)[NOUT],
     double2 *dst = reinterpret_cast<double2 *>(a.out[o] + (size_t)c.j * a.ld) + c.b0 + s;
     const size_t mstride = (size_t)a.J * a.ld / 2;
     for (int k = c.lane; k <= M; k += 32) {
-      const double2 zk = x[__ldg(a.pos + k)];
-      const double2 z2 = x[__ldg(a.pos + (k == 0 ? 0 : N2 - k))];
+      const double2 zk = x[__ldg(a.pos_z + k)];
+      const double2 z2 = x[__ldg(a.pos_z + (k == 0 ? 0 : N2 - k))];
       const double2 zc = make_double2(z2.x, -z2.y);
       const double2 S = make_double2(zk.x + zc.x, zk.y + zc.y);     // 2 Ge
       const double2 D = make_double2(zk.y - zc.y, -(zk.x - zc.x));  // 2 Go

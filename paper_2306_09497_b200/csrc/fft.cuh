@@ -31,7 +31,9 @@ struct FftArgs {
   int ns[FFT_MAXST];
   const double2 *tw;   // [N2]  e^{2 pi i e / N2}
   const double2 *twh;  // [N2]  e^{2 pi i k / I}
-  const int *pos;      // [N2]  slot of natural index k in digit-reversed order
+  const int *pos_z;    // [N2]  slot of spectral index k (c2r input / r2c output order)
+  const int *pos_g;    // [N2]  slot of grid pair r (g[2r], g[2r+1]) (c2r output / r2c input)
+  int pfa;             // 1: prime-factor (coprime radices, no twiddles), 0: Cooley-Tukey
   int rgen;            // largest non-unrolled radix (per-warp scratch, complex), 0 if none
   int nslices, ld, spb, nwarps;
   int scale_mode;      // FOP_SYNTH_GRID: 0 none, 1 times 1/(a cos)
@@ -48,5 +50,12 @@ __host__ __device__ constexpr int fft_rows_per_slice(int op) {
   return op == FOP_NONLINEAR ? 6 : ((op == FOP_SYNTH2_GRID || op == FOP_VORTDIV || op == FOP_CORIOLIS) ? 2 : 1);
 }
 bool fft_small_radix(int R);
+
+// "lane = row" variant (fft_lanes.cu): slices per CTA for each op (32 rows / live fields)
+__host__ __device__ constexpr int fft_lane_slices(int op) {
+  return op == FOP_NONLINEAR ? 4 : ((op == FOP_SYNTH_GRID || op == FOP_ANALYSIS) ? 32 : 16);
+}
+int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st);
+bool fft_lanes_ok(const FftArgs &a);
 
 }  // namespace swe

@@ -232,20 +232,53 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
       twh[e] = make_double2((double)cosl(th2), (double)sinl(th2));
     }
     if ((rc = upload(&pl->tw, tw)) || (rc = upload(&pl->twh, twh))) return rc;
-    // digit-reversal: natural index perm(i) sits in slot i (fft.cu), pos = perm^-1
-    std::vector<int> pos(N2);
-    for (int i = 0; i < N2; ++i) {
-      int rem = i, n = N2, mult = 1, res = 0;
-      for (int s = pl->nst - 1; s >= 0; --s) {
-        n /= pl->radix[s];
-        const int q = rem / n;
-        rem -= q * n;
-        res += q * mult;
-        mult *= pl->radix[s];
+    // slot maps (fft.cu): pos_z = spectral index -> slot, pos_g = grid pair -> slot
+    std::vector<int> pos_z(N2), pos_g(N2);
+    pl->pfa = 1;
+    for (int s = 0; s < pl->nst; ++s)
+      for (int t = s + 1; t < pl->nst; ++t) {
+        int x = pl->radix[s], y = pl->radix[t];
+        while (y) { const int r = x % y; x = y; y = r; }
+        if (x != 1) pl->pfa = 0;
       }
-      pos[res] = i;
+    if (pl->pfa) {
+      // Good-Thomas: slot p(i) = sum_s i_s * prod_{t<s} r_t;
+      // spectral (Ruritanian) n = sum_s (N/r_s) i_s mod N; grid (CRT) i_s = n mod r_s
+      std::vector<int> idx(pl->nst, 0);
+      for (int p = 0; p < N2; ++p) {
+        int rem = p;
+        long long n = 0;
+        for (int s = 0; s < pl->nst; ++s) {
+          idx[s] = rem % pl->radix[s];
+          rem /= pl->radix[s];
+          n += (long long)(N2 / pl->radix[s]) * idx[s];
+        }
+        pos_z[(int)(n % N2)] = p;
+      }
+      for (int n = 0; n < N2; ++n) {
+        int p = 0, mult = 1;
+        for (int s = 0; s < pl->nst; ++s) {
+          p += (n % pl->radix[s]) * mult;
+          mult *= pl->radix[s];
+        }
+        pos_g[n] = p;
+      }
+    } else {
+      // Cooley-Tukey: digit-reversed spectral slots, natural grid slots
+      for (int i = 0; i < N2; ++i) {
+        int rem = i, n = N2, mult = 1, res = 0;
+        for (int s = pl->nst - 1; s >= 0; --s) {
+          n /= pl->radix[s];
+          const int q = rem / n;
+          rem -= q * n;
+          res += q * mult;
+          mult *= pl->radix[s];
+        }
+        pos_z[res] = i;
+        pos_g[i] = i;
+      }
     }
-    if ((rc = upload(&pl->fft_pos, pos))) return rc;
+    if ((rc = upload(&pl->fft_pos_z, pos_z)) || (rc = upload(&pl->fft_pos_g, pos_g))) return rc;
     pl->rgen = 0;
     for (int s = 0; s < pl->nst; ++s)
       if (!fft_small_radix(pl->radix[s])) pl->rgen = std::max(pl->rgen, pl->radix[s]);
@@ -302,7 +335,8 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->wsin2);
   cudaFree(pl->tw);
   cudaFree(pl->twh);
-  cudaFree(pl->fft_pos);
+  cudaFree(pl->fft_pos_z);
+  cudaFree(pl->fft_pos_g);
   cudaFree(pl->synth_items);
   cudaFree(pl->anal_items);
   delete pl;

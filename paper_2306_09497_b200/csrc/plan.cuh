@@ -46,7 +46,8 @@ struct swe_plan {
   double *lap_eig = nullptr, *inv_lap = nullptr, *eps = nullptr;
   double *coslat = nullptr, *inv_acos = nullptr, *fcor = nullptr, *wq = nullptr, *wsin2 = nullptr;
   double2 *tw = nullptr, *twh = nullptr;
-  int *fft_pos = nullptr;
+  int *fft_pos_z = nullptr, *fft_pos_g = nullptr;
+  int pfa = 0;
   int rgen = 0;
   int2 *synth_items = nullptr, *anal_items = nullptr;
   int n_synth_items = 0, n_anal_items = 0;

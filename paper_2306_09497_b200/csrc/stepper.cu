@@ -25,6 +25,49 @@ int work_reserve(swe_plan *pl, int B);
 
 namespace {
 
+// ---- live profiling: CUDA events around each launch, per kernel class -------
+// class 0: Legendre synthesis GEMM, 1: Legendre analysis GEMM, 2: FFT/grid,
+// 3: spectral elementwise.  `work` is algorithmic flops (0,1) or bytes (2,3).
+constexpr int NCLS = 4;
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double work;
+};
+bool g_prof = false;
+int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
+std::vector<ProfRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+size_t g_pool_used = 0;
+
+cudaEvent_t pool_event() {
+  if (g_pool_used == g_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_pool.push_back(e);
+  }
+  return g_pool[g_pool_used++];
+}
+
+struct ProfScope {
+  bool on;
+  ProfRec rec;
+  cudaStream_t st;
+  ProfScope(int cls, double work, cudaStream_t s) : on(g_prof), st(s) {
+    if (!on) return;
+    rec.cls = cls;
+    rec.work = work;
+    rec.a = pool_event();
+    rec.b = pool_event();
+    cudaEventRecord(rec.a, st);
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(rec.b, st);
+    g_recs.push_back(rec);
+  }
+};
+
 struct Run {
   swe_plan *pl;
   int B;
@@ -72,15 +115,25 @@ void set_out(LegArgs &a, int i, double *dst, LegTerm t0, const LegTerm *t1, cons
   }
 }
 
+// algorithmic flops of a Legendre launch: every term is a (J/2) x K x 2B real
+// contraction after N/S folding -> 2 * (J/2) * K * 2B = 2 J K B flops
+double leg_flops(const Run &r, const LegArgs &a) {
+  int terms = 0;
+  for (int i = 0; i < a.nout; ++i) terms += a.out[i].nterms;
+  return 2.0 * r.pl->J * (double)r.pl->K * r.B * terms;
+}
+
 int synth(const Run &r, LegArgs &a) {
   a.items = r.pl->synth_items;
   a.nitems = r.pl->n_synth_items;
+  ProfScope ps(0, leg_flops(r, a), r.st);
   return leg_synth_launch(a, (int)((r.ld + SY_BN - 1) / SY_BN), r.st);
 }
 
 int anal(const Run &r, LegArgs &a) {
   a.items = r.pl->anal_items;
   a.nitems = r.pl->n_anal_items;
+  ProfScope ps(1, leg_flops(r, a), r.st);
   return leg_anal_launch(a, (int)((r.ld + AN_BN - 1) / AN_BN), r.st);
 }
 
@@ -105,7 +158,9 @@ int fft(const Run &r, int op, FftArgs &a) {
   }
   a.tw = pl->tw;
   a.twh = pl->twh;
-  a.pos = pl->fft_pos;
+  a.pos_z = pl->fft_pos_z;
+  a.pos_g = pl->fft_pos_g;
+  a.pfa = pl->pfa;
   a.rgen = pl->rgen;
   a.nslices = r.B;
   a.ld = (int)r.ld;
@@ -116,6 +171,16 @@ int fft(const Run &r, int op, FftArgs &a) {
   a.wsin2 = pl->wsin2;
   a.inv_I = 1.0 / pl->I;
   a.inv_a = 1.0 / pl->a;
+  static const int io[6][4] = {{1, 0, 0, 1}, {2, 0, 0, 2}, {0, 1, 1, 0},
+                               {0, 2, 2, 0}, {2, 2, 0, 0}, {7, 4, 0, 0}};
+  const double spec_row = 16.0 * (pl->M + 1) * pl->J * r.B, grid_row = 8.0 * pl->I * pl->J * r.B;
+  const double bytes = (io[op][0] + io[op][1]) * spec_row + (io[op][2] + io[op][3]) * grid_row;
+  // path: lane = row kernel for small-radix lengths with enough slices, else warp-per-row
+  const bool lanes = g_fft_path == 2 || (g_fft_path == 0 && r.B >= 8);
+  if (lanes && fft_lanes_ok(a)) {
+    ProfScope ps(2, bytes, r.st);
+    return fft_lanes_launch(op, a, r.st);
+  }
   const int rows = fft_rows_per_slice(op);
   const size_t rowb = (size_t)pl->N2 * sizeof(double2);
   const size_t scrb = (size_t)pl->rgen * sizeof(double2);
@@ -133,6 +198,7 @@ int fft(const Run &r, int op, FftArgs &a) {
   }
   a.spb = spb;
   a.nwarps = nw;
+  ProfScope ps(2, bytes, r.st);
   return fft_launch(op, a, (int)smem, r.st);
 }
 
@@ -275,9 +341,12 @@ int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *con
   int active = B;
   for (int it = 0; it < cfg.implicit_max_iter && active > 0; ++it) {
     if ((rc = eval_coriolis(r, dst[1], dst[2], b.LC[0], b.LC[1]))) return rc;
-    if ((rc = helm(K, B, Rc, b.LC[0], b.LC[1], alpha, pl->eps, w.phibar, dst, w.flags, w.stats,
-                   r.st)))
-      return rc;
+    {
+      ProfScope ps(3, 11.0 * 16.0 * K * B, r.st);  // rhs 3 + lc 2 + old 3 in, new 3 out
+      if ((rc = helm(K, B, Rc, b.LC[0], b.LC[1], alpha, pl->eps, w.phibar, dst, w.flags, w.stats,
+                     r.st)))
+        return rc;
+    }
     SWE_CUDA(cudaMemsetAsync(w.counter, 0, sizeof(int), r.st));
     if ((rc = decide(B, w.stats, w.flags, w.iters, w.counter, cfg.implicit_tol, r.st))) return rc;
     SWE_CUDA(cudaMemcpyAsync(w.h_counter, w.counter, sizeof(int), cudaMemcpyDeviceToHost, r.st));
@@ -588,6 +657,41 @@ int swe_state_stats(const swe_plan *pl, const double *state, int batch, double *
 }
 
 long long swe_kernel_launches(void) { return g_launches; }
+
+int swe_set_option(const char *key, int value) {
+  if (key && strcmp(key, "fft_path") == 0 && value >= 0 && value <= 2) {
+    g_fft_path = value;
+    return OK;
+  }
+  set_error("unknown option %s=%d", key ? key : "(null)", value);
+  return E_SHAPE;
+}
+
+int swe_profile(int enable) {
+  g_prof = enable != 0;
+  if (g_prof) {
+    g_recs.clear();
+    g_pool_used = 0;
+  }
+  return OK;
+}
+
+int swe_profile_read(double *ms_out, double *work_out, long long *count_out) {
+  for (int c = 0; c < NCLS; ++c) {
+    if (ms_out) ms_out[c] = 0.0;
+    if (work_out) work_out[c] = 0.0;
+    if (count_out) count_out[c] = 0;
+  }
+  for (const ProfRec &r : g_recs) {
+    SWE_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    SWE_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    if (ms_out) ms_out[r.cls] += ms;
+    if (work_out) work_out[r.cls] += r.work;
+    if (count_out) count_out[r.cls] += 1;
+  }
+  return OK;
+}
 const char *swe_last_error(void) { return last_error(); }
 
 }  // extern "C"

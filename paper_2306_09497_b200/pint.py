@@ -1,0 +1,527 @@
+"""Batched (and slice-sharded) FAS-MGRIT / Parareal driver.
+
+Mirror of `/root/reference/pkg/src/pintswe/pint.py`: PintBlowUpError (:33-41),
+LevelSpec (:44-53), PintConfig (:55-95), IterationTrace (:122-135),
+speedup_report (:146-154), SweProblem (:157-194), MgritEngine (:197-400),
+mgrit_run / parareal_run / fine_serial_cpoints (:403-430).
+
+Differences are in execution only, never in the iterates:
+* every sweep (F, C, residual, tau) is ONE batched propagator call over all
+  slices instead of a thread-pool task per slice (pint.py:209-219);
+* level arrays are tensors [points, ...] (for the SWE: [points, 3, K]
+  complex128 on the GPU);
+* with a `comm` (torch.distributed), level-0 slices are sharded in
+  contiguous blocks over ranks; a rank sends its last C-point to rank+1 before
+  every F-sweep (the only data dependence between slices, pint.py:229-231),
+  the coarsest serial sweep (pint.py:306-320) runs redundantly on every rank
+  after an all-gather of its forcing, and blow-up flags are all-reduced.
+Each slice's arithmetic does not depend on the batch it rides in, so traces
+are bitwise identical for any batch composition and any number of ranks
+(the reference's worker-count contract).
+The SL-SI-SETTLS history policy (pint.py:103-119) is out of scope (IMEX only).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import time
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+F_THEN_V = "F_then_V"
+V_CYCLE = "V"
+
+
+class PintBlowUpError(RuntimeError):
+    """Non-finite or runaway state detected; carries the partial trace."""
+
+    def __init__(self, iteration: int, slice_index: int, trace: "IterationTrace"):
+        super().__init__(f"blow-up at iteration {iteration}, slice {slice_index}")
+        self.iteration = iteration
+        self.slice_index = slice_index
+        self.trace = trace
+
+
+@dataclasses.dataclass(frozen=True)
+class LevelSpec:
+    index: int
+    M: int
+    stepper: object  # steppers.StepperConfig
+
+    @property
+    def dt(self) -> float:
+        return self.stepper.dt
+
+
+@dataclasses.dataclass(frozen=True)
+class PintConfig:
+    levels: tuple
+    T: float
+    N0: int
+    cfactor: int = 2
+    nrelax: int = 0
+    max_iters: int = 10
+    chunk_size: int = 0
+    cycle: str = F_THEN_V
+
+    def __post_init__(self):
+        L = len(self.levels)
+        if L < 2:
+            raise ValueError("need at least two levels")
+        if self.cfactor < 2:
+            raise ValueError("coarsening factor must be >= 2")
+        if self.nrelax < 0 or self.max_iters < 0 or self.chunk_size < 0:
+            raise ValueError("nrelax, max_iters and chunk_size must be >= 0")
+        if self.cycle not in (F_THEN_V, V_CYCLE):
+            raise ValueError(f"unknown cycle {self.cycle!r}")
+        dt0 = self.levels[0].dt
+        if abs(self.N0 * dt0 - self.T) > 1e-9 * max(self.T, 1.0):
+            raise ValueError("N0 * dt_0 must equal the horizon T")
+        for lv in range(1, L):
+            ratio = self.levels[lv].dt / self.levels[lv - 1].dt
+            if abs(ratio - self.cfactor) > 1e-9:
+                raise ValueError("level time steps must follow dt_{l+1} = cfactor*dt_l")
+            if self.levels[lv].M > self.levels[0].M:
+                raise ValueError("coarse levels cannot exceed the fine truncation")
+        if self.N0 % self.cfactor ** (L - 1) != 0:
+            raise ValueError("N0 must be divisible by cfactor^(nlevels-1)")
+
+    @property
+    def nlevels(self) -> int:
+        return len(self.levels)
+
+    def points_on(self, level: int) -> int:
+        return self.N0 // self.cfactor ** level
+
+    @property
+    def exact_convergence_bound(self) -> int:
+        return int(np.ceil(self.N0 / ((self.nrelax + 1) * self.cfactor)))
+
+
+class SnapshotList(list):
+    """One iteration's C-point snapshots; items materialise as problem states."""
+
+    def __init__(self, problem, tensor):
+        super().__init__(range(tensor.shape[0]))
+        self.tensor = tensor
+        self._problem = problem
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        n = len(self)
+        if i < 0:
+            i += n
+        return self._problem.wrap(0, self.tensor[i:i + 1])
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
+@dataclasses.dataclass
+class IterationTrace:
+    """Level-0 C-point snapshots per iteration (iteration 0: initial guess)."""
+
+    times: np.ndarray
+    snapshots: list
+    wall_times: list
+    config: PintConfig
+    blowup: Optional[dict] = None
+    fine_reference: Optional[Sequence] = None
+    fine_steps: list = dataclasses.field(default_factory=list)
+
+    @property
+    def iterations(self) -> int:
+        return len(self.snapshots) - 1
+
+
+@dataclasses.dataclass(frozen=True)
+class SpeedupRecord:
+    iteration: int
+    wall_time: float
+    cumulative_time: float
+    speedup: float
+
+
+def speedup_report(trace: IterationTrace, t_ref: float):
+    """pint.py:146-154."""
+    out, cum = [], 0.0
+    for k, wt in enumerate(trace.wall_times):
+        cum += wt
+        out.append(SpeedupRecord(k, wt, cum, t_ref / cum if cum > 0 else 0.0))
+    return out
+
+
+class Comm:
+    """Slice-block exchange over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def halo(self, send: torch.Tensor, recv: torch.Tensor):
+        """send -> rank+1, recv <- rank-1 (first/last rank skip)."""
+        d = self.dist
+        ops = []
+        if self.rank + 1 < self.size:
+            ops.append(d.P2POp(d.isend, send.contiguous(), self.rank + 1, self.group))
+        buf = None
+        if self.rank > 0:
+            buf = torch.empty_like(recv)
+            ops.append(d.P2POp(d.irecv, buf, self.rank - 1, self.group))
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+        if buf is not None:
+            recv.copy_(buf)
+
+    def all_gather(self, local: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.size * local.shape[0],) + tuple(local.shape[1:]),
+                          dtype=local.dtype, device=local.device)
+        if out.is_complex():
+            self.dist.all_gather_into_tensor(torch.view_as_real(out),
+                                             torch.view_as_real(local.contiguous()), group=self.group)
+        else:
+            self.dist.all_gather_into_tensor(out, local.contiguous(), group=self.group)
+        return out
+
+    def min_int(self, v: int) -> int:
+        t = torch.tensor([v], dtype=torch.int64,
+                         device="cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return int(t[0])
+
+
+class MgritEngine:
+    """FAS-MGRIT / Parareal over a batched problem (pint.py:197-400 semantics).
+
+    The problem provides step_batch(level, x), restrict_batch(level, x),
+    prolong_batch(level, x), stats_batch(level, x) -> (finite, max_abs) and
+    wrap(level, x) (tensors with a leading point axis).
+    """
+
+    def __init__(self, problem, config: PintConfig, comm: Optional[Comm] = None):
+        self.problem = problem
+        self.cfg = config
+        self.m = config.cfactor
+        self.L = config.nlevels
+        self.comm = comm
+        self.G = comm.size if comm else 1
+        self.g = comm.rank if comm else 0
+        self.fine_steps = 0
+        for lv in range(self.L - 1):
+            n = config.points_on(lv) // self.m
+            if n % self.G:
+                raise ValueError(f"level {lv}: {n} slices do not split over {self.G} ranks")
+        if self.G > 1:
+            n1 = config.points_on(1) // self.G     # coarse points per rank, level 1
+            if self.L > 2 and n1 % self.m:
+                raise ValueError("rank blocks must align with coarse slices")
+
+    # slices owned by this rank on `level` (1-based slice indices)
+    def _own(self, level: int, n: int):
+        S = n // self.G
+        return self.g * S + 1, (self.g + 1) * S
+
+    def _step(self, level, x):
+        if level == 0:
+            self.fine_steps += x.shape[0]
+        return self.problem.step_batch(level, x)
+
+    def _exchange_halo(self, level, u):
+        if self.G == 1:
+            return
+        n = (u.shape[0] - 1) // self.m
+        lo, hi = self._own(level, n)
+        self.comm.halo(u[self.m * hi], u[self.m * (lo - 1)])
+
+    # -- relaxation sweeps (pint.py:223-263) ------------------------------------
+    def _f_sweep(self, level, u, g):
+        m = self.m
+        n = (u.shape[0] - 1) // m
+        lo, hi = self._own(level, n)
+        self._exchange_halo(level, u)
+        left = torch.arange(m * (lo - 1), m * hi, m, device=u.device)
+        x = u[left]
+        for s in range(1, m):
+            x = self._step(level, x)
+            if g is not None:
+                x = x + g[left + s]
+            u[left + s] = x
+
+    def _c_sweep(self, level, u, g):
+        m = self.m
+        n = (u.shape[0] - 1) // m
+        lo, hi = self._own(level, n)
+        cp = torch.arange(m * lo, m * hi + 1, m, device=u.device)
+        x = self._step(level, u[cp - 1])
+        if g is not None:
+            x = x + g[cp]
+        u[cp] = x
+
+    def relax_fcf(self, level, u, g, nrelax):
+        self._f_sweep(level, u, g)
+        for _ in range(nrelax):
+            self._c_sweep(level, u, g)
+            self._f_sweep(level, u, g)
+
+    # -- FAS components (pint.py:267-304) ----------------------------------------
+    def _residual(self, level, u, g, lo, hi):
+        m = self.m
+        cp = torch.arange(m * lo, m * hi + 1, m, device=u.device)
+        prop = self._step(level, u[cp - 1])
+        if g is not None:
+            prop = prop + g[cp]
+        return prop - u[cp]
+
+    def _fas_restrict(self, level, u, g):
+        """Returns ubar, gbar as full-length coarse arrays (valid on owned points + halo)."""
+        m = self.m
+        n = (u.shape[0] - 1) // m
+        lo, hi = self._own(level, n)
+        pr = self.problem
+        cps = torch.arange(m * (lo - 1), m * hi + 1, m, device=u.device)   # halo + owned
+        ub_local = pr.restrict_batch(level, u[cps])
+        r = self._residual(level, u, g, lo, hi)
+        tau = ub_local[1:] - self._step(level + 1, ub_local[:-1])
+        gb_local = pr.restrict_batch(level, r) + tau
+        ubar = pr.zeros(level + 1, n + 1)
+        gbar = pr.zeros(level + 1, n + 1)
+        ubar[lo - 1:hi + 1] = ub_local
+        gbar[lo:hi + 1] = gb_local
+        if lo > 1:
+            # point 0 (the initial condition) is known everywhere; the serial
+            # coarsest sweep of every rank starts from it
+            ubar[0:1] = pr.restrict_batch(level, u[0:1])
+        return ubar, gbar
+
+    def _coarsest_solve(self, u, g):
+        """Serial sweep on the coarsest level (pint.py:306-320); with ranks, every
+        rank gathers the forcing and runs the identical sweep."""
+        lv = self.L - 1
+        n = u.shape[0] - 1
+        if self.G > 1:
+            lo, hi = self._own_points(lv, n)
+            g = torch.cat([g[:1], self.comm.all_gather(g[lo:hi + 1])])
+        for j in range(1, n + 1):
+            new = self._step(lv, u[j - 1:j])
+            if g is not None:
+                new = new + g[j:j + 1]
+            u[j:j + 1] = new
+
+    def _own_points(self, level, npts):
+        S = npts // self.G
+        return self.g * S + 1, (self.g + 1) * S
+
+    def _cycle(self, level, u, g, kind):
+        if level == self.L - 1:
+            self._coarsest_solve(u, g)
+            return
+        m = self.m
+        n = (u.shape[0] - 1) // m
+        lo, hi = self._own(level, n)
+        self.relax_fcf(level, u, g, self.cfg.nrelax)
+        ubar, gbar = self._fas_restrict(level, u, g)
+        v = ubar.clone()
+        self._cycle(level + 1, v, gbar, kind)
+        own = torch.arange(lo, hi + 1, device=u.device)
+        err = v[own] - ubar[own]
+        u[m * own] = u[m * own] + self.problem.prolong_batch(level + 1, err)
+        self._f_sweep(level, u, g)
+        if kind == F_THEN_V and level + 1 < self.L - 1:
+            self._cycle(level, u, g, V_CYCLE)
+
+    # -- driver (pint.py:341-400) ----------------------------------------------------
+    def _initial_guess(self, u0):
+        """Serial level-1 run prolonged to level 0 (also when L = 3, pint.py:341-353)."""
+        n1 = self.cfg.points_on(1)
+        pr = self.problem
+        v = pr.zeros(1, n1 + 1)
+        v[0:1] = pr.restrict_batch(0, u0)
+        for j in range(1, n1 + 1):
+            v[j:j + 1] = self._step(1, v[j - 1:j])
+        return pr.prolong_batch(1, v)
+
+    def _cpoints(self, u):
+        """All level-0 C-points (gathered across ranks)."""
+        m = self.m
+        n = (u.shape[0] - 1) // m
+        if self.G == 1:
+            return u[::m].clone()
+        lo, hi = self._own(0, n)
+        mine = u[m * lo: m * hi + 1: m]
+        return torch.cat([u[0:1], self.comm.all_gather(mine)])
+
+    def run(self, u0, fine_reference=None, initial_cpoints=None, keep_snapshots=True,
+            sync=None) -> IterationTrace:
+        """u0: tensor [1, ...] on level 0.  sync(): device barrier for wall times."""
+        cfg = self.cfg
+        m = self.m
+        n0, n1 = cfg.N0, cfg.points_on(1)
+        sync = sync or (lambda: None)
+        times = np.arange(n1 + 1) * (m * cfg.levels[0].dt)
+        sync()
+        t0 = time.perf_counter()
+        if initial_cpoints is None:
+            guess = self._initial_guess(u0)
+        else:
+            if len(initial_cpoints) != n1 + 1:
+                raise ValueError("initial_cpoints must cover every C-point")
+            guess = initial_cpoints.clone()
+        sync()
+        trace = IterationTrace(times=times, snapshots=[SnapshotList(self.problem, guess)],
+                               wall_times=[time.perf_counter() - t0], config=cfg,
+                               fine_reference=fine_reference)
+        _, mx0 = self.problem.stats_batch(0, u0)
+        limit = 1e10 * max(float(mx0[0]), 1e-300)
+        self._check_finite(trace, 0, guess, limit)
+        u = self.problem.zeros(0, n0 + 1)
+        u[0:1] = u0
+        idx = torch.arange(1, n1 + 1, device=u.device)
+        u[m * idx] = guess[1:]
+        for s in range(1, m):
+            u[m * (idx - 1) + s] = guess[:-1]
+        for k in range(1, cfg.max_iters + 1):
+            sync()
+            t0 = time.perf_counter()
+            f0 = self.fine_steps
+            self._cycle(0, u, None, cfg.cycle)
+            sync()
+            trace.wall_times.append(time.perf_counter() - t0)
+            trace.fine_steps.append(self.fine_steps - f0)
+            snap = self._cpoints(u)
+            trace.snapshots.append(SnapshotList(self.problem, snap) if keep_snapshots else None)
+            self._check_finite(trace, k, snap, limit)
+        return trace
+
+    def _check_finite(self, trace, iteration, snap, limit):
+        fin, mx = self.problem.stats_batch(0, snap)
+        bad = (~fin) | (mx > limit)
+        first = int(torch.nonzero(bad)[0]) if bool(bad.any()) else 1 << 60
+        if self.comm is not None:
+            first = self.comm.min_int(first)
+        if first < (1 << 60):
+            trace.blowup = {"iteration": iteration, "slice": first}
+            raise PintBlowUpError(iteration, first, trace)
+
+
+def mgrit_run(problem, config: PintConfig, u0, workers: int = 1, fine_reference=None,
+              initial_cpoints=None, comm: Optional[Comm] = None) -> IterationTrace:
+    """Run MGRIT (pint.py:403-408); `workers` is accepted for API parity (the
+    batch replaces the thread pool)."""
+    x0 = problem.as_batch(0, u0)
+    ic = None if initial_cpoints is None else problem.as_batch(0, initial_cpoints)
+    return MgritEngine(problem, config, comm).run(x0, fine_reference, ic)
+
+
+def parareal_run(problem, config: PintConfig, u0, workers: int = 1, fine_reference=None,
+                 initial_cpoints=None, comm: Optional[Comm] = None) -> IterationTrace:
+    """Parareal = two-level F-relaxation MGRIT (pint.py:411-418)."""
+    if config.nlevels != 2 or config.nrelax != 0:
+        raise ValueError("Parareal requires nlevels=2 and nrelax=0")
+    return mgrit_run(problem, config, u0, workers, fine_reference, initial_cpoints, comm)
+
+
+def fine_serial_cpoints(problem, config: PintConfig, u0):
+    """Serial fine solution at the level-0 C-points (pint.py:421-430)."""
+    x = problem.as_batch(0, u0)
+    out = [x.clone()]
+    for _ in range(config.points_on(1)):
+        for _ in range(config.cfactor):
+            x = problem.step_batch(0, x)
+        out.append(x.clone())
+    return SnapshotList(problem, torch.cat(out))
+
+
+class SweProblem:
+    """Shallow-water levels on the GPU (pint.py:157-194), batched and per-state.
+
+    Batched protocol (used by MgritEngine): tensors [points, 3, K] complex128.
+    Per-state protocol (drop-in for the reference engine): step/restrict/
+    prolong/copy/max_abs/is_finite/tracks_history on PrognosticState objects.
+    """
+
+    def __init__(self, config: PintConfig, geometry=None, phibar: Optional[float] = None):
+        from .spharm import SphereGeometry, get_grid
+        from .steppers import IMEX
+        self.config = config
+        self.geometry = geometry or SphereGeometry()
+        self.grids = [get_grid(spec.M, self.geometry) for spec in config.levels]
+        self.level_cfgs = [spec.stepper for spec in config.levels]
+        for c in self.level_cfgs:
+            if c.scheme != IMEX:
+                raise NotImplementedError("GPU SweProblem supports IMEX levels only")
+        self.phibar = phibar
+        self.step_calls = 0
+
+    # -- batched protocol --------------------------------------------------------
+    def _pb(self, n, dev):
+        return torch.full((n,), float(self.phibar), dtype=torch.float64, device=dev)
+
+    def as_batch(self, level, value):
+        from .dynamics import PrognosticState
+        if isinstance(value, PrognosticState):
+            if self.phibar is None:
+                self.phibar = value.phibar
+            return value.data
+        if isinstance(value, (list, tuple)):
+            return torch.cat([self.as_batch(level, v) for v in value])
+        return value
+
+    def wrap(self, level, x):
+        from .dynamics import PrognosticState
+        return PrognosticState(self.grids[level], x, self._pb(x.shape[0], x.device))
+
+    def zeros(self, level, n):
+        g = self.grids[level]
+        return torch.zeros((n, 3, g.n_modes), dtype=torch.complex128, device=f"cuda:{g.device}")
+
+    def step_batch(self, level, x):
+        from .steppers import imex_steps_inplace
+        st = self.wrap(level, x.clone())
+        self.step_calls += x.shape[0]
+        imex_steps_inplace(st, self.level_cfgs[level], 1)
+        return st.data
+
+    def restrict_batch(self, level, x):
+        from .spharm import truncate_pad
+        return truncate_pad(x, self.grids[level], self.grids[level + 1])
+
+    def prolong_batch(self, level, x):
+        from .spharm import truncate_pad
+        return truncate_pad(x, self.grids[level], self.grids[level - 1])
+
+    def stats_batch(self, level, x):
+        st = self.wrap(level, x)
+        mx = st.max_abs_each()
+        return st._fin.bool(), mx
+
+    # -- per-state protocol (pint.py:172-194) --------------------------------------
+    def step(self, level, value, prev=None):
+        from .steppers import StepperState, advance
+        self.step_calls += value.batch
+        return advance(StepperState(value, prev), self.level_cfgs[level]).current
+
+    def restrict(self, level, value):
+        return value.to_truncation(self.grids[level + 1])
+
+    def prolong(self, level, value):
+        return value.to_truncation(self.grids[level - 1])
+
+    def copy(self, value):
+        return value.copy()
+
+    def max_abs(self, value) -> float:
+        return value.max_abs()
+
+    def is_finite(self, value) -> bool:
+        return value.is_finite()
+
+    def tracks_history(self, level) -> bool:
+        return False

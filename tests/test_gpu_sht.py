@@ -47,8 +47,16 @@ def test_transforms_match_reference_goldens(gpu, name):
     assert rel_diff(xi, g["vd_xi"]) < TOL and rel_diff(de, g["vd_delta"]) < TOL
 
 
+@pytest.fixture(params=[1, 2], ids=["fft_rows", "fft_lanes"])
+def fft_path(request):
+    from paper_2306_09497_b200 import _lib
+    _lib.set_option("fft_path", request.param)
+    yield request.param
+    _lib.set_option("fft_path", 0)
+
+
 @pytest.mark.parametrize("M", [1, 2, 5, 8, 13, 16, 31, 32, 51, 64, 100, 256])
-def test_batched_transforms_match_oracle(gpu, M):
+def test_batched_transforms_match_oracle(gpu, fft_path, M):
     from oracle.sht import random_bandlimited
     grid = gpu.get_grid(M)
     sph = oracle(M)

@@ -61,7 +61,17 @@ def test_imex_steps_match_reference(mods, name):
         assert np.array_equal(s.data[0].cpu().numpy(), g[key + "_in"])
 
 
-def test_batched_step_matches_oracle_per_slice(mods):
+@pytest.mark.parametrize("path", [1, 2], ids=["fft_rows", "fft_lanes"])
+def test_batched_step_matches_oracle_per_slice(mods, path):
+    from paper_2306_09497_b200 import _lib
+    _lib.set_option("fft_path", path)
+    try:
+        _batched_step_check(mods)
+    finally:
+        _lib.set_option("fft_path", 0)
+
+
+def _batched_step_check(mods):
     """B slices with different states step in lockstep; each matches its own serial run."""
     spharm, dynamics, steppers, _ = mods
     from oracle.sht import OracleSphere
