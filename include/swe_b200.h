@@ -106,7 +106,9 @@ long long swe_kernel_launches(void);
  * FFT stage) and launch counts (all outputs HOST, nullable). */
 int swe_profile(int enable);
 /* Tuning switches.  "fft_path": 0 auto, 1 warp-per-row FFT kernel, 2 lane=row
- * FFT kernel (falls back to 1 where its radix/size limits do not hold). */
+ * FFT kernel (falls back to 1 where its radix/size limits do not hold).
+ * "leg_path": 0 auto, 1 small-batch Legendre kernels, 2 / 3 wide-tile kernels
+ * with 128 / 64 columns per CTA.  Results are identical on every path. */
 int swe_set_option(const char *key, int value);
 int swe_profile_read(double *ms_out, double *work_out, long long *count_out);
 const char *swe_last_error(void);

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128) leg_synth_kernel(const __grid_constant__ 
       const int r = i / (SY_BN / 2), cc = (i - r * (SY_BN / 2)) * 2;
       const int par = r / SY_KT, tt = t0 + (r - par * SY_KT);
       const bool v = (tt < (par ? no : ne)) && (c0 + cc < ld);
-      const size_t k = (size_t)off + par + 2 * tt;
+      const size_t k = (size_t)off + (par ? ne : 0) + tt;  // parity-split row
       const double *src = T.src + (v ? k * ld + c0 + cc : 0);
       if (T.phi0 != nullptr && v && k == 0) {
         // phi_prime: subtract phibar*sqrt(2) from Re of mode (0,0) (dynamics.py:52-56)
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(128) leg_synth_kernel(const __grid_constant__ 
       const int par = tid / SY_KT, tt = t0 + (tid - par * SY_KT);
       double s = 0.0;
       if (tt < (par ? no : ne)) {
-        const int k = off + par + 2 * tt;
+        const int k = off + (par ? ne : 0) + tt;
         s = T.sign * (T.scale ? T.scale[k] : 1.0) * (T.times_im ? (double)m : 1.0);
       }
       sm.S[stage][tid] = s;
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(128) leg_anal_kernel(const __grid_constant__ L
   for (int i = 0; i < 2; ++i) {
     const int tt = r0 + i * 8 + g;
     if (tt >= nt) continue;
-    const size_t k = (size_t)off + wpar + 2 * tt;
+    const size_t k = (size_t)off + (wpar ? ne : 0) + tt;  // parity-split row
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = c0 + wc * 32 + j * 8 + 2 * t;

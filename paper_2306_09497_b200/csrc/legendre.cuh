@@ -48,6 +48,10 @@ struct LegArgs {
 // Launch helpers (legendre.cu).  items/tiles are prepared by the plan.
 int leg_synth_launch(const LegArgs &a, int ncoltiles, cudaStream_t st);
 int leg_anal_launch(const LegArgs &a, int ncoltiles, cudaStream_t st);
+// wide-tile variants (legendre_v2.cu): column tile bn = 64 (4 warps) or 128 (8 warps)
+int leg_synth_v2_launch(const LegArgs &a, int bn, cudaStream_t st);
+int leg_anal_v2_launch(const LegArgs &a, int bn, cudaStream_t st);
+constexpr int V2_ABR = 32;  // analysis modes per parity per CTA
 
 constexpr int SY_BM = 64;   // latitude pairs per CTA
 constexpr int SY_BN = 64;   // real columns per CTA

@@ -177,10 +177,15 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
   std::vector<int> offs(M + 2, 0);
   for (int m = 0; m <= M; ++m) offs[m + 1] = offs[m] + (M + 1 - m);
   pl->h_offsets = offs;
+  // internal (device) spectral order = table row order: per m block the even n-m
+  // modes, then the odd ones.  perm maps the reference's packed index to it.
   std::vector<double> lap(K), inv(K), eps(K);
+  std::vector<int> perm(K);
   for (int m = 0; m <= M; ++m)
     for (int n = m; n <= M; ++n) {
-      const int k = offs[m] + n - m;
+      const int d = n - m, ne = (M + 2 - m) / 2;
+      const int k = offs[m] + ((d & 1) ? ne + (d >> 1) : (d >> 1));
+      perm[offs[m] + d] = k;
       const double nn1 = (double)n * (n + 1.0);
       lap[k] = -nn1 / (a * a);                      // spharm.py:195-197
       inv[k] = nn1 > 0 ? -(a * a) / nn1 : 0.0;      // spharm.py:198-200
@@ -193,7 +198,8 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
     fc[j] = 2.0 * omega * pl->mu[j];
     wsq[j] = pl->w[j] / (1.0 - pl->mu[j] * pl->mu[j]);
   }
-  if ((rc = upload(&pl->offsets, offs)) || (rc = upload(&pl->lap_eig, lap)) ||
+  if ((rc = upload(&pl->offsets, offs)) || (rc = upload(&pl->perm, perm)) ||
+      (rc = upload(&pl->lap_eig, lap)) ||
       (rc = upload(&pl->inv_lap, inv)) || (rc = upload(&pl->eps, eps)) ||
       (rc = upload(&pl->coslat, coslv)) || (rc = upload(&pl->inv_acos, iac)) ||
       (rc = upload(&pl->fcor, fc)) || (rc = upload(&pl->wq, pl->w)) ||
@@ -295,9 +301,17 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
       const int rt = (ne + AN_BR - 1) / AN_BR;
       for (int t = 0; t < rt; ++t) an.push_back(make_int2(m, t));
     }
+    std::vector<int2> an2;
+    for (int m = 0; m <= M; ++m) {
+      const int ne = (M + 2 - m) / 2;
+      for (int t = 0; t < (ne + V2_ABR - 1) / V2_ABR; ++t) an2.push_back(make_int2(m, t));
+    }
     pl->n_synth_items = (int)sy.size();
     pl->n_anal_items = (int)an.size();
-    if ((rc = upload(&pl->synth_items, sy)) || (rc = upload(&pl->anal_items, an))) return rc;
+    pl->n_anal_items_v2 = (int)an2.size();
+    if ((rc = upload(&pl->synth_items, sy)) || (rc = upload(&pl->anal_items, an)) ||
+        (rc = upload(&pl->anal_items_v2, an2)))
+      return rc;
   }
   *out = pl;
   return OK;
@@ -325,6 +339,7 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->P);
   cudaFree(pl->H);
   cudaFree(pl->offsets);
+  cudaFree(pl->perm);
   cudaFree(pl->lap_eig);
   cudaFree(pl->inv_lap);
   cudaFree(pl->eps);
@@ -339,6 +354,7 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->fft_pos_g);
   cudaFree(pl->synth_items);
   cudaFree(pl->anal_items);
+  cudaFree(pl->anal_items_v2);
   delete pl;
 }
 

@@ -5,7 +5,8 @@
 // w/(1-mu^2), f = 2 Omega mu.  HBM layout (doubles):
 //   P, H          [K rows][Jp]   row = offset[m] + (n-m even ? (n-m)/2 : ne(m) + (n-m-1)/2),
 //                                column = latitude pair p (north row), zero for p >= Jh
-//   spectral      [K][ld]        packed mode (m-major, n = m..M) x column 2*slice + re/im
+//   spectral      [K][ld]        mode row in the same parity-split order as the tables
+//                                x column 2*slice + re/im (boundary: reference packing)
 //   half / F      [M+1][J][ld]   order m x latitude row x column
 #pragma once
 
@@ -43,6 +44,7 @@ struct swe_plan {
   // device tables
   double *P = nullptr, *H = nullptr;
   int *offsets = nullptr;
+  int *perm = nullptr;  // [K] reference packed index -> internal (parity-split) row
   double *lap_eig = nullptr, *inv_lap = nullptr, *eps = nullptr;
   double *coslat = nullptr, *inv_acos = nullptr, *fcor = nullptr, *wq = nullptr, *wsin2 = nullptr;
   double2 *tw = nullptr, *twh = nullptr;
@@ -51,6 +53,8 @@ struct swe_plan {
   int rgen = 0;
   int2 *synth_items = nullptr, *anal_items = nullptr;
   int n_synth_items = 0, n_anal_items = 0;
+  int2 *anal_items_v2 = nullptr;
+  int n_anal_items_v2 = 0;
   int nst = 0;
   int radix[swe::FFT_MAXST], ns[swe::FFT_MAXST];
   std::vector<int> h_offsets;

@@ -10,7 +10,9 @@
 namespace swe {
 
 // ---- layout: boundary [B][F][K] complex <-> internal F x [K][B] complex ------
-__global__ void k_to_internal(const double2 *__restrict__ src, SpecPtrs dst, int B, int F, int K) {
+// perm[k] = internal row of the reference's packed index k (parity-split order)
+__global__ void k_to_internal(const double2 *__restrict__ src, SpecPtrs dst, int B, int F, int K,
+                              const int *__restrict__ perm) {
   __shared__ double2 tile[32][33];
   const int f = blockIdx.z, k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -21,17 +23,18 @@ __global__ void k_to_internal(const double2 *__restrict__ src, SpecPtrs dst, int
   double2 *d = reinterpret_cast<double2 *>(dst.p[f]);
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int k = k0 + r, b = b0 + threadIdx.x;
-    if (b < B && k < K) d[(size_t)k * B + b] = tile[threadIdx.x][r];
+    if (b < B && k < K) d[(size_t)perm[k] * B + b] = tile[threadIdx.x][r];
   }
 }
 
-__global__ void k_to_boundary(SpecPtrsC src, double2 *__restrict__ dst, int B, int F, int K) {
+__global__ void k_to_boundary(SpecPtrsC src, double2 *__restrict__ dst, int B, int F, int K,
+                              const int *__restrict__ perm) {
   __shared__ double2 tile[32][33];
   const int f = blockIdx.z, k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
   const double2 *s = reinterpret_cast<const double2 *>(src.p[f]);
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int k = k0 + r, b = b0 + threadIdx.x;
-    if (b < B && k < K) tile[r][threadIdx.x] = s[(size_t)k * B + b];
+    if (b < B && k < K) tile[r][threadIdx.x] = s[(size_t)perm[k] * B + b];
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -40,16 +43,18 @@ __global__ void k_to_boundary(SpecPtrsC src, double2 *__restrict__ dst, int B, i
   }
 }
 
-int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, cudaStream_t st) {
+int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, const int *perm,
+                cudaStream_t st) {
   dim3 grid((K + 31) / 32, (B + 31) / 32, F), blk(32, 8);
-  k_to_internal<<<grid, blk, 0, st>>>(reinterpret_cast<const double2 *>(src), dst, B, F, K);
+  k_to_internal<<<grid, blk, 0, st>>>(reinterpret_cast<const double2 *>(src), dst, B, F, K, perm);
   SWE_LAUNCH_CHECK();
   return OK;
 }
 
-int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, cudaStream_t st) {
+int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, const int *perm,
+                cudaStream_t st) {
   dim3 grid((K + 31) / 32, (B + 31) / 32, F), blk(32, 8);
-  k_to_boundary<<<grid, blk, 0, st>>>(src, reinterpret_cast<double2 *>(dst), B, F, K);
+  k_to_boundary<<<grid, blk, 0, st>>>(src, reinterpret_cast<double2 *>(dst), B, F, K, perm);
   SWE_LAUNCH_CHECK();
   return OK;
 }

@@ -20,8 +20,10 @@ struct Ptr3C {
   const double *p[3];
 };
 
-int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, cudaStream_t st);
-int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, cudaStream_t st);
+int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, const int *perm,
+                cudaStream_t st);
+int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, const int *perm,
+                cudaStream_t st);
 int lin_rhs(int K, int B, const double *const U[3], const double *lcx, const double *lcd,
             double alpha, const double *eps, const double *phibar, double *const R[3],
             cudaStream_t st);

@@ -36,6 +36,7 @@ struct ProfRec {
 };
 bool g_prof = false;
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
+int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
 std::vector<ProfRec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 size_t g_pool_used = 0;
@@ -123,17 +124,33 @@ double leg_flops(const Run &r, const LegArgs &a) {
   return 2.0 * r.pl->J * (double)r.pl->K * r.B * terms;
 }
 
+// Legendre kernel choice -> 0: legendre.cu (small batches), else v2 column tile 64 or 128
+int leg_bn(const Run &r) {
+  switch (g_leg_path) {
+    case 1: return 0;
+    case 2: return 128;
+    case 3: return 64;
+    default: return r.ld > 32 ? 64 : 0;
+  }
+}
+
 int synth(const Run &r, LegArgs &a) {
   a.items = r.pl->synth_items;
   a.nitems = r.pl->n_synth_items;
   ProfScope ps(0, leg_flops(r, a), r.st);
+  if (const int bn = leg_bn(r)) return leg_synth_v2_launch(a, bn, r.st);
   return leg_synth_launch(a, (int)((r.ld + SY_BN - 1) / SY_BN), r.st);
 }
 
 int anal(const Run &r, LegArgs &a) {
+  ProfScope ps(1, leg_flops(r, a), r.st);
+  if (const int bn = leg_bn(r)) {
+    a.items = r.pl->anal_items_v2;
+    a.nitems = r.pl->n_anal_items_v2;
+    return leg_anal_v2_launch(a, bn, r.st);
+  }
   a.items = r.pl->anal_items;
   a.nitems = r.pl->n_anal_items;
-  ProfScope ps(1, leg_flops(r, a), r.st);
   return leg_anal_launch(a, (int)((r.ld + AN_BN - 1) / AN_BN), r.st);
 }
 
@@ -499,7 +516,7 @@ int swe_synthesis(swe_plan *pl, const double *spec, double *grid, int batch, voi
   if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
   Run r = make_run(pl, batch, stream);
   SpecPtrs d = {{r.spec(0)}};
-  if ((rc = to_internal(spec, d, batch, 1, pl->K, r.st))) return rc;
+  if ((rc = to_internal(spec, d, batch, 1, pl->K, pl->perm, r.st))) return rc;
   LegArgs a = leg_args(r);
   a.nout = 1;
   set_out(a, 0, r.half(0), term(pl->P, r.spec(0)), nullptr, pl->H);
@@ -526,7 +543,7 @@ int swe_analysis(swe_plan *pl, const double *grid, double *spec, int batch, void
   set_out(a, 0, r.spec(0), term(pl->P, r.fsp(0)), nullptr, pl->H);
   if ((rc = anal(r, a))) return rc;
   SpecPtrsC s = {{r.spec(0)}};
-  return to_boundary(s, spec, batch, 1, pl->K, r.st);
+  return to_boundary(s, spec, batch, 1, pl->K, pl->perm, r.st);
 }
 
 int swe_uv_from_vortdiv(swe_plan *pl, const double *xi, const double *delta, double *u, double *v,
@@ -535,8 +552,8 @@ int swe_uv_from_vortdiv(swe_plan *pl, const double *xi, const double *delta, dou
   if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
   Run r = make_run(pl, batch, stream);
   SpecPtrs d0 = {{r.spec(0)}}, d1 = {{r.spec(1)}};
-  if ((rc = to_internal(xi, d0, batch, 1, pl->K, r.st))) return rc;
-  if ((rc = to_internal(delta, d1, batch, 1, pl->K, r.st))) return rc;
+  if ((rc = to_internal(xi, d0, batch, 1, pl->K, pl->perm, r.st))) return rc;
+  if ((rc = to_internal(delta, d1, batch, 1, pl->K, pl->perm, r.st))) return rc;
   const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
   LegArgs a = leg_args(r);
   a.nout = 2;
@@ -574,8 +591,8 @@ int swe_vortdiv_from_uv(swe_plan *pl, const double *u, const double *v, double *
   set_out(a, 1, r.spec(1), term(P, r.fsp(0), 1.0, 1), &hd, H);
   if ((rc = anal(r, a))) return rc;
   SpecPtrsC s0 = {{r.spec(0)}}, s1 = {{r.spec(1)}};
-  if ((rc = to_boundary(s0, xi, batch, 1, pl->K, r.st))) return rc;
-  return to_boundary(s1, delta, batch, 1, pl->K, r.st);
+  if ((rc = to_boundary(s0, xi, batch, 1, pl->K, pl->perm, r.st))) return rc;
+  return to_boundary(s1, delta, batch, 1, pl->K, pl->perm, r.st);
 }
 
 int swe_tendency(swe_plan *pl, int kind, const double *state, const double *phibar, double *out,
@@ -590,7 +607,7 @@ int swe_tendency(swe_plan *pl, int kind, const double *state, const double *phib
   const Bufs b = bufs(r);
   const int K = pl->K;
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
-  if ((rc = to_internal(state, d, batch, 3, K, r.st))) return rc;
+  if ((rc = to_internal(state, d, batch, 3, K, pl->perm, r.st))) return rc;
   const size_t n = (size_t)K * batch;
   for (int f = 0; f < 3; ++f) SWE_CUDA(cudaMemsetAsync(b.K1[f], 0, n * 16, r.st));
   const double *Uc[3] = {b.U[0], b.U[1], b.U[2]};
@@ -614,7 +631,7 @@ int swe_tendency(swe_plan *pl, int kind, const double *state, const double *phib
     if ((rc = axpy3(n, k1c, k2c, none, 1.0, k1, r.st))) return rc;
   }
   SpecPtrsC s = {{b.K1[0], b.K1[1], b.K1[2]}};
-  return to_boundary(s, out, batch, 3, K, r.st);
+  return to_boundary(s, out, batch, 3, K, pl->perm, r.st);
 }
 
 int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
@@ -630,13 +647,13 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
   Run r = make_run(pl, batch, stream);
   const Bufs b = bufs(r);
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
-  if ((rc = to_internal(state, d, batch, 3, pl->K, r.st))) return rc;
+  if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st))) return rc;
   for (int s = 0; s < nsteps; ++s) {
     rc = imex_internal(r, *cfg, iters_out ? iters_out + (size_t)s * 2 * batch : nullptr, resid_out);
     if (rc) return rc;
   }
   SpecPtrsC s = {{b.U[0], b.U[1], b.U[2]}};
-  return to_boundary(s, state, batch, 3, pl->K, r.st);
+  return to_boundary(s, state, batch, 3, pl->K, pl->perm, r.st);
 }
 
 int swe_truncate_pad(const swe_plan *src, const swe_plan *dst, const double *in, double *out,
@@ -661,6 +678,10 @@ long long swe_kernel_launches(void) { return g_launches; }
 int swe_set_option(const char *key, int value) {
   if (key && strcmp(key, "fft_path") == 0 && value >= 0 && value <= 2) {
     g_fft_path = value;
+    return OK;
+  }
+  if (key && strcmp(key, "leg_path") == 0 && value >= 0 && value <= 3) {
+    g_leg_path = value;
     return OK;
   }
   set_error("unknown option %s=%d", key ? key : "(null)", value);

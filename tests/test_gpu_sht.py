@@ -47,12 +47,34 @@ def test_transforms_match_reference_goldens(gpu, name):
     assert rel_diff(xi, g["vd_xi"]) < TOL and rel_diff(de, g["vd_delta"]) < TOL
 
 
-@pytest.fixture(params=[1, 2], ids=["fft_rows", "fft_lanes"])
+@pytest.fixture(params=[(1, 1), (2, 2), (1, 2)], ids=["rows_narrow", "lanes_wide", "rows_wide"])
 def fft_path(request):
+    """Force each FFT kernel (warp-per-row / lane=row) and Legendre tiling
+    (64- / 128-column) so every code path is parity-checked at every M."""
     from paper_2306_09497_b200 import _lib
-    _lib.set_option("fft_path", request.param)
+    _lib.set_option("fft_path", request.param[0])
+    _lib.set_option("leg_path", request.param[1])
     yield request.param
     _lib.set_option("fft_path", 0)
+    _lib.set_option("leg_path", 0)
+
+
+@pytest.mark.parametrize("B", [33, 40, 64, 70])
+def test_wide_batches_match_oracle(gpu, B):
+    """Batches that fill / overflow the 128-column tiles (default auto paths)."""
+    from oracle.sht import random_bandlimited
+    M = 51
+    grid = gpu.get_grid(M)
+    sph = oracle(M)
+    rng = np.random.default_rng(B)
+    c = random_bandlimited(sph, rng, batch=(B,))
+    assert rel_diff(grid.synthesis(c), sph.synthesis(c)) < TOL
+    u, v = grid.uv_from_vortdiv(c, c[::-1].copy())
+    uo, vo = sph.uv_from_vortdiv(c, c[::-1].copy())
+    assert rel_diff(u, uo) < TOL and rel_diff(v, vo) < TOL
+    xi, de = grid.vortdiv_from_uv(u, v)
+    xo, do = sph.vortdiv_from_uv(uo, vo)
+    assert rel_diff(xi, xo) < TOL and rel_diff(de, do) < TOL
 
 
 @pytest.mark.parametrize("M", [1, 2, 5, 8, 13, 16, 31, 32, 51, 64, 100, 256])
