@@ -124,31 +124,42 @@ SWE_DEV void warp_fft(double2 *x, double2 *scr, const FftArgs &a, int lane) {
 
 struct Ctx {
   double2 *rows, *scr;
-  int j, b0, nsl, tid, nthr, warp, lane, nw;
+  int p, jn, js, eq, b0, nsl, tid, nthr, warp, lane, nw;
 };
 
 SWE_DEV double2 *row_of(const FftArgs &a, const Ctx &c, int f, int s) {
   return c.rows + (size_t)(f * a.spb + s) * a.N2;
 }
 
-// Half spectrum X[0..M] (global [m][J][ld]) -> Z in digit-reversed order, where
-// IDFT_N2(Z)[r] = g[2r] + i g[2r+1] and g = irfft(X * I, n = I) (Im X[0] dropped):
-//   Z[k] = (X[k] + conj X[N2-k]) + i w^k (X[k] - conj X[N2-k]),  w = e^{2 pi i / I}
-SWE_DEV void load_half_z(const FftArgs &a, const Ctx &c, const double *src, int f) {
+// One hemisphere row h of field f for pair p: half spectrum X = E + O (north) or
+// E - O (south) from the parity-split Legendre output [m][2][Jp][ld], written as
+// Z in spectral slot order:  Z[k] = (X[k] + conj X[N2-k]) + i w^k (X[k] - conj X[N2-k])
+// with w = e^{2 pi i / I}, so IDFT_N2(Z)[r] = g[2r] + i g[2r+1],
+// g = irfft(X * I, n = I) (numpy drops Im X[0]).  sub (nullable) is
+// subtracted from E at m = 0 (phi_prime, dynamics.py:52-56).
+SWE_DEV void load_eo(const FftArgs &a, const Ctx &c, const double *src, int f, int h,
+                     const double *sub) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1;
-  const double2 *base = reinterpret_cast<const double2 *>(src + (size_t)c.j * a.ld) + c.b0;
-  const size_t mstride = (size_t)a.J * a.ld / 2;  // in double2
+  const size_t eo = (size_t)a.Jp * a.ld / 2;
+  const double2 *base = reinterpret_cast<const double2 *>(src + (size_t)c.p * a.ld) + c.b0;
+  const size_t mstride = 2 * eo;
+  const double sg = h ? -1.0 : 1.0;
   for (int idx = c.tid; idx < npair * c.nsl; idx += c.nthr) {
     const int k = idx / c.nsl, s = idx - k * c.nsl;
     double2 *x = row_of(a, c, f, s);
+    const int k2 = k == 0 ? N2 : N2 - k;
+    const double2 z = make_double2(0.0, 0.0);
+    double2 e = k <= M ? __ldg(base + (size_t)k * mstride + s) : z;
+    const double2 o = k <= M ? __ldg(base + (size_t)k * mstride + eo + s) : z;
+    const double2 e2 = k2 <= M ? __ldg(base + (size_t)k2 * mstride + s) : z;
+    const double2 o2 = k2 <= M ? __ldg(base + (size_t)k2 * mstride + eo + s) : z;
+    if (sub != nullptr && k == 0) e.x -= sub[c.b0 + s];
+    const double2 Xk = make_double2(e.x + sg * o.x, e.y + sg * o.y);
+    const double2 Xc = make_double2(e2.x + sg * o2.x, e2.y + sg * o2.y);
     if (k == 0) {
-      const double x0 = __ldg(base + s).x;
-      x[__ldg(a.pos_z)] = make_double2(x0, x0);
+      x[__ldg(a.pos_z)] = make_double2(Xk.x, Xk.x);
       continue;
     }
-    const int k2 = N2 - k;
-    const double2 Xk = k <= M ? __ldg(base + (size_t)k * mstride + s) : make_double2(0.0, 0.0);
-    const double2 Xc = k2 <= M ? __ldg(base + (size_t)k2 * mstride + s) : make_double2(0.0, 0.0);
     const double2 A = make_double2(Xk.x + Xc.x, Xk.y - Xc.y);
     const double2 D = make_double2(Xk.x - Xc.x, Xk.y + Xc.y);
     const double2 Bk = cm(D, __ldg(a.twh + k));
@@ -162,18 +173,20 @@ SWE_DEV void load_half_z(const FftArgs &a, const Ctx &c, const double *src, int 
   }
 }
 
-SWE_DEV void load_grid(const FftArgs &a, const Ctx &c, const double *src, int f) {
+SWE_DEV int row_j(const Ctx &c, int h) { return h ? c.js : c.jn; }
+
+SWE_DEV void load_grid(const FftArgs &a, const Ctx &c, const double *src, int f, int h) {
   for (int s = 0; s < c.nsl; ++s) {
-    const double *g = src + ((size_t)(c.b0 + s) * a.J + c.j) * a.I;
+    const double *g = src + ((size_t)(c.b0 + s) * a.J + row_j(c, h)) * a.I;
     double *r = reinterpret_cast<double *>(row_of(a, c, f, s));
     // grid sample n is component n&1 of transform slot pos_g[n/2]
     for (int n = c.tid; n < a.I; n += c.nthr) r[2 * __ldg(a.pos_g + (n >> 1)) + (n & 1)] = __ldg(g + n);
   }
 }
 
-SWE_DEV void store_grid(const FftArgs &a, const Ctx &c, double *dst, int f, double scale) {
+SWE_DEV void store_grid(const FftArgs &a, const Ctx &c, double *dst, int f, int h, double scale) {
   for (int s = 0; s < c.nsl; ++s) {
-    double *g = dst + ((size_t)(c.b0 + s) * a.J + c.j) * a.I;
+    double *g = dst + ((size_t)(c.b0 + s) * a.J + row_j(c, h)) * a.I;
     const double *r = reinterpret_cast<const double *>(row_of(a, c, f, s));
     for (int n = c.tid; n < a.I; n += c.nthr) g[n] = r[2 * __ldg(a.pos_g + (n >> 1)) + (n & 1)] * scale;
   }
@@ -181,7 +194,6 @@ SWE_DEV void store_grid(const FftArgs &a, const Ctx &c, double *dst, int f, doub
 
 SWE_DEV double2 *warp_scr(const FftArgs &a, const Ctx &c) { return c.scr + (size_t)c.warp * a.rgen; }
 
-// inverse transforms of fields [f0, f0+nf) (rows loaded by load_half_z)
 SWE_DEV void c2r_fields(const FftArgs &a, const Ctx &c, int f0, int nf) {
   for (int task = c.warp; task < nf * c.nsl; task += c.nw) {
     const int f = f0 + task / c.nsl, s = task % c.nsl;
@@ -189,29 +201,38 @@ SWE_DEV void c2r_fields(const FftArgs &a, const Ctx &c, int f0, int nf) {
   }
 }
 
-// forward transforms of fields fld[o]; store fm[k] * scale[o] (k = 0..M) to a.out[o]
-//   fm[k] = (1/I) sum_n g[n] w^{-nk} = (Ge[k] + w^{-k} Go[k]) / I
+// forward transforms of fields fld[o] of hemisphere h; fm[k] = (Ge + w^{-k} Go)/I.
+// h = 0: stash scale*fm_N in the F+ slot (and F- on the equator);
+// h = 1: F+ = stash + scale*fm_S, F- = stash - scale*fm_S.
 template <int NOUT>
 SWE_DEV void r2c_outputs(const FftArgs &a, const Ctx &c, const int (&fld)[NOUT],
-                         const double (&scale)[NOUT]) {
+                         const double (&scale)[NOUT], int h) {
   const int N2 = a.N2, M = a.M;
+  const size_t pm = (size_t)a.Jp * a.ld / 2;
   for (int task = c.warp; task < NOUT * c.nsl; task += c.nw) {
     const int o = task / c.nsl, s = task % c.nsl;
     double2 *x = row_of(a, c, fld[o], s);
     warp_fft(x, warp_scr(a, c), a, c.lane);
-    const double h = 0.5 * scale[o];
-    double2 *dst = reinterpret_cast<double2 *>(a.out[o] + (size_t)c.j * a.ld) + c.b0 + s;
-    const size_t mstride = (size_t)a.J * a.ld / 2;
+    const double hs = 0.5 * scale[o];
+    double2 *dst = reinterpret_cast<double2 *>(a.out[o] + (size_t)c.p * a.ld) + c.b0 + s;
     for (int k = c.lane; k <= M; k += 32) {
       const double2 zk = x[__ldg(a.pos_z + k)];
       const double2 z2 = x[__ldg(a.pos_z + (k == 0 ? 0 : N2 - k))];
-      const double2 zc = make_double2(z2.x, -z2.y);
-      const double2 S = make_double2(zk.x + zc.x, zk.y + zc.y);     // 2 Ge
-      const double2 D = make_double2(zk.y - zc.y, -(zk.x - zc.x));  // 2 Go
+      const double2 Sg = make_double2(zk.x + z2.x, zk.y - z2.y);     // 2 Ge
+      const double2 D = make_double2(zk.y + z2.y, -(zk.x - z2.x));   // 2 Go
       double2 w = __ldg(a.twh + k);
       w.y = -w.y;
       const double2 t = cm(w, D);
-      dst[(size_t)k * mstride] = make_double2((S.x + t.x) * h, (S.y + t.y) * h);
+      const double2 v = make_double2((Sg.x + t.x) * hs, (Sg.y + t.y) * hs);
+      double2 *d = dst + (size_t)k * 2 * pm;
+      if (h == 0) {
+        d[0] = v;
+        if (c.eq) d[pm] = v;
+      } else {
+        const double2 n = d[0];
+        d[0] = make_double2(n.x + v.x, n.y + v.y);
+        d[pm] = make_double2(n.x - v.x, n.y - v.y);
+      }
     }
   }
 }
@@ -222,7 +243,10 @@ template <int OP>
 __global__ void __launch_bounds__(256) fft_kernel(const __grid_constant__ FftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Ctx c;
-  c.j = blockIdx.x;
+  c.p = blockIdx.x;
+  c.jn = c.p;
+  c.js = a.J - 1 - c.p;
+  c.eq = c.js == c.jn;
   c.b0 = blockIdx.y * a.spb;
   c.nsl = min(a.spb, a.nslices - c.b0);
   c.tid = threadIdx.x;
@@ -232,8 +256,8 @@ __global__ void __launch_bounds__(256) fft_kernel(const __grid_constant__ FftArg
   c.nw = blockDim.x >> 5;
   c.rows = reinterpret_cast<double2 *>(smem_raw);
   c.scr = c.rows + (size_t)fft_rows_per_slice(OP) * a.spb * a.N2;
-  const int j = c.j;
-  const double ia = a.inv_acos[j];
+  const int p = c.p;
+  const double ia = a.inv_acos[p];
   const int I = a.I;
 
   auto pointwise = [&](auto fn) {
@@ -244,96 +268,101 @@ __global__ void __launch_bounds__(256) fft_kernel(const __grid_constant__ FftArg
   };
   auto rd = [&](int f, int s) { return reinterpret_cast<double *>(row_of(a, c, f, s)); };
 
-  if constexpr (OP == FOP_SYNTH_GRID) {
-    load_half_z(a, c, a.in[0], 0);
+  // north row, then south row (skipped on the equator); spectra of the north
+  // pass are stashed in the output's F+ slot and folded by the south pass
+  for (int h = 0; h < 2 - c.eq; ++h) {
+    if constexpr (OP == FOP_SYNTH_GRID) {
+      load_eo(a, c, a.in[0], 0, h, nullptr);
+      __syncthreads();
+      c2r_fields(a, c, 0, 1);
+      __syncthreads();
+      store_grid(a, c, a.gout[0], 0, h, a.scale_mode ? ia : 1.0);
+    } else if constexpr (OP == FOP_SYNTH2_GRID) {
+      load_eo(a, c, a.in[0], 0, h, nullptr);
+      load_eo(a, c, a.in[1], 1, h, nullptr);
+      __syncthreads();
+      c2r_fields(a, c, 0, 2);
+      __syncthreads();
+      store_grid(a, c, a.gout[0], 0, h, ia);
+      store_grid(a, c, a.gout[1], 1, h, ia);
+    } else if constexpr (OP == FOP_ANALYSIS) {
+      load_grid(a, c, a.gin[0], 0, h);
+      __syncthreads();
+      const int f[1] = {0};
+      const double sc[1] = {a.wq[p] * a.inv_I};
+      r2c_outputs<1>(a, c, f, sc, h);
+    } else if constexpr (OP == FOP_VORTDIV) {
+      load_grid(a, c, a.gin[0], 0, h);
+      load_grid(a, c, a.gin[1], 1, h);
+      __syncthreads();
+      const double cs = a.coslat[p];
+      pointwise([&](int s, int n) {
+        rd(0, s)[n] *= cs;
+        rd(1, s)[n] *= cs;
+      });
+      __syncthreads();
+      const int f[2] = {0, 1};
+      const double w = a.wsin2[p] * a.inv_I * a.inv_a;
+      const double sc[2] = {w, w};
+      r2c_outputs<2>(a, c, f, sc, h);
+    } else if constexpr (OP == FOP_CORIOLIS) {
+      // linear_coriolis (dynamics.py:129-135); f = 2 Omega mu flips sign in the south
+      load_eo(a, c, a.in[0], 0, h, nullptr);
+      load_eo(a, c, a.in[1], 1, h, nullptr);
+      __syncthreads();
+      c2r_fields(a, c, 0, 2);
+      __syncthreads();
+      const double cs = a.coslat[p], fc = h ? -a.fcor[p] : a.fcor[p];
+      pointwise([&](int s, int n) {
+        double *u = rd(0, s), *v = rd(1, s);
+        u[n] = (fc * (u[n] * ia)) * cs;
+        v[n] = (fc * (v[n] * ia)) * cs;
+      });
+      __syncthreads();
+      const int f[2] = {0, 1};
+      const double w = a.wsin2[p] * a.inv_I * a.inv_a;
+      const double sc[2] = {w, w};
+      r2c_outputs<2>(a, c, f, sc, h);
+    } else if constexpr (OP == FOP_NONLINEAR) {
+      // nonlinear_advection + nonlinear_rest (dynamics.py:142-160)
+      // in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi, 5 Phi (phi_prime applied here), 6 delta
+      for (int f = 0; f < 4; ++f) load_eo(a, c, a.in[f], f, h, nullptr);
+      __syncthreads();
+      c2r_fields(a, c, 0, 4);
+      __syncthreads();
+      pointwise([&](int s, int n) {
+        double *r0 = rd(0, s), *r1 = rd(1, s), *r2 = rd(2, s), *r3 = rd(3, s);
+        const double u = r0[n] * ia, v = r1[n] * ia, gx = r2[n] * ia, gy = r3[n] * ia;
+        r0[n] = u;
+        r1[n] = v;
+        r2[n] = -(u * gx + v * gy);
+        r3[n] = 0.5 * (u * u + v * v);
+      });
+      load_eo(a, c, a.in[4], 4, h, nullptr);
+      __syncthreads();
+      c2r_fields(a, c, 4, 1);
+      __syncthreads();
+      const double cs = a.coslat[p];
+      pointwise([&](int s, int n) {
+        double *r0 = rd(0, s), *r1 = rd(1, s);
+        const double xi = rd(4, s)[n];
+        r0[n] = (xi * r0[n]) * cs;
+        r1[n] = (xi * r1[n]) * cs;
+      });
+      __syncthreads();
+      load_eo(a, c, a.in[5], 4, h, a.phisub);
+      load_eo(a, c, a.in[6], 5, h, nullptr);
+      __syncthreads();
+      c2r_fields(a, c, 4, 2);
+      __syncthreads();
+      pointwise([&](int s, int n) { rd(2, s)[n] -= rd(4, s)[n] * rd(5, s)[n]; });
+      __syncthreads();
+      const int f[4] = {2, 3, 0, 1};
+      const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
+      const double sc[4] = {w, w, wv, wv};
+      r2c_outputs<4>(a, c, f, sc, h);
+    }
     __syncthreads();
-    c2r_fields(a, c, 0, 1);
-    __syncthreads();
-    store_grid(a, c, a.gout[0], 0, a.scale_mode ? ia : 1.0);
-  } else if constexpr (OP == FOP_SYNTH2_GRID) {
-    load_half_z(a, c, a.in[0], 0);
-    load_half_z(a, c, a.in[1], 1);
-    __syncthreads();
-    c2r_fields(a, c, 0, 2);
-    __syncthreads();
-    store_grid(a, c, a.gout[0], 0, ia);
-    store_grid(a, c, a.gout[1], 1, ia);
-  } else if constexpr (OP == FOP_ANALYSIS) {
-    load_grid(a, c, a.gin[0], 0);
-    __syncthreads();
-    const int f[1] = {0};
-    const double sc[1] = {a.wq[j] * a.inv_I};
-    r2c_outputs<1>(a, c, f, sc);
-  } else if constexpr (OP == FOP_VORTDIV) {
-    load_grid(a, c, a.gin[0], 0);
-    load_grid(a, c, a.gin[1], 1);
-    __syncthreads();
-    const double cs = a.coslat[j];
-    pointwise([&](int s, int n) {
-      rd(0, s)[n] *= cs;
-      rd(1, s)[n] *= cs;
-    });
-    __syncthreads();
-    const int f[2] = {0, 1};
-    const double w = a.wsin2[j] * a.inv_I * a.inv_a;
-    const double sc[2] = {w, w};
-    r2c_outputs<2>(a, c, f, sc);
-  } else if constexpr (OP == FOP_CORIOLIS) {
-    // linear_coriolis (dynamics.py:129-135): f*u, f*v, then vortdiv_from_uv
-    load_half_z(a, c, a.in[0], 0);
-    load_half_z(a, c, a.in[1], 1);
-    __syncthreads();
-    c2r_fields(a, c, 0, 2);
-    __syncthreads();
-    const double cs = a.coslat[j], fc = a.fcor[j];
-    pointwise([&](int s, int n) {
-      double *u = rd(0, s), *v = rd(1, s);
-      u[n] = (fc * (u[n] * ia)) * cs;
-      v[n] = (fc * (v[n] * ia)) * cs;
-    });
-    __syncthreads();
-    const int f[2] = {0, 1};
-    const double w = a.wsin2[j] * a.inv_I * a.inv_a;
-    const double sc[2] = {w, w};
-    r2c_outputs<2>(a, c, f, sc);
-  } else if constexpr (OP == FOP_NONLINEAR) {
-    // nonlinear_advection + nonlinear_rest (dynamics.py:142-160)
-    // in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi, 5 Phi', 6 delta (half spectra)
-    for (int f = 0; f < 4; ++f) load_half_z(a, c, a.in[f], f);
-    __syncthreads();
-    c2r_fields(a, c, 0, 4);
-    __syncthreads();
-    pointwise([&](int s, int n) {
-      double *r0 = rd(0, s), *r1 = rd(1, s), *r2 = rd(2, s), *r3 = rd(3, s);
-      const double u = r0[n] * ia, v = r1[n] * ia, gx = r2[n] * ia, gy = r3[n] * ia;
-      r0[n] = u;
-      r1[n] = v;
-      r2[n] = -(u * gx + v * gy);
-      r3[n] = 0.5 * (u * u + v * v);
-    });
-    load_half_z(a, c, a.in[4], 4);
-    __syncthreads();
-    c2r_fields(a, c, 4, 1);
-    __syncthreads();
-    const double cs = a.coslat[j];
-    pointwise([&](int s, int n) {
-      double *r0 = rd(0, s), *r1 = rd(1, s);
-      const double xi = rd(4, s)[n];
-      r0[n] = (xi * r0[n]) * cs;
-      r1[n] = (xi * r1[n]) * cs;
-    });
-    __syncthreads();
-    load_half_z(a, c, a.in[5], 4);
-    load_half_z(a, c, a.in[6], 5);
-    __syncthreads();
-    c2r_fields(a, c, 4, 2);
-    __syncthreads();
-    pointwise([&](int s, int n) { rd(2, s)[n] -= rd(4, s)[n] * rd(5, s)[n]; });
-    __syncthreads();
-    const int f[4] = {2, 3, 0, 1};
-    const double w = a.wq[j] * a.inv_I, wv = a.wsin2[j] * a.inv_I * a.inv_a;
-    const double sc[4] = {w, w, wv, wv};
-    r2c_outputs<4>(a, c, f, sc);
   }
 }
 
@@ -348,7 +377,7 @@ static int launch_op(const FftArgs &a, int smem, cudaStream_t st) {
     SWE_CUDA(cudaFuncSetAttribute(fft_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = smem;
   }
-  dim3 grid(a.J, (a.nslices + a.spb - 1) / a.spb);
+  dim3 grid(a.Jh, (a.nslices + a.spb - 1) / a.spb);
   fft_kernel<OP><<<grid, a.nwarps * 32, smem, st>>>(a);
   SWE_LAUNCH_CHECK();
   return OK;

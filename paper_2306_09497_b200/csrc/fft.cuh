@@ -2,11 +2,13 @@
 //
 // Reference: np.fft.irfft / rfft calls of SphereGrid (spharm.py:241, :257,
 // :267, :325-326) and the grid products of dynamics.py:129-160.  One CTA owns
-// one latitude row j and `spb` consecutive slices; every field of that row is
-// inverse-transformed into shared memory, combined pointwise, and
-// forward-transformed, so grid values never touch HBM.  The real transforms
-// of even length I are done as complex transforms of length N2 = I/2
-// (mixed-radix Stockham, one warp per row).
+// one latitude pair (north row p, south row J-1-p) and a block of slices;
+// every field of both rows is inverse-transformed into shared memory (north =
+// E + O, south = E - O of the parity-split Legendre output), combined
+// pointwise, forward-transformed and folded into F+- = w (f_N +- f_S) for the
+// analysis GEMM, so grid values never touch HBM.  The real transforms of even
+// length I are complex transforms of length N2 = I/2 (in-place mixed-radix
+// Cooley-Tukey or prime-factor).
 #pragma once
 
 #include "common.cuh"
@@ -39,8 +41,10 @@ struct FftArgs {
   int scale_mode;      // FOP_SYNTH_GRID: 0 none, 1 times 1/(a cos)
   const double *coslat, *inv_acos, *fcor, *wq, *wsin2;  // per latitude row [J]
   double inv_I, inv_a;
-  const double *in[FFT_MAXF];   // half spectra [m][J][ld]
-  double *out[FFT_MAXF];        // F spectra    [m][J][ld]
+  int Jh, Jp;                   // latitude pairs (incl. equator), padded pair count
+  const double *phisub;         // [slice] phibar*sqrt2*P_00, subtracted from field 5 (FOP_NONLINEAR)
+  const double *in[FFT_MAXF];   // E/O half spectra      [m][2][Jp][ld]
+  double *out[FFT_MAXF];        // F+/F- analysis inputs [m][2][Jp][ld]
   const double *gin[2];         // grids [slice][J][I]
   double *gout[2];
 };
@@ -51,9 +55,10 @@ __host__ __device__ constexpr int fft_rows_per_slice(int op) {
 }
 bool fft_small_radix(int R);
 
-// "lane = row" variant (fft_lanes.cu): slices per CTA for each op (32 rows / live fields)
+// "lane = row" variant (fft_lanes.cu): slices per CTA for each op
+// (32 rows = fields x 2 hemispheres x slices)
 __host__ __device__ constexpr int fft_lane_slices(int op) {
-  return op == FOP_NONLINEAR ? 4 : ((op == FOP_SYNTH_GRID || op == FOP_ANALYSIS) ? 32 : 16);
+  return op == FOP_NONLINEAR ? 2 : ((op == FOP_SYNTH_GRID || op == FOP_ANALYSIS) ? 16 : 8);
 }
 int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st);
 bool fft_lanes_ok(const FftArgs &a);

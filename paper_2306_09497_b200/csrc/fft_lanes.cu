@@ -1,12 +1,16 @@
 // Longitude FFT stage, "lane = row" variant for small-radix lengths.
 //
-// One CTA owns one latitude row j and up to 32 transform rows (fields x
-// slices).  Shared memory holds X[k][32]: the 32 rows of one frequency/sample
-// index form one 512-byte line, so lane r of every warp works on row r and each
-// butterfly access is a conflict-free full line; all lanes of a warp execute
-// the same butterfly, so twiddles are warp-uniform broadcasts.  Warps split
-// the butterflies of a stage.  Same digit-reversed in-place Cooley-Tukey
-// (DIT inverse / DIF forward) and the same fused grid products as fft.cu.
+// One CTA owns one latitude PAIR p (north row p, south row J-1-p) and S
+// slices; its 32 transform rows are (field, hemisphere, slice), row index
+// (f*2 + h)*S + s.  Shared memory holds X[slot][32]: the 32 rows of one slot
+// form one 512-byte line, lane r works on row r, every butterfly access is a
+// conflict-free full line and all lanes share the butterfly's twiddles.
+// Inputs are the parity-split Legendre outputs E/O ([m][2][Jp][ld]):
+// north = E + O, south = E - O.  Outputs are the folded analysis inputs
+// F+- = w (f_north +- f_south) ([m][2][Jp][ld]); on the equator (J odd) the
+// south row coincides with the north row and F+ = F- = w f_north.
+// Transform algebra (real packing, Cooley-Tukey / prime-factor, slot maps) is
+// shared with fft.cu.
 #include "fft.cuh"
 #include "fft_core.cuh"
 
@@ -61,10 +65,11 @@ SWE_DEV void lane_run_stage(double2 *X, int N2, int Lp, int R, double dir, const
 
 struct LCtx {
   double2 *X;
-  int j, b0, nsl, S, tid, nthr, warp, lane, nw;
+  int p, jn, js, eq, b0, nsl, S, tid, nthr, warp, lane, nw;
 };
 
-// inverse transforms of all 32 rows: pos_z order in, pos_g order out
+SWE_DEV int lrow(const LCtx &c, int f, int h, int s) { return (f * 2 + h) * c.S + s; }
+
 SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
   int Lp = 1;
   for (int s = 0; s < a.nst; ++s) {
@@ -75,7 +80,6 @@ SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
   }
 }
 
-// forward transforms of all 32 rows: pos_g order in, pos_z order out
 SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
   if (a.pfa) {
     int Lp = 1;
@@ -95,46 +99,62 @@ SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
   }
 }
 
-// half spectrum of field f (rows f*S + s) -> Z in digit-reversed order (see fft.cu)
-SWE_DEV void lane_load_half_z(const FftArgs &a, const LCtx &c, const double *src, int f) {
+// Z of one hemisphere row from its half spectrum X (see fft.cu build comment):
+//   Z[k] = (X[k] + conj X[N2-k]) + i w^k (X[k] - conj X[N2-k])
+SWE_DEV void put_z(const FftArgs &a, const LCtx &c, int row, int k, double2 Xk, double2 Xc) {
+  const int N2 = a.N2;
+  if (k == 0) {
+    c.X[__ldg(a.pos_z) * LW + row] = make_double2(Xk.x, Xk.x);
+    return;
+  }
+  const int k2 = N2 - k;
+  const double2 A = make_double2(Xk.x + Xc.x, Xk.y - Xc.y);
+  const double2 D = make_double2(Xk.x - Xc.x, Xk.y + Xc.y);
+  const double2 Bk = cm(D, __ldg(a.twh + k));
+  c.X[__ldg(a.pos_z + k) * LW + row] = make_double2(A.x - Bk.y, A.y + Bk.x);
+  if (k2 != k) {
+    const double2 A2 = make_double2(Xc.x + Xk.x, Xc.y - Xk.y);
+    const double2 D2 = make_double2(Xc.x - Xk.x, Xc.y + Xk.y);
+    const double2 B2 = cm(D2, __ldg(a.twh + k2));
+    c.X[__ldg(a.pos_z + k2) * LW + row] = make_double2(A2.x - B2.y, A2.y + B2.x);
+  }
+}
+
+// field f: E/O half spectra [m][2][Jp][ld] of pair p -> Z of its north and south rows.
+// sub (nullable, per slice) is subtracted from E at m = 0 (phi_prime, dynamics.py:52-56).
+SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, const double *src, int f,
+                          const double *sub) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1, S = c.S;
-  const double2 *base = reinterpret_cast<const double2 *>(src + (size_t)c.j * a.ld) + c.b0;
-  const size_t mstride = (size_t)a.J * a.ld / 2;
+  const size_t eo = (size_t)a.Jp * a.ld / 2;  // E -> O offset (double2)
+  const double2 *base = reinterpret_cast<const double2 *>(src + (size_t)c.p * a.ld) + c.b0;
+  const size_t mstride = 2 * eo;
   const int total = npair * S;
-  constexpr int U = 4;  // items per thread in flight (8 independent global loads)
+  constexpr int U = 2;
   for (int i0 = c.tid; i0 < total; i0 += U * c.nthr) {
-    double2 xk[U], xc[U];
+    double2 e[U], o[U], e2[U], o2[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
       const int k = idx / S, s = idx - k * S;
       const bool ok = idx < total && s < c.nsl;
       const int k2 = k == 0 ? N2 : N2 - k;
-      xk[u] = (ok && k <= M) ? __ldg(base + (size_t)k * mstride + s) : make_double2(0.0, 0.0);
-      xc[u] = (ok && k2 <= M) ? __ldg(base + (size_t)k2 * mstride + s) : make_double2(0.0, 0.0);
+      const double2 z = make_double2(0.0, 0.0);
+      const double2 *pk = base + (size_t)k * mstride + s, *pk2 = base + (size_t)k2 * mstride + s;
+      e[u] = (ok && k <= M) ? __ldg(pk) : z;
+      o[u] = (ok && k <= M) ? __ldg(pk + eo) : z;
+      e2[u] = (ok && k2 <= M) ? __ldg(pk2) : z;
+      o2[u] = (ok && k2 <= M) ? __ldg(pk2 + eo) : z;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
       const int k = idx / S, s = idx - k * S;
       if (idx >= total || s >= c.nsl) continue;
-      const int row = f * S + s;
-      const double2 Xk = xk[u], Xc = xc[u];
-      if (k == 0) {
-        c.X[__ldg(a.pos_z) * LW + row] = make_double2(Xk.x, Xk.x);
-        continue;
-      }
-      const int k2 = N2 - k;
-      const double2 A = make_double2(Xk.x + Xc.x, Xk.y - Xc.y);
-      const double2 D = make_double2(Xk.x - Xc.x, Xk.y + Xc.y);
-      const double2 Bk = cm(D, __ldg(a.twh + k));
-      c.X[__ldg(a.pos_z + k) * LW + row] = make_double2(A.x - Bk.y, A.y + Bk.x);
-      if (k2 != k) {
-        const double2 A2 = make_double2(Xc.x + Xk.x, Xc.y - Xk.y);
-        const double2 D2 = make_double2(Xc.x - Xk.x, Xc.y + Xk.y);
-        const double2 B2 = cm(D2, __ldg(a.twh + k2));
-        c.X[__ldg(a.pos_z + k2) * LW + row] = make_double2(A2.x - B2.y, A2.y + B2.x);
-      }
+      if (sub != nullptr && k == 0) e[u].x -= sub[c.b0 + s];
+      put_z(a, c, lrow(c, f, 0, s), k, make_double2(e[u].x + o[u].x, e[u].y + o[u].y),
+            make_double2(e2[u].x + o2[u].x, e2[u].y + o2[u].y));
+      put_z(a, c, lrow(c, f, 1, s), k, make_double2(e[u].x - o[u].x, e[u].y - o[u].y),
+            make_double2(e2[u].x - o2[u].x, e2[u].y - o2[u].y));
     }
   }
 }
@@ -144,44 +164,63 @@ SWE_DEV double &gval(const FftArgs &a, const LCtx &c, int n, int row) {
   double *p = reinterpret_cast<double *>(c.X + __ldg(a.pos_g + (n >> 1)) * LW + row);
   return p[n & 1];
 }
-// component h (0/1) of transform slot p of row r (pointwise ops need no map)
 SWE_DEV double &gslot(const LCtx &c, int p, int h, int row) {
   return reinterpret_cast<double *>(c.X + p * LW + row)[h];
 }
 
 SWE_DEV void lane_load_grid(const FftArgs &a, const LCtx &c, const double *src, int f) {
-  for (int s = 0; s < c.nsl; ++s) {
-    const double *g = src + ((size_t)(c.b0 + s) * a.J + c.j) * a.I;
-    for (int n = c.tid; n < a.I; n += c.nthr) gval(a, c, n, f * c.S + s) = __ldg(g + n);
+  for (int h = 0; h < 2; ++h) {
+    const int j = (h && !c.eq) ? c.js : c.jn;
+    for (int s = 0; s < c.nsl; ++s) {
+      const double *g = src + ((size_t)(c.b0 + s) * a.J + j) * a.I;
+      for (int n = c.tid; n < a.I; n += c.nthr) gval(a, c, n, lrow(c, f, h, s)) = __ldg(g + n);
+    }
   }
 }
 
 SWE_DEV void lane_store_grid(const FftArgs &a, const LCtx &c, double *dst, int f, double scale) {
-  for (int s = 0; s < c.nsl; ++s) {
-    double *g = dst + ((size_t)(c.b0 + s) * a.J + c.j) * a.I;
-    for (int n = c.tid; n < a.I; n += c.nthr) g[n] = gval(a, c, n, f * c.S + s) * scale;
+  for (int h = 0; h < 2 - c.eq; ++h) {
+    const int j = h ? c.js : c.jn;
+    for (int s = 0; s < c.nsl; ++s) {
+      double *g = dst + ((size_t)(c.b0 + s) * a.J + j) * a.I;
+      for (int n = c.tid; n < a.I; n += c.nthr) g[n] = gval(a, c, n, lrow(c, f, h, s)) * scale;
+    }
   }
 }
 
-// fm[k] * scale (k = 0..M) of rows orow*S + s -> a.out[o]  (see fft.cu r2c_outputs)
-SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, int orow, int o, double scale) {
-  const int N2 = a.N2, M = a.M, S = c.S;
+// fm[k] (k = 0..M) of rows (f, h, s): fm = (Ge + w^{-k} Go) / I, see fft.cu;
+// F+ = scale (fm_N + fm_S), F- = scale (fm_N - fm_S)  ->  a.out[o] [m][2][Jp][ld]
+SWE_DEV double2 row_fm(const FftArgs &a, const LCtx &c, int row, int k) {
+  const int N2 = a.N2;
+  const double2 zk = c.X[__ldg(a.pos_z + k) * LW + row];
+  const double2 z2 = c.X[__ldg(a.pos_z + (k == 0 ? 0 : N2 - k)) * LW + row];
+  const double2 Sg = make_double2(zk.x + z2.x, zk.y - z2.y);
+  const double2 D = make_double2(zk.y + z2.y, -(zk.x - z2.x));
+  double2 w = __ldg(a.twh + k);
+  w.y = -w.y;
+  const double2 t = cm(w, D);
+  return make_double2(Sg.x + t.x, Sg.y + t.y);  // 2 * I * fm
+}
+
+SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, int f, int o, double scale) {
+  const int M = a.M, S = c.S;
   const double h = 0.5 * scale;
-  double2 *dst = reinterpret_cast<double2 *>(a.out[o] + (size_t)c.j * a.ld) + c.b0;
-  const size_t mstride = (size_t)a.J * a.ld / 2;
+  const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
+  double2 *dst = reinterpret_cast<double2 *>(a.out[o] + (size_t)c.p * a.ld) + c.b0;
   for (int idx = c.tid; idx < (M + 1) * S; idx += c.nthr) {
     const int k = idx / S, s = idx - k * S;
     if (s >= c.nsl) continue;
-    const int row = orow * S + s;
-    const double2 zk = c.X[__ldg(a.pos_z + k) * LW + row];
-    const double2 z2 = c.X[__ldg(a.pos_z + (k == 0 ? 0 : N2 - k)) * LW + row];
-    const double2 zc = make_double2(z2.x, -z2.y);
-    const double2 Sg = make_double2(zk.x + zc.x, zk.y + zc.y);
-    const double2 D = make_double2(zk.y - zc.y, -(zk.x - zc.x));
-    double2 w = __ldg(a.twh + k);
-    w.y = -w.y;
-    const double2 t = cm(w, D);
-    dst[(size_t)k * mstride + s] = make_double2((Sg.x + t.x) * h, (Sg.y + t.y) * h);
+    const double2 fn = row_fm(a, c, lrow(c, f, 0, s), k);
+    double2 *d = dst + (size_t)k * 2 * pm + s;
+    if (c.eq) {
+      const double2 v = make_double2(fn.x * h, fn.y * h);
+      d[0] = v;
+      d[pm] = v;
+    } else {
+      const double2 fs = row_fm(a, c, lrow(c, f, 1, s), k);
+      d[0] = make_double2((fn.x + fs.x) * h, (fn.y + fs.y) * h);
+      d[pm] = make_double2((fn.x - fs.x) * h, (fn.y - fs.y) * h);
+    }
   }
 }
 
@@ -193,7 +232,10 @@ __global__ void __launch_bounds__(256) fft_lanes_kernel(const __grid_constant__ 
   LCtx c;
   c.X = reinterpret_cast<double2 *>(smem_raw);
   c.S = fft_lane_slices(OP);
-  c.j = blockIdx.x;
+  c.p = blockIdx.x;
+  c.jn = c.p;
+  c.js = a.J - 1 - c.p;
+  c.eq = c.js == c.jn;
   c.b0 = blockIdx.y * c.S;
   c.nsl = min(c.S, a.nslices - c.b0);
   c.tid = threadIdx.x;
@@ -201,12 +243,12 @@ __global__ void __launch_bounds__(256) fft_lanes_kernel(const __grid_constant__ 
   c.warp = threadIdx.x >> 5;
   c.lane = threadIdx.x & 31;
   c.nw = blockDim.x >> 5;
-  const int j = c.j, I = a.I, S = c.S;
-  const double ia = a.inv_acos[j];
+  const int p = c.p, I = a.I, S = c.S;
+  const double ia = a.inv_acos[p];
 
   if constexpr (OP == FOP_SYNTH_GRID || OP == FOP_SYNTH2_GRID) {
     constexpr int NF = OP == FOP_SYNTH_GRID ? 1 : 2;
-    for (int f = 0; f < NF; ++f) lane_load_half_z(a, c, a.in[f], f);
+    for (int f = 0; f < NF; ++f) lane_load_eo(a, c, a.in[f], f, nullptr);
     __syncthreads();
     lane_ifft(a, c);
     const double sc = (OP == FOP_SYNTH2_GRID || a.scale_mode) ? ia : 1.0;
@@ -216,7 +258,7 @@ __global__ void __launch_bounds__(256) fft_lanes_kernel(const __grid_constant__ 
     for (int f = 0; f < NF; ++f) lane_load_grid(a, c, a.gin[f], f);
     __syncthreads();
     if constexpr (OP == FOP_VORTDIV) {
-      const double cs = a.coslat[j];
+      const double cs = a.coslat[p];
       for (int idx = c.tid; idx < a.N2 * LW; idx += c.nthr) {
         c.X[idx].x *= cs;
         c.X[idx].y *= cs;
@@ -224,45 +266,47 @@ __global__ void __launch_bounds__(256) fft_lanes_kernel(const __grid_constant__ 
       __syncthreads();
     }
     lane_fft(a, c);
-    const double w = OP == FOP_ANALYSIS ? a.wq[j] * a.inv_I : a.wsin2[j] * a.inv_I * a.inv_a;
+    const double w = OP == FOP_ANALYSIS ? a.wq[p] * a.inv_I : a.wsin2[p] * a.inv_I * a.inv_a;
     for (int f = 0; f < NF; ++f) lane_extract(a, c, f, f, w);
   } else if constexpr (OP == FOP_CORIOLIS) {
-    // linear_coriolis (dynamics.py:129-135): f u, f v -> vortdiv_from_uv
-    lane_load_half_z(a, c, a.in[0], 0);
-    lane_load_half_z(a, c, a.in[1], 1);
+    // linear_coriolis (dynamics.py:129-135): f u, f v -> vortdiv_from_uv; f = -f on the south row
+    lane_load_eo(a, c, a.in[0], 0, nullptr);
+    lane_load_eo(a, c, a.in[1], 1, nullptr);
     __syncthreads();
     lane_ifft(a, c);
-    const double cs = a.coslat[j], fc = a.fcor[j];
+    const double cs = a.coslat[p], fc = a.fcor[p];
     for (int idx = c.tid; idx < a.N2 * LW; idx += c.nthr) {
+      const int row = idx & (LW - 1);
+      const double fr = ((row / S) & 1) ? -fc : fc;
       const double2 z = c.X[idx];
-      c.X[idx] = make_double2((fc * (z.x * ia)) * cs, (fc * (z.y * ia)) * cs);
+      c.X[idx] = make_double2((fr * (z.x * ia)) * cs, (fr * (z.y * ia)) * cs);
     }
     __syncthreads();
     lane_fft(a, c);
-    const double w = a.wsin2[j] * a.inv_I * a.inv_a;
+    const double w = a.wsin2[p] * a.inv_I * a.inv_a;
     lane_extract(a, c, 0, 0, w);
     lane_extract(a, c, 1, 1, w);
   } else if constexpr (OP == FOP_NONLINEAR) {
-    // nonlinear_advection + nonlinear_rest (dynamics.py:142-160); rows f*S + s,
-    // in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi, 5 Phi', 6 delta
-    for (int f = 0; f < 7; ++f) lane_load_half_z(a, c, a.in[f], f);
+    // nonlinear_advection + nonlinear_rest (dynamics.py:142-160)
+    // in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi, 5 Phi (phi_prime applied here), 6 delta
+    for (int f = 0; f < 7; ++f) lane_load_eo(a, c, a.in[f], f, f == 5 ? a.phisub : nullptr);
     __syncthreads();
     lane_ifft(a, c);
-    const double cs = a.coslat[j];
-    for (int idx = c.tid; idx < I * S; idx += c.nthr) {
-      const int n = idx / S, s = idx - n * S, p = n >> 1, h = n & 1;
-      const double u = gslot(c, p, h, s) * ia, v = gslot(c, p, h, S + s) * ia;
-      const double gx = gslot(c, p, h, 2 * S + s) * ia, gy = gslot(c, p, h, 3 * S + s) * ia;
-      const double xi = gslot(c, p, h, 4 * S + s), ph = gslot(c, p, h, 5 * S + s);
-      const double de = gslot(c, p, h, 6 * S + s);
-      gslot(c, p, h, s) = -(u * gx + v * gy) - ph * de;   // -(V.grad Phi) - Phi' delta
-      gslot(c, p, h, S + s) = 0.5 * (u * u + v * v);     // kinetic energy
-      gslot(c, p, h, 2 * S + s) = (xi * u) * cs;          // (xi u) cos
-      gslot(c, p, h, 3 * S + s) = (xi * v) * cs;          // (xi v) cos
+    const double cs = a.coslat[p];
+    for (int idx = c.tid; idx < I * 2 * S; idx += c.nthr) {
+      const int n = idx / (2 * S), hs = idx - n * 2 * S, pp = n >> 1, hh = n & 1;
+      const int h = hs / S, s = hs - h * S;
+      auto R = [&](int f) -> double & { return gslot(c, pp, hh, lrow(c, f, h, s)); };
+      const double u = R(0) * ia, v = R(1) * ia, gx = R(2) * ia, gy = R(3) * ia;
+      const double xi = R(4), ph = R(5), de = R(6);
+      R(0) = -(u * gx + v * gy) - ph * de;   // -(V.grad Phi) - Phi' delta
+      R(1) = 0.5 * (u * u + v * v);          // kinetic energy
+      R(2) = (xi * u) * cs;                  // (xi u) cos
+      R(3) = (xi * v) * cs;                  // (xi v) cos
     }
     __syncthreads();
     lane_fft(a, c);
-    const double w = a.wq[j] * a.inv_I, wv = a.wsin2[j] * a.inv_I * a.inv_a;
+    const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
     lane_extract(a, c, 0, 0, w);
     lane_extract(a, c, 1, 1, w);
     lane_extract(a, c, 2, 2, wv);
@@ -279,7 +323,7 @@ static int launch_lanes(const FftArgs &a, int smem, int nthreads, cudaStream_t s
     attr = smem;
   }
   const int S = fft_lane_slices(OP);
-  dim3 grid(a.J, (a.nslices + S - 1) / S);
+  dim3 grid(a.Jh, (a.nslices + S - 1) / S);
   fft_lanes_kernel<OP><<<grid, nthreads, smem, st>>>(a);
   SWE_LAUNCH_CHECK();
   return OK;

@@ -124,23 +124,20 @@ __global__ void __launch_bounds__(128) leg_synth_kernel(const __grid_constant__ 
   }
   cp_async_wait<0>();
 
-  // epilogue: north = E + O, south = E - O, layout [m][j][ld]
-  const int J = args.J, Jh = args.Jh;
-  double *dst = o.dst + (size_t)m * J * ld;
+  // epilogue: E and O planes of [m][2][Jp][ld] (the FFT stage forms north = E + O,
+  // south = E - O)
+  const int Jh = args.Jh;
+  double *dE = o.dst + (size_t)m * 2 * Jp * ld, *dO = dE + (size_t)Jp * ld;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int p = p0 + wr * 32 + i * 8 + g;
     if (p >= Jh) continue;
-    const int js = J - 1 - p;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = c0 + wc * 32 + j * 8 + 2 * t;
       if (col >= ld) continue;
-      const double er = accE[i][j][0], ei = accE[i][j][1];
-      const double orr = accO[i][j][0], oi = accO[i][j][1];
-      *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) = make_double2(er + orr, ei + oi);
-      if (js != p)
-        *reinterpret_cast<double2 *>(dst + (size_t)js * ld + col) = make_double2(er - orr, ei - oi);
+      *reinterpret_cast<double2 *>(dE + (size_t)p * ld + col) = make_double2(accE[i][j][0], accE[i][j][1]);
+      *reinterpret_cast<double2 *>(dO + (size_t)p * ld + col) = make_double2(accO[i][j][0], accO[i][j][1]);
     }
   }
 }
@@ -169,7 +166,7 @@ __global__ void __launch_bounds__(128) leg_anal_kernel(const __grid_constant__ L
   const LegOut &o = args.out[blockIdx.z];
   const int2 item = args.items[blockIdx.x];
   const int m = item.x, r0 = item.y * AN_BR, c0 = blockIdx.y * AN_BN;
-  const int M = args.M, J = args.J, Jh = args.Jh, Jp = args.Jp, ld = args.ld;
+  const int M = args.M, Jh = args.Jh, Jp = args.Jp, ld = args.ld;
   const int km = M + 1 - m, ne = (km + 1) >> 1, no = km >> 1;
   const int off = args.offsets[m];
   const int nch_t = Jp / AN_KP;
@@ -188,16 +185,16 @@ __global__ void __launch_bounds__(128) leg_anal_kernel(const __grid_constant__ L
       const size_t row = (size_t)off + (par ? ne : 0) + tt;
       cp_async16(&sm.A[stage][r][cc], T.tab + (v ? row * Jp + q0 + cc : 0), v);
     }
-    // north rows j = p, south rows j = J-1-p (none for the equator / padding)
-    const double *base = T.src + (size_t)m * J * ld;
+    // folded rows F+ (hs 0) and F- (hs 1) of [m][2][Jp][ld], pairs q0..q0+15
+    const double *base = T.src + (size_t)m * 2 * Jp * ld;
     for (int i = tid; i < 2 * AN_KP * (AN_BN / 2); i += 128) {
       const int hs = i / (AN_KP * (AN_BN / 2));
       const int rem = i - hs * (AN_KP * (AN_BN / 2));
       const int pr = rem / (AN_BN / 2), cc = (rem - pr * (AN_BN / 2)) * 2;
       const int p = q0 + pr;
-      const int jrow = hs ? (J - 1 - p) : p;
-      const bool v = (p < Jh) && (c0 + cc < ld) && (hs == 0 || jrow != p);
-      cp_async16(&sm.F[stage][hs][pr][cc], base + (v ? (size_t)jrow * ld + c0 + cc : 0), v);
+      const bool v = (p < Jh) && (c0 + cc < ld);
+      cp_async16(&sm.F[stage][hs][pr][cc],
+                 base + (v ? ((size_t)hs * Jp + p) * ld + c0 + cc : 0), v);
     }
   };
 
@@ -216,14 +213,6 @@ __global__ void __launch_bounds__(128) leg_anal_kernel(const __grid_constant__ L
     cp_async_wait<AN_STAGES - 2>();
     __syncthreads();
     const int st = c % AN_STAGES;
-    // fold: F+ = N + S, F- = N - S (in place)
-    for (int i = tid; i < AN_KP * AN_BN; i += 128) {
-      const int pr = i / AN_BN, cc = i - pr * AN_BN;
-      const double n = sm.F[st][0][pr][cc], s = sm.F[st][1][pr][cc];
-      sm.F[st][0][pr][cc] = n + s;
-      sm.F[st][1][pr][cc] = n - s;
-    }
-    __syncthreads();
     {
       const int cn = c + AN_STAGES - 1;
       if (cn < nch) load_chunk(cn, cn % AN_STAGES);

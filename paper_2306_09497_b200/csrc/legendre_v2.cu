@@ -141,41 +141,18 @@ __global__ void __launch_bounds__(BN * 2) leg_synth_v2(const __grid_constant__ L
   }
   cp_async_wait<0>();
 
-  // epilogue: O warps park accumulators in shared memory, E warps combine:
-  // north = E + O, south = E - O  (staging reused: [BN/32 tiles][4][8][32][2])
-  __syncthreads();
-  double *park = reinterpret_cast<double *>(smem_raw);
-  const int slot = wph * (BN / 64) + wch;
-  if (wpar == 1) {
+  // epilogue: each warp stores its parity plane of [m][2][Jp][ld] (E or O);
+  // the FFT stage forms north = E + O, south = E - O
+  double *dst = o.dst + ((size_t)m * 2 + wpar) * Jp * ld;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
+    const int p = pw0 + i * 8 + g;
+    if (p >= Jh) continue;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        double *q = park + ((((size_t)slot * 4 + i) * 8 + j) * 32 + lane) * 2;
-        q[0] = acc[i][j][0];
-        q[1] = acc[i][j][1];
-      }
-  }
-  __syncthreads();
-  if (wpar == 0) {
-    const int J = args.J;
-    double *dst = o.dst + (size_t)m * J * ld;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int p = pw0 + i * 8 + g;
-      if (p >= Jh) continue;
-      const int js = J - 1 - p;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int col = c0 + wch * 64 + j * 8 + 2 * t;
-        if (col >= ld) continue;
-        const double *q = park + ((((size_t)slot * 4 + i) * 8 + j) * 32 + lane) * 2;
-        const double er = acc[i][j][0], ei = acc[i][j][1], orr = q[0], oi = q[1];
-        *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) = make_double2(er + orr, ei + oi);
-        if (js != p)
-          *reinterpret_cast<double2 *>(dst + (size_t)js * ld + col) =
-              make_double2(er - orr, ei - oi);
-      }
+    for (int j = 0; j < 8; ++j) {
+      const int col = c0 + wch * 64 + j * 8 + 2 * t;
+      if (col >= ld) continue;
+      *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
   }
 }
@@ -199,7 +176,7 @@ __global__ void __launch_bounds__(BN * 2) leg_anal_v2(const __grid_constant__ Le
   const LegOut &o = args.out[blockIdx.z];
   const int2 item = args.items[blockIdx.x];
   const int m = item.x, r0 = item.y * VA_BR, c0 = blockIdx.y * BN;
-  const int M = args.M, J = args.J, Jh = args.Jh, Jp = args.Jp, ld = args.ld;
+  const int M = args.M, Jh = args.Jh, Jp = args.Jp, ld = args.ld;
   const int km = M + 1 - m, ne = (km + 1) >> 1, no = km >> 1;
   const int off = args.offsets[m];
   const int nch_t = Jp / VA_KP;
@@ -221,15 +198,15 @@ __global__ void __launch_bounds__(BN * 2) leg_anal_v2(const __grid_constant__ Le
       const size_t row = (size_t)off + (par ? ne : 0) + tt;
       cp_async16(&sm.A[stage][r][cc], T.tab + (v ? row * Jp + q0 + cc : 0), v);
     }
-    // north rows p and south rows J-1-p: 2 x 16 x BN columns
-    const double *base = T.src + (size_t)m * J * ld;
+    // folded rows F+ (hs 0) and F- (hs 1) of [m][2][Jp][ld]: 2 x 16 x BN columns
+    const double *base = T.src + (size_t)m * 2 * Jp * ld;
 #pragma unroll
     for (int i = tid; i < 16 * BN; i += NT) {
       const int rr = i / (BN / 2), cc = (i % (BN / 2)) * 2;
       const int hs = rr >> 4, pr = rr & 15, p = q0 + pr;
-      const int jrow = hs ? (J - 1 - p) : p;
-      const bool v = (p < Jh) && (c0 + cc < ld) && (hs == 0 || jrow != p);
-      cp_async16(&sm.F[stage][hs][pr][cc], base + (v ? (size_t)jrow * ld + c0 + cc : 0), v);
+      const bool v = (p < Jh) && (c0 + cc < ld);
+      cp_async16(&sm.F[stage][hs][pr][cc],
+                 base + (v ? ((size_t)hs * Jp + p) * ld + c0 + cc : 0), v);
     }
   };
 
@@ -248,14 +225,6 @@ __global__ void __launch_bounds__(BN * 2) leg_anal_v2(const __grid_constant__ Le
     cp_async_wait<VA_ST - 2>();
     __syncthreads();
     const int st = c % VA_ST;
-    // fold: F+ = N + S, F- = N - S (in place)
-    for (int i = tid; i < VA_KP * BN; i += NT) {
-      const int pr = i / BN, cc = i % BN;
-      const double n = sm.F[st][0][pr][cc], s = sm.F[st][1][pr][cc];
-      sm.F[st][0][pr][cc] = n + s;
-      sm.F[st][1][pr][cc] = n - s;
-    }
-    __syncthreads();
     {
       const int cn = c + VA_ST - 1;
       if (cn < nch) load_chunk(cn, cn % VA_ST);

@@ -364,7 +364,7 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaDeviceSynchronize());
   work_free(w);
   const size_t ld = 2 * (size_t)B;
-  const size_t spec = (size_t)pl->K * ld, half = (size_t)(pl->M + 1) * pl->J * ld;
+  const size_t spec = (size_t)pl->K * ld, half = (size_t)(pl->M + 1) * 2 * pl->Jp * ld;
   SWE_CUDA(cudaMalloc(&w.spec, NSPEC * spec * sizeof(double)));
   SWE_CUDA(cudaMalloc(&w.half, NHALF * half * sizeof(double)));
   SWE_CUDA(cudaMalloc(&w.fspec, NF * half * sizeof(double)));

@@ -27,7 +27,7 @@ struct Work {
   int *iters = nullptr;     // [cap]
   int *counter = nullptr;   // device counter (active slices)
   int *h_counter = nullptr; // pinned host mirror
-  double *phi0 = nullptr;   // [cap] phibar*sqrt(2)
+  double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
 };
 

@@ -247,7 +247,9 @@ __global__ void k_phi0(int B, const double *phibar, double *pb, double *phi0) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) {
     pb[b] = phibar[b];
-    phi0[b] = phibar[b] * 1.4142135623730951;  // SQRT2 (dynamics.py:20, :52-56)
+    // phi_prime subtracts phibar*SQRT2 from mode (0,0) (dynamics.py:20, :52-56);
+    // its synthesis is that times P_00 = 1/sqrt(2) at every latitude
+    phi0[b] = (phibar[b] * 1.4142135623730951) * (1.0 / sqrt(2.0));
   }
 }
 

@@ -75,8 +75,10 @@ struct Run {
   size_t ld;
   cudaStream_t st;
   double *spec(int i) const { return pl->ws.spec + (size_t)i * pl->K * ld; }
-  double *half(int i) const { return pl->ws.half + (size_t)i * (pl->M + 1) * pl->J * ld; }
-  double *fsp(int i) const { return pl->ws.fspec + (size_t)i * (pl->M + 1) * pl->J * ld; }
+  // E/O half spectra and F+/F- analysis inputs: [m][2][Jp][ld] each
+  size_t plane() const { return (size_t)(pl->M + 1) * 2 * pl->Jp * ld; }
+  double *half(int i) const { return pl->ws.half + (size_t)i * plane(); }
+  double *fsp(int i) const { return pl->ws.fspec + (size_t)i * plane(); }
 };
 
 LegArgs leg_args(const Run &r) {
@@ -188,6 +190,9 @@ int fft(const Run &r, int op, FftArgs &a) {
   a.wsin2 = pl->wsin2;
   a.inv_I = 1.0 / pl->I;
   a.inv_a = 1.0 / pl->a;
+  a.Jh = pl->Jh;
+  a.Jp = pl->Jp;
+  a.phisub = pl->ws.phi0;
   static const int io[6][4] = {{1, 0, 0, 1}, {2, 0, 0, 2}, {0, 1, 1, 0},
                                {0, 2, 2, 0}, {2, 2, 0, 0}, {7, 4, 0, 0}};
   const double spec_row = 16.0 * (pl->M + 1) * pl->J * r.B, grid_row = 8.0 * pl->I * pl->J * r.B;
@@ -268,7 +273,7 @@ int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], d
     set_out(a, 2, r.half(2), term(P, U[0], 1.0, 1), nullptr, H);          // d_lambda Phi
     set_out(a, 3, r.half(3), term(H, U[0], 1.0), nullptr, H);             // H Phi
     set_out(a, 4, r.half(4), term(P, U[1]), nullptr, H);                  // xi
-    set_out(a, 5, r.half(5), term(P, U[0], 1.0, 0, nullptr, pl->ws.phi0), nullptr, H);  // Phi'
+    set_out(a, 5, r.half(5), term(P, U[0]), nullptr, H);  // Phi (phi_prime shift in the FFT)
     set_out(a, 6, r.half(6), term(P, U[2]), nullptr, H);                  // delta
     if ((rc = synth(r, a))) return rc;
   }
@@ -508,7 +513,7 @@ long long swe_plan_bytes(const swe_plan *pl) {
   if (!pl) return 0;
   const size_t ld = 2 * (size_t)pl->ws.cap;
   return (long long)(pl->table_bytes + 8 * ld * ((size_t)NSPEC * pl->K +
-                                               (size_t)(NHALF + NF) * (pl->M + 1) * pl->J));
+                                               (size_t)(NHALF + NF) * (pl->M + 1) * 2 * pl->Jp));
 }
 
 int swe_synthesis(swe_plan *pl, const double *spec, double *grid, int batch, void *stream) {
