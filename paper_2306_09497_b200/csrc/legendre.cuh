@@ -52,6 +52,11 @@ int leg_anal_launch(const LegArgs &a, int ncoltiles, cudaStream_t st);
 int leg_synth_v2_launch(const LegArgs &a, int bn, cudaStream_t st);
 int leg_anal_v2_launch(const LegArgs &a, int bn, cudaStream_t st);
 constexpr int V2_ABR = 32;  // analysis modes per parity per CTA
+// warp-specialised persistent variants (legendre_v3.cu): TMA bulk-copy producer warp,
+// 8 DMMA consumer warps, 128-column tiles, one CTA per SM
+constexpr int V3_ABR = 32;  // v3 analysis modes per parity per work unit
+int leg_synth_v3_launch(const LegArgs &a, cudaStream_t st);
+int leg_anal_v3_launch(const LegArgs &a, cudaStream_t st);
 
 constexpr int SY_BM = 64;   // latitude pairs per CTA
 constexpr int SY_BN = 64;   // real columns per CTA

@@ -1,0 +1,399 @@
+// Legendre GEMMs, warp-specialised persistent variant (the hot path for
+// batches of >= 32 slices).
+//
+// Same contraction as legendre.cu / legendre_v2.cu.  Structure for the sm_100a
+// DMMA issue model (each DMMA.8x8x4 holds its warp 16 cycles; 1 DMMA per 16
+// cycles per SM sub-partition saturates the FP64 tensor pipe):
+//   * warp 0 is the producer: its lanes stream table rows and spectral rows
+//     into shared memory with TMA bulk copies (cp.async.bulk ... complete_tx)
+//     and arrive on a per-stage "full" mbarrier; rows are padded in shared
+//     memory so fragment loads are bank-conflict free;
+//   * 8 consumer warps only wait on "full", load fragments and issue DMMAs,
+//     then arrive on the stage's "empty" mbarrier (no CTA-wide barriers);
+//   * the grid is persistent (one CTA per SM); work units (order m, row tile,
+//     column tile, output) are strided over CTAs heaviest first, and the
+//     producer runs ahead into the next unit while consumers store results.
+// Synthesis: CTA tile 64 latitude pairs x BN columns, consumer warp = one
+//   parity class (E/O) x 32 pairs x 64 columns, 16 modes per parity per stage.
+// Analysis: CTA tile 64 even + 64 odd modes x BN columns, consumer warp = one
+//   parity x 32 modes x 64 columns, 16 latitude pairs per stage; it reads the
+//   folded F+/F- rows written by the FFT stage.
+#include "legendre.cuh"
+
+namespace swe {
+
+namespace {
+
+// 3 warpgroups: warpgroup 0 = producer (warp 0; warps 1-3 exit), warpgroups 1-2 =
+// 8 consumer warps.  setmaxnreg moves registers from the producer warpgroup to the
+// consumers (compiled budget 65536/384 = 168 per thread -> 56 / 224).
+constexpr int V3_BN = 128, V3_NC = 8, V3_NT = 384, V3_CW0 = 4;
+constexpr int S3_KT = 16, S3_NS = 4, S3_LDA = 64 + 4, S3_LDB = V3_BN + 4;
+constexpr int A3_KP = 16, A3_NS = 4, A3_LDA = A3_KP + 4, A3_LDB = V3_BN + 4;
+constexpr int A3_BR = V3_ABR;  // analysis modes per parity per unit
+constexpr int A3_RW = A3_BR / 2, A3_FR = A3_RW / 8;  // rows / 8-row fragments per consumer warp
+
+struct Synth3Stage {
+  double A[2 * S3_KT][S3_LDA];
+  double B[2 * S3_KT][S3_LDB];
+  double S[2 * S3_KT];
+};
+struct Synth3Smem {
+  Synth3Stage st[S3_NS];
+  unsigned long long full[S3_NS], empty[S3_NS];
+};
+struct Anal3Stage {
+  double A[2 * A3_BR][A3_LDA];
+  double F[2][A3_KP][A3_LDB];
+};
+struct Anal3Smem {
+  Anal3Stage st[A3_NS];
+  unsigned long long full[A3_NS], empty[A3_NS];
+};
+
+SWE_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+SWE_DEV void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+SWE_DEV void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+SWE_DEV void mbar_arrive_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+SWE_DEV void mbar_wait(unsigned long long *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+SWE_DEV void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async copies have landed
+SWE_DEV void cp_async_arrive(unsigned long long *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on `bar` in bytes
+SWE_DEV void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+SWE_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory"); }
+SWE_DEV void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory"); }
+
+SWE_DEV double flip_sign(double x, unsigned long long mask) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)mask);
+}
+
+struct Unit {
+  int m, tile, c0, out;
+};
+SWE_DEV Unit decode(const LegArgs &a, int u, int ncol, int tile_w) {
+  Unit x;
+  x.out = u % a.nout;
+  const int r = u / a.nout;
+  const int col = r % ncol;
+  const int2 it = a.items[r / ncol];
+  x.m = it.x;
+  x.tile = it.y * tile_w;
+  x.c0 = col * V3_BN;
+  return x;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__ LegArgs args) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Synth3Smem &sm = *reinterpret_cast<Synth3Smem *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int M = args.M, Jp = args.Jp, ld = args.ld, Jh = args.Jh;
+  const int ncol = (ld + V3_BN - 1) / V3_BN;
+  const int nunits = args.nitems * ncol * args.nout;
+  if (tid == 0) {
+    for (int s = 0; s < S3_NS; ++s) {
+      mbar_init(&sm.full[s], 32);
+      mbar_init(&sm.empty[s], V3_NC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp < V3_CW0) {
+    // ------------------------------------------------------------ producer
+    regs_dec();
+    if (warp != 0) return;
+    int it = 0;
+    const int r = lane, par = r >> 4;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const Unit x = decode(args, u, ncol, 64);
+      const LegOut &o = args.out[x.out];
+      const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
+      const int off = args.offsets[x.m];
+      const int nch_t = (ne + S3_KT - 1) / S3_KT;
+      const unsigned abytes = (unsigned)min(64, Jp - x.tile) * 8u;
+      const int bcols = min(V3_BN, ld - x.c0);
+      for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+        const int s = it % S3_NS;
+        mbar_wait(&sm.empty[s], ((it / S3_NS) & 1) ^ 1);
+        const int term = c / nch_t, tt = (c - term * nch_t) * S3_KT + (r & 15);
+        const LegTerm &T = o.t[term];
+        Synth3Stage &S = sm.st[s];
+        const bool v = tt < (par ? no : ne);
+        const int k = off + (par ? ne : 0) + tt;
+        S.S[r] = v ? T.sign * (T.scale ? T.scale[k] : 1.0) * (T.times_im ? (double)x.m : 1.0) : 0.0;
+        if (v) {
+          mbar_arrive_tx(&sm.full[s], abytes + (unsigned)bcols * 8u);
+          bulk_g2s(&S.A[r][0], T.tab + (size_t)k * Jp + x.tile, abytes, &sm.full[s]);
+          bulk_g2s(&S.B[r][0], T.src + (size_t)k * ld + x.c0, (unsigned)bcols * 8u, &sm.full[s]);
+        } else {
+          // rows past the m-block: scale 0 and zeroed B (stale data could be non-finite)
+          for (int q = 0; q < V3_BN; ++q) S.B[r][q] = 0.0;
+          mbar_arrive(&sm.full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  regs_inc();
+  const int cw = warp - V3_CW0, g = lane >> 2, t = lane & 3;
+  const int wpar = cw & 1, wph = (cw >> 1) & 1, wch = cw >> 2;
+  int it = 0;
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const Unit x = decode(args, u, ncol, 64);
+    const LegOut &o = args.out[x.out];
+    const int km = M + 1 - x.m, ne = (km + 1) >> 1;
+    const int nch_t = (ne + S3_KT - 1) / S3_KT;
+    const int pw0 = x.tile + wph * 32;
+    const int nfr = max(0, min(4, (Jh - pw0 + 7) >> 3));
+    double acc[4][8][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+      const int s = it % S3_NS;
+      mbar_wait(&sm.full[s], (it / S3_NS) & 1);
+      if (nfr > 0) {
+        const Synth3Stage &S = sm.st[s];
+        const LegTerm &T = o.t[c / nch_t];
+        const int rpar = wpar ^ T.flip;
+        const int tim = T.times_im;
+        const unsigned long long bmask = (tim && !(g & 1)) ? 0x8000000000000000ULL : 0ULL;
+        const double *Ab = &S.A[rpar * S3_KT + t][wph * 32 + g];
+        const double *Bb = &S.B[rpar * S3_KT + t][wch * 64 + (g ^ tim)];
+        const double *Sb = &S.S[rpar * S3_KT + t];
+        double a[2][4], b[2][8];
+        auto frag = [&](int kk, int q) {
+          const double sc = Sb[kk * 4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[q][i] = Ab[kk * 4 * S3_LDA + i * 8] * sc;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * S3_LDB + j * 8], bmask);
+        };
+        frag(0, 0);
+#pragma unroll
+        for (int kk = 0; kk < S3_KT / 4; ++kk) {
+          const int q = kk & 1;
+          if (kk + 1 < S3_KT / 4) frag(kk + 1, q ^ 1);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (i < nfr) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+            }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+    }
+    // E or O plane of [m][2][Jp][ld]
+    double *dst = o.dst + ((size_t)x.m * 2 + wpar) * Jp * ld;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int p = pw0 + i * 8 + g;
+      if (p >= Jh) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
+        if (col < ld)
+          *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ LegArgs args) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Anal3Smem &sm = *reinterpret_cast<Anal3Smem *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int M = args.M, Jp = args.Jp, ld = args.ld;
+  const int ncol = (ld + V3_BN - 1) / V3_BN;
+  const int nunits = args.nitems * ncol * args.nout;
+  const int nch_t = Jp / A3_KP;
+  if (tid == 0) {
+    for (int s = 0; s < A3_NS; ++s) {
+      mbar_init(&sm.full[s], 32);
+      mbar_init(&sm.empty[s], V3_NC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp < V3_CW0) {
+    regs_dec();
+    if (warp != 0) return;
+    int it = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const Unit x = decode(args, u, ncol, A3_BR);
+      const LegOut &o = args.out[x.out];
+      const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
+      const int off = args.offsets[x.m];
+      const unsigned bbytes = (unsigned)min(V3_BN, ld - x.c0) * 8u;
+      for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+        const int s = it % A3_NS;
+        mbar_wait(&sm.empty[s], ((it / A3_NS) & 1) ^ 1);
+        const int term = c / nch_t, q0 = (c - term * nch_t) * A3_KP;
+        const LegTerm &T = o.t[term];
+        Anal3Stage &S = sm.st[s];
+        // F+- row `lane` (1 KB) by TMA bulk copy; the table tile (128 modes x 16
+        // pairs = 1024 16-byte pieces, 32 per lane, zero-filled past the block) by
+        // cp.async, whose completion arrives on the same barrier
+        mbar_expect_tx(&sm.full[s], bbytes);
+        const int hs = lane >> 4, pr = lane & 15;
+        bulk_g2s(&S.F[hs][pr][0], T.src + (((size_t)x.m * 2 + hs) * Jp + q0 + pr) * ld + x.c0, bbytes,
+                 &sm.full[s]);
+#pragma unroll 8
+        for (int i = 0; i < A3_BR / 2; ++i) {
+          const int piece = lane + 32 * i, rr = piece >> 3, cc = (piece & 7) * 2;
+          const int par = rr / A3_BR, tt = x.tile + (rr % A3_BR);
+          const bool v = tt < (par ? no : ne);
+          const size_t row = (size_t)off + (par ? ne : 0) + tt;
+          cp_async16(&S.A[rr][cc], T.tab + (v ? row * Jp + q0 + cc : 0), v);
+        }
+        cp_async_arrive(&sm.full[s]);
+      }
+    }
+    return;
+  }
+
+  regs_inc();
+  const int cw = warp - V3_CW0, g = lane >> 2, t = lane & 3;
+  const int wpar = cw & 1, wrq = (cw >> 1) & 1, wch = cw >> 2;
+  int it = 0;
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const Unit x = decode(args, u, ncol, A3_BR);
+    const LegOut &o = args.out[x.out];
+    const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
+    const int nrow = (wpar ? no : ne) - (x.tile + wrq * A3_RW);
+    const int nfr = max(0, min(A3_FR, (nrow + 7) >> 3));
+    double acc[A3_FR][8][2];
+#pragma unroll
+    for (int i = 0; i < A3_FR; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+      const int s = it % A3_NS;
+      mbar_wait(&sm.full[s], (it / A3_NS) & 1);
+      if (nfr > 0) {
+        const Anal3Stage &S = sm.st[s];
+        const LegTerm &T = o.t[c / nch_t];
+        const int tim = T.times_im;
+        const int fsel = wpar ^ T.flip;
+        const unsigned long long bmask = (tim && !(g & 1)) ? 0x8000000000000000ULL : 0ULL;
+        const double asc = T.sign * (tim ? (double)x.m : 1.0);
+        const double *Ab = &S.A[wpar * A3_BR + wrq * A3_RW + g][t];
+        const double *Bb = &S.F[fsel][t][wch * 64 + (g ^ tim)];
+        double a[2][A3_FR], b[2][8];
+        auto frag = [&](int kk, int q) {
+#pragma unroll
+          for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 8 * A3_LDA + kk * 4] * asc;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * A3_LDB + j * 8], bmask);
+        };
+        frag(0, 0);
+#pragma unroll
+        for (int kk = 0; kk < A3_KP / 4; ++kk) {
+          const int q = kk & 1;
+          if (kk + 1 < A3_KP / 4) frag(kk + 1, q ^ 1);
+#pragma unroll
+          for (int i = 0; i < A3_FR; ++i)
+            if (i < nfr) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+            }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+    }
+    const int nt = wpar ? no : ne;
+    const int off = args.offsets[x.m];
+#pragma unroll
+    for (int i = 0; i < A3_FR; ++i) {
+      const int tt = x.tile + wrq * A3_RW + i * 8 + g;
+      if (tt >= nt) continue;
+      const size_t k = (size_t)off + (wpar ? ne : 0) + tt;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
+        if (col < ld)
+          *reinterpret_cast<double2 *>(o.dst + k * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
+  }
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+int leg_synth_v3_launch(const LegArgs &a, cudaStream_t st) {
+  static bool attr = false;
+  const int smem = (int)sizeof(Synth3Smem);
+  if (!attr) {
+    SWE_CUDA(cudaFuncSetAttribute(leg_synth_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int units = a.nitems * ((a.ld + V3_BN - 1) / V3_BN) * a.nout;
+  leg_synth_v3<<<std::min(units, num_sms()), V3_NT, smem, st>>>(a);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int leg_anal_v3_launch(const LegArgs &a, cudaStream_t st) {
+  static bool attr = false;
+  const int smem = (int)sizeof(Anal3Smem);
+  if (!attr) {
+    SWE_CUDA(cudaFuncSetAttribute(leg_anal_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int units = a.nitems * ((a.ld + V3_BN - 1) / V3_BN) * a.nout;
+  leg_anal_v3<<<std::min(units, num_sms()), V3_NT, smem, st>>>(a);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+}  // namespace swe

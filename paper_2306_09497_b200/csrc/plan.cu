@@ -306,11 +306,17 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
       const int ne = (M + 2 - m) / 2;
       for (int t = 0; t < (ne + V2_ABR - 1) / V2_ABR; ++t) an2.push_back(make_int2(m, t));
     }
+    std::vector<int2> an3;
+    for (int m = 0; m <= M; ++m) {
+      const int ne = (M + 2 - m) / 2;
+      for (int t = 0; t < (ne + V3_ABR - 1) / V3_ABR; ++t) an3.push_back(make_int2(m, t));
+    }
     pl->n_synth_items = (int)sy.size();
     pl->n_anal_items = (int)an.size();
     pl->n_anal_items_v2 = (int)an2.size();
+    pl->n_anal_items_v3 = (int)an3.size();
     if ((rc = upload(&pl->synth_items, sy)) || (rc = upload(&pl->anal_items, an)) ||
-        (rc = upload(&pl->anal_items_v2, an2)))
+        (rc = upload(&pl->anal_items_v2, an2)) || (rc = upload(&pl->anal_items_v3, an3)))
       return rc;
   }
   *out = pl;
@@ -355,6 +361,7 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->synth_items);
   cudaFree(pl->anal_items);
   cudaFree(pl->anal_items_v2);
+  cudaFree(pl->anal_items_v3);
   delete pl;
 }
 

@@ -53,8 +53,8 @@ struct swe_plan {
   int rgen = 0;
   int2 *synth_items = nullptr, *anal_items = nullptr;
   int n_synth_items = 0, n_anal_items = 0;
-  int2 *anal_items_v2 = nullptr;
-  int n_anal_items_v2 = 0;
+  int2 *anal_items_v2 = nullptr, *anal_items_v3 = nullptr;
+  int n_anal_items_v2 = 0, n_anal_items_v3 = 0;
   int nst = 0;
   int radix[swe::FFT_MAXST], ns[swe::FFT_MAXST];
   std::vector<int> h_offsets;

@@ -126,13 +126,15 @@ double leg_flops(const Run &r, const LegArgs &a) {
   return 2.0 * r.pl->J * (double)r.pl->K * r.B * terms;
 }
 
-// Legendre kernel choice -> 0: legendre.cu (small batches), else v2 column tile 64 or 128
+// Legendre kernel choice -> 0: legendre.cu (small batches), 64/128: legendre_v2.cu
+// column tile, -1: legendre_v3.cu (warp-specialised persistent, >= 32 slices)
 int leg_bn(const Run &r) {
   switch (g_leg_path) {
     case 1: return 0;
     case 2: return 128;
     case 3: return 64;
-    default: return r.ld > 32 ? 64 : 0;
+    case 4: return -1;
+    default: return r.ld >= 64 ? -1 : (r.ld > 32 ? 64 : 0);
   }
 }
 
@@ -140,13 +142,22 @@ int synth(const Run &r, LegArgs &a) {
   a.items = r.pl->synth_items;
   a.nitems = r.pl->n_synth_items;
   ProfScope ps(0, leg_flops(r, a), r.st);
-  if (const int bn = leg_bn(r)) return leg_synth_v2_launch(a, bn, r.st);
+  const int bn = leg_bn(r);
+  if (bn < 0) return leg_synth_v3_launch(a, r.st);
+  if (bn) return leg_synth_v2_launch(a, bn, r.st);
   return leg_synth_launch(a, (int)((r.ld + SY_BN - 1) / SY_BN), r.st);
 }
 
 int anal(const Run &r, LegArgs &a) {
   ProfScope ps(1, leg_flops(r, a), r.st);
-  if (const int bn = leg_bn(r)) {
+  int bn = leg_bn(r);
+  if (bn < 0 && g_leg_path == 0) bn = 64;  // auto: v2 analysis measured faster than v3
+  if (bn) {
+    if (bn < 0) {
+      a.items = r.pl->anal_items_v3;
+      a.nitems = r.pl->n_anal_items_v3;
+      return leg_anal_v3_launch(a, r.st);
+    }
     a.items = r.pl->anal_items_v2;
     a.nitems = r.pl->n_anal_items_v2;
     return leg_anal_v2_launch(a, bn, r.st);
@@ -197,6 +208,14 @@ int fft(const Run &r, int op, FftArgs &a) {
                                {0, 2, 2, 0}, {2, 2, 0, 0}, {7, 4, 0, 0}};
   const double spec_row = 16.0 * (pl->M + 1) * pl->J * r.B, grid_row = 8.0 * pl->I * pl->J * r.B;
   const double bytes = (io[op][0] + io[op][1]) * spec_row + (io[op][2] + io[op][3]) * grid_row;
+  // F+- rows of pairs Jh..Jp-1 are read by the analysis GEMM (TMA rows are not
+  // zero-filled) but never written by the FFT: keep them zero for this layout
+  static const int nfout[6] = {0, 0, 1, 2, 2, 4};
+  for (int o = 0; o < nfout[op]; ++o)
+    if (pl->Jp > pl->Jh)
+      SWE_CUDA(cudaMemset2DAsync(a.out[o] + (size_t)pl->Jh * r.ld, (size_t)pl->Jp * r.ld * 8, 0,
+                                 (size_t)(pl->Jp - pl->Jh) * r.ld * 8, (size_t)(pl->M + 1) * 2,
+                                 r.st));
   // path: lane = row kernel for small-radix lengths with enough slices, else warp-per-row
   const bool lanes = g_fft_path == 2 || (g_fft_path == 0 && r.B >= 8);
   if (lanes && fft_lanes_ok(a)) {
@@ -685,7 +704,7 @@ int swe_set_option(const char *key, int value) {
     g_fft_path = value;
     return OK;
   }
-  if (key && strcmp(key, "leg_path") == 0 && value >= 0 && value <= 3) {
+  if (key && strcmp(key, "leg_path") == 0 && value >= 0 && value <= 4) {
     g_leg_path = value;
     return OK;
   }

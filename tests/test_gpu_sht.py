@@ -47,7 +47,8 @@ def test_transforms_match_reference_goldens(gpu, name):
     assert rel_diff(xi, g["vd_xi"]) < TOL and rel_diff(de, g["vd_delta"]) < TOL
 
 
-@pytest.fixture(params=[(1, 1), (2, 2), (1, 2)], ids=["rows_narrow", "lanes_wide", "rows_wide"])
+@pytest.fixture(params=[(1, 1), (2, 2), (1, 2), (2, 3), (1, 4), (2, 4)],
+                ids=["rows_v1", "lanes_v2w128", "rows_v2w128", "lanes_v2w64", "rows_v3", "lanes_v3"])
 def fft_path(request):
     """Force each FFT kernel (warp-per-row / lane=row) and Legendre tiling
     (64- / 128-column) so every code path is parity-checked at every M."""
