@@ -56,9 +56,9 @@ __host__ __device__ constexpr int fft_rows_per_slice(int op) {
 bool fft_small_radix(int R);
 
 // "lane = row" variant (fft_lanes.cu): slices per CTA for each op
-// (32 rows = fields x 2 hemispheres x slices)
+// (16 rows = fields x 2 hemispheres x slices)
 __host__ __device__ constexpr int fft_lane_slices(int op) {
-  return op == FOP_NONLINEAR ? 2 : ((op == FOP_SYNTH_GRID || op == FOP_ANALYSIS) ? 16 : 8);
+  return op == FOP_NONLINEAR ? 1 : ((op == FOP_SYNTH_GRID || op == FOP_ANALYSIS) ? 8 : 4);
 }
 int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st);
 bool fft_lanes_ok(const FftArgs &a);

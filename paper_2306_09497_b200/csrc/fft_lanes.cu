@@ -1,10 +1,10 @@
 // Longitude FFT stage, "lane = row" variant for small-radix lengths.
 //
 // One CTA owns one latitude PAIR p (north row p, south row J-1-p) and S
-// slices; its 32 transform rows are (field, hemisphere, slice), row index
-// (f*2 + h)*S + s.  Shared memory holds X[slot][32]: the 32 rows of one slot
-// form one 512-byte line, lane r works on row r, every butterfly access is a
-// conflict-free full line and all lanes share the butterfly's twiddles.
+// slices; its 16 transform rows are (field, hemisphere, slice), row index
+// (f*2 + h)*S + s.  Shared memory holds X[slot][16]: the 16 rows of one slot
+// form one 256-byte line, half-warp lane r works on row r, every butterfly
+// access is a conflict-free full line and a half-warp shares its twiddles.
 // Inputs are the parity-split Legendre outputs E/O ([m][2][Jp][ld]):
 // north = E + O, south = E - O.  Outputs are the folded analysis inputs
 // F+- = w (f_north +- f_south) ([m][2][Jp][ld]); on the equator (J odd) the
@@ -20,7 +20,8 @@ using namespace fftcore;
 
 namespace {
 
-constexpr int LW = 32;  // rows per CTA (lanes)
+constexpr int LW = 16;  // rows per CTA: a half-warp covers them, so each warp runs two
+                        // butterflies per instruction and two CTAs fit on an SM
 
 // MODE 0 DIT, 1 DIF, 2 prime-factor (no twiddles); see fft.cu
 template <int R, int MODE>
@@ -37,15 +38,16 @@ SWE_DEV void lane_stage(double2 *X, int N2, int Lp, double dir, const double2 *t
     }
   }
   const int L = Lp * R, nbf = N2 / R, tws = N2 / L;
-  for (int bf = warp; bf < nbf; bf += nw) {
+  const int row = lane & (LW - 1);
+  for (int bf = 2 * warp + (lane >> 4); bf < nbf; bf += 2 * nw) {
     const int g = bf / Lp, k = bf - g * Lp, base = g * L + k;
     double2 v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      v[q] = X[(base + q * Lp) * LW + lane];
+      v[q] = X[(base + q * Lp) * LW + row];
       if (MODE == 0 && q && k) v[q] = cm(v[q], twd(tw, q * k * tws, dir));
     }
-    dft_store<R>(v, dir, cr, sr, X + base * LW + lane, Lp * LW, tw, MODE == 1 ? k * tws : 0);
+    dft_store<R>(v, dir, cr, sr, X + base * LW + row, Lp * LW, tw, MODE == 1 ? k * tws : 0);
   }
 }
 
@@ -227,7 +229,7 @@ SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, int f, int o, double 
 }  // namespace
 
 template <int OP>
-__global__ void __launch_bounds__(256) fft_lanes_kernel(const __grid_constant__ FftArgs a) {
+__global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant__ FftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LCtx c;
   c.X = reinterpret_cast<double2 *>(smem_raw);
