@@ -136,8 +136,10 @@ __global__ void __launch_bounds__(128) leg_synth_kernel(const __grid_constant__ 
     for (int j = 0; j < 4; ++j) {
       const int col = c0 + wc * 32 + j * 8 + 2 * t;
       if (col >= ld) continue;
-      *reinterpret_cast<double2 *>(dE + (size_t)p * ld + col) = make_double2(accE[i][j][0], accE[i][j][1]);
-      *reinterpret_cast<double2 *>(dO + (size_t)p * ld + col) = make_double2(accO[i][j][0], accO[i][j][1]);
+      // m = 0: irfft ignores Im of the mean bin, so store it as 0 (spharm.py:257)
+      const double z = m ? 1.0 : 0.0;
+      *reinterpret_cast<double2 *>(dE + (size_t)p * ld + col) = make_double2(accE[i][j][0], z * accE[i][j][1]);
+      *reinterpret_cast<double2 *>(dO + (size_t)p * ld + col) = make_double2(accO[i][j][0], z * accO[i][j][1]);
     }
   }
 }
@@ -156,7 +158,8 @@ constexpr int AN_LDB = AN_BN + 4;
 
 struct AnalSmem {
   double A[AN_STAGES][2 * AN_BR][AN_LDA];
-  double F[AN_STAGES][2][AN_KP][AN_LDB];  // raw north/south, then F+ / F-
+  double F[AN_STAGES][2][AN_KP][AN_LDB];  // F+ / F-
+  double Ps[AN_STAGES][AN_KP];            // per-pair scale (LegTerm::pscale)
 };
 }  // namespace
 
@@ -194,8 +197,9 @@ __global__ void __launch_bounds__(128) leg_anal_kernel(const __grid_constant__ L
       const int p = q0 + pr;
       const bool v = (p < Jh) && (c0 + cc < ld);
       cp_async16(&sm.F[stage][hs][pr][cc],
-                 base + (v ? ((size_t)hs * Jp + p) * ld + c0 + cc : 0), v);
+                 base + (v ? ((size_t)(hs ^ T.swap_pm) * Jp + p) * ld + c0 + cc : 0), v);
     }
+    if (tid < AN_KP) sm.Ps[stage][tid] = T.pscale ? T.pscale[q0 + tid] : 1.0;
   };
 
   double acc[2][4][2];
@@ -229,7 +233,8 @@ __global__ void __launch_bounds__(128) leg_anal_kernel(const __grid_constant__ L
 #pragma unroll
       for (int i = 0; i < 2; ++i) a[i] = sm.A[st][wpar * AN_BR + i * 8 + g][kk * 4 + t];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sm.F[st][fsel][kk * 4 + t][wc * 32 + j * 8 + bsel] * fac;
+      for (int j = 0; j < 4; ++j)
+        b[j] = sm.F[st][fsel][kk * 4 + t][wc * 32 + j * 8 + bsel] * (fac * sm.Ps[st][kk * 4 + t]);
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll

@@ -20,12 +20,14 @@ namespace swe {
 // (0,0) mode only, x.re -= phi0[slice] (phi_prime, dynamics.py:52-56).
 struct LegTerm {
   const double *tab;    // P or H table, row stride Jp
-  const double *src;    // synthesis: spectral [K][ld]; analysis: grid spectra [m][J][ld]
+  const double *src;    // synthesis: spectral [K][ld]; analysis: F+/F- planes [m][2][Jp][ld]
   const double *scale;  // per packed mode (synthesis only), nullable
   const double *phi0;   // per slice, nullable (synthesis only)
+  const double *pscale; // analysis only, nullable: per latitude pair factor on F+-
   double sign;
   int times_im;
-  int flip;  // 0: P-like parity, 1: H-like (odd in mu for even n-m)
+  int flip;     // 0: P-like parity, 1: H-like (odd in mu for even n-m)
+  int swap_pm;  // analysis only: read plane 1 as F+ and plane 0 as F- (E/O input)
 };
 
 struct LegOut {

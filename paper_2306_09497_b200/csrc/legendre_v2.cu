@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(BN * 2) leg_synth_v2(const __grid_constant__ L
     for (int j = 0; j < 8; ++j) {
       const int col = c0 + wch * 64 + j * 8 + 2 * t;
       if (col >= ld) continue;
-      *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      // m = 0: irfft ignores Im of the mean bin, so store it as 0 (spharm.py:257)
+      *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) =
+          make_double2(acc[i][j][0], m ? acc[i][j][1] : 0.0);
     }
   }
 }
@@ -165,6 +167,7 @@ template <int BN>
 struct AnalSmemV2 {
   double A[VA_ST][2 * VA_BR][VA_LDA];
   double F[VA_ST][2][VA_KP][BN + 4];
+  double Ps[VA_ST][VA_KP];  // per-pair scale (LegTerm::pscale)
 };
 }  // namespace
 
@@ -206,8 +209,9 @@ __global__ void __launch_bounds__(BN * 2) leg_anal_v2(const __grid_constant__ Le
       const int hs = rr >> 4, pr = rr & 15, p = q0 + pr;
       const bool v = (p < Jh) && (c0 + cc < ld);
       cp_async16(&sm.F[stage][hs][pr][cc],
-                 base + (v ? ((size_t)hs * Jp + p) * ld + c0 + cc : 0), v);
+                 base + (v ? ((size_t)(hs ^ T.swap_pm) * Jp + p) * ld + c0 + cc : 0), v);
     }
+    if (tid < VA_KP) sm.Ps[stage][tid] = T.pscale ? T.pscale[q0 + tid] : 1.0;
   };
 
   double acc[2][8][2];
@@ -240,8 +244,9 @@ __global__ void __launch_bounds__(BN * 2) leg_anal_v2(const __grid_constant__ Le
     const double *Bb = &sm.F[st][fsel][t][wch * 64 + (g ^ tim)];
     double a[2][2], b[2][8];
     auto frag = [&](int kk, int q) {
+      const double ak = asc * sm.Ps[st][kk * 4 + t];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) a[q][i] = Ab[i * 8 * VA_LDA + kk * 4] * asc;
+      for (int i = 0; i < 2; ++i) a[q][i] = Ab[i * 8 * VA_LDA + kk * 4] * ak;
 #pragma unroll
       for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * (BN + 4) + j * 8], bmask);
     };

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
         const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
         if (col < ld)
           *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) =
-              make_double2(acc[i][j][0], acc[i][j][1]);
+              make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);  // Im of m = 0 is dropped
       }
     }
   }
@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
         // cp.async, whose completion arrives on the same barrier
         mbar_expect_tx(&sm.full[s], bbytes);
         const int hs = lane >> 4, pr = lane & 15;
-        bulk_g2s(&S.F[hs][pr][0], T.src + (((size_t)x.m * 2 + hs) * Jp + q0 + pr) * ld + x.c0, bbytes,
+        bulk_g2s(&S.F[hs][pr][0],
+                 T.src + (((size_t)x.m * 2 + (hs ^ T.swap_pm)) * Jp + q0 + pr) * ld + x.c0, bbytes,
                  &sm.full[s]);
 #pragma unroll 8
         for (int i = 0; i < A3_BR / 2; ++i) {
@@ -318,12 +319,18 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
         const int fsel = wpar ^ T.flip;
         const unsigned long long bmask = (tim && !(g & 1)) ? 0x8000000000000000ULL : 0ULL;
         const double asc = T.sign * (tim ? (double)x.m : 1.0);
+        // per-pair scale of this lane's k row for each k-step (read-only, L1-cached)
+        double ps[A3_KP / 4];
+        const int q0 = (c % nch_t) * A3_KP;
+#pragma unroll
+        for (int kk = 0; kk < A3_KP / 4; ++kk)
+          ps[kk] = T.pscale ? __ldg(T.pscale + q0 + kk * 4 + t) : 1.0;
         const double *Ab = &S.A[wpar * A3_BR + wrq * A3_RW + g][t];
         const double *Bb = &S.F[fsel][t][wch * 64 + (g ^ tim)];
         double a[2][A3_FR], b[2][8];
         auto frag = [&](int kk, int q) {
 #pragma unroll
-          for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 8 * A3_LDA + kk * 4] * asc;
+          for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 8 * A3_LDA + kk * 4] * (asc * ps[kk]);
 #pragma unroll
           for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * A3_LDB + j * 8], bmask);
         };

@@ -205,6 +205,11 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
       (rc = upload(&pl->fcor, fc)) || (rc = upload(&pl->wq, pl->w)) ||
       (rc = upload(&pl->wsin2, wsq)))
     return rc;
+  {
+    std::vector<double> cs(Jp, 0.0);
+    for (int p = 0; p < Jh; ++p) cs[p] = 2.0 * (wsq[p] / a) * (fc[p] / a);
+    if ((rc = upload(&pl->cor_scale, cs))) return rc;
+  }
 
   // Legendre tables on the device (north pairs only)
   const size_t tab = (size_t)K * Jp;
@@ -354,6 +359,7 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->fcor);
   cudaFree(pl->wq);
   cudaFree(pl->wsin2);
+  cudaFree(pl->cor_scale);
   cudaFree(pl->tw);
   cudaFree(pl->twh);
   cudaFree(pl->fft_pos_z);

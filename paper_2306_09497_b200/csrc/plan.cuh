@@ -47,6 +47,7 @@ struct swe_plan {
   int *perm = nullptr;  // [K] reference packed index -> internal (parity-split) row
   double *lap_eig = nullptr, *inv_lap = nullptr, *eps = nullptr;
   double *coslat = nullptr, *inv_acos = nullptr, *fcor = nullptr, *wq = nullptr, *wsin2 = nullptr;
+  double *cor_scale = nullptr;  // [Jp] 2 w f / ((1 - mu^2) a^2) per pair (FFT-free Coriolis)
   double2 *tw = nullptr, *twh = nullptr;
   int *fft_pos_z = nullptr, *fft_pos_g = nullptr;
   int pfa = 0;

@@ -37,6 +37,7 @@ struct ProfRec {
 bool g_prof = false;
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
 int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
+int g_fast_coriolis = 1;  // 1: exact FFT-free Coriolis (eval_coriolis), 0: FFT round trip
 std::vector<ProfRec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 size_t g_pool_used = 0;
@@ -103,7 +104,29 @@ LegTerm term(const double *tab, const double *src, double sign = 1.0, int times_
   t.sign = sign;
   t.times_im = times_im;
   t.flip = 0;
+  t.pscale = nullptr;
+  t.swap_pm = 0;
   return t;
+}
+
+// analysis term reading synthesis E/O planes as F+ = O, F- = E with a per-pair scale
+LegTerm term_eo(const double *tab, const double *src, double sign, int times_im,
+                const double *pscale) {
+  LegTerm t = term(tab, src, sign, times_im);
+  t.pscale = pscale;
+  t.swap_pm = 1;
+  return t;
+}
+
+// rows Jh..Jp-1 of [m][2][Jp][ld] planes are never written but may be read
+// (TMA/bulk copies do not zero-fill): keep them zero
+int zero_pad_rows(const Run &r, double *planes) {
+  swe_plan *pl = r.pl;
+  if (pl->Jp > pl->Jh)
+    SWE_CUDA(cudaMemset2DAsync(planes + (size_t)pl->Jh * r.ld, (size_t)pl->Jp * r.ld * 8, 0,
+                               (size_t)(pl->Jp - pl->Jh) * r.ld * 8, (size_t)(pl->M + 1) * 2,
+                               r.st));
+  return OK;
 }
 
 void set_out(LegArgs &a, int i, double *dst, LegTerm t0, const LegTerm *t1, const double *H) {
@@ -244,6 +267,14 @@ int fft(const Run &r, int op, FftArgs &a) {
 }
 
 // L_C(xi, delta) = (0, -div(fV), curl(fV))  (dynamics.py:129-135)
+//
+// The grid work of linear_coriolis between irfft and rfft (u -> f u cos/(a cos))
+// only scales each latitude row, and rfft(irfft(X) * s) = s X on the retained
+// band (no longitude wavenumbers are created; irfft drops Im X[0], which the
+// synthesis already stores as 0).  So the folded analysis input is exactly
+//   F+ = c_p * 2 O,  F- = c_p * 2 E,  c_p = w_p f_p / ((1 - mu_p^2) a^2),
+// and the analysis GEMM reads the synthesis E/O planes directly: no FFT pass.
+// With fast_coriolis = 0 the pseudospectral FFT round trip is kept (testing).
 int eval_coriolis(const Run &r, const double *xi, const double *de, double *oxi, double *ode) {
   swe_plan *pl = r.pl;
   const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
@@ -256,6 +287,16 @@ int eval_coriolis(const Run &r, const double *xi, const double *de, double *oxi,
     set_out(a, 0, r.half(0), term(P, de, 1.0, 1, il), &hu, H);
     set_out(a, 1, r.half(1), term(P, xi, 1.0, 1, il), &hv, H);
     if ((rc = synth(r, a))) return rc;
+  }
+  if (g_fast_coriolis) {
+    if ((rc = zero_pad_rows(r, r.half(0))) || (rc = zero_pad_rows(r, r.half(1)))) return rc;
+    LegArgs a = leg_args(r);
+    a.nout = 2;
+    const double *cs = pl->cor_scale;
+    LegTerm hx = term_eo(H, r.half(1), 1.0, 0, cs), hd = term_eo(H, r.half(0), 1.0, 0, cs);
+    set_out(a, 0, oxi, term_eo(P, r.half(0), -1.0, 1, cs), &hx, H);
+    set_out(a, 1, ode, term_eo(P, r.half(1), 1.0, 1, cs), &hd, H);
+    return anal(r, a);
   }
   {
     FftArgs f;
@@ -702,6 +743,10 @@ long long swe_kernel_launches(void) { return g_launches; }
 int swe_set_option(const char *key, int value) {
   if (key && strcmp(key, "fft_path") == 0 && value >= 0 && value <= 2) {
     g_fft_path = value;
+    return OK;
+  }
+  if (key && strcmp(key, "fast_coriolis") == 0 && (value == 0 || value == 1)) {
+    g_fast_coriolis = value;
     return OK;
   }
   if (key && strcmp(key, "leg_path") == 0 && value >= 0 && value <= 4) {
