@@ -243,13 +243,13 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Anal3Smem &sm = *reinterpret_cast<Anal3Smem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int M = args.M, Jp = args.Jp, ld = args.ld;
+  const int M = args.M, Jp = args.Jp, ld = args.ld, Jh = args.Jh;
   const int ncol = (ld + V3_BN - 1) / V3_BN;
   const int nunits = args.nitems * ncol * args.nout;
   const int nch_t = Jp / A3_KP;
   if (tid == 0) {
     for (int s = 0; s < A3_NS; ++s) {
-      mbar_init(&sm.full[s], 32);
+      mbar_init(&sm.full[s], 128);  // every producer-warpgroup thread arrives
       mbar_init(&sm.empty[s], V3_NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -258,35 +258,38 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
 
   if (warp < V3_CW0) {
     regs_dec();
-    if (warp != 0) return;
+    // the whole producer warpgroup (128 threads) streams each stage with
+    // zero-filling cp.async: table tile (2*A3_BR modes x 16 pairs) and the F+/F-
+    // rows (2 x 16 pairs x 128 columns); every thread arrives on "full" once its
+    // own copies have landed (cp.async.mbarrier.arrive.noinc)
+    const int ptid = tid;  // 0..127
     int it = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       const Unit x = decode(args, u, ncol, A3_BR);
       const LegOut &o = args.out[x.out];
       const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
       const int off = args.offsets[x.m];
-      const unsigned bbytes = (unsigned)min(V3_BN, ld - x.c0) * 8u;
       for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
         const int s = it % A3_NS;
         mbar_wait(&sm.empty[s], ((it / A3_NS) & 1) ^ 1);
         const int term = c / nch_t, q0 = (c - term * nch_t) * A3_KP;
         const LegTerm &T = o.t[term];
         Anal3Stage &S = sm.st[s];
-        // F+- row `lane` (1 KB) by TMA bulk copy; the table tile (128 modes x 16
-        // pairs = 1024 16-byte pieces, 32 per lane, zero-filled past the block) by
-        // cp.async, whose completion arrives on the same barrier
-        mbar_expect_tx(&sm.full[s], bbytes);
-        const int hs = lane >> 4, pr = lane & 15;
-        bulk_g2s(&S.F[hs][pr][0],
-                 T.src + (((size_t)x.m * 2 + (hs ^ T.swap_pm)) * Jp + q0 + pr) * ld + x.c0, bbytes,
-                 &sm.full[s]);
-#pragma unroll 8
-        for (int i = 0; i < A3_BR / 2; ++i) {
-          const int piece = lane + 32 * i, rr = piece >> 3, cc = (piece & 7) * 2;
+#pragma unroll
+        for (int piece = ptid; piece < 2 * A3_BR * 8; piece += 128) {
+          const int rr = piece >> 3, cc = (piece & 7) * 2;
           const int par = rr / A3_BR, tt = x.tile + (rr % A3_BR);
           const bool v = tt < (par ? no : ne);
           const size_t row = (size_t)off + (par ? ne : 0) + tt;
           cp_async16(&S.A[rr][cc], T.tab + (v ? row * Jp + q0 + cc : 0), v);
+        }
+        const double *fb = T.src + (size_t)x.m * 2 * Jp * ld + x.c0;
+#pragma unroll 4
+        for (int piece = ptid; piece < 2 * A3_KP * (V3_BN / 2); piece += 128) {
+          const int rr = piece / (V3_BN / 2), cc = (piece % (V3_BN / 2)) * 2;
+          const int hs = rr / A3_KP, pr = rr % A3_KP, p = q0 + pr;
+          const bool v = (p < Jh) && (x.c0 + cc < ld);
+          cp_async16(&S.F[hs][pr][cc], fb + (v ? ((size_t)(hs ^ T.swap_pm) * Jp + p) * ld + cc : 0), v);
         }
         cp_async_arrive(&sm.full[s]);
       }

@@ -108,64 +108,82 @@ __global__ void k_lin_tend(int K, int B, const double *U0, const double *U2, con
 
 // u = helm(rhs + alpha*lc) (steppers.py:61-71, :96-99) for active slices, with the
 // per-slice convergence statistics of steppers.py:100-109 accumulated in stats:
-// stats[b*8 + f] = max|new_f|, stats[b*8 + 3 + f] = max|new_f - old_f|.
-__global__ void k_helm(int K, int B, const double *R0, const double *R1, const double *R2,
-                       const double *lcx, const double *lcd, double alpha, const double *eps,
-                       const double *phibar, double *U0, double *U1, double *U2,
-                       const int *active, double *stats) {
+// stats[b*8 + f] = max|new_f|^2, stats[b*8 + 3 + f] = max|new_f - old_f|^2, as
+// ordered bit patterns (squared magnitudes are >= 0, NaN sorts above Inf, so an
+// unsigned max keeps NaN like np.max); k_decide takes the square roots.
+SWE_DEV unsigned long long sqmag_bits(double x, double y) {
+  return (unsigned long long)__double_as_longlong(x * x + y * y);
+}
+__global__ void __launch_bounds__(256) k_helm(int K, int B, const double *R0, const double *R1,
+                                              const double *R2, const double *lcx,
+                                              const double *lcd, double alpha, const double *eps,
+                                              const double *phibar, double *U0, double *U1,
+                                              double *U2, const int *active, double *stats) {
   // block: 32 slices x 8 mode rows; grid.x over slice tiles, grid.y over modes
-  __shared__ double red[8][32][6];
+  constexpr int UN = 4;  // modes per thread in flight
+  __shared__ unsigned long long red[8][32][6];
   const int b = blockIdx.x * 32 + threadIdx.x;
-  double mx[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long mx[6] = {0, 0, 0, 0, 0, 0};
   const bool act = (b < B) && (active == nullptr || active[b]);
   if (act) {
-    const double pb = phibar[b];
-    for (int k = blockIdx.y * blockDim.y + threadIdx.y; k < K; k += gridDim.y * blockDim.y) {
-      const size_t i = (size_t)k * B + b;
-      const double2 rp = ld2(R0, i);
-      double2 rx = ld2(R1, i), rd = ld2(R2, i);
-      if (lcx) {
-        rx = add2(rx, sc2(alpha, ld2(lcx, i)));
-        rd = add2(rd, sc2(alpha, ld2(lcd, i)));
-      }
-      const double e = eps[k];
-      const double denom = 1.0 + alpha * alpha * pb * e;
-      const double apb = alpha * pb;
-      const double2 ph = make_double2((rp.x - apb * rd.x) / denom, (rp.y - apb * rd.y) / denom);
-      const double ae = alpha * e;
-      const double2 de = make_double2(rd.x + ae * ph.x, rd.y + ae * ph.y);
-      if (stats) {
-        const double2 o0 = ld2(U0, i), o1 = ld2(U1, i), o2 = ld2(U2, i);
-        mx[0] = fmax(mx[0], hypot(ph.x, ph.y));
-        mx[1] = fmax(mx[1], hypot(rx.x, rx.y));
-        mx[2] = fmax(mx[2], hypot(de.x, de.y));
-        mx[3] = fmax(mx[3], hypot(ph.x - o0.x, ph.y - o0.y));
-        mx[4] = fmax(mx[4], hypot(rx.x - o1.x, rx.y - o1.y));
-        mx[5] = fmax(mx[5], hypot(de.x - o2.x, de.y - o2.y));
-        // NaN must survive the max (np.max propagates it)
-        for (int q = 0; q < 3; ++q) {
-          const double2 nv = q == 0 ? ph : (q == 1 ? rx : de);
-          const double2 ov = q == 0 ? o0 : (q == 1 ? o1 : o2);
-          if (isnan(nv.x) || isnan(nv.y)) mx[q] = nan("");
-          if (isnan(nv.x - ov.x) || isnan(nv.y - ov.y)) mx[3 + q] = nan("");
+    const double pb = phibar[b], apb = alpha * pb, aap = alpha * alpha * pb;
+    const int k0 = blockIdx.y * blockDim.y + threadIdx.y, stride = gridDim.y * blockDim.y;
+    for (int kb = k0; kb < K; kb += UN * stride) {
+      double2 rp[UN], rx[UN], rd[UN], o0[UN], o1[UN], o2[UN];
+      double e[UN];
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {
+        const int k = kb + u * stride;
+        if (k < K) {
+          const size_t i = (size_t)k * B + b;
+          rp[u] = ld2(R0, i);
+          rx[u] = ld2(R1, i);
+          rd[u] = ld2(R2, i);
+          if (lcx) {
+            rx[u] = add2(rx[u], sc2(alpha, ld2(lcx, i)));
+            rd[u] = add2(rd[u], sc2(alpha, ld2(lcd, i)));
+          }
+          e[u] = eps[k];
+          if (stats) {
+            o0[u] = ld2(U0, i);
+            o1[u] = ld2(U1, i);
+            o2[u] = ld2(U2, i);
+          }
         }
       }
-      st2(U0, i, ph);
-      st2(U1, i, rx);
-      st2(U2, i, de);
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {
+        const int k = kb + u * stride;
+        if (k >= K) continue;
+        const size_t i = (size_t)k * B + b;
+        const double denom = 1.0 + aap * e[u];
+        const double2 ph = make_double2((rp[u].x - apb * rd[u].x) / denom,
+                                        (rp[u].y - apb * rd[u].y) / denom);
+        const double ae = alpha * e[u];
+        const double2 de = make_double2(rd[u].x + ae * ph.x, rd[u].y + ae * ph.y);
+        if (stats) {
+          mx[0] = max(mx[0], sqmag_bits(ph.x, ph.y));
+          mx[1] = max(mx[1], sqmag_bits(rx[u].x, rx[u].y));
+          mx[2] = max(mx[2], sqmag_bits(de.x, de.y));
+          mx[3] = max(mx[3], sqmag_bits(ph.x - o0[u].x, ph.y - o0[u].y));
+          mx[4] = max(mx[4], sqmag_bits(rx[u].x - o1[u].x, rx[u].y - o1[u].y));
+          mx[5] = max(mx[5], sqmag_bits(de.x - o2[u].x, de.y - o2[u].y));
+        }
+        st2(U0, i, ph);
+        st2(U1, i, rx[u]);
+        st2(U2, i, de);
+      }
     }
   }
   if (!stats) return;
+#pragma unroll
   for (int q = 0; q < 6; ++q) red[threadIdx.y][threadIdx.x][q] = mx[q];
   __syncthreads();
   if (threadIdx.y == 0 && act) {
     for (int q = 0; q < 6; ++q) {
-      double v = red[0][threadIdx.x][q];
-      for (int r = 1; r < blockDim.y; ++r) {
-        const double w = red[r][threadIdx.x][q];
-        v = (isnan(w) || isnan(v)) ? nan("") : fmax(v, w);
-      }
-      atomic_max_nonneg(stats + (size_t)b * 8 + q, v);
+      unsigned long long v = red[0][threadIdx.x][q];
+      for (int r = 1; r < blockDim.y; ++r) v = max(v, red[r][threadIdx.x][q]);
+      atomicMax(reinterpret_cast<unsigned long long *>(stats) + (size_t)b * 8 + q, v);
     }
   }
 }
@@ -177,14 +195,16 @@ __global__ void k_decide(int B, double *stats, int *active, int *iters, int *cou
   double *s = stats + (size_t)b * 8;
   if (active[b]) {
     iters[b] += 1;
-    double overall = fmax(fmax(s[0], s[1]), s[2]);
-    if (isnan(s[0]) || isnan(s[1]) || isnan(s[2])) overall = nan("");
+    double v[6];
+    for (int q = 0; q < 6; ++q) v[q] = sqrt(s[q]);  // NaN stays NaN
+    double overall = fmax(fmax(v[0], v[1]), v[2]);
+    if (isnan(v[0]) || isnan(v[1]) || isnan(v[2])) overall = nan("");
     overall = (overall > 1e-300 || isnan(overall)) ? overall : 1e-300;
     bool done = true;
     for (int f = 0; f < 3; ++f) {
       const double tiny = 1e-13 * overall;
-      const double scale = (s[f] >= tiny || isnan(s[f])) ? s[f] : tiny;
-      if (s[3 + f] > tol * scale) done = false;
+      const double scale = (v[f] >= tiny || isnan(v[f])) ? v[f] : tiny;
+      if (v[3 + f] > tol * scale) done = false;
     }
     if (done) active[b] = 0;
     else atomicAdd(counter, 1);

@@ -173,8 +173,7 @@ int synth(const Run &r, LegArgs &a) {
 
 int anal(const Run &r, LegArgs &a) {
   ProfScope ps(1, leg_flops(r, a), r.st);
-  int bn = leg_bn(r);
-  if (bn < 0 && g_leg_path == 0) bn = 64;  // auto: v2 analysis measured faster than v3
+  const int bn = leg_bn(r);
   if (bn) {
     if (bn < 0) {
       a.items = r.pl->anal_items_v3;
