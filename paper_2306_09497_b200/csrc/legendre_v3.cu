@@ -160,8 +160,10 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
           bulk_g2s(&S.A[r][0], T.tab + (size_t)k * Jp + x.tile, abytes, &sm.full[s]);
           bulk_g2s(&S.B[r][0], T.src + (size_t)k * ld + x.c0, (unsigned)bcols * 8u, &sm.full[s]);
         } else {
-          // rows past the m-block: scale 0 and zeroed B (stale data could be non-finite)
+          // rows past the m-block: scale 0 and zeroed A and B rows (shared memory left
+          // by an earlier kernel may hold non-finite values, and 0 * NaN = NaN)
           for (int q = 0; q < V3_BN; ++q) S.B[r][q] = 0.0;
+          for (int q = 0; q < 64; ++q) S.A[r][q] = 0.0;
           mbar_arrive(&sm.full[s]);
         }
       }

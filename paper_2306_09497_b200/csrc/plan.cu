@@ -210,6 +210,39 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
     for (int p = 0; p < Jh; ++p) cs[p] = 2.0 * (wsq[p] / a) * (fc[p] / a);
     if ((rc = upload(&pl->cor_scale, cs))) return rc;
   }
+  {
+    // L_C(xi, delta) = (0, -div(fV), curl(fV)) with f = 2 Omega mu is tridiagonal in n
+    // per order m (mu P_n = eps_{n+1} P_{n+1} + eps_n P_{n-1}, H_n = -n eps_{n+1} P_{n+1}
+    // + (n+1) eps_n P_{n-1}, V = (psi, chi) from inverse Laplacians of (xi, delta)):
+    //   div_n  = 2W [ (n+1)/n eps_n d_{n-1} + n/(n+1) eps_{n+1} d_{n+1} - i m/(n(n+1)) x_n ]
+    //   curl_n = 2W [ (n+1)/n eps_n x_{n-1} + n/(n+1) eps_{n+1} x_{n+1} + i m/(n(n+1)) d_n ]
+    // The pseudospectral evaluation (dynamics.py:129-135) equals this exactly: its
+    // integrands are polynomials of degree <= 2M+2 < 2J, which Gauss quadrature
+    // integrates exactly.  Modes n = 0 never reach V (inverse Laplacian), modes
+    // n > M are truncated, and m = 0 uses real parts only (irfft/rfft).
+    std::vector<int2> nb(K);
+    std::vector<double4> cf(K);
+    auto row = [&](int m, int n) {
+      const int d = n - m, ne = (M + 2 - m) / 2;
+      return offs[m] + ((d & 1) ? ne + (d >> 1) : (d >> 1));
+    };
+    auto epsh = [](int m, int n) {
+      return n > m ? sqrt(((double)n * n - (double)m * m) / (4.0 * n * n - 1.0)) : 0.0;
+    };
+    const double w2 = 2.0 * omega;
+    for (int m = 0; m <= M; ++m)
+      for (int n = m; n <= M; ++n) {
+        const int k = row(m, n);
+        nb[k].x = (n - 1 >= m && n - 1 >= 1) ? row(m, n - 1) : -1;
+        nb[k].y = n + 1 <= M ? row(m, n + 1) : -1;
+        const double nn1 = (double)n * (n + 1.0);
+        cf[k].x = n > 0 ? w2 * epsh(m, n) * ((n + 1.0) / n) : 0.0;
+        cf[k].y = w2 * epsh(m, n + 1) * (n / (n + 1.0));
+        cf[k].z = nn1 > 0 ? w2 * (m / nn1) : 0.0;
+        cf[k].w = m == 0 ? 1.0 : 0.0;
+      }
+    if ((rc = upload(&pl->cor_nb, nb)) || (rc = upload(&pl->cor_cf, cf))) return rc;
+  }
 
   // Legendre tables on the device (north pairs only)
   const size_t tab = (size_t)K * Jp;
@@ -360,6 +393,8 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->wq);
   cudaFree(pl->wsin2);
   cudaFree(pl->cor_scale);
+  cudaFree(pl->cor_nb);
+  cudaFree(pl->cor_cf);
   cudaFree(pl->tw);
   cudaFree(pl->twh);
   cudaFree(pl->fft_pos_z);

@@ -48,6 +48,8 @@ struct swe_plan {
   double *lap_eig = nullptr, *inv_lap = nullptr, *eps = nullptr;
   double *coslat = nullptr, *inv_acos = nullptr, *fcor = nullptr, *wq = nullptr, *wsin2 = nullptr;
   double *cor_scale = nullptr;  // [Jp] 2 w f / ((1 - mu^2) a^2) per pair (FFT-free Coriolis)
+  int2 *cor_nb = nullptr;       // [K] internal rows of modes n-1, n+1 (-1: none) (spectral Coriolis)
+  double4 *cor_cf = nullptr;    // [K] (c_lo, c_hi, c_im, m == 0) of the spectral Coriolis operator
   double2 *tw = nullptr, *twh = nullptr;
   int *fft_pos_z = nullptr, *fft_pos_g = nullptr;
   int pfa = 0;

@@ -114,20 +114,65 @@ __global__ void k_lin_tend(int K, int B, const double *U0, const double *U2, con
 SWE_DEV unsigned long long sqmag_bits(double x, double y) {
   return (unsigned long long)__double_as_longlong(x * x + y * y);
 }
-__global__ void __launch_bounds__(256) k_helm(int K, int B, const double *R0, const double *R1,
+// L_C at internal row k, slice b: lx = -div(fV), ld = curl(fV)   (plan.cu cor_cf)
+SWE_DEV void cor_at(const CorOp &c, int k, int b, int B, double2 &lx, double2 &ld) {
+  const int2 nb = __ldg(c.nb + k);
+  const double4 cf = c.cf[k];
+  const size_t i = (size_t)k * B + b;
+  const double2 x = ld2(c.x, i), d = ld2(c.d, i);
+  double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
+  if (nb.x >= 0) {
+    xl = ld2(c.x, (size_t)nb.x * B + b);
+    dl = ld2(c.d, (size_t)nb.x * B + b);
+  }
+  if (nb.y >= 0) {
+    xh = ld2(c.x, (size_t)nb.y * B + b);
+    dh = ld2(c.d, (size_t)nb.y * B + b);
+  }
+  // div = clo d_{n-1} + chi d_{n+1} - i cim x ; curl = clo x_{n-1} + chi x_{n+1} + i cim d
+  lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * x.y),
+                    -(cf.x * dl.y + cf.y * dh.y - cf.z * x.x));
+  ld = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * d.y, cf.x * xl.y + cf.y * xh.y + cf.z * d.x);
+  if (cf.w != 0.0) {  // m = 0: real fields (the imaginary inputs never enter)
+    lx.y = 0.0;
+    ld.y = 0.0;
+  }
+}
+
+__global__ void k_coriolis(int K, int B, CorOp c, double *lcx, double *lcd) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
+    double2 lx, ld;
+    cor_at(c, k, b, B, lx, ld);
+    st2(lcx, _i, lx);
+    st2(lcd, _i, ld);
+  }
+}
+
+template <int UN>  // modes per thread in flight
+__global__ void __launch_bounds__(256, UN == 4 ? 1 : 2) k_helm(int K, int B, const double *R0, const double *R1,
                                               const double *R2, const double *lcx,
                                               const double *lcd, double alpha, const double *eps,
                                               const double *phibar, double *U0, double *U1,
-                                              double *U2, const int *active, double *stats) {
+                                              double *U2, const int *active, double *stats,
+                                              CorOp cor) {
   // block: 32 slices x 8 mode rows; grid.x over slice tiles, grid.y over modes
-  constexpr int UN = 4;  // modes per thread in flight
   __shared__ unsigned long long red[8][32][6];
   const int b = blockIdx.x * 32 + threadIdx.x;
   unsigned long long mx[6] = {0, 0, 0, 0, 0, 0};
+  const bool fused = cor.x != nullptr;
+  const double *O1 = fused ? cor.x : U1, *O2 = fused ? cor.d : U2;
   const bool act = (b < B) && (active == nullptr || active[b]);
+  const int k0 = blockIdx.y * blockDim.y + threadIdx.y, stride = gridDim.y * blockDim.y;
+  if (fused && b < B && !act) {  // converged slice: carry its iterate into the new buffers
+    for (int k = k0; k < K; k += stride) {
+      const size_t i = (size_t)k * B + b;
+      st2(U1, i, ld2(O1, i));
+      st2(U2, i, ld2(O2, i));
+    }
+  }
   if (act) {
     const double pb = phibar[b], apb = alpha * pb, aap = alpha * alpha * pb;
-    const int k0 = blockIdx.y * blockDim.y + threadIdx.y, stride = gridDim.y * blockDim.y;
     for (int kb = k0; kb < K; kb += UN * stride) {
       double2 rp[UN], rx[UN], rd[UN], o0[UN], o1[UN], o2[UN];
       double e[UN];
@@ -139,15 +184,20 @@ __global__ void __launch_bounds__(256) k_helm(int K, int B, const double *R0, co
           rp[u] = ld2(R0, i);
           rx[u] = ld2(R1, i);
           rd[u] = ld2(R2, i);
-          if (lcx) {
+          if (fused) {
+            double2 lx, ld;
+            cor_at(cor, k, b, B, lx, ld);
+            rx[u] = add2(rx[u], sc2(alpha, lx));
+            rd[u] = add2(rd[u], sc2(alpha, ld));
+          } else if (lcx) {
             rx[u] = add2(rx[u], sc2(alpha, ld2(lcx, i)));
             rd[u] = add2(rd[u], sc2(alpha, ld2(lcd, i)));
           }
           e[u] = eps[k];
           if (stats) {
             o0[u] = ld2(U0, i);
-            o1[u] = ld2(U1, i);
-            o2[u] = ld2(U2, i);
+            o1[u] = ld2(O1, i);
+            o2[u] = ld2(O2, i);
           }
         }
       }
@@ -356,13 +406,24 @@ int lin_tend(int K, int B, const double *U0, const double *U2, const double *lcx
   return OK;
 }
 
+int coriolis_spec(int K, int B, const CorOp &c, double *lcx, double *lcd, cudaStream_t st) {
+  k_coriolis<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, c, lcx, lcd);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
 int helm(int K, int B, const double *const R[3], const double *lcx, const double *lcd,
          double alpha, const double *eps, const double *phibar, double *const U[3],
-         const int *active, double *stats, cudaStream_t st) {
+         const int *active, double *stats, cudaStream_t st, const CorOp *cor) {
   const int ybl = std::max(1, std::min((K + 7) / 8, (148 * 8) / ((B + 31) / 32)));
   dim3 grid((B + 31) / 32, ybl), blk(32, 8);
-  k_helm<<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0], U[1],
-                                U[2], active, stats);
+  CorOp c = cor ? *cor : CorOp{nullptr, nullptr, nullptr, nullptr};
+  if (cor)
+    k_helm<2><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
+                                     U[1], U[2], active, stats, c);
+  else
+    k_helm<4><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
+                                     U[1], U[2], active, stats, c);
   SWE_LAUNCH_CHECK();
   return OK;
 }

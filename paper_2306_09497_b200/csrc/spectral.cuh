@@ -30,9 +30,19 @@ int lin_rhs(int K, int B, const double *const U[3], const double *lcx, const dou
 int lin_tend(int K, int B, const double *U0, const double *U2, const double *lcx,
              const double *lcd, const double *eps, const double *phibar, double *const T[3],
              cudaStream_t st);
+// spectral Coriolis operator (plan.cu cor_nb / cor_cf) applied to (x, d) = (xi, delta)
+struct CorOp {
+  const double *x, *d;
+  const int2 *nb;
+  const double4 *cf;
+};
+int coriolis_spec(int K, int B, const CorOp &c, double *lcx, double *lcd, cudaStream_t st);
+// cor.x != nullptr: L_C is evaluated inline from (cor.x, cor.d), the previous
+// iterate, and the new xi/delta go to U[1], U[2] (distinct buffers; slices that
+// are no longer active copy their iterate across)
 int helm(int K, int B, const double *const R[3], const double *lcx, const double *lcd,
          double alpha, const double *eps, const double *phibar, double *const U[3],
-         const int *active, double *stats, cudaStream_t st);
+         const int *active, double *stats, cudaStream_t st, const CorOp *cor = nullptr);
 int decide(int B, double *stats, int *active, int *iters, int *counter, double tol,
            cudaStream_t st);
 int fill_int(int *p, int n, int v, cudaStream_t st);

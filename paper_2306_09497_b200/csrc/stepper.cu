@@ -37,7 +37,9 @@ struct ProfRec {
 bool g_prof = false;
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
 int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
-int g_fast_coriolis = 1;  // 1: exact FFT-free Coriolis (eval_coriolis), 0: FFT round trip
+// Coriolis operator (eval_coriolis): 2 spectral three-term recurrence, fused into the
+// fixed-point Helmholtz update (default); 1 FFT-free Legendre pair; 0 FFT round trip
+int g_fast_coriolis = 2;
 std::vector<ProfRec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 size_t g_pool_used = 0;
@@ -278,6 +280,10 @@ int eval_coriolis(const Run &r, const double *xi, const double *de, double *oxi,
   swe_plan *pl = r.pl;
   const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
   int rc;
+  if (g_fast_coriolis == 2) {
+    ProfScope ps(3, 8.0 * 16.0 * pl->K * r.B, r.st);  // 2 fields in (x3 rows, cached), 2 out
+    return coriolis_spec(pl->K, r.B, CorOp{xi, de, pl->cor_nb, pl->cor_cf}, oxi, ode, r.st);
+  }
   {
     LegArgs a = leg_args(r);
     a.nout = 2;
@@ -420,9 +426,21 @@ int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *con
   if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
   SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * 8 * B, r.st));
   int active = B;
+  // spectral Coriolis: L_C of the previous iterate is evaluated inside the Helmholtz
+  // update, so xi/delta ping-pong between dst and the LC buffers
+  const bool fused = g_fast_coriolis == 2;
+  double *cur[3] = {dst[0], dst[1], dst[2]}, *nxt[3] = {dst[0], b.LC[0], b.LC[1]};
   for (int it = 0; it < cfg.implicit_max_iter && active > 0; ++it) {
-    if ((rc = eval_coriolis(r, dst[1], dst[2], b.LC[0], b.LC[1]))) return rc;
-    {
+    if (fused) {
+      ProfScope ps(3, 9.0 * 16.0 * K * B, r.st);  // rhs 3 + old 3 in, new 3 out
+      const CorOp c{cur[1], cur[2], pl->cor_nb, pl->cor_cf};
+      if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, nxt, w.flags, w.stats,
+                     r.st, &c)))
+        return rc;
+      std::swap(cur[1], nxt[1]);
+      std::swap(cur[2], nxt[2]);
+    } else {
+      if ((rc = eval_coriolis(r, dst[1], dst[2], b.LC[0], b.LC[1]))) return rc;
       ProfScope ps(3, 11.0 * 16.0 * K * B, r.st);  // rhs 3 + lc 2 + old 3 in, new 3 out
       if ((rc = helm(K, B, Rc, b.LC[0], b.LC[1], alpha, pl->eps, w.phibar, dst, w.flags, w.stats,
                      r.st)))
@@ -434,6 +452,9 @@ int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *con
     SWE_CUDA(cudaStreamSynchronize(r.st));
     active = *w.h_counter;
   }
+  if (cur[1] != dst[1])
+    for (int f = 1; f < 3; ++f)
+      SWE_CUDA(cudaMemcpyAsync(dst[f], cur[f], (size_t)K * B * 16, cudaMemcpyDeviceToDevice, r.st));
   if (iters_host) {
     std::vector<int> it(B);
     SWE_CUDA(cudaMemcpyAsync(it.data(), w.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, r.st));
@@ -744,7 +765,7 @@ int swe_set_option(const char *key, int value) {
     g_fft_path = value;
     return OK;
   }
-  if (key && strcmp(key, "fast_coriolis") == 0 && (value == 0 || value == 1)) {
+  if (key && strcmp(key, "fast_coriolis") == 0 && value >= 0 && value <= 2) {
     g_fast_coriolis = value;
     return OK;
   }

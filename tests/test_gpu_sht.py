@@ -146,3 +146,43 @@ def test_constant_field(gpu):
     assert abs(c[grid.mode_index(0, 0)] - 3.25 * math.sqrt(2)) < 1e-12
     c[grid.mode_index(0, 0)] = 0.0
     assert np.abs(c).max() < 1e-12
+
+
+@pytest.mark.parametrize("leg", [1, 2, 3, 4])
+def test_stale_nonfinite_workspace(gpu, leg):
+    """Workspaces and shared memory left holding NaN by an earlier call (a blown-up
+    slice) must not leak into a later, finite call on any Legendre kernel."""
+    from paper_2306_09497_b200 import _lib, dynamics
+    from oracle.sht import random_bandlimited
+    M, B = 51, 40
+    grid, sph = gpu.get_grid(M), oracle(M)
+    rng = np.random.default_rng(11)
+    c = random_bandlimited(sph, rng, batch=(B,))
+    g = sph.synthesis(c)
+    nan_s = np.full((B, grid.n_modes), np.nan + 0j)
+    nan_g = np.full((B, grid.nlat, grid.nlon), np.nan)
+    bad = dynamics.PrognosticState.from_fields(grid, nan_s, nan_s, nan_s, [1.0] * B)
+    good = dynamics.PrognosticState.from_fields(grid, 1e3 * c, 1e-5 * c, 1e-6 * c, [3e4] * B)
+
+    def poison():
+        for fast in (0, 1, 2):
+            _lib.set_option("fast_coriolis", fast)
+            dynamics.linear_coriolis(bad)
+        dynamics.nonlinear(bad)
+        grid.synthesis(nan_s)
+        grid.analysis(nan_g)
+
+    _lib.set_option("leg_path", leg)
+    try:
+        poison()
+        assert rel_diff(np.asarray(grid.synthesis(c)), g) < TOL
+        poison()
+        assert rel_diff(np.asarray(grid.analysis(g)), c) < TOL
+        for fast in (0, 1, 2):
+            poison()
+            _lib.set_option("fast_coriolis", fast)
+            t = dynamics.linear_coriolis(good)
+            assert all(np.isfinite(x.cpu().numpy()).all() for x in t), fast
+    finally:
+        _lib.set_option("leg_path", 0)
+        _lib.set_option("fast_coriolis", 2)

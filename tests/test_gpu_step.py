@@ -61,14 +61,19 @@ def test_imex_steps_match_reference(mods, name):
         assert np.array_equal(s.data[0].cpu().numpy(), g[key + "_in"])
 
 
-@pytest.mark.parametrize("path", [1, 2], ids=["fft_rows", "fft_lanes"])
-def test_batched_step_matches_oracle_per_slice(mods, path):
+@pytest.mark.parametrize("path,cor", [(1, 2), (2, 2), (2, 1), (2, 0)],
+                         ids=["fft_rows", "fft_lanes", "cor_legendre", "cor_fft"])
+def test_batched_step_matches_oracle_per_slice(mods, path, cor):
+    """Per-slice states and Coriolis fixed-point iteration counts, on both FFT kernels
+    and all three Coriolis evaluations (spectral / FFT-free Legendre / FFT)."""
     from paper_2306_09497_b200 import _lib
     _lib.set_option("fft_path", path)
+    _lib.set_option("fast_coriolis", cor)
     try:
         _batched_step_check(mods)
     finally:
         _lib.set_option("fft_path", 0)
+        _lib.set_option("fast_coriolis", 2)
 
 
 def _batched_step_check(mods):
@@ -131,8 +136,9 @@ def test_nonconvergence_raises(mods):
 
 @pytest.mark.parametrize("M", [16, 51, 64, 256])
 def test_fft_free_coriolis_equals_pseudospectral(mods, M):
-    """The FFT-free Coriolis (rfft(irfft(X) * s) = s X on the band) agrees with the
-    FFT round trip to roundoff, batched, on every path."""
+    """The FFT-free Coriolis (rfft(irfft(X) * s) = s X on the band) and the spectral
+    three-term recurrence (plan.cu cor_cf, the default) agree with the FFT round
+    trip to roundoff, batched, on every path."""
     spharm, dynamics, _, _ = mods
     from paper_2306_09497_b200 import _lib
     from oracle.sht import OracleSphere, random_bandlimited
@@ -153,17 +159,47 @@ def test_fft_free_coriolis_equals_pseudospectral(mods, M):
                                              [9.80616 * 29400.0] * B)
     try:
         outs = []
-        for fast in (0, 1):
+        for fast in (0, 1, 2):
             _lib.set_option("fast_coriolis", fast)
             t = dynamics.linear_coriolis(s)
             outs.append(np.stack([x.cpu().numpy() for x in t]))
     finally:
-        _lib.set_option("fast_coriolis", 1)
+        _lib.set_option("fast_coriolis", 2)
     for f in (1, 2):
-        assert np.abs(outs[0][f] - outs[1][f]).max() <= 1e-13 * np.abs(outs[0][f]).max()
+        # FFT-free: same arithmetic minus the FFT pair; spectral: exact recurrence, so
+        # it differs by the pseudospectral path's own quadrature roundoff (~1e-13)
+        for alt, tol in ((1, 1e-13), (2, 1e-12)):
+            err = np.abs(outs[0][f] - outs[alt][f]).max() / np.abs(outs[0][f]).max()
+            assert err <= tol, (f, alt, err)
     if sph is not None:
         from oracle.swe import OracleState, linear_coriolis
         o = linear_coriolis(OracleState(sph, 1e3 * c[0], 1e-5 * c[1], 1e-6 * c[2],
                                         np.full(B, 9.80616 * 29400.0)))
         for f in (1, 2):
-            assert np.abs(outs[1][f] - o[f]).max() <= 1e-12 * np.abs(o[f]).max()
+            for alt in (1, 2):
+                assert np.abs(outs[alt][f] - o[f]).max() <= 1e-12 * np.abs(o[f]).max()
+
+
+def test_spectral_coriolis_edge_modes(mods):
+    """Inputs the pseudospectral path drops (Im of m = 0, the n = 0 modes) are
+    dropped by the spectral recurrence too; m = M and n = M rows included."""
+    spharm, dynamics, _, _ = mods
+    from paper_2306_09497_b200 import _lib
+    from oracle.sht import OracleSphere
+    from oracle.swe import OracleState, linear_coriolis
+    M, B = 12, 3
+    grid, sph = spharm.get_grid(M), OracleSphere(M)
+    rng = np.random.default_rng(7)
+    c = [rng.standard_normal((B, grid.n_modes)) + 1j * rng.standard_normal((B, grid.n_modes))
+         for _ in range(3)]
+    s = dynamics.PrognosticState.from_fields(grid, c[0], c[1], c[2], [3e4] * B)
+    o = linear_coriolis(OracleState(sph, c[0], c[1], c[2], np.full(B, 3e4)))
+    try:
+        for fast in (0, 1, 2):
+            _lib.set_option("fast_coriolis", fast)
+            t = dynamics.linear_coriolis(s)
+            for f in (1, 2):
+                got = t[f].cpu().numpy()
+                assert np.abs(got - o[f]).max() <= 1e-12 * np.abs(o[f]).max(), (fast, f)
+    finally:
+        _lib.set_option("fast_coriolis", 2)
