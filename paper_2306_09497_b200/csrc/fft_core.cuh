@@ -15,12 +15,10 @@ SWE_DEV double2 twd(const double2 *tw, int e, double dir) {
   return w;
 }
 
-// y_t = sum_q v_q exp(dir 2 pi i q t / R), optionally times exp(dir 2 pi i t kt / N2),
-// stored to dst[t*stride].  cr/sr hold cos/sin(2 pi e / R) for e = 0..(R-1)/2.
+// y_t = sum_q v_q exp(dir 2 pi i q t / R); cr/sr hold cos/sin(2 pi e / R) for
+// e = 0..(R-1)/2 (v is clobbered)
 template <int R>
-SWE_DEV void dft_store(double2 (&v)[R], double dir, const double *cr, const double *sr,
-                       double2 *dst, int stride, const double2 *tw, int kt) {
-  double2 y[R];
+SWE_DEV void dft(double2 (&v)[R], double dir, const double *cr, const double *sr, double2 (&y)[R]) {
   if constexpr (R == 2) {
     y[0] = make_double2(v[0].x + v[1].x, v[0].y + v[1].y);
     y[1] = make_double2(v[0].x - v[1].x, v[0].y - v[1].y);
@@ -62,6 +60,14 @@ SWE_DEV void dft_store(double2 (&v)[R], double dir, const double *cr, const doub
       y[R - t] = make_double2(re + dir * sy, im - dir * sx);
     }
   }
+}
+
+// dft, optionally times exp(dir 2 pi i t kt / N2), stored to dst[t*stride]
+template <int R>
+SWE_DEV void dft_store(double2 (&v)[R], double dir, const double *cr, const double *sr,
+                       double2 *dst, int stride, const double2 *tw, int kt) {
+  double2 y[R];
+  dft<R>(v, dir, cr, sr, y);
 #pragma unroll
   for (int t = 0; t < R; ++t) dst[t * stride] = (kt && t) ? cm(y[t], twd(tw, t * kt, dir)) : y[t];
 }

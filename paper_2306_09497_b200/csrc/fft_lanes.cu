@@ -23,11 +23,18 @@ namespace {
 constexpr int LW = 16;  // rows per CTA: a half-warp covers them, so each warp runs two
                         // butterflies per instruction and two CTAs fit on an SM
 
-// MODE 0 DIT, 1 DIF, 2 prime-factor (no twiddles); see fft.cu
-template <int R, int MODE>
+// Shared-memory position of (slot, row): the 16 rows of a slot stay one 256-byte
+// line, permuted by the slot (XOR swizzle), so that accesses to one row across
+// consecutive slots (put_z, the grid products, extraction) spread over the banks
+// while a butterfly's 16 (or 8) rows of one slot remain a conflict-free line.
+SWE_DEV int xs(int slot, int row) { return slot * LW + (row ^ ((slot << 1) & (LW - 1))); }
+
+// MODE 0 DIT, 1 DIF, 2 prime-factor (no twiddles); see fft.cu.  RW rows take part
+// (RW lanes per butterfly, 32/RW butterflies per warp instruction).
+template <int R, int MODE, int RW>
 SWE_DEV void lane_stage(double2 *X, int N2, int Lp, double dir, const double2 *tw, int warp,
                         int nw, int lane) {
-  constexpr int H = (R - 1) / 2;
+  constexpr int H = (R - 1) / 2, BW = 32 / RW;
   double cr[H + 1], sr[H + 1];
   if constexpr (R != 2 && R != 4) {
 #pragma unroll
@@ -38,30 +45,33 @@ SWE_DEV void lane_stage(double2 *X, int N2, int Lp, double dir, const double2 *t
     }
   }
   const int L = Lp * R, nbf = N2 / R, tws = N2 / L;
-  const int row = lane & (LW - 1);
-  for (int bf = 2 * warp + (lane >> 4); bf < nbf; bf += 2 * nw) {
+  const int row = lane & (RW - 1);
+  for (int bf = BW * warp + lane / RW; bf < nbf; bf += BW * nw) {
     const int g = bf / Lp, k = bf - g * Lp, base = g * L + k;
-    double2 v[R];
+    double2 v[R], y[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      v[q] = X[(base + q * Lp) * LW + row];
+      v[q] = X[xs(base + q * Lp, row)];
       if (MODE == 0 && q && k) v[q] = cm(v[q], twd(tw, q * k * tws, dir));
     }
-    dft_store<R>(v, dir, cr, sr, X + base * LW + row, Lp * LW, tw, MODE == 1 ? k * tws : 0);
+    dft<R>(v, dir, cr, sr, y);
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+      X[xs(base + t * Lp, row)] = (MODE == 1 && t && k) ? cm(y[t], twd(tw, t * k * tws, dir)) : y[t];
   }
 }
 
-template <int MODE>
+template <int MODE, int RW>
 SWE_DEV void lane_run_stage(double2 *X, int N2, int Lp, int R, double dir, const double2 *tw,
                             int warp, int nw, int lane) {
   switch (R) {
-    case 2: lane_stage<2, MODE>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 3: lane_stage<3, MODE>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 4: lane_stage<4, MODE>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 5: lane_stage<5, MODE>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 7: lane_stage<7, MODE>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 11: lane_stage<11, MODE>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    default: lane_stage<13, MODE>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 2: lane_stage<2, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 3: lane_stage<3, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 4: lane_stage<4, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 5: lane_stage<5, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 7: lane_stage<7, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 11: lane_stage<11, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    default: lane_stage<13, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
   }
 }
 
@@ -75,18 +85,20 @@ SWE_DEV int lrow(const LCtx &c, int f, int h, int s) { return (f * 2 + h) * c.S 
 SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
   int Lp = 1;
   for (int s = 0; s < a.nst; ++s) {
-    if (a.pfa) lane_run_stage<2>(c.X, a.N2, Lp, a.radix[s], 1.0, a.tw, c.warp, c.nw, c.lane);
-    else lane_run_stage<0>(c.X, a.N2, Lp, a.radix[s], 1.0, a.tw, c.warp, c.nw, c.lane);
+    if (a.pfa) lane_run_stage<2, LW>(c.X, a.N2, Lp, a.radix[s], 1.0, a.tw, c.warp, c.nw, c.lane);
+    else lane_run_stage<0, LW>(c.X, a.N2, Lp, a.radix[s], 1.0, a.tw, c.warp, c.nw, c.lane);
     Lp *= a.radix[s];
     __syncthreads();
   }
 }
 
+// forward transform of rows 0..RW-1
+template <int RW = LW>
 SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
   if (a.pfa) {
     int Lp = 1;
     for (int s = 0; s < a.nst; ++s) {
-      lane_run_stage<2>(c.X, a.N2, Lp, a.radix[s], -1.0, a.tw, c.warp, c.nw, c.lane);
+      lane_run_stage<2, RW>(c.X, a.N2, Lp, a.radix[s], -1.0, a.tw, c.warp, c.nw, c.lane);
       Lp *= a.radix[s];
       __syncthreads();
     }
@@ -95,7 +107,7 @@ SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
   int L = a.N2;
   for (int s = a.nst - 1; s >= 0; --s) {
     const int R = a.radix[s];
-    lane_run_stage<1>(c.X, a.N2, L / R, R, -1.0, a.tw, c.warp, c.nw, c.lane);
+    lane_run_stage<1, RW>(c.X, a.N2, L / R, R, -1.0, a.tw, c.warp, c.nw, c.lane);
     L /= R;
     __syncthreads();
   }
@@ -106,19 +118,19 @@ SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
 SWE_DEV void put_z(const FftArgs &a, const LCtx &c, int row, int k, double2 Xk, double2 Xc) {
   const int N2 = a.N2;
   if (k == 0) {
-    c.X[__ldg(a.pos_z) * LW + row] = make_double2(Xk.x, Xk.x);
+    c.X[xs(__ldg(a.pos_z), row)] = make_double2(Xk.x, Xk.x);
     return;
   }
   const int k2 = N2 - k;
   const double2 A = make_double2(Xk.x + Xc.x, Xk.y - Xc.y);
   const double2 D = make_double2(Xk.x - Xc.x, Xk.y + Xc.y);
   const double2 Bk = cm(D, __ldg(a.twh + k));
-  c.X[__ldg(a.pos_z + k) * LW + row] = make_double2(A.x - Bk.y, A.y + Bk.x);
+  c.X[xs(__ldg(a.pos_z + k), row)] = make_double2(A.x - Bk.y, A.y + Bk.x);
   if (k2 != k) {
     const double2 A2 = make_double2(Xc.x + Xk.x, Xc.y - Xk.y);
     const double2 D2 = make_double2(Xc.x - Xk.x, Xc.y + Xk.y);
     const double2 B2 = cm(D2, __ldg(a.twh + k2));
-    c.X[__ldg(a.pos_z + k2) * LW + row] = make_double2(A2.x - B2.y, A2.y + B2.x);
+    c.X[xs(__ldg(a.pos_z + k2), row)] = make_double2(A2.x - B2.y, A2.y + B2.x);
   }
 }
 
@@ -163,11 +175,11 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, const double *src, in
 
 // grid sample n of row r lives in X[pos_g[n/2]][r].{x,y}
 SWE_DEV double &gval(const FftArgs &a, const LCtx &c, int n, int row) {
-  double *p = reinterpret_cast<double *>(c.X + __ldg(a.pos_g + (n >> 1)) * LW + row);
+  double *p = reinterpret_cast<double *>(c.X + xs(__ldg(a.pos_g + (n >> 1)), row));
   return p[n & 1];
 }
 SWE_DEV double &gslot(const LCtx &c, int p, int h, int row) {
-  return reinterpret_cast<double *>(c.X + p * LW + row)[h];
+  return reinterpret_cast<double *>(c.X + xs(p, row))[h];
 }
 
 SWE_DEV void lane_load_grid(const FftArgs &a, const LCtx &c, const double *src, int f) {
@@ -194,8 +206,8 @@ SWE_DEV void lane_store_grid(const FftArgs &a, const LCtx &c, double *dst, int f
 // F+ = scale (fm_N + fm_S), F- = scale (fm_N - fm_S)  ->  a.out[o] [m][2][Jp][ld]
 SWE_DEV double2 row_fm(const FftArgs &a, const LCtx &c, int row, int k) {
   const int N2 = a.N2;
-  const double2 zk = c.X[__ldg(a.pos_z + k) * LW + row];
-  const double2 z2 = c.X[__ldg(a.pos_z + (k == 0 ? 0 : N2 - k)) * LW + row];
+  const double2 zk = c.X[xs(__ldg(a.pos_z + k), row)];
+  const double2 z2 = c.X[xs(__ldg(a.pos_z + (k == 0 ? 0 : N2 - k)), row)];
   const double2 Sg = make_double2(zk.x + z2.x, zk.y - z2.y);
   const double2 D = make_double2(zk.y + z2.y, -(zk.x - z2.x));
   double2 w = __ldg(a.twh + k);
@@ -234,11 +246,13 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
   LCtx c;
   c.X = reinterpret_cast<double2 *>(smem_raw);
   c.S = fft_lane_slices(OP);
-  c.p = blockIdx.x;
+  // consecutive CTAs take consecutive slice groups of one pair: they share the
+  // 32-byte sectors of the [m][2][Jp][ld] rows, which then hit in L2
+  c.p = blockIdx.y;
   c.jn = c.p;
   c.js = a.J - 1 - c.p;
   c.eq = c.js == c.jn;
-  c.b0 = blockIdx.y * c.S;
+  c.b0 = blockIdx.x * c.S;
   c.nsl = min(c.S, a.nslices - c.b0);
   c.tid = threadIdx.x;
   c.nthr = blockDim.x;
@@ -278,7 +292,7 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
     lane_ifft(a, c);
     const double cs = a.coslat[p], fc = a.fcor[p];
     for (int idx = c.tid; idx < a.N2 * LW; idx += c.nthr) {
-      const int row = idx & (LW - 1);
+      const int row = (idx & (LW - 1)) ^ (((idx / LW) << 1) & (LW - 1));  // undo xs()
       const double fr = ((row / S) & 1) ? -fc : fc;
       const double2 z = c.X[idx];
       c.X[idx] = make_double2((fr * (z.x * ia)) * cs, (fr * (z.y * ia)) * cs);
@@ -295,9 +309,10 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
     __syncthreads();
     lane_ifft(a, c);
     const double cs = a.coslat[p];
+    // lanes: (slot, hemisphere, x/y) fastest, so a half-warp reads one bank each
     for (int idx = c.tid; idx < I * 2 * S; idx += c.nthr) {
-      const int n = idx / (2 * S), hs = idx - n * 2 * S, pp = n >> 1, hh = n & 1;
-      const int h = hs / S, s = hs - h * S;
+      const int s = idx / (2 * I), r = idx - s * 2 * I;
+      const int pp = r >> 2, h = (r >> 1) & 1, hh = r & 1;
       auto R = [&](int f) -> double & { return gslot(c, pp, hh, lrow(c, f, h, s)); };
       const double u = R(0) * ia, v = R(1) * ia, gx = R(2) * ia, gy = R(3) * ia;
       const double xi = R(4), ph = R(5), de = R(6);
@@ -307,7 +322,7 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
       R(3) = (xi * v) * cs;                  // (xi v) cos
     }
     __syncthreads();
-    lane_fft(a, c);
+    lane_fft<8>(a, c);  // only the 4 product fields x 2 hemispheres (rows 0..7, S = 1)
     const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
     lane_extract(a, c, 0, 0, w);
     lane_extract(a, c, 1, 1, w);
@@ -325,7 +340,7 @@ static int launch_lanes(const FftArgs &a, int smem, int nthreads, cudaStream_t s
     attr = smem;
   }
   const int S = fft_lane_slices(OP);
-  dim3 grid(a.Jh, (a.nslices + S - 1) / S);
+  dim3 grid((a.nslices + S - 1) / S, a.Jh);
   fft_lanes_kernel<OP><<<grid, nthreads, smem, st>>>(a);
   SWE_LAUNCH_CHECK();
   return OK;
