@@ -46,8 +46,9 @@ SWE_DEV void lane_stage(double2 *X, int N2, int Lp, double dir, const double2 *t
   }
   const int L = Lp * R, nbf = N2 / R, tws = N2 / L;
   const int row = lane & (RW - 1);
+  const float inv_lp = 1.0f / (float)Lp;  // exact quotient for bf < 2^12 (N2 <= 4096)
   for (int bf = BW * warp + lane / RW; bf < nbf; bf += BW * nw) {
-    const int g = bf / Lp, k = bf - g * Lp, base = g * L + k;
+    const int g = (int)(((float)bf + 0.5f) * inv_lp), k = bf - g * Lp, base = g * L + k;
     double2 v[R], y[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
@@ -115,60 +116,68 @@ SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
 
 // Z of one hemisphere row from its half spectrum X (see fft.cu build comment):
 //   Z[k] = (X[k] + conj X[N2-k]) + i w^k (X[k] - conj X[N2-k])
-SWE_DEV void put_z(const FftArgs &a, const LCtx &c, int row, int k, double2 Xk, double2 Xc) {
-  const int N2 = a.N2;
+// (w1, w2) = twh[k], twh[N2-k] and (z1, z2) = pos_z[k], pos_z[N2-k], prefetched
+SWE_DEV void put_z(const LCtx &c, int row, int k, int k2, double2 Xk, double2 Xc, double2 w1,
+                   double2 w2, int z1, int z2) {
   if (k == 0) {
-    c.X[xs(__ldg(a.pos_z), row)] = make_double2(Xk.x, Xk.x);
+    c.X[xs(z1, row)] = make_double2(Xk.x, Xk.x);
     return;
   }
-  const int k2 = N2 - k;
   const double2 A = make_double2(Xk.x + Xc.x, Xk.y - Xc.y);
   const double2 D = make_double2(Xk.x - Xc.x, Xk.y + Xc.y);
-  const double2 Bk = cm(D, __ldg(a.twh + k));
-  c.X[xs(__ldg(a.pos_z + k), row)] = make_double2(A.x - Bk.y, A.y + Bk.x);
+  const double2 Bk = cm(D, w1);
+  c.X[xs(z1, row)] = make_double2(A.x - Bk.y, A.y + Bk.x);
   if (k2 != k) {
     const double2 A2 = make_double2(Xc.x + Xk.x, Xc.y - Xk.y);
     const double2 D2 = make_double2(Xc.x - Xk.x, Xc.y + Xk.y);
-    const double2 B2 = cm(D2, __ldg(a.twh + k2));
-    c.X[xs(__ldg(a.pos_z + k2), row)] = make_double2(A2.x - B2.y, A2.y + B2.x);
+    const double2 B2 = cm(D2, w2);
+    c.X[xs(z2, row)] = make_double2(A2.x - B2.y, A2.y + B2.x);
   }
 }
 
-// field f: E/O half spectra [m][2][Jp][ld] of pair p -> Z of its north and south rows.
-// sub (nullable, per slice) is subtracted from E at m = 0 (phi_prime, dynamics.py:52-56).
-SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, const double *src, int f,
-                          const double *sub) {
+// fields a.in[0..nf-1]: E/O half spectra [m][2][Jp][ld] of pair p -> Z of their north
+// and south rows.  One flattened loop over (field, k pair, slice) keeps many loads in
+// flight; field `subf` has phisub subtracted from E at m = 0 (phi_prime,
+// dynamics.py:52-56).
+SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1, S = c.S;
   const size_t eo = (size_t)a.Jp * a.ld / 2;  // E -> O offset (double2)
-  const double2 *base = reinterpret_cast<const double2 *>(src + (size_t)c.p * a.ld) + c.b0;
   const size_t mstride = 2 * eo;
-  const int total = npair * S;
+  const int per = npair * S, total = nf * per;
   constexpr int U = 2;
   for (int i0 = c.tid; i0 < total; i0 += U * c.nthr) {
-    double2 e[U], o[U], e2[U], o2[U];
+    double2 e[U], o[U], e2[U], o2[U], w1[U], w2[U];
+    int z1[U], z2[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
-      const int k = idx / S, s = idx - k * S;
+      const int f = idx / per, r = idx - f * per, k = r / S, s = r - k * S;
       const bool ok = idx < total && s < c.nsl;
       const int k2 = k == 0 ? N2 : N2 - k;
       const double2 z = make_double2(0.0, 0.0);
+      const double2 *base =
+          reinterpret_cast<const double2 *>(a.in[ok ? f : 0] + (size_t)c.p * a.ld) + c.b0;
       const double2 *pk = base + (size_t)k * mstride + s, *pk2 = base + (size_t)k2 * mstride + s;
       e[u] = (ok && k <= M) ? __ldg(pk) : z;
       o[u] = (ok && k <= M) ? __ldg(pk + eo) : z;
       e2[u] = (ok && k2 <= M) ? __ldg(pk2) : z;
       o2[u] = (ok && k2 <= M) ? __ldg(pk2 + eo) : z;
+      w1[u] = ok ? __ldg(a.twh + k) : z;
+      w2[u] = (ok && k) ? __ldg(a.twh + k2) : z;
+      z1[u] = ok ? __ldg(a.pos_z + k) : 0;
+      z2[u] = (ok && k) ? __ldg(a.pos_z + k2) : 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
-      const int k = idx / S, s = idx - k * S;
+      const int f = idx / per, r = idx - f * per, k = r / S, s = r - k * S;
       if (idx >= total || s >= c.nsl) continue;
-      if (sub != nullptr && k == 0) e[u].x -= sub[c.b0 + s];
-      put_z(a, c, lrow(c, f, 0, s), k, make_double2(e[u].x + o[u].x, e[u].y + o[u].y),
-            make_double2(e2[u].x + o2[u].x, e2[u].y + o2[u].y));
-      put_z(a, c, lrow(c, f, 1, s), k, make_double2(e[u].x - o[u].x, e[u].y - o[u].y),
-            make_double2(e2[u].x - o2[u].x, e2[u].y - o2[u].y));
+      if (f == subf && k == 0) e[u].x -= a.phisub[c.b0 + s];
+      const int k2 = N2 - k;
+      put_z(c, lrow(c, f, 0, s), k, k2, make_double2(e[u].x + o[u].x, e[u].y + o[u].y),
+            make_double2(e2[u].x + o2[u].x, e2[u].y + o2[u].y), w1[u], w2[u], z1[u], z2[u]);
+      put_z(c, lrow(c, f, 1, s), k, k2, make_double2(e[u].x - o[u].x, e[u].y - o[u].y),
+            make_double2(e2[u].x - o2[u].x, e2[u].y - o2[u].y), w1[u], w2[u], z1[u], z2[u]);
     }
   }
 }
@@ -203,35 +212,37 @@ SWE_DEV void lane_store_grid(const FftArgs &a, const LCtx &c, double *dst, int f
 }
 
 // fm[k] (k = 0..M) of rows (f, h, s): fm = (Ge + w^{-k} Go) / I, see fft.cu;
-// F+ = scale (fm_N + fm_S), F- = scale (fm_N - fm_S)  ->  a.out[o] [m][2][Jp][ld]
-SWE_DEV double2 row_fm(const FftArgs &a, const LCtx &c, int row, int k) {
-  const int N2 = a.N2;
-  const double2 zk = c.X[xs(__ldg(a.pos_z + k), row)];
-  const double2 z2 = c.X[xs(__ldg(a.pos_z + (k == 0 ? 0 : N2 - k)), row)];
-  const double2 Sg = make_double2(zk.x + z2.x, zk.y - z2.y);
-  const double2 D = make_double2(zk.y + z2.y, -(zk.x - z2.x));
-  double2 w = __ldg(a.twh + k);
-  w.y = -w.y;
+// F+ = scale (fm_N + fm_S), F- = scale (fm_N - fm_S)  ->  a.out[f] [m][2][Jp][ld]
+// (z1, z2) = slots of Z[k], Z[N2-k]; w = conj twh[k]
+SWE_DEV double2 row_fm(const LCtx &c, int row, int z1, int z2, double2 w) {
+  const double2 zk = c.X[xs(z1, row)];
+  const double2 zc = c.X[xs(z2, row)];
+  const double2 Sg = make_double2(zk.x + zc.x, zk.y - zc.y);
+  const double2 D = make_double2(zk.y + zc.y, -(zk.x - zc.x));
   const double2 t = cm(w, D);
   return make_double2(Sg.x + t.x, Sg.y + t.y);  // 2 * I * fm
 }
 
-SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, int f, int o, double scale) {
-  const int M = a.M, S = c.S;
-  const double h = 0.5 * scale;
+// fields 0..nf-1 -> a.out[f], scaled by w01 (fields 0, 1) or w23 (2, 3); one flattened loop
+SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, int nf, double w01, double w23) {
+  const int M = a.M, S = c.S, N2 = a.N2, per = (M + 1) * S;
   const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
-  double2 *dst = reinterpret_cast<double2 *>(a.out[o] + (size_t)c.p * a.ld) + c.b0;
-  for (int idx = c.tid; idx < (M + 1) * S; idx += c.nthr) {
-    const int k = idx / S, s = idx - k * S;
+  for (int idx = c.tid; idx < nf * per; idx += c.nthr) {
+    const int f = idx / per, r = idx - f * per, k = r / S, s = r - k * S;
     if (s >= c.nsl) continue;
-    const double2 fn = row_fm(a, c, lrow(c, f, 0, s), k);
-    double2 *d = dst + (size_t)k * 2 * pm + s;
+    const int z1 = __ldg(a.pos_z + k), z2 = __ldg(a.pos_z + (k == 0 ? 0 : N2 - k));
+    double2 w = __ldg(a.twh + k);
+    w.y = -w.y;
+    const double h = 0.5 * (f < 2 ? w01 : w23);
+    double2 *d = reinterpret_cast<double2 *>(a.out[f] + (size_t)c.p * a.ld) + c.b0 +
+                 (size_t)k * 2 * pm + s;
+    const double2 fn = row_fm(c, lrow(c, f, 0, s), z1, z2, w);
     if (c.eq) {
       const double2 v = make_double2(fn.x * h, fn.y * h);
       d[0] = v;
       d[pm] = v;
     } else {
-      const double2 fs = row_fm(a, c, lrow(c, f, 1, s), k);
+      const double2 fs = row_fm(c, lrow(c, f, 1, s), z1, z2, w);
       d[0] = make_double2((fn.x + fs.x) * h, (fn.y + fs.y) * h);
       d[pm] = make_double2((fn.x - fs.x) * h, (fn.y - fs.y) * h);
     }
@@ -264,7 +275,7 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
 
   if constexpr (OP == FOP_SYNTH_GRID || OP == FOP_SYNTH2_GRID) {
     constexpr int NF = OP == FOP_SYNTH_GRID ? 1 : 2;
-    for (int f = 0; f < NF; ++f) lane_load_eo(a, c, a.in[f], f, nullptr);
+    lane_load_eo(a, c, NF, -1);
     __syncthreads();
     lane_ifft(a, c);
     const double sc = (OP == FOP_SYNTH2_GRID || a.scale_mode) ? ia : 1.0;
@@ -283,11 +294,10 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
     }
     lane_fft(a, c);
     const double w = OP == FOP_ANALYSIS ? a.wq[p] * a.inv_I : a.wsin2[p] * a.inv_I * a.inv_a;
-    for (int f = 0; f < NF; ++f) lane_extract(a, c, f, f, w);
+    lane_extract(a, c, NF, w, w);
   } else if constexpr (OP == FOP_CORIOLIS) {
     // linear_coriolis (dynamics.py:129-135): f u, f v -> vortdiv_from_uv; f = -f on the south row
-    lane_load_eo(a, c, a.in[0], 0, nullptr);
-    lane_load_eo(a, c, a.in[1], 1, nullptr);
+    lane_load_eo(a, c, 2, -1);
     __syncthreads();
     lane_ifft(a, c);
     const double cs = a.coslat[p], fc = a.fcor[p];
@@ -300,12 +310,11 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
     __syncthreads();
     lane_fft(a, c);
     const double w = a.wsin2[p] * a.inv_I * a.inv_a;
-    lane_extract(a, c, 0, 0, w);
-    lane_extract(a, c, 1, 1, w);
+    lane_extract(a, c, 2, w, w);
   } else if constexpr (OP == FOP_NONLINEAR) {
     // nonlinear_advection + nonlinear_rest (dynamics.py:142-160)
     // in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi, 5 Phi (phi_prime applied here), 6 delta
-    for (int f = 0; f < 7; ++f) lane_load_eo(a, c, a.in[f], f, f == 5 ? a.phisub : nullptr);
+    lane_load_eo(a, c, 7, 5);
     __syncthreads();
     lane_ifft(a, c);
     const double cs = a.coslat[p];
@@ -324,10 +333,7 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
     __syncthreads();
     lane_fft<8>(a, c);  // only the 4 product fields x 2 hemispheres (rows 0..7, S = 1)
     const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
-    lane_extract(a, c, 0, 0, w);
-    lane_extract(a, c, 1, 1, w);
-    lane_extract(a, c, 2, 2, wv);
-    lane_extract(a, c, 3, 3, wv);
+    lane_extract(a, c, 4, w, wv);
   }
 }
 
