@@ -136,9 +136,10 @@ SWE_DEV double2 *row_of(const FftArgs &a, const Ctx &c, int f, int s) {
 // Z in spectral slot order:  Z[k] = (X[k] + conj X[N2-k]) + i w^k (X[k] - conj X[N2-k])
 // with w = e^{2 pi i / I}, so IDFT_N2(Z)[r] = g[2r] + i g[2r+1],
 // g = irfft(X * I, n = I) (numpy drops Im X[0]).  sub (nullable) is
-// subtracted from E at m = 0 (phi_prime, dynamics.py:52-56).
+// subtracted from E at m = 0 (phi_prime, dynamics.py:52-56); imk: X -> i m X
+// (longitude derivative of the synthesised field).
 SWE_DEV void load_eo(const FftArgs &a, const Ctx &c, const double *src, int f, int h,
-                     const double *sub) {
+                     const double *sub, bool imk = false) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1;
   const size_t eo = (size_t)a.Jp * a.ld / 2;
   const double2 *base = reinterpret_cast<const double2 *>(src + (size_t)c.p * a.ld) + c.b0;
@@ -154,8 +155,12 @@ SWE_DEV void load_eo(const FftArgs &a, const Ctx &c, const double *src, int f, i
     const double2 e2 = k2 <= M ? __ldg(base + (size_t)k2 * mstride + s) : z;
     const double2 o2 = k2 <= M ? __ldg(base + (size_t)k2 * mstride + eo + s) : z;
     if (sub != nullptr && k == 0) e.x -= sub[c.b0 + s];
-    const double2 Xk = make_double2(e.x + sg * o.x, e.y + sg * o.y);
-    const double2 Xc = make_double2(e2.x + sg * o2.x, e2.y + sg * o2.y);
+    double2 Xk = make_double2(e.x + sg * o.x, e.y + sg * o.y);
+    double2 Xc = make_double2(e2.x + sg * o2.x, e2.y + sg * o2.y);
+    if (imk) {
+      Xk = make_double2(-(double)k * Xk.y, (double)k * Xk.x);
+      Xc = make_double2(-(double)k2 * Xc.y, (double)k2 * Xc.x);
+    }
     if (k == 0) {
       x[__ldg(a.pos_z)] = make_double2(Xk.x, Xk.x);
       continue;
@@ -326,7 +331,8 @@ __global__ void __launch_bounds__(256) fft_kernel(const __grid_constant__ FftArg
     } else if constexpr (OP == FOP_NONLINEAR) {
       // nonlinear_advection + nonlinear_rest (dynamics.py:142-160)
       // in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi, 5 Phi (phi_prime applied here), 6 delta
-      for (int f = 0; f < 4; ++f) load_eo(a, c, a.in[f], f, h, nullptr);
+      for (int f = 0; f < 4; ++f)
+        load_eo(a, c, (f == 2 && a.dlam) ? a.in[5] : a.in[f], f, h, nullptr, f == 2 && a.dlam);
       __syncthreads();
       c2r_fields(a, c, 0, 4);
       __syncthreads();

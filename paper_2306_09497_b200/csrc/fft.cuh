@@ -43,6 +43,8 @@ struct FftArgs {
   double inv_I, inv_a;
   int Jh, Jp;                   // latitude pairs (incl. equator), padded pair count
   const double *phisub;         // [slice] phibar*sqrt2*P_00, subtracted from field 5 (FOP_NONLINEAR)
+  int dlam;                     // FOP_NONLINEAR: field 2 (d_lambda Phi) is i m times field 5's
+                                // half spectrum (in[2] unused): saves one synthesis term
   const double *in[FFT_MAXF];   // E/O half spectra      [m][2][Jp][ld]
   double *out[FFT_MAXF];        // F+/F- analysis inputs [m][2][Jp][ld]
   const double *gin[2];         // grids [slice][J][I]

@@ -138,7 +138,7 @@ SWE_DEV void put_z(const LCtx &c, int row, int k, int k2, double2 Xk, double2 Xc
 // fields a.in[0..nf-1]: E/O half spectra [m][2][Jp][ld] of pair p -> Z of their north
 // and south rows.  One flattened loop over (field, k pair, slice) keeps many loads in
 // flight; field `subf` has phisub subtracted from E at m = 0 (phi_prime,
-// dynamics.py:52-56).
+// dynamics.py:52-56).  With a.dlam, field 2 is i m times field 5 (d_lambda Phi).
 SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1, S = c.S;
   const size_t eo = (size_t)a.Jp * a.ld / 2;  // E -> O offset (double2)
@@ -155,8 +155,9 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
       const bool ok = idx < total && s < c.nsl;
       const int k2 = k == 0 ? N2 : N2 - k;
       const double2 z = make_double2(0.0, 0.0);
+      const int fs = (f == 2 && a.dlam) ? 5 : f;
       const double2 *base =
-          reinterpret_cast<const double2 *>(a.in[ok ? f : 0] + (size_t)c.p * a.ld) + c.b0;
+          reinterpret_cast<const double2 *>(a.in[ok ? fs : 0] + (size_t)c.p * a.ld) + c.b0;
       const double2 *pk = base + (size_t)k * mstride + s, *pk2 = base + (size_t)k2 * mstride + s;
       e[u] = (ok && k <= M) ? __ldg(pk) : z;
       o[u] = (ok && k <= M) ? __ldg(pk + eo) : z;
@@ -174,6 +175,13 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
       if (idx >= total || s >= c.nsl) continue;
       if (f == subf && k == 0) e[u].x -= a.phisub[c.b0 + s];
       const int k2 = N2 - k;
+      if (f == 2 && a.dlam) {  // i m X (m = k for e/o, N2 - k for e2/o2)
+        const double mk = k, mk2 = k2;
+        e[u] = make_double2(-mk * e[u].y, mk * e[u].x);
+        o[u] = make_double2(-mk * o[u].y, mk * o[u].x);
+        e2[u] = make_double2(-mk2 * e2[u].y, mk2 * e2[u].x);
+        o2[u] = make_double2(-mk2 * o2[u].y, mk2 * o2[u].x);
+      }
       put_z(c, lrow(c, f, 0, s), k, k2, make_double2(e[u].x + o[u].x, e[u].y + o[u].y),
             make_double2(e2[u].x + o2[u].x, e2[u].y + o2[u].y), w1[u], w2[u], z1[u], z2[u]);
       put_z(c, lrow(c, f, 1, s), k, k2, make_double2(e[u].x - o[u].x, e[u].y - o[u].y),

@@ -331,22 +331,23 @@ int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], d
   int rc;
   {
     LegArgs a = leg_args(r);
-    a.nout = 7;
+    a.nout = 6;
+    // d_lambda Phi = i m (P Phi) is formed in the FFT loader from output 5 (FftArgs::dlam)
     LegTerm hu = term(H, U[1], -1.0, 0, il), hv = term(H, U[2], 1.0, 0, il);
     set_out(a, 0, r.half(0), term(P, U[2], 1.0, 1, il), &hu, H);          // u
     set_out(a, 1, r.half(1), term(P, U[1], 1.0, 1, il), &hv, H);          // v
-    set_out(a, 2, r.half(2), term(P, U[0], 1.0, 1), nullptr, H);          // d_lambda Phi
-    set_out(a, 3, r.half(3), term(H, U[0], 1.0), nullptr, H);             // H Phi
-    set_out(a, 4, r.half(4), term(P, U[1]), nullptr, H);                  // xi
-    set_out(a, 5, r.half(5), term(P, U[0]), nullptr, H);  // Phi (phi_prime shift in the FFT)
-    set_out(a, 6, r.half(6), term(P, U[2]), nullptr, H);                  // delta
+    set_out(a, 2, r.half(3), term(H, U[0], 1.0), nullptr, H);             // H Phi
+    set_out(a, 3, r.half(4), term(P, U[1]), nullptr, H);                  // xi
+    set_out(a, 4, r.half(5), term(P, U[0]), nullptr, H);  // Phi (phi_prime shift in the FFT)
+    set_out(a, 5, r.half(6), term(P, U[2]), nullptr, H);                  // delta
     if ((rc = synth(r, a))) return rc;
   }
   {
     FftArgs f;
     memset(&f, 0, sizeof(f));
-    for (int i = 0; i < 7; ++i) f.in[i] = r.half(i);
+    for (int i = 0; i < 7; ++i) f.in[i] = i == 2 ? nullptr : r.half(i);
     for (int i = 0; i < 4; ++i) f.out[i] = r.fsp(i);
+    f.dlam = 1;
     if ((rc = fft(r, FOP_NONLINEAR, f))) return rc;
   }
   {
