@@ -370,6 +370,7 @@ void work_free(Work &w) {
   cudaFree(w.iters);
   cudaFree(w.counter);
   cudaFreeHost(w.h_counter);
+  cudaFreeHost(w.h_iters);
   cudaFree(w.phi0);
   cudaFree(w.phibar);
   w = Work();
@@ -421,6 +422,7 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaMalloc(&w.iters, (size_t)B * sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.counter, sizeof(int)));
   SWE_CUDA(cudaMallocHost(&w.h_counter, sizeof(int)));
+  SWE_CUDA(cudaMallocHost(&w.h_iters, (size_t)B * sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.phi0, (size_t)B * sizeof(double)));
   SWE_CUDA(cudaMalloc(&w.phibar, (size_t)B * sizeof(double)));
   w.cap = B;

@@ -27,6 +27,7 @@ struct Work {
   int *iters = nullptr;     // [cap]
   int *counter = nullptr;   // device counter (active slices)
   int *h_counter = nullptr; // pinned host mirror
+  int *h_iters = nullptr;   // [cap] pinned host mirror of iters
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
 };
@@ -62,5 +63,6 @@ struct swe_plan {
   int radix[swe::FFT_MAXST], ns[swe::FFT_MAXST];
   std::vector<int> h_offsets;
   swe::Work ws;
+  int iter_guess = 1;  // fixed-point iterations launched before the first host check
   size_t table_bytes = 0;
 };

@@ -155,22 +155,27 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 2) k_helm(int K, int B, con
                                               const double *lcd, double alpha, const double *eps,
                                               const double *phibar, double *U0, double *U1,
                                               double *U2, const int *active, double *stats,
-                                              CorOp cor) {
+                                              CorOp cor, const int *iters, int *counter) {
   // block: 32 slices x 8 mode rows; grid.x over slice tiles, grid.y over modes
   __shared__ unsigned long long red[8][32][6];
   const int b = blockIdx.x * 32 + threadIdx.x;
   unsigned long long mx[6] = {0, 0, 0, 0, 0, 0};
   const bool fused = cor.x != nullptr;
-  const double *O1 = fused ? cor.x : U1, *O2 = fused ? cor.d : U2;
+  if (counter && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+    *counter = 0;  // k_decide (stream-ordered after this kernel) counts afresh
   const bool act = (b < B) && (active == nullptr || active[b]);
-  const int k0 = blockIdx.y * blockDim.y + threadIdx.y, stride = gridDim.y * blockDim.y;
-  if (fused && b < B && !act) {  // converged slice: carry its iterate into the new buffers
-    for (int k = k0; k < K; k += stride) {
-      const size_t i = (size_t)k * B + b;
-      st2(U1, i, ld2(O1, i));
-      st2(U2, i, ld2(O2, i));
-    }
+  // fused: xi/delta ping-pong per slice between A = (cor.x, cor.d) and B = (U1, U2);
+  // the current iterate of slice b is in B when iters[b] is odd
+  CorOp src = cor;
+  double *W1 = U1, *W2 = U2;
+  if (fused && act && (iters[b] & 1)) {
+    src.x = U1;
+    src.d = U2;
+    W1 = const_cast<double *>(cor.x);
+    W2 = const_cast<double *>(cor.d);
   }
+  const double *O1 = fused ? src.x : U1, *O2 = fused ? src.d : U2;
+  const int k0 = blockIdx.y * blockDim.y + threadIdx.y, stride = gridDim.y * blockDim.y;
   if (act) {
     const double pb = phibar[b], apb = alpha * pb, aap = alpha * alpha * pb;
     for (int kb = k0; kb < K; kb += UN * stride) {
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 2) k_helm(int K, int B, con
           rd[u] = ld2(R2, i);
           if (fused) {
             double2 lx, ld;
-            cor_at(cor, k, b, B, lx, ld);
+            cor_at(src, k, b, B, lx, ld);
             rx[u] = add2(rx[u], sc2(alpha, lx));
             rd[u] = add2(rd[u], sc2(alpha, ld));
           } else if (lcx) {
@@ -220,8 +225,8 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 2) k_helm(int K, int B, con
           mx[5] = max(mx[5], sqmag_bits(de.x - o2[u].x, de.y - o2[u].y));
         }
         st2(U0, i, ph);
-        st2(U1, i, rx[u]);
-        st2(U2, i, de);
+        st2(W1, i, rx[u]);
+        st2(W2, i, de);
       }
     }
   }
@@ -234,6 +239,86 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 2) k_helm(int K, int B, con
       unsigned long long v = red[0][threadIdx.x][q];
       for (int r = 1; r < blockDim.y; ++r) v = max(v, red[r][threadIdx.x][q]);
       atomicMax(reinterpret_cast<unsigned long long *>(stats) + (size_t)b * 8 + q, v);
+    }
+  }
+}
+
+// Crank-Nicolson half step prologue (steppers.py:143-152) in one pass:
+//   X   = x0 + s (x1 + x2)                  (x1, x2 nullable: the Heun combination)
+//   R   = X + alpha (L_G X + L_C X)         (L_C spectral, omitted when c.nb == null)
+//   dst = helm(R)                           (first fixed-point iterate, no L_C)
+SWE_DEV double2 comb(const Ptr3C &x0, const Ptr3C &x1, const Ptr3C &x2, double s, int f,
+                     size_t i) {
+  if (!x1.p[f]) return ld2(x0.p[f], i);
+  const double2 a = ld2(x1.p[f], i), b = ld2(x2.p[f], i);
+  return add2(ld2(x0.p[f], i), sc2(s, make_double2(a.x + b.x, a.y + b.y)));
+}
+
+__global__ void __launch_bounds__(256) k_cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2,
+                                                  double s, double alpha, const double *eps,
+                                                  const double *phibar, CorOp c, Ptr3 R,
+                                                  Ptr3 dst) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
+    const double2 ph = comb(x0, x1, x2, s, 0, _i), xi = comb(x0, x1, x2, s, 1, _i),
+                  de = comb(x0, x1, x2, s, 2, _i);
+    const double pb = phibar[b], e = eps[k];
+    double2 lx = make_double2(0.0, 0.0), lc = lx;
+    if (c.nb) {  // L_C of X (plan.cu cor_cf), neighbours combined on the fly
+      const int2 nb = c.nb[k];
+      const double4 cf = c.cf[k];
+      double2 xl = lx, dl = lx, xh = lx, dh = lx;
+      if (nb.x >= 0) {
+        xl = comb(x0, x1, x2, s, 1, (size_t)nb.x * B + b);
+        dl = comb(x0, x1, x2, s, 2, (size_t)nb.x * B + b);
+      }
+      if (nb.y >= 0) {
+        xh = comb(x0, x1, x2, s, 1, (size_t)nb.y * B + b);
+        dh = comb(x0, x1, x2, s, 2, (size_t)nb.y * B + b);
+      }
+      lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * xi.y),
+                        -(cf.x * dl.y + cf.y * dh.y - cf.z * xi.x));
+      lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * de.y,
+                        cf.x * xl.y + cf.y * xh.y + cf.z * de.x);
+      if (cf.w != 0.0) {
+        lx.y = 0.0;
+        lc.y = 0.0;
+      }
+    }
+    // rhs = X + alpha * (L_G X + L_C X)  (as k_lin_rhs)
+    const double2 lphi = make_double2(-pb * de.x, -pb * de.y);
+    const double2 lde = add2(sc2(e, ph), lc);
+    const double2 r0 = add2(ph, sc2(alpha, lphi)), r1 = add2(xi, sc2(alpha, lx)),
+                  r2 = add2(de, sc2(alpha, lde));
+    st2(R.p[0], _i, r0);
+    st2(R.p[1], _i, r1);
+    st2(R.p[2], _i, r2);
+    // helm(R) (as k_helm without L_C)
+    const double apb = alpha * pb, denom = 1.0 + alpha * alpha * pb * e;
+    const double2 nph = make_double2((r0.x - apb * r2.x) / denom, (r0.y - apb * r2.y) / denom);
+    const double ae = alpha * e;
+    st2(dst.p[0], _i, nph);
+    st2(dst.p[1], _i, r1);
+    st2(dst.p[2], _i, make_double2(r2.x + ae * nph.x, r2.y + ae * nph.y));
+  }
+}
+
+// Fixed-point epilogue: slices whose iterate ended in the B buffers (odd iteration
+// count) copy xi/delta back to A = u[1], u[2]; with dtnu != 0 the viscosity
+// factor (dynamics.py:191-200) is applied to every slice on the way.
+__global__ void k_cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2,
+                            const int *iters, const double *nn1a2, double dtnu, double halfq) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
+    const bool odd = iters && (iters[b] & 1);
+    if (dtnu != 0.0) {
+      const double bh = 1.0 / (1.0 + dtnu * pow(nn1a2[k], halfq));
+      st2(u.p[0], _i, sc2(bh, ld2(u.p[0], _i)));
+      st2(u.p[1], _i, sc2(bh, ld2(odd ? b1 : u.p[1], _i)));
+      st2(u.p[2], _i, sc2(bh, ld2(odd ? b2 : u.p[2], _i)));
+    } else if (odd) {
+      st2(u.p[1], _i, ld2(b1, _i));
+      st2(u.p[2], _i, ld2(b2, _i));
     }
   }
 }
@@ -414,16 +499,33 @@ int coriolis_spec(int K, int B, const CorOp &c, double *lcx, double *lcd, cudaSt
 
 int helm(int K, int B, const double *const R[3], const double *lcx, const double *lcd,
          double alpha, const double *eps, const double *phibar, double *const U[3],
-         const int *active, double *stats, cudaStream_t st, const CorOp *cor) {
+         const int *active, double *stats, cudaStream_t st, const CorOp *cor, const int *iters,
+         int *counter) {
   const int ybl = std::max(1, std::min((K + 7) / 8, (148 * 8) / ((B + 31) / 32)));
   dim3 grid((B + 31) / 32, ybl), blk(32, 8);
   CorOp c = cor ? *cor : CorOp{nullptr, nullptr, nullptr, nullptr};
   if (cor)
     k_helm<2><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
-                                     U[1], U[2], active, stats, c);
+                                     U[1], U[2], active, stats, c, iters, counter);
   else
     k_helm<4><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
-                                     U[1], U[2], active, stats, c);
+                                     U[1], U[2], active, stats, c, iters, counter);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+             const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
+             cudaStream_t st) {
+  k_cn_start<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, x0, x1, x2, s, alpha, eps, phibar, c,
+                                                     R, dst);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2, const int *iters,
+              const double *nn1a2, double dtnu, double halfq, cudaStream_t st) {
+  k_cn_finish<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, u, b1, b2, iters, nn1a2, dtnu, halfq);
   SWE_LAUNCH_CHECK();
   return OK;
 }

@@ -37,12 +37,19 @@ struct CorOp {
   const double4 *cf;
 };
 int coriolis_spec(int K, int B, const CorOp &c, double *lcx, double *lcd, cudaStream_t st);
-// cor.x != nullptr: L_C is evaluated inline from (cor.x, cor.d), the previous
-// iterate, and the new xi/delta go to U[1], U[2] (distinct buffers; slices that
-// are no longer active copy their iterate across)
+// cor != nullptr: L_C is evaluated inline from the previous iterate, which for
+// slice b is in A = (cor->x, cor->d) when iters[b] is even and in B = (U[1], U[2])
+// when odd; the new xi/delta go to the other pair (Phi stays in U[0]).
+// counter (nullable) is zeroed for the k_decide that follows.
 int helm(int K, int B, const double *const R[3], const double *lcx, const double *lcd,
          double alpha, const double *eps, const double *phibar, double *const U[3],
-         const int *active, double *stats, cudaStream_t st, const CorOp *cor = nullptr);
+         const int *active, double *stats, cudaStream_t st, const CorOp *cor = nullptr,
+         const int *iters = nullptr, int *counter = nullptr);
+int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+             const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
+             cudaStream_t st);
+int cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2, const int *iters,
+              const double *nn1a2, double dtnu, double halfq, cudaStream_t st);
 int decide(int B, double *stats, int *active, int *iters, int *counter, double tol,
            cudaStream_t st);
 int fill_int(int *p, int n, int v, cudaStream_t st);

@@ -402,7 +402,8 @@ Bufs bufs(const Run &r) {
   return b;
 }
 
-// (I - a L) dst = (I + a L) src   (steppers.py:143-152, :74-118)
+// (I - a L) dst = (I + a L) src   (steppers.py:143-152, :74-118), with L_C evaluated
+// by the Legendre transforms (g_fast_coriolis 0 / 1); see cn_half_spec for the default
 int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *const src[3],
             double *const dst[3], double alpha, int *iters_host, double *resid_host) {
   swe_plan *pl = r.pl;
@@ -427,21 +428,9 @@ int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *con
   if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
   SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * 8 * B, r.st));
   int active = B;
-  // spectral Coriolis: L_C of the previous iterate is evaluated inside the Helmholtz
-  // update, so xi/delta ping-pong between dst and the LC buffers
-  const bool fused = g_fast_coriolis == 2;
-  double *cur[3] = {dst[0], dst[1], dst[2]}, *nxt[3] = {dst[0], b.LC[0], b.LC[1]};
   for (int it = 0; it < cfg.implicit_max_iter && active > 0; ++it) {
-    if (fused) {
-      ProfScope ps(3, 9.0 * 16.0 * K * B, r.st);  // rhs 3 + old 3 in, new 3 out
-      const CorOp c{cur[1], cur[2], pl->cor_nb, pl->cor_cf};
-      if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, nxt, w.flags, w.stats,
-                     r.st, &c)))
-        return rc;
-      std::swap(cur[1], nxt[1]);
-      std::swap(cur[2], nxt[2]);
-    } else {
-      if ((rc = eval_coriolis(r, dst[1], dst[2], b.LC[0], b.LC[1]))) return rc;
+    if ((rc = eval_coriolis(r, dst[1], dst[2], b.LC[0], b.LC[1]))) return rc;
+    {
       ProfScope ps(3, 11.0 * 16.0 * K * B, r.st);  // rhs 3 + lc 2 + old 3 in, new 3 out
       if ((rc = helm(K, B, Rc, b.LC[0], b.LC[1], alpha, pl->eps, w.phibar, dst, w.flags, w.stats,
                      r.st)))
@@ -453,14 +442,104 @@ int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *con
     SWE_CUDA(cudaStreamSynchronize(r.st));
     active = *w.h_counter;
   }
-  if (cur[1] != dst[1])
-    for (int f = 1; f < 3; ++f)
-      SWE_CUDA(cudaMemcpyAsync(dst[f], cur[f], (size_t)K * B * 16, cudaMemcpyDeviceToDevice, r.st));
   if (iters_host) {
     std::vector<int> it(B);
     SWE_CUDA(cudaMemcpyAsync(it.data(), w.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, r.st));
     SWE_CUDA(cudaStreamSynchronize(r.st));
     for (int i = 0; i < B; ++i) iters_host[2 * i] = it[i];
+  }
+  if (active > 0) {
+    // residual of the unconverged slices (steppers.py:113-118)
+    if ((rc = eval_coriolis(r, dst[1], dst[2], b.LC[0], b.LC[1]))) return rc;
+    SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * B, r.st));
+    Ptr3C u = {{dst[0], dst[1], dst[2]}}, rr = {{b.R[0], b.R[1], b.R[2]}};
+    if ((rc = resid(K, B, u, rr, b.LC[0], b.LC[1], alpha, pl->eps, w.phibar, w.stats, r.st)))
+      return rc;
+    std::vector<double> res(B);
+    std::vector<int> fl(B);
+    SWE_CUDA(cudaMemcpyAsync(res.data(), w.stats, sizeof(double) * B, cudaMemcpyDeviceToHost, r.st));
+    SWE_CUDA(cudaMemcpyAsync(fl.data(), w.flags, sizeof(int) * B, cudaMemcpyDeviceToHost, r.st));
+    SWE_CUDA(cudaStreamSynchronize(r.st));
+    double worst = 0.0;
+    for (int i = 0; i < B; ++i) {
+      if (!fl[i]) res[i] = 0.0;
+      worst = std::max(worst, res[i]);
+      if (resid_host) resid_host[i] = res[i];
+    }
+    set_error("Coriolis iteration did not converge; residual %.3e", worst);
+    return E_NOCONV;
+  }
+  return OK;
+}
+
+// Crank-Nicolson half step with the spectral Coriolis operator (g_fast_coriolis == 2
+// or explicit Coriolis): X = x0 + s (x1 + x2); dst = (I - a L)^-1 (I + a L) X, then
+// the viscosity factor when dtnu != 0.  One fused prologue (k_cn_start), the
+// fixed-point iterations (k_helm with inline L_C and per-slice ping-pong, k_decide),
+// one epilogue (k_cn_finish).  Iterations are launched in batches of the last
+// observed count without host round trips; surplus launches find no active slice.
+int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
+                 const double *const x0[3], const double *const x1[3],
+                 const double *const x2[3], double s, double *const dst[3], double alpha,
+                 double dtnu, int *iters_host, double *resid_host) {
+  swe_plan *pl = r.pl;
+  const int K = pl->K, B = r.B;
+  const bool impl = cfg.coriolis_implicit != 0 && pl->omega != 0.0;
+  Work &w = pl->ws;
+  int rc;
+  const CorOp cor{nullptr, nullptr, impl ? pl->cor_nb : nullptr, impl ? pl->cor_cf : nullptr};
+  {
+    ProfScope ps(3, (x1 ? 12.0 : 6.0) * 16.0 * K * B, r.st);
+    Ptr3C X0 = {{x0[0], x0[1], x0[2]}}, X1 = {{nullptr, nullptr, nullptr}}, X2 = X1;
+    if (x1) {
+      X1 = {{x1[0], x1[1], x1[2]}};
+      X2 = {{x2[0], x2[1], x2[2]}};
+    }
+    Ptr3 R = {{b.R[0], b.R[1], b.R[2]}}, D = {{dst[0], dst[1], dst[2]}};
+    if ((rc = cn_start(K, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, cor, R, D, r.st))) return rc;
+  }
+  int active = 0;
+  if (impl) {
+    if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
+    SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * 8 * B, r.st));
+    const double *Rc[3] = {b.R[0], b.R[1], b.R[2]};
+    double *const U[3] = {dst[0], b.LC[0], b.LC[1]};
+    const CorOp c{dst[1], dst[2], pl->cor_nb, pl->cor_cf};
+    int launched = 0, batch = std::max(1, pl->iter_guess), maxit = 0;
+    active = B;
+    while (launched < cfg.implicit_max_iter && active > 0) {
+      const int n = std::min(batch, cfg.implicit_max_iter - launched);
+      for (int j = 0; j < n; ++j) {
+        {
+          ProfScope ps(3, 9.0 * 16.0 * K * B, r.st);  // rhs 3 + old 3 in, new 3 out
+          if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, U, w.flags,
+                         w.stats, r.st, &c, w.iters, w.counter)))
+            return rc;
+        }
+        if ((rc = decide(B, w.stats, w.flags, w.iters, w.counter, cfg.implicit_tol, r.st)))
+          return rc;
+      }
+      launched += n;
+      batch = 1;
+      SWE_CUDA(cudaMemcpyAsync(w.h_counter, w.counter, sizeof(int), cudaMemcpyDeviceToHost, r.st));
+      SWE_CUDA(cudaMemcpyAsync(w.h_iters, w.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, r.st));
+      SWE_CUDA(cudaStreamSynchronize(r.st));
+      active = *w.h_counter;
+    }
+    for (int i = 0; i < B; ++i) {
+      maxit = std::max(maxit, w.h_iters[i]);
+      if (iters_host) iters_host[2 * i] = w.h_iters[i];
+    }
+    if (active == 0) pl->iter_guess = std::max(1, maxit);
+  } else if (iters_host) {
+    for (int i = 0; i < B; ++i) iters_host[2 * i] = 0;
+  }
+  {
+    ProfScope ps(3, (dtnu != 0.0 ? 6.0 : 4.0) * 16.0 * K * B, r.st);
+    Ptr3 u = {{dst[0], dst[1], dst[2]}};
+    if ((rc = cn_finish(K, B, u, b.LC[0], b.LC[1], impl ? w.iters : nullptr, pl->eps,
+                        active > 0 ? 0.0 : dtnu, cfg.visc_order / 2.0, r.st)))
+      return rc;
   }
   if (active > 0) {
     // residual of the unconverged slices (steppers.py:113-118)
@@ -493,10 +572,16 @@ int imex_internal(const Run &r, const swe_stepper_cfg &cfg, int *iters_host, dou
   const size_t n = (size_t)pl->K * r.B;
   int rc;
   std::vector<int> it2(iters_host ? 2 * r.B : 0);
+  const bool spec = g_fast_coriolis == 2 || !cfg.coriolis_implicit;
   // U* = CN_half(U)
-  if ((rc = cn_half(r, cfg, b, b.U, b.US, dt / 4.0, iters_host ? it2.data() : nullptr,
-                    resid_host)))
+  if (spec) {
+    if ((rc = cn_half_spec(r, cfg, b, b.U, nullptr, nullptr, 0.0, b.US, dt / 4.0, 0.0,
+                           iters_host ? it2.data() : nullptr, resid_host)))
+      return rc;
+  } else if ((rc = cn_half(r, cfg, b, b.U, b.US, dt / 4.0, iters_host ? it2.data() : nullptr,
+                           resid_host))) {
     return rc;
+  }
   // Heun on the explicit part (steppers.py:162-166)
   const double *USc[3] = {b.US[0], b.US[1], b.US[2]};
   if ((rc = explicit_tendency(r, cfg, USc, b.K1, b.TMP, b.LC[0], b.LC[1]))) return rc;
@@ -506,6 +591,15 @@ int imex_internal(const Run &r, const swe_stepper_cfg &cfg, int *iters_host, dou
   if ((rc = axpy3(n, us, k1, none, dt, mid, r.st))) return rc;
   const double *MIDc[3] = {b.MID[0], b.MID[1], b.MID[2]};
   if ((rc = explicit_tendency(r, cfg, MIDc, b.K2, b.TMP, b.LC[0], b.LC[1]))) return rc;
+  if (spec) {
+    // U_new = visc(CN_half(U* + dt/2 (K1 + K2)))
+    const double dtnu = dt * cfg.visc_nu;
+    if ((rc = cn_half_spec(r, cfg, b, b.US, b.K1, b.K2, 0.5 * dt, b.U, dt / 4.0, dtnu,
+                           iters_host ? it2.data() + 1 : nullptr, resid_host)))
+      return rc;
+    if (iters_host) memcpy(iters_host, it2.data(), sizeof(int) * 2 * r.B);
+    return OK;
+  }
   if ((rc = axpy3(n, us, k1, k2, 0.5 * dt, mid, r.st))) return rc;
   // U_new = CN_half(U_exp)
   if ((rc = cn_half(r, cfg, b, b.MID, b.U, dt / 4.0, iters_host ? it2.data() + 1 : nullptr,
