@@ -28,6 +28,9 @@ struct Work {
   int *counter = nullptr;   // device counter (active slices)
   int *h_counter = nullptr; // pinned host mirror
   int *h_iters = nullptr;   // [cap] pinned host mirror of iters
+  // mapped (zero-copy) host words [1 + cap]: active count, then iters; written by
+  // k_publish so the per-half-step check does not queue behind bulk D2H copies
+  int *h_pub = nullptr, *d_pub = nullptr;
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
 };

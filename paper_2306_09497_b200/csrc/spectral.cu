@@ -530,6 +530,17 @@ int cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2, const in
   return OK;
 }
 
+// copy the active count and the iteration counts to mapped host memory
+__global__ void k_publish(int B, const int *counter, const int *iters, volatile int *pub) {
+  for (int i = threadIdx.x; i <= B; i += blockDim.x) pub[i] = i == 0 ? *counter : iters[i - 1];
+}
+
+int publish(int B, const int *counter, const int *iters, int *pub, cudaStream_t st) {
+  k_publish<<<1, 256, 0, st>>>(B, counter, iters, pub);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
 int decide(int B, double *stats, int *active, int *iters, int *counter, double tol,
            cudaStream_t st) {
   k_decide<<<(B + 127) / 128, 128, 0, st>>>(B, stats, active, iters, counter, tol);

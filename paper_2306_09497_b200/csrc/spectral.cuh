@@ -45,6 +45,7 @@ int helm(int K, int B, const double *const R[3], const double *lcx, const double
          double alpha, const double *eps, const double *phibar, double *const U[3],
          const int *active, double *stats, cudaStream_t st, const CorOp *cor = nullptr,
          const int *iters = nullptr, int *counter = nullptr);
+int publish(int B, const int *counter, const int *iters, int *pub, cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
              cudaStream_t st);

@@ -521,14 +521,16 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
       }
       launched += n;
       batch = 1;
-      SWE_CUDA(cudaMemcpyAsync(w.h_counter, w.counter, sizeof(int), cudaMemcpyDeviceToHost, r.st));
-      SWE_CUDA(cudaMemcpyAsync(w.h_iters, w.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, r.st));
+      // zero-copy publish instead of cudaMemcpy: a small D2H copy would wait behind
+      // bulk transfers other streams queue on the copy engine (HostPipeline)
+      if ((rc = publish(B, w.counter, w.iters, w.d_pub, r.st))) return rc;
       SWE_CUDA(cudaStreamSynchronize(r.st));
-      active = *w.h_counter;
+      active = reinterpret_cast<volatile int *>(w.h_pub)[0];
     }
     for (int i = 0; i < B; ++i) {
-      maxit = std::max(maxit, w.h_iters[i]);
-      if (iters_host) iters_host[2 * i] = w.h_iters[i];
+      const int it = reinterpret_cast<volatile int *>(w.h_pub)[1 + i];
+      maxit = std::max(maxit, it);
+      if (iters_host) iters_host[2 * i] = it;
     }
     if (active == 0) pl->iter_guess = std::max(1, maxit);
   } else if (iters_host) {

@@ -23,7 +23,7 @@ import torch
 
 from . import _lib
 from .dynamics import PrognosticState, ViscositySpec
-from .spharm import _ptr, _stream
+from .spharm import SphereGrid, _ptr, _stream
 
 IMEX = "imex"
 SL_SI_SETTLS = "sl_si_settls"
@@ -124,3 +124,76 @@ def propagate(sstate: StepperState, t0: float, t1: float, cfg: StepperConfig) ->
     if nsteps == 0:
         return StepperState(sstate.current.copy(), None)
     return StepperState(imex_steps_inplace(sstate.current.copy(), cfg, nsteps), None)
+
+
+class HostPipeline:
+    """IMEX steps on host-resident batches, copies overlapped with compute.
+
+    submit(i) queues the host->device copy of batch i on its own stream and only
+    then launches the steps of batch i-1 (deferred by one submission), whose
+    device->host copy goes to a third stream.  So for batches submitted back to
+    back, H2D(i) and D2H(i-2) run while batch i-1 steps (PCIe is full duplex),
+    and a stream of host batches runs at the device step rate once the copies fit
+    under it.  `depth` device buffers rotate; host buffers must be pinned for the
+    copies to be asynchronous.  flush() launches the last deferred batch and
+    waits for every copy back.
+    """
+
+    def __init__(self, grid: SphereGrid, cfg: StepperConfig, batch: int, nsteps: int = 1,
+                 depth: int = 3):
+        if cfg.scheme != IMEX:
+            raise NotImplementedError("the GPU propagator implements the IMEX scheme only")
+        self.grid, self.cfg, self.batch, self.nsteps = grid, cfg, int(batch), int(nsteps)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.compute = torch.cuda.current_stream()
+        self.h2d, self.d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        self.slots = [torch.empty((batch, 3, grid.n_modes), dtype=torch.complex128, device=dev)
+                      for _ in range(depth)]
+        self.pbs = [torch.empty(batch, dtype=torch.float64, device=dev) for _ in range(depth)]
+        self.free = [None] * depth  # event: the slot's last D2H finished
+        self.pending = None         # (slot, ready event, host_out) awaiting its steps
+        self.i = 0
+
+    def _run(self, j, ready, host_out):
+        d, pb = self.slots[j], self.pbs[j]
+        self.compute.wait_event(ready)
+        with torch.cuda.stream(self.compute):
+            imex_steps_inplace(PrognosticState(self.grid, d, pb), self.cfg, self.nsteps)
+            done = torch.cuda.Event()
+            done.record(self.compute)
+        self.d2h.wait_event(done)
+        with torch.cuda.stream(self.d2h):
+            host_out.copy_(d, non_blocking=True)
+            out = torch.cuda.Event(enable_timing=True)
+            out.record(self.d2h)
+        self.free[j] = out
+
+    def submit(self, host_data: torch.Tensor, host_phibar: torch.Tensor, host_out: torch.Tensor):
+        """Queue batch host_data ([batch, 3, K] complex128, pinned) with its phibar;
+        host_out receives the advanced state (valid after flush())."""
+        if tuple(host_data.shape) != (self.batch, 3, self.grid.n_modes):
+            raise ValueError(f"host batch must be [{self.batch}, 3, {self.grid.n_modes}]")
+        j = self.i % len(self.slots)
+        self.i += 1
+        with torch.cuda.stream(self.h2d):
+            if self.free[j] is not None:
+                self.h2d.wait_event(self.free[j])
+            self.slots[j].copy_(host_data, non_blocking=True)
+            self.pbs[j].copy_(host_phibar, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self.h2d)
+        if self.pending is not None:
+            self._run(*self.pending)
+        self.pending = (j, ready, host_out)
+
+    def flush(self) -> torch.cuda.Event:
+        """Launch the deferred batch, wait for all copies back; returns the event of
+        the last device->host copy."""
+        if self.pending is not None:
+            self._run(*self.pending)
+            self.pending = None
+        last = self.free[(self.i - 1) % len(self.slots)]
+        for e in self.free:
+            if e is not None:
+                e.synchronize()
+        return last
