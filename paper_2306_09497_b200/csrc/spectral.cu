@@ -114,12 +114,15 @@ __global__ void k_lin_tend(int K, int B, const double *U0, const double *U2, con
 SWE_DEV unsigned long long sqmag_bits(double x, double y) {
   return (unsigned long long)__double_as_longlong(x * x + y * y);
 }
-// L_C at internal row k, slice b: lx = -div(fV), ld = curl(fV)   (plan.cu cor_cf)
-SWE_DEV void cor_at(const CorOp &c, int k, int b, int B, double2 &lx, double2 &ld) {
+// L_C at internal row k, slice b: lx = -div(fV), ld = curl(fV)   (plan.cu cor_cf);
+// x, d return xi, delta of row k
+SWE_DEV void cor_at(const CorOp &c, int k, int b, int B, double2 &lx, double2 &ld, double2 &x,
+                    double2 &d) {
   const int2 nb = __ldg(c.nb + k);
   const double4 cf = c.cf[k];
   const size_t i = (size_t)k * B + b;
-  const double2 x = ld2(c.x, i), d = ld2(c.d, i);
+  x = ld2(c.x, i);
+  d = ld2(c.d, i);
   double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
   if (nb.x >= 0) {
     xl = ld2(c.x, (size_t)nb.x * B + b);
@@ -142,15 +145,15 @@ SWE_DEV void cor_at(const CorOp &c, int k, int b, int B, double2 &lx, double2 &l
 __global__ void k_coriolis(int K, int B, CorOp c, double *lcx, double *lcd) {
   FOR_KB(K, B) {
     const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
-    double2 lx, ld;
-    cor_at(c, k, b, B, lx, ld);
+    double2 lx, ld, x, d;
+    cor_at(c, k, b, B, lx, ld, x, d);
     st2(lcx, _i, lx);
     st2(lcd, _i, ld);
   }
 }
 
 template <int UN>  // modes per thread in flight
-__global__ void __launch_bounds__(256, UN == 4 ? 1 : 2) k_helm(int K, int B, const double *R0, const double *R1,
+__global__ void __launch_bounds__(256, UN == 4 ? 1 : 3) k_helm(int K, int B, const double *R0, const double *R1,
                                               const double *R2, const double *lcx,
                                               const double *lcd, double alpha, const double *eps,
                                               const double *phibar, double *U0, double *U1,
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 2) k_helm(int K, int B, con
           rd[u] = ld2(R2, i);
           if (fused) {
             double2 lx, ld;
-            cor_at(src, k, b, B, lx, ld);
+            cor_at(src, k, b, B, lx, ld, o1[u], o2[u]);
             rx[u] = add2(rx[u], sc2(alpha, lx));
             rd[u] = add2(rd[u], sc2(alpha, ld));
           } else if (lcx) {
@@ -201,8 +204,10 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 2) k_helm(int K, int B, con
           e[u] = eps[k];
           if (stats) {
             o0[u] = ld2(U0, i);
-            o1[u] = ld2(O1, i);
-            o2[u] = ld2(O2, i);
+            if (!fused) {
+              o1[u] = ld2(O1, i);
+              o2[u] = ld2(O2, i);
+            }
           }
         }
       }
@@ -505,7 +510,7 @@ int helm(int K, int B, const double *const R[3], const double *lcx, const double
   dim3 grid((B + 31) / 32, ybl), blk(32, 8);
   CorOp c = cor ? *cor : CorOp{nullptr, nullptr, nullptr, nullptr};
   if (cor)
-    k_helm<2><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
+    k_helm<1><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
                                      U[1], U[2], active, stats, c, iters, counter);
   else
     k_helm<4><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
