@@ -45,6 +45,11 @@ struct LegArgs {
   const int *offsets;  // [M+2] packed-mode block offsets
   const int2 *items;   // (m, tile) work items, heaviest first
   int nitems;
+  // v3 dynamic scheduling: device ticket counter (never reset, per plan/stream),
+  // this launch's first ticket, and the host mirror of the next free ticket
+  unsigned long long *sched;
+  unsigned long long sched_base;
+  unsigned long long *sched_next;
 };
 
 // Launch helpers (legendre.cu).  items/tiles are prepared by the plan.

@@ -33,22 +33,25 @@ constexpr int A3_KP = 16, A3_NS = 4, A3_LDA = A3_KP + 4, A3_LDB = V3_BN + 4;
 constexpr int A3_BR = V3_ABR;  // analysis modes per parity per unit
 constexpr int A3_RW = A3_BR / 2, A3_FR = A3_RW / 8;  // rows / 8-row fragments per consumer warp
 
-struct Synth3Stage {
+struct alignas(128) Synth3Stage {
   double A[2 * S3_KT][S3_LDA];
   double B[2 * S3_KT][S3_LDB];
   double S[2 * S3_KT];
+  int unit;  // work unit this stage belongs to (first stage of a unit), -1: no more work
 };
 struct Synth3Smem {
   Synth3Stage st[S3_NS];
   unsigned long long full[S3_NS], empty[S3_NS];
 };
-struct Anal3Stage {
+struct alignas(128) Anal3Stage {
   double A[2 * A3_BR][A3_LDA];
   double F[2][A3_KP][A3_LDB];
+  int unit;
 };
 struct Anal3Smem {
   Anal3Stage st[A3_NS];
   unsigned long long full[A3_NS], empty[A3_NS];
+  int next;  // unit handed from producer thread 0 to the producer warpgroup
 };
 
 SWE_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -114,6 +117,14 @@ SWE_DEV Unit decode(const LegArgs &a, int u, int ncol, int tile_w) {
   return x;
 }
 
+// Dynamic work distribution: units are claimed from a 64-bit counter that is
+// never reset; this launch owns tickets [sched_base, sched_base + nunits + grid)
+// (each CTA draws one ticket past the end), so no per-launch memset is needed.
+SWE_DEV int claim(const LegArgs &a) {
+  const unsigned long long t = atomicAdd(a.sched, 1ULL);
+  return (int)(t - a.sched_base);
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__ LegArgs args) {
@@ -138,7 +149,17 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     if (warp != 0) return;
     int it = 0;
     const int r = lane, par = r >> 4;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    while (true) {
+      int u = 0;
+      if (lane == 0) u = claim(args);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= nunits) {  // terminal stage: tells the consumers to stop
+        const int s = it % S3_NS;
+        mbar_wait(&sm.empty[s], ((it / S3_NS) & 1) ^ 1);
+        if (lane == 0) sm.st[s].unit = -1;
+        mbar_arrive(&sm.full[s]);
+        break;
+      }
       const Unit x = decode(args, u, ncol, 64);
       const LegOut &o = args.out[x.out];
       const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
@@ -152,6 +173,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
         const int term = c / nch_t, tt = (c - term * nch_t) * S3_KT + (r & 15);
         const LegTerm &T = o.t[term];
         Synth3Stage &S = sm.st[s];
+        if (lane == 0) S.unit = u;  // published by lane 0's arrive (release)
         const bool v = tt < (par ? no : ne);
         const int k = off + (par ? ne : 0) + tt;
         S.S[r] = v ? T.sign * (T.scale ? T.scale[k] : 1.0) * (T.times_im ? (double)x.m : 1.0) : 0.0;
@@ -176,7 +198,13 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
   const int cw = warp - V3_CW0, g = lane >> 2, t = lane & 3;
   const int wpar = cw & 1, wph = (cw >> 1) & 1, wch = cw >> 2;
   int it = 0;
-  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+  while (true) {
+    {
+      const int s = it % S3_NS;
+      mbar_wait(&sm.full[s], (it / S3_NS) & 1);
+    }
+    const int u = sm.st[it % S3_NS].unit;
+    if (u < 0) break;
     const Unit x = decode(args, u, ncol, 64);
     const LegOut &o = args.out[x.out];
     const int km = M + 1 - x.m, ne = (km + 1) >> 1;
@@ -190,7 +218,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
       for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
       const int s = it % S3_NS;
-      mbar_wait(&sm.full[s], (it / S3_NS) & 1);
+      if (c > 0) mbar_wait(&sm.full[s], (it / S3_NS) & 1);
       if (nfr > 0) {
         const Synth3Stage &S = sm.st[s];
         const LegTerm &T = o.t[c / nch_t];
@@ -251,7 +279,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
   const int nch_t = Jp / A3_KP;
   if (tid == 0) {
     for (int s = 0; s < A3_NS; ++s) {
-      mbar_init(&sm.full[s], 128);  // every producer-warpgroup thread arrives
+      mbar_init(&sm.full[s], 129);  // every producer thread (cp.async) + thread 0's unit store
       mbar_init(&sm.empty[s], V3_NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -266,7 +294,22 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     // own copies have landed (cp.async.mbarrier.arrive.noinc)
     const int ptid = tid;  // 0..127
     int it = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    while (true) {
+      // thread 0 claims the next unit and hands it to the warpgroup (named barrier 1)
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (ptid == 0) sm.next = claim(args);
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      const int u = sm.next;
+      if (u >= nunits) {  // terminal stage: tells the consumers to stop
+        const int s = it % A3_NS;
+        mbar_wait(&sm.empty[s], ((it / A3_NS) & 1) ^ 1);
+        if (ptid == 0) {
+          sm.st[s].unit = -1;
+          mbar_arrive(&sm.full[s]);
+        }
+        cp_async_arrive(&sm.full[s]);
+        break;
+      }
       const Unit x = decode(args, u, ncol, A3_BR);
       const LegOut &o = args.out[x.out];
       const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
@@ -293,6 +336,10 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
           const bool v = (p < Jh) && (x.c0 + cc < ld);
           cp_async16(&S.F[hs][pr][cc], fb + (v ? ((size_t)(hs ^ T.swap_pm) * Jp + p) * ld + cc : 0), v);
         }
+        if (ptid == 0) {
+          S.unit = u;
+          mbar_arrive(&sm.full[s]);  // release: publishes S.unit
+        }
         cp_async_arrive(&sm.full[s]);
       }
     }
@@ -303,7 +350,10 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
   const int cw = warp - V3_CW0, g = lane >> 2, t = lane & 3;
   const int wpar = cw & 1, wrq = (cw >> 1) & 1, wch = cw >> 2;
   int it = 0;
-  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+  while (true) {
+    mbar_wait(&sm.full[it % A3_NS], (it / A3_NS) & 1);
+    const int u = sm.st[it % A3_NS].unit;
+    if (u < 0) break;
     const Unit x = decode(args, u, ncol, A3_BR);
     const LegOut &o = args.out[x.out];
     const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
@@ -316,7 +366,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
       for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
       const int s = it % A3_NS;
-      mbar_wait(&sm.full[s], (it / A3_NS) & 1);
+      if (c > 0) mbar_wait(&sm.full[s], (it / A3_NS) & 1);
       if (nfr > 0) {
         const Anal3Stage &S = sm.st[s];
         const LegTerm &T = o.t[c / nch_t];
@@ -390,7 +440,11 @@ int leg_synth_v3_launch(const LegArgs &a, cudaStream_t st) {
     attr = true;
   }
   const int units = a.nitems * ((a.ld + V3_BN - 1) / V3_BN) * a.nout;
-  leg_synth_v3<<<std::min(units, num_sms()), V3_NT, smem, st>>>(a);
+  const int grid = std::min(units, num_sms());
+  LegArgs b = a;
+  b.sched_base = *a.sched_next;
+  *a.sched_next += (unsigned long long)(units + grid);
+  leg_synth_v3<<<grid, V3_NT, smem, st>>>(b);
   SWE_LAUNCH_CHECK();
   return OK;
 }
@@ -403,7 +457,11 @@ int leg_anal_v3_launch(const LegArgs &a, cudaStream_t st) {
     attr = true;
   }
   const int units = a.nitems * ((a.ld + V3_BN - 1) / V3_BN) * a.nout;
-  leg_anal_v3<<<std::min(units, num_sms()), V3_NT, smem, st>>>(a);
+  const int grid = std::min(units, num_sms());
+  LegArgs b = a;
+  b.sched_base = *a.sched_next;
+  *a.sched_next += (unsigned long long)(units + grid);
+  leg_anal_v3<<<grid, V3_NT, smem, st>>>(b);
   SWE_LAUNCH_CHECK();
   return OK;
 }

@@ -372,6 +372,7 @@ void work_free(Work &w) {
   cudaFreeHost(w.h_counter);
   cudaFreeHost(w.h_iters);
   cudaFreeHost(w.h_pub);
+  cudaFree(w.sched);
   cudaFree(w.phi0);
   cudaFree(w.phibar);
   w = Work();
@@ -426,6 +427,8 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaMallocHost(&w.h_iters, (size_t)B * sizeof(int)));
   SWE_CUDA(cudaHostAlloc(&w.h_pub, (size_t)(B + 1) * sizeof(int), cudaHostAllocMapped));
   SWE_CUDA(cudaHostGetDevicePointer(&w.d_pub, w.h_pub, 0));
+  SWE_CUDA(cudaMalloc(&w.sched, sizeof(unsigned long long)));
+  SWE_CUDA(cudaMemset(w.sched, 0, sizeof(unsigned long long)));
   SWE_CUDA(cudaMalloc(&w.phi0, (size_t)B * sizeof(double)));
   SWE_CUDA(cudaMalloc(&w.phibar, (size_t)B * sizeof(double)));
   w.cap = B;

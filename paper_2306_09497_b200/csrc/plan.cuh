@@ -31,6 +31,8 @@ struct Work {
   // mapped (zero-copy) host words [1 + cap]: active count, then iters; written by
   // k_publish so the per-half-step check does not queue behind bulk D2H copies
   int *h_pub = nullptr, *d_pub = nullptr;
+  unsigned long long *sched = nullptr;  // Legendre v3 work-unit ticket counter (device)
+  unsigned long long sched_next = 0;    // host mirror: next unissued ticket
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
 };

@@ -93,6 +93,8 @@ LegArgs leg_args(const Run &r) {
   a.Jp = r.pl->Jp;
   a.ld = (int)r.ld;
   a.offsets = r.pl->offsets;
+  a.sched = r.pl->ws.sched;
+  a.sched_next = &r.pl->ws.sched_next;
   return a;
 }
 

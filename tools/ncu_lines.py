@@ -35,8 +35,21 @@ def main():
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = next(r for r in rows if r and r[0] == "Address")
-    data = [dict(zip(hdr, r)) for r in rows[rows.index(hdr) + 1:] if len(r) == len(hdr)]
+    # the page holds one block per profiled launch: "Kernel Name", header, rows;
+    # keep the first block of the requested kernel
+    data, hdr, cur, taken = [], None, "", False
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            if data:
+                taken = True
+            cur = r[1] if len(r) > 1 else ""
+            continue
+        if r and r[0] == "Address":
+            hdr = r
+            continue
+        if taken or hdr is None or kname not in cur or len(r) != len(hdr):
+            continue
+        data.append(dict(zip(hdr, r)))
     base = int(data[0]["Address"], 16)
     lm = line_map(cubin, kname)
     agg = collections.Counter()
