@@ -108,7 +108,10 @@ int swe_profile(int enable);
 /* Tuning switches.  "fft_path": 0 auto, 1 warp-per-row FFT kernel, 2 lane=row
  * FFT kernel (falls back to 1 where its radix/size limits do not hold).
  * "leg_path": 0 auto, 1 small-batch Legendre kernels, 2 / 3 wide-tile kernels
- * with 128 / 64 columns per CTA.  Results are identical on every path. */
+ * with 128 / 64 columns per CTA, 4 warp-specialised persistent kernels.
+ * "fast_coriolis": 2 (default) spectral three-term recurrence, 1 FFT-free
+ * Legendre pair, 0 pseudospectral FFT round trip.  Results agree to roundoff
+ * on every path (within 1e-12 relative between the fast_coriolis modes). */
 int swe_set_option(const char *key, int value);
 int swe_profile_read(double *ms_out, double *work_out, long long *count_out);
 const char *swe_last_error(void);

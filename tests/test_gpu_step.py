@@ -234,3 +234,34 @@ def test_host_pipeline_matches_inplace(mods):
     pipe.flush()
     for i in range(nb):
         assert torch.equal(outs[i], want[i]), i
+
+
+@pytest.mark.parametrize("M", [51, 256])
+@pytest.mark.parametrize("path", [1, 2], ids=["fft_rows", "fft_lanes"])
+def test_nonlinear_prime_factor_sizes(mods, M, path):
+    """Nonlinear tendency on prime-factor FFT lengths (N2 = 77 = 7*11 at M=51,
+    385 = 5*7*11 at M=256, the benchmark size) on both FFT kernels, batched,
+    against the oracle."""
+    spharm, dynamics, _, _ = mods
+    from paper_2306_09497_b200 import _lib
+    from oracle.sht import OracleSphere, random_bandlimited
+    from oracle.swe import OracleState, nonlinear_advection, nonlinear_rest
+    grid, sph = spharm.get_grid(M), OracleSphere(M)
+    rng = np.random.default_rng(M + path)
+    B = 3
+    c = [random_bandlimited(sph, rng, batch=(B,)) for _ in range(3)]
+    phi = 3e5 * c[0]
+    phi[:, 0] += 9.80616 * 29400.0 * np.sqrt(2.0)
+    xi, de = 1e-5 * c[1], 1e-6 * c[2]
+    pb = np.full(B, 9.80616 * 29400.0)
+    o = OracleState(sph, phi, xi, de, pb)
+    want = [a + b for a, b in zip(nonlinear_advection(o), nonlinear_rest(o))]
+    s = dynamics.PrognosticState.from_fields(grid, phi, xi, de, pb)
+    _lib.set_option("fft_path", path)
+    try:
+        got = dynamics.nonlinear(s)
+    finally:
+        _lib.set_option("fft_path", 0)
+    for f in range(3):
+        g = got[f].cpu().numpy()
+        assert np.abs(g - want[f]).max() <= 1e-11 * np.abs(want[f]).max(), f
