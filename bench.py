@@ -189,6 +189,34 @@ def make_states(grid, n, seed):
     return s
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernels from the newest committed
+    `ncu --set full` capture (profiles/*_kernels.json, tools/ncu_summary.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                          "profiles", "*_kernels.json")), key=os.path.getmtime)
+    if not files:
+        return {}
+    try:
+        recs = json.load(open(files[-1]))
+    except (OSError, ValueError):
+        return {}
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def dram(r):
+        u = scale.get(r.get("dram__bytes_read.sum:unit", "byte"), 1.0)
+        return ((r.get("dram__bytes_read.sum") or 0) + (r.get("dram__bytes_write.sum") or 0)) * u
+
+    leg = [dram(r) for r in recs if r["kernel"].startswith(("leg_synth_v3", "leg_anal_v3"))]
+    fft = [dram(r) for r in recs if "fft_lanes_kernel" in r["kernel"]]
+    out = {"source": "profiles/" + os.path.basename(files[-1])}
+    if leg:
+        out["legendre"] = sum(leg) / len(leg)
+    if fft:
+        out["fft"] = sum(fft) / len(fft)
+    return out
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -284,17 +312,22 @@ def run_ours(args):
     peaks = load_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
     share = {k: round(v[0] / max(total_ms, 1e-9), 4) for k, v in prof.items()}
+    traffic = ncu_traffic()
     if leg_ms >= fft_ms:
         ach = leg_flops / (leg_ms * 1e-3) / 1e12
-        roof = {"kernel": "leg_synth_kernel + leg_anal_kernel (FP64 DMMA, parity-folded)",
+        roof = {"kernel": "leg_synth_v3 + leg_anal_v3 (FP64 DMMA.8x8x4, parity-folded)",
                 "bound": "tensor", "achieved": ach, "peak": peak64, "unit": "TFLOP/s",
-                "frac": ach / peak64, "traffic": None,
+                "frac": ach / peak64, "traffic": traffic.get("legendre"),
+                "traffic_unit": "DRAM bytes per launch (mean of synthesis and analysis)",
+                "traffic_source": traffic.get("source"),
                 "peak_source": "cuBLAS DGEMM 8192^3 measured live in bench.py (burst)",
                 "work_per_unit": "2*J*K flops per slice per Legendre term (folded)"}
     else:
         ach = fft_bytes / (fft_ms * 1e-3) / 1e9
-        roof = {"kernel": "fft_kernel (FFT + grid products)", "bound": "hbm", "achieved": ach,
-                "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+        roof = {"kernel": "fft_lanes_kernel (FFT + grid products)", "bound": "hbm",
+                "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": traffic.get("fft"), "traffic_unit": "DRAM bytes per launch",
+                "traffic_source": traffic.get("source"),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     it_arr = np.concatenate(its)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

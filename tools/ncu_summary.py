@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (run here, no GPU needed).
 
-    python tools/ncu_summary.py <tag> <launches.csv> <full.ncu-rep>
+    python tools/ncu_summary.py <tag> <launches.csv> <full.ncu-rep>[,<more.ncu-rep>...]
 
 Writes profiles/<tag>_launches.csv (per-kernel aggregate of the launch list),
 profiles/<tag>_kernels.json (selected metrics of the full capture per launch)
@@ -90,7 +90,7 @@ def main():
         fh.write("kernel,launches,total_us,share\n")
         for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
             fh.write(f"{k},{n},{us:.1f},{us / tot:.4f}\n")
-    full = full_table(rep)
+    full = [r for one in rep.split(",") for r in full_table(one)]
     with open(os.path.join(ROOT, "profiles", f"{tag}_kernels.json"), "w") as fh:
         json.dump(full, fh, indent=1)
     lines = [f"# ncu summary {tag}", "", "## Launch list (ncu, cold cache, serialised)", "",
@@ -102,8 +102,8 @@ def main():
               "| --- | --- | --- | --- | --- | --- | --- | --- | --- | --- |"]
     for r in full:
         us = r.get("gpu__time_duration.sum", 0)
-        if r.get("gpu__time_duration.sum:unit") == "nsecond":
-            us = us / 1e3
+        us *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+               "msecond": 1e3}.get(r.get("gpu__time_duration.sum:unit"), 1.0)
         dr = (r.get("dram__bytes_read.sum", 0) or 0) + (r.get("dram__bytes_write.sum", 0) or 0)
         unit = r.get("dram__bytes_read.sum:unit", "byte")
         mb = dr * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1e-6)
