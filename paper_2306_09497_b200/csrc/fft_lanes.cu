@@ -156,13 +156,26 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
       const int k2 = k == 0 ? N2 : N2 - k;
       const double2 z = make_double2(0.0, 0.0);
       const int fs = (f == 2 && a.dlam) ? 5 : f;
-      const double2 *base =
-          reinterpret_cast<const double2 *>(a.in[ok ? fs : 0] + (size_t)c.p * a.ld) + c.b0;
-      const double2 *pk = base + (size_t)k * mstride + s, *pk2 = base + (size_t)k2 * mstride + s;
+      const double2 *pk, *pk2;
+      size_t eoo;
+      if (a.in_pm) {  // [Jh][ld/2][M+1][E,O]: this (pair, slice) is one contiguous block
+        const int nsl = a.ld >> 1;
+        const double2 *blk = reinterpret_cast<const double2 *>(a.in[ok ? fs : 0]) +
+                             ((size_t)c.p * (M + 1) * nsl + c.b0 + s) * 2;
+        pk = blk + (size_t)2 * nsl * k;
+        pk2 = blk + (size_t)2 * nsl * k2;
+        eoo = 1;
+      } else {
+        const double2 *base =
+            reinterpret_cast<const double2 *>(a.in[ok ? fs : 0] + (size_t)c.p * a.ld) + c.b0;
+        pk = base + (size_t)k * mstride + s;
+        pk2 = base + (size_t)k2 * mstride + s;
+        eoo = eo;
+      }
       e[u] = (ok && k <= M) ? __ldg(pk) : z;
-      o[u] = (ok && k <= M) ? __ldg(pk + eo) : z;
+      o[u] = (ok && k <= M) ? __ldg(pk + eoo) : z;
       e2[u] = (ok && k2 <= M) ? __ldg(pk2) : z;
-      o2[u] = (ok && k2 <= M) ? __ldg(pk2 + eo) : z;
+      o2[u] = (ok && k2 <= M) ? __ldg(pk2 + eoo) : z;
       w1[u] = ok ? __ldg(a.twh + k) : z;
       w2[u] = (ok && k) ? __ldg(a.twh + k2) : z;
       z1[u] = ok ? __ldg(a.pos_z + k) : 0;

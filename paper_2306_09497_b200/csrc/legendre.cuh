@@ -33,6 +33,10 @@ struct LegTerm {
 struct LegOut {
   LegTerm t[2];
   int nterms;
+  // synthesis output layout: 0 = planes [m][E,O][Jp][ld]; 1 = pair-major
+  // [Jh][ld/2 slices][M+1][E,O] complex, so one (pair, slice) of a field is one
+  // contiguous 16(M+1)-double block for the FFT loader (legendre_v3.cu only)
+  int layout;
   double *dst;  // synthesis: [m][J][ld] (north/south rows); analysis: [K][ld]
 };
 

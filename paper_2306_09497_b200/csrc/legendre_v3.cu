@@ -252,18 +252,37 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
-    // E or O plane of [m][2][Jp][ld]
-    double *dst = o.dst + ((size_t)x.m * 2 + wpar) * Jp * ld;
+    if (o.layout == 0) {
+      // E or O plane of [m][2][Jp][ld]
+      double *dst = o.dst + ((size_t)x.m * 2 + wpar) * Jp * ld;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int p = pw0 + i * 8 + g;
-      if (p >= Jh) continue;
+      for (int i = 0; i < 4; ++i) {
+        const int p = pw0 + i * 8 + g;
+        if (p >= Jh) continue;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
-        if (col < ld)
-          *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) =
-              make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);  // Im of m = 0 is dropped
+        for (int j = 0; j < 8; ++j) {
+          const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
+          if (col < ld)
+            *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) =
+                make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);  // Im of m = 0 is dropped
+        }
+      }
+    } else {
+      // pair-major [Jh][ld/2][M+1][E,O]: E and O of one (pair, slice, m) share a
+      // 32-byte sector, written by the two parity warps of this unit
+      double2 *dst = reinterpret_cast<double2 *>(o.dst);
+      const int nsl = ld >> 1;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int p = pw0 + i * 8 + g;
+        if (p >= Jh) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
+          if (col < ld)
+            dst[(((size_t)p * (M + 1) + x.m) * nsl + (col >> 1)) * 2 + wpar] =
+                make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);
+        }
       }
     }
   }

@@ -201,6 +201,17 @@ int fft_tasks_per_slice(int op) {
   }
 }
 
+// the lane = row FFT kernel takes this plan / batch (same rule as fft())
+bool fft_uses_lanes(const Run &r) {
+  FftArgs a;
+  memset(&a, 0, sizeof(a));
+  a.N2 = r.pl->N2;
+  a.nst = r.pl->nst;
+  for (int s = 0; s < r.pl->nst; ++s) a.radix[s] = r.pl->radix[s];
+  const bool lanes = g_fft_path == 2 || (g_fft_path == 0 && r.B >= 8);
+  return lanes && fft_lanes_ok(a);
+}
+
 int fft(const Run &r, int op, FftArgs &a) {
   swe_plan *pl = r.pl;
   a.M = pl->M;
@@ -247,6 +258,10 @@ int fft(const Run &r, int op, FftArgs &a) {
   if (lanes && fft_lanes_ok(a)) {
     ProfScope ps(2, bytes, r.st);
     return fft_lanes_launch(op, a, r.st);
+  }
+  if (a.in_pm) {
+    set_error("internal: pair-major FFT input needs the lane kernel");
+    return E_SHAPE;
   }
   const int rows = fft_rows_per_slice(op);
   const size_t rowb = (size_t)pl->N2 * sizeof(double2);
@@ -330,6 +345,7 @@ int eval_coriolis(const Run &r, const double *xi, const double *de, double *oxi,
 int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], double *tmp) {
   swe_plan *pl = r.pl;
   const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
+  const bool pm = leg_bn(r) < 0 && fft_uses_lanes(r);
   int rc;
   {
     LegArgs a = leg_args(r);
@@ -342,6 +358,9 @@ int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], d
     set_out(a, 3, r.half(4), term(P, U[1]), nullptr, H);                  // xi
     set_out(a, 4, r.half(5), term(P, U[0]), nullptr, H);  // Phi (phi_prime shift in the FFT)
     set_out(a, 5, r.half(6), term(P, U[2]), nullptr, H);                  // delta
+    // warp-specialised synthesis + lane FFT: hand over in the pair-major layout
+    if (pm)
+      for (int i = 0; i < a.nout; ++i) a.out[i].layout = 1;
     if ((rc = synth(r, a))) return rc;
   }
   {
@@ -350,6 +369,7 @@ int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], d
     for (int i = 0; i < 7; ++i) f.in[i] = i == 2 ? nullptr : r.half(i);
     for (int i = 0; i < 4; ++i) f.out[i] = r.fsp(i);
     f.dlam = 1;
+    f.in_pm = pm;
     if ((rc = fft(r, FOP_NONLINEAR, f))) return rc;
   }
   {
