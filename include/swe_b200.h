@@ -96,6 +96,19 @@ int swe_truncate_pad(const swe_plan *src, const swe_plan *dst, const double *in,
 int swe_state_stats(const swe_plan *plan, const double *state, int batch, double *max_abs_out,
                     int *finite_out, void *stream);
 
+/* On-device diagnostics (diagnostics.py:46-118), deterministic reductions.
+ * Kinetic-energy spectrum of states [batch][3][K]: energy[b][n-1], n = 1..M
+ * (DEVICE output [batch][M]). */
+int swe_ke_spectrum(const swe_plan *plan, const double *state, int batch, double *energy,
+                    void *stream);
+/* Windowed spectral error terms for fields x, y ([K] complex on this plan) and
+ * rnorms[i] (HOST, 1..M, nr <= 64): out[2i] = max|x - y|, out[2i+1] = max|y| over
+ * m, n <= rnorms[i] (DEVICE output [2 nr]). */
+int swe_window_maxdiff(const swe_plan *plan, const double *x, const double *y,
+                       const int *rnorms, int nr, double *out, void *stream);
+/* out[0] = sum (x - y)^2, out[1] = sum y^2 over n doubles (DEVICE output [2]). */
+int swe_grid_sqdiff(const double *x, const double *y, long long n, double *out, void *stream);
+
 /* Number of this library's kernels launched since load (evidence counter). */
 long long swe_kernel_launches(void);
 /* Live per-launch profiling with CUDA events on the launching stream.

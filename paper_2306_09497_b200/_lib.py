@@ -20,7 +20,7 @@ EXPORTS = (
     "swe_synthesis", "swe_analysis", "swe_uv_from_vortdiv", "swe_vortdiv_from_uv",
     "swe_tendency", "swe_imex_step", "swe_truncate_pad", "swe_state_stats",
     "swe_kernel_launches", "swe_last_error", "swe_profile", "swe_profile_read",
-    "swe_set_option",
+    "swe_set_option", "swe_ke_spectrum", "swe_window_maxdiff", "swe_grid_sqdiff",
 )
 
 
@@ -70,6 +70,9 @@ def load(path: str = LIB_PATH):
         "swe_profile": (I, [I]),
         "swe_profile_read": (I, [P, P, P]),
         "swe_set_option": (I, [ctypes.c_char_p, I]),
+        "swe_ke_spectrum": (I, [P, P, I, P, P]),
+        "swe_window_maxdiff": (I, [P, P, P, P, I, P, P]),
+        "swe_grid_sqdiff": (I, [P, P, ctypes.c_longlong, P, P]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)
