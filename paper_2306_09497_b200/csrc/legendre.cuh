@@ -49,11 +49,9 @@ struct LegArgs {
   const int *offsets;  // [M+2] packed-mode block offsets
   const int2 *items;   // (m, tile) work items, heaviest first
   int nitems;
-  // v3 dynamic scheduling: device ticket counter (never reset, per plan/stream),
-  // this launch's first ticket, and the host mirror of the next free ticket
+  // v3 dynamic scheduling: device [ticket counter, CTAs done] (per plan / stream;
+  // zero between launches)
   unsigned long long *sched;
-  unsigned long long sched_base;
-  unsigned long long *sched_next;
 };
 
 // Launch helpers (legendre.cu).  items/tiles are prepared by the plan.

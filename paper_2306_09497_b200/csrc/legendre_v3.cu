@@ -117,12 +117,18 @@ SWE_DEV Unit decode(const LegArgs &a, int u, int ncol, int tile_w) {
   return x;
 }
 
-// Dynamic work distribution: units are claimed from a 64-bit counter that is
-// never reset; this launch owns tickets [sched_base, sched_base + nunits + grid)
-// (each CTA draws one ticket past the end), so no per-launch memset is needed.
+// Dynamic work distribution: units are claimed from a device counter
+// (sched[0]); every CTA draws one ticket past the end and then checks in on
+// sched[1]; the last CTA to check in resets both, so the next launch (stream
+// ordered, or the next replay of a CUDA graph) starts from zero without a memset.
 SWE_DEV int claim(const LegArgs &a) {
-  const unsigned long long t = atomicAdd(a.sched, 1ULL);
-  return (int)(t - a.sched_base);
+  return (int)atomicAdd(a.sched, 1ULL);
+}
+SWE_DEV void sched_done(const LegArgs &a) {
+  if (atomicAdd(a.sched + 1, 1ULL) == gridDim.x - 1) {
+    a.sched[0] = 0;
+    a.sched[1] = 0;
+  }
 }
 
 }  // namespace
@@ -156,7 +162,10 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
       if (u >= nunits) {  // terminal stage: tells the consumers to stop
         const int s = it % S3_NS;
         mbar_wait(&sm.empty[s], ((it / S3_NS) & 1) ^ 1);
-        if (lane == 0) sm.st[s].unit = -1;
+        if (lane == 0) {
+          sm.st[s].unit = -1;
+          sched_done(args);
+        }
         mbar_arrive(&sm.full[s]);
         break;
       }
@@ -324,6 +333,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
         mbar_wait(&sm.empty[s], ((it / A3_NS) & 1) ^ 1);
         if (ptid == 0) {
           sm.st[s].unit = -1;
+          sched_done(args);
           mbar_arrive(&sm.full[s]);
         }
         cp_async_arrive(&sm.full[s]);
@@ -460,10 +470,7 @@ int leg_synth_v3_launch(const LegArgs &a, cudaStream_t st) {
   }
   const int units = a.nitems * ((a.ld + V3_BN - 1) / V3_BN) * a.nout;
   const int grid = std::min(units, num_sms());
-  LegArgs b = a;
-  b.sched_base = *a.sched_next;
-  *a.sched_next += (unsigned long long)(units + grid);
-  leg_synth_v3<<<grid, V3_NT, smem, st>>>(b);
+  leg_synth_v3<<<grid, V3_NT, smem, st>>>(a);
   SWE_LAUNCH_CHECK();
   return OK;
 }
@@ -477,10 +484,7 @@ int leg_anal_v3_launch(const LegArgs &a, cudaStream_t st) {
   }
   const int units = a.nitems * ((a.ld + V3_BN - 1) / V3_BN) * a.nout;
   const int grid = std::min(units, num_sms());
-  LegArgs b = a;
-  b.sched_base = *a.sched_next;
-  *a.sched_next += (unsigned long long)(units + grid);
-  leg_anal_v3<<<grid, V3_NT, smem, st>>>(b);
+  leg_anal_v3<<<grid, V3_NT, smem, st>>>(a);
   SWE_LAUNCH_CHECK();
   return OK;
 }

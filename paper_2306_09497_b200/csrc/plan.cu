@@ -361,6 +361,14 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
   return OK;
 }
 
+void graphs_clear(swe_plan *pl) {
+  for (auto &g : pl->graphs) {  // entries seen once hold no graph yet
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
+  pl->graphs.clear();
+}
+
 void work_free(Work &w) {
   cudaFree(w.spec);
   cudaFree(w.half);
@@ -373,6 +381,9 @@ void work_free(Work &w) {
   cudaFreeHost(w.h_iters);
   cudaFreeHost(w.h_pub);
   cudaFree(w.sched);
+  cudaFree(w.loop);
+  cudaFree(w.hdone);
+  cudaFreeHost(w.h_fail);
   cudaFree(w.phi0);
   cudaFree(w.phibar);
   w = Work();
@@ -382,6 +393,9 @@ void plan_destroy(swe_plan *pl) {
   if (!pl) return;
   cudaSetDevice(pl->device);
   cudaDeviceSynchronize();
+  graphs_clear(pl);
+  for (auto &c : pl->cap)
+    if (c) cudaStreamDestroy(c);
   work_free(pl->ws);
   cudaFree(pl->P);
   cudaFree(pl->H);
@@ -413,6 +427,7 @@ int work_reserve(swe_plan *pl, int B) {
   Work &w = pl->ws;
   if (B <= w.cap) return OK;
   SWE_CUDA(cudaDeviceSynchronize());
+  graphs_clear(pl);
   work_free(w);
   const size_t ld = 2 * (size_t)B;
   const size_t spec = (size_t)pl->K * ld, half = (size_t)(pl->M + 1) * 2 * pl->Jp * ld;
@@ -427,8 +442,13 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaMallocHost(&w.h_iters, (size_t)B * sizeof(int)));
   SWE_CUDA(cudaHostAlloc(&w.h_pub, (size_t)(B + 1) * sizeof(int), cudaHostAllocMapped));
   SWE_CUDA(cudaHostGetDevicePointer(&w.d_pub, w.h_pub, 0));
-  SWE_CUDA(cudaMalloc(&w.sched, sizeof(unsigned long long)));
-  SWE_CUDA(cudaMemset(w.sched, 0, sizeof(unsigned long long)));
+  SWE_CUDA(cudaMalloc(&w.loop, sizeof(int)));
+  SWE_CUDA(cudaMalloc(&w.hdone, sizeof(unsigned)));
+  SWE_CUDA(cudaMemset(w.hdone, 0, sizeof(unsigned)));
+  SWE_CUDA(cudaHostAlloc(&w.h_fail, sizeof(int), cudaHostAllocMapped));
+  SWE_CUDA(cudaHostGetDevicePointer(&w.d_fail, w.h_fail, 0));
+  SWE_CUDA(cudaMalloc(&w.sched, 2 * sizeof(unsigned long long)));
+  SWE_CUDA(cudaMemset(w.sched, 0, 2 * sizeof(unsigned long long)));
   SWE_CUDA(cudaMalloc(&w.phi0, (size_t)B * sizeof(double)));
   SWE_CUDA(cudaMalloc(&w.phibar, (size_t)B * sizeof(double)));
   w.cap = B;

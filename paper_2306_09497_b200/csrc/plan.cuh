@@ -31,13 +31,15 @@ struct Work {
   // mapped (zero-copy) host words [1 + cap]: active count, then iters; written by
   // k_publish so the per-half-step check does not queue behind bulk D2H copies
   int *h_pub = nullptr, *d_pub = nullptr;
-  unsigned long long *sched = nullptr;  // Legendre v3 work-unit ticket counter (device)
-  unsigned long long sched_next = 0;    // host mirror: next unissued ticket
+  unsigned long long *sched = nullptr;  // Legendre v3 work-unit scheduler [2] (device)
+  int *loop = nullptr;                  // graph mode: fixed-point iteration counter (device)
+  unsigned *hdone = nullptr;            // k_helm last-block detection (device, zero between launches)
+  int *h_fail = nullptr, *d_fail = nullptr;  // graph mode: unconverged-solve flag (mapped)
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
 };
 
-constexpr int NSPEC = 22;
+constexpr int NSPEC = 25;  // 21-23: input backup of a graph-mode call
 constexpr int NHALF = 7;
 constexpr int NF = 4;
 
@@ -68,6 +70,17 @@ struct swe_plan {
   int radix[swe::FFT_MAXST], ns[swe::FFT_MAXST];
   std::vector<int> h_offsets;
   swe::Work ws;
+  // CUDA graphs of one IMEX step (stepper.cu), keyed by batch, stepper config and
+  // tuning switches; invalidated when the workspace is reallocated
+  struct StepGraph {
+    int B;
+    double dt, nu, tol;
+    int order, cor_impl, nonlin, max_iter, opts;
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+  };
+  std::vector<StepGraph> graphs;
+  cudaStream_t cap[2] = {nullptr, nullptr};  // capture streams (step, fixed-point body)
   int iter_guess = 1;  // fixed-point iterations launched before the first host check
   size_t table_bytes = 0;
 };

@@ -152,13 +152,39 @@ __global__ void k_coriolis(int K, int B, CorOp c, double *lcx, double *lcd) {
   }
 }
 
+// convergence decision of slice b (steppers.py:100-112) from the max-norm
+// statistics; resets them.  Returns whether the slice stays active.
+SWE_DEV bool decide_slice(int b, double *stats, int *active, int *iters, double tol) {
+  double *s = stats + (size_t)b * 8;
+  bool still = false;
+  if (active[b]) {
+    iters[b] += 1;
+    double v[6];
+    for (int q = 0; q < 6; ++q) v[q] = sqrt(s[q]);  // NaN stays NaN
+    double overall = fmax(fmax(v[0], v[1]), v[2]);
+    if (isnan(v[0]) || isnan(v[1]) || isnan(v[2])) overall = nan("");
+    overall = (overall > 1e-300 || isnan(overall)) ? overall : 1e-300;
+    bool done = true;
+    for (int f = 0; f < 3; ++f) {
+      const double tiny = 1e-13 * overall;
+      const double scale = (v[f] >= tiny || isnan(v[f])) ? v[f] : tiny;
+      if (v[3 + f] > tol * scale) done = false;
+    }
+    if (done) active[b] = 0;
+    else still = true;
+  }
+  for (int q = 0; q < 8; ++q) s[q] = 0.0;
+  return still;
+}
+
 template <int UN>  // modes per thread in flight
 __global__ void __launch_bounds__(256, UN == 4 ? 1 : 3) k_helm(int K, int B, const double *R0, const double *R1,
                                               const double *R2, const double *lcx,
                                               const double *lcd, double alpha, const double *eps,
                                               const double *phibar, double *U0, double *U1,
                                               double *U2, const int *active, double *stats,
-                                              CorOp cor, const int *iters, int *counter) {
+                                              CorOp cor, int *iters, int *counter,
+                                              double tol, unsigned *hdone) {
   // block: 32 slices x 8 mode rows; grid.x over slice tiles, grid.y over modes
   __shared__ unsigned long long red[8][32][6];
   const int b = blockIdx.x * 32 + threadIdx.x;
@@ -246,6 +272,28 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 3) k_helm(int K, int B, con
       atomicMax(reinterpret_cast<unsigned long long *>(stats) + (size_t)b * 8 + q, v);
     }
   }
+  if (!hdone) return;
+  // the last block to finish decides every slice (k_decide fused: one launch less
+  // per fixed-point iteration); hdone returns to 0 for the next launch
+  __shared__ bool last;
+  __shared__ int cnt;
+  __threadfence();
+  __syncthreads();
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nthr = blockDim.x * blockDim.y;
+  if (tid == 0) {
+    last = atomicAdd(hdone, 1u) == gridDim.x * gridDim.y - 1;
+    cnt = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int bb = tid; bb < B; bb += nthr)
+    if (decide_slice(bb, stats, const_cast<int *>(active), iters, tol)) atomicAdd(&cnt, 1);
+  __syncthreads();
+  if (tid == 0) {
+    *counter = cnt;
+    *hdone = 0;
+  }
 }
 
 // Crank-Nicolson half step prologue (steppers.py:143-152) in one pass:
@@ -312,7 +360,9 @@ __global__ void __launch_bounds__(256) k_cn_start(int K, int B, Ptr3C x0, Ptr3C 
 // count) copy xi/delta back to A = u[1], u[2]; with dtnu != 0 the viscosity
 // factor (dynamics.py:191-200) is applied to every slice on the way.
 __global__ void k_cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2,
-                            const int *iters, const double *nn1a2, double dtnu, double halfq) {
+                            const int *iters, const double *nn1a2, double dtnu, double halfq,
+                            const int *counter, int *fail) {
+  if (fail && blockIdx.x == 0 && threadIdx.x == 0 && *counter > 0) *fail = 1;
   FOR_KB(K, B) {
     const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
     const bool odd = iters && (iters[b] & 1);
@@ -328,28 +378,19 @@ __global__ void k_cn_finish(int K, int B, Ptr3 u, const double *b1, const double
   }
 }
 
+// CUDA-graph fixed point: WHILE-node condition after each iteration (the host
+// loop's `active > 0 && it < max_iter`, steppers.py:96-112, evaluated on device)
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int *counter, int *loop,
+                            int max_iter) {
+  const int it = ++*loop;
+  cudaGraphSetConditional(h, (*counter > 0 && it < max_iter) ? 1u : 0u);
+}
+
 // per-slice convergence decision (steppers.py:100-112); resets stats
 __global__ void k_decide(int B, double *stats, int *active, int *iters, int *counter, double tol) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  double *s = stats + (size_t)b * 8;
-  if (active[b]) {
-    iters[b] += 1;
-    double v[6];
-    for (int q = 0; q < 6; ++q) v[q] = sqrt(s[q]);  // NaN stays NaN
-    double overall = fmax(fmax(v[0], v[1]), v[2]);
-    if (isnan(v[0]) || isnan(v[1]) || isnan(v[2])) overall = nan("");
-    overall = (overall > 1e-300 || isnan(overall)) ? overall : 1e-300;
-    bool done = true;
-    for (int f = 0; f < 3; ++f) {
-      const double tiny = 1e-13 * overall;
-      const double scale = (v[f] >= tiny || isnan(v[f])) ? v[f] : tiny;
-      if (v[3 + f] > tol * scale) done = false;
-    }
-    if (done) active[b] = 0;
-    else atomicAdd(counter, 1);
-  }
-  for (int q = 0; q < 8; ++q) s[q] = 0.0;
+  if (decide_slice(b, stats, active, iters, tol)) atomicAdd(counter, 1);
 }
 
 __global__ void k_fill_int(int *p, int n, int v) {
@@ -504,17 +545,17 @@ int coriolis_spec(int K, int B, const CorOp &c, double *lcx, double *lcd, cudaSt
 
 int helm(int K, int B, const double *const R[3], const double *lcx, const double *lcd,
          double alpha, const double *eps, const double *phibar, double *const U[3],
-         const int *active, double *stats, cudaStream_t st, const CorOp *cor, const int *iters,
-         int *counter) {
+         const int *active, double *stats, cudaStream_t st, const CorOp *cor, int *iters,
+         int *counter, double tol, unsigned *hdone) {
   const int ybl = std::max(1, std::min((K + 7) / 8, (148 * 8) / ((B + 31) / 32)));
   dim3 grid((B + 31) / 32, ybl), blk(32, 8);
   CorOp c = cor ? *cor : CorOp{nullptr, nullptr, nullptr, nullptr};
   if (cor)
     k_helm<1><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
-                                     U[1], U[2], active, stats, c, iters, counter);
+                                     U[1], U[2], active, stats, c, iters, counter, tol, hdone);
   else
     k_helm<4><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
-                                     U[1], U[2], active, stats, c, iters, counter);
+                                     U[1], U[2], active, stats, c, iters, counter, tol, hdone);
   SWE_LAUNCH_CHECK();
   return OK;
 }
@@ -529,8 +570,17 @@ int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
 }
 
 int cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2, const int *iters,
-              const double *nn1a2, double dtnu, double halfq, cudaStream_t st) {
-  k_cn_finish<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, u, b1, b2, iters, nn1a2, dtnu, halfq);
+              const double *nn1a2, double dtnu, double halfq, cudaStream_t st,
+              const int *counter, int *fail) {
+  k_cn_finish<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, u, b1, b2, iters, nn1a2, dtnu, halfq,
+                                                      counter, fail);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+int loop_cond(cudaGraphConditionalHandle h, const int *counter, int *loop, int max_iter,
+              cudaStream_t st) {
+  k_loop_cond<<<1, 1, 0, st>>>(h, counter, loop, max_iter);
   SWE_LAUNCH_CHECK();
   return OK;
 }

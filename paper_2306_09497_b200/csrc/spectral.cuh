@@ -40,17 +40,24 @@ int coriolis_spec(int K, int B, const CorOp &c, double *lcx, double *lcd, cudaSt
 // cor != nullptr: L_C is evaluated inline from the previous iterate, which for
 // slice b is in A = (cor->x, cor->d) when iters[b] is even and in B = (U[1], U[2])
 // when odd; the new xi/delta go to the other pair (Phi stays in U[0]).
-// counter (nullable) is zeroed for the k_decide that follows.
+// counter (nullable) is zeroed for the k_decide that follows; with hdone (a
+// zeroed device word) the kernel's last block makes that decision itself
+// (k_decide fused) and writes the active count to *counter.
 int helm(int K, int B, const double *const R[3], const double *lcx, const double *lcd,
          double alpha, const double *eps, const double *phibar, double *const U[3],
          const int *active, double *stats, cudaStream_t st, const CorOp *cor = nullptr,
-         const int *iters = nullptr, int *counter = nullptr);
+         int *iters = nullptr, int *counter = nullptr, double tol = 0.0,
+         unsigned *hdone = nullptr);
 int publish(int B, const int *counter, const int *iters, int *pub, cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
              cudaStream_t st);
+// counter/fail (nullable): graph mode records an unconverged fixed point in *fail
 int cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2, const int *iters,
-              const double *nn1a2, double dtnu, double halfq, cudaStream_t st);
+              const double *nn1a2, double dtnu, double halfq, cudaStream_t st,
+              const int *counter = nullptr, int *fail = nullptr);
+int loop_cond(cudaGraphConditionalHandle h, const int *counter, int *loop, int max_iter,
+              cudaStream_t st);
 int decide(int B, double *stats, int *active, int *iters, int *counter, double tol,
            cudaStream_t st);
 int fill_int(int *p, int n, int v, cudaStream_t st);

@@ -35,6 +35,8 @@ struct ProfRec {
   double work;
 };
 bool g_prof = false;
+bool g_capturing = false;  // a step graph is being captured: no events, no host syncs
+int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
 int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
 // Coriolis operator (eval_coriolis): 2 spectral three-term recurrence, fused into the
@@ -57,7 +59,7 @@ struct ProfScope {
   bool on;
   ProfRec rec;
   cudaStream_t st;
-  ProfScope(int cls, double work, cudaStream_t s) : on(g_prof), st(s) {
+  ProfScope(int cls, double work, cudaStream_t s) : on(g_prof && !g_capturing), st(s) {
     if (!on) return;
     rec.cls = cls;
     rec.work = work;
@@ -77,6 +79,8 @@ struct Run {
   int B;
   size_t ld;
   cudaStream_t st;
+  bool graph = false;          // capturing a step graph (cn_half_spec builds a WHILE node)
+  cudaStream_t st2 = nullptr;  // capture stream of the fixed-point body
   double *spec(int i) const { return pl->ws.spec + (size_t)i * pl->K * ld; }
   // E/O half spectra and F+/F- analysis inputs: [m][2][Jp][ld] each
   size_t plane() const { return (size_t)(pl->M + 1) * 2 * pl->Jp * ld; }
@@ -94,7 +98,6 @@ LegArgs leg_args(const Run &r) {
   a.ld = (int)r.ld;
   a.offsets = r.pl->offsets;
   a.sched = r.pl->ws.sched;
-  a.sched_next = &r.pl->ws.sched_next;
   return a;
 }
 
@@ -208,7 +211,8 @@ bool fft_uses_lanes(const Run &r) {
   a.N2 = r.pl->N2;
   a.nst = r.pl->nst;
   for (int s = 0; s < r.pl->nst; ++s) a.radix[s] = r.pl->radix[s];
-  const bool lanes = g_fft_path == 2 || (g_fft_path == 0 && r.B >= 8);
+  // the nonlinear pass (one slice per CTA anyway) takes the lane kernel at any batch
+  const bool lanes = g_fft_path == 2 || g_fft_path == 0;
   return lanes && fft_lanes_ok(a);
 }
 
@@ -254,7 +258,8 @@ int fft(const Run &r, int op, FftArgs &a) {
                                  (size_t)(pl->Jp - pl->Jh) * r.ld * 8, (size_t)(pl->M + 1) * 2,
                                  r.st));
   // path: lane = row kernel for small-radix lengths with enough slices, else warp-per-row
-  const bool lanes = g_fft_path == 2 || (g_fft_path == 0 && r.B >= 8);
+  const bool lanes =
+      g_fft_path == 2 || (g_fft_path == 0 && (r.B >= 8 || op == FOP_NONLINEAR));
   if (lanes && fft_lanes_ok(a)) {
     ProfScope ps(2, bytes, r.st);
     return fft_lanes_launch(op, a, r.st);
@@ -521,6 +526,45 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     if ((rc = cn_start(K, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, cor, R, D, r.st))) return rc;
   }
   int active = 0;
+  if (impl && r.graph) {
+    // CUDA graph: the iteration loop is a conditional WHILE node whose body (Helmholtz
+    // with inline L_C, decision, condition update) runs until no slice is active or
+    // max_iter is reached; an unconverged exit raises *d_fail in the epilogue
+    if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
+    SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * 8 * B, r.st));
+    SWE_CUDA(cudaMemsetAsync(w.loop, 0, sizeof(int), r.st));
+    SWE_CUDA(cudaMemsetAsync(w.counter, 0, sizeof(int), r.st));
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t g;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    SWE_CUDA(cudaStreamGetCaptureInfo(r.st, &cst, nullptr, &g, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    SWE_CUDA(cudaGraphConditionalHandleCreate(&h, g, cfg.implicit_max_iter > 0 ? 1u : 0u,
+                                              cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {cudaGraphNodeTypeConditional};
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    SWE_CUDA(cudaGraphAddNode(&node, g, deps, nd, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    SWE_CUDA(cudaStreamBeginCaptureToGraph(r.st2, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    const double *Rc[3] = {b.R[0], b.R[1], b.R[2]};
+    double *const U[3] = {dst[0], b.LC[0], b.LC[1]};
+    const CorOp c{dst[1], dst[2], pl->cor_nb, pl->cor_cf};
+    if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, U, w.flags, w.stats,
+                   r.st2, &c, w.iters, w.counter, cfg.implicit_tol, w.hdone)) ||
+        (rc = loop_cond(h, w.counter, w.loop, cfg.implicit_max_iter, r.st2)))
+      return rc;
+    cudaGraph_t body_out;
+    SWE_CUDA(cudaStreamEndCapture(r.st2, &body_out));
+    SWE_CUDA(cudaStreamUpdateCaptureDependencies(r.st, &node, 1, cudaStreamSetCaptureDependencies));
+    Ptr3 u = {{dst[0], dst[1], dst[2]}};
+    return cn_finish(K, B, u, b.LC[0], b.LC[1], w.iters, pl->eps, dtnu, cfg.visc_order / 2.0, r.st,
+                     w.counter, w.d_fail);
+  }
   if (impl) {
     if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
     SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * 8 * B, r.st));
@@ -534,12 +578,11 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
       for (int j = 0; j < n; ++j) {
         {
           ProfScope ps(3, 9.0 * 16.0 * K * B, r.st);  // rhs 3 + old 3 in, new 3 out
+          // the kernel's last block takes the per-slice decision (k_decide fused)
           if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, U, w.flags,
-                         w.stats, r.st, &c, w.iters, w.counter)))
+                         w.stats, r.st, &c, w.iters, w.counter, cfg.implicit_tol, w.hdone)))
             return rc;
         }
-        if ((rc = decide(B, w.stats, w.flags, w.iters, w.counter, cfg.implicit_tol, r.st)))
-          return rc;
       }
       launched += n;
       batch = 1;
@@ -635,6 +678,63 @@ int imex_internal(const Run &r, const swe_stepper_cfg &cfg, int *iters_host, dou
     Ptr3 u = {{b.U[0], b.U[1], b.U[2]}};
     if ((rc = visc(pl->K, r.B, u, pl->eps, dt * cfg.visc_nu, cfg.visc_order / 2.0, r.st))) return rc;
   }
+  return OK;
+}
+
+int options_key() { return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8); }
+
+// CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
+// capture stream on the second call with a given key (the first runs eagerly:
+// kernel attributes set, code paths warmed).  *exec stays null when the step
+// cannot be captured (Coriolis modes that need host-driven loops).
+int step_graph(const Run &r, const swe_stepper_cfg &cfg, cudaGraphExec_t *exec) {
+  swe_plan *pl = r.pl;
+  *exec = nullptr;
+  if (g_fast_coriolis != 2 && cfg.coriolis_implicit) return OK;
+  const int opts = options_key();
+  for (auto &g : pl->graphs)
+    if (g.B == r.B && g.dt == cfg.dt && g.nu == cfg.visc_nu && g.tol == cfg.implicit_tol &&
+        g.order == cfg.visc_order && g.cor_impl == cfg.coriolis_implicit &&
+        g.nonlin == cfg.include_nonlinear && g.max_iter == cfg.implicit_max_iter &&
+        g.opts == opts) {
+      if (!g.exec) {  // seen once: capture now
+        Run rr = r;
+        for (auto &c : pl->cap)
+          if (!c) SWE_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+        rr.st = pl->cap[0];
+        rr.st2 = pl->cap[1];
+        rr.graph = true;
+        g_capturing = true;
+        cudaError_t e = cudaStreamBeginCapture(rr.st, cudaStreamCaptureModeRelaxed);
+        int rc = e == cudaSuccess ? imex_internal(rr, cfg, nullptr, nullptr) : E_CUDA;
+        cudaGraph_t graph = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(rr.st, &graph);
+        g_capturing = false;
+        if (e != cudaSuccess || rc || e2 != cudaSuccess) {
+          if (graph) cudaGraphDestroy(graph);
+          cudaGetLastError();
+          set_error("step graph capture failed: %s", cudaGetErrorString(e ? e : e2));
+          return rc ? rc : E_CUDA;
+        }
+        SWE_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+        g.graph = graph;
+      }
+      *exec = g.exec;
+      return OK;
+    }
+  swe_plan::StepGraph g;
+  g.B = r.B;
+  g.dt = cfg.dt;
+  g.nu = cfg.visc_nu;
+  g.tol = cfg.implicit_tol;
+  g.order = cfg.visc_order;
+  g.cor_impl = cfg.coriolis_implicit;
+  g.nonlin = cfg.include_nonlinear;
+  g.max_iter = cfg.implicit_max_iter;
+  g.opts = opts;
+  g.graph = nullptr;
+  g.exec = nullptr;
+  pl->graphs.push_back(g);
   return OK;
 }
 
@@ -852,10 +952,33 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
   const Bufs b = bufs(r);
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
   if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st))) return rc;
-  for (int s = 0; s < nsteps; ++s) {
-    rc = imex_internal(r, *cfg, iters_out ? iters_out + (size_t)s * 2 * batch : nullptr, resid_out);
-    if (rc) return rc;
+  cudaGraphExec_t exec = nullptr;
+  // graphs replay unprofiled launches: the per-class profile (swe_profile) keeps the
+  // eager path
+  if (g_graphs && !g_prof && !iters_out && nsteps > 0 && (rc = step_graph(r, *cfg, &exec)))
+    return rc;
+  if (exec) {
+    // one graph launch per step, one host check per call; an unconverged solve
+    // (flagged on device) reruns the call on the host-driven path from the saved
+    // input so the error and residual are reported exactly as steppers.py does
+    const size_t bytes = (size_t)pl->K * r.ld * sizeof(double);
+    for (int f = 0; f < 3; ++f)
+      SWE_CUDA(cudaMemcpyAsync(r.spec(21 + f), b.U[f], bytes, cudaMemcpyDeviceToDevice, r.st));
+    SWE_CUDA(cudaMemsetAsync(pl->ws.d_fail, 0, sizeof(int), r.st));
+    for (int s = 0; s < nsteps; ++s) SWE_CUDA(cudaGraphLaunch(exec, r.st));
+    SWE_CUDA(cudaStreamSynchronize(r.st));
+    if (*reinterpret_cast<volatile int *>(pl->ws.h_fail)) {
+      for (int f = 0; f < 3; ++f)
+        SWE_CUDA(cudaMemcpyAsync(b.U[f], r.spec(21 + f), bytes, cudaMemcpyDeviceToDevice, r.st));
+      exec = nullptr;
+    }
   }
+  if (!exec)
+    for (int s = 0; s < nsteps; ++s) {
+      rc = imex_internal(r, *cfg, iters_out ? iters_out + (size_t)s * 2 * batch : nullptr,
+                         resid_out);
+      if (rc) return rc;
+    }
   SpecPtrsC s = {{b.U[0], b.U[1], b.U[2]}};
   return to_boundary(s, state, batch, 3, pl->K, pl->perm, r.st);
 }
@@ -882,6 +1005,10 @@ long long swe_kernel_launches(void) { return g_launches; }
 int swe_set_option(const char *key, int value) {
   if (key && strcmp(key, "fft_path") == 0 && value >= 0 && value <= 2) {
     g_fft_path = value;
+    return OK;
+  }
+  if (key && strcmp(key, "graphs") == 0 && (value == 0 || value == 1)) {
+    g_graphs = value;
     return OK;
   }
   if (key && strcmp(key, "fast_coriolis") == 0 && value >= 0 && value <= 2) {

@@ -265,3 +265,43 @@ def test_nonlinear_prime_factor_sizes(mods, M, B, path):
     for f in range(3):
         g = got[f].cpu().numpy()
         assert np.abs(g - want[f]).max() <= 1e-11 * np.abs(want[f]).max(), f
+
+
+@pytest.mark.parametrize("M,B", [(32, 3), (51, 40)])
+def test_step_graph_matches_eager(mods, M, B):
+    """Replayed CUDA step graphs (fixed point as a WHILE node) give bitwise the
+    eager host-driven result; first call eager, second captures, later replay."""
+    spharm, dynamics, steppers, scenarios = mods
+    import torch
+    from paper_2306_09497_b200 import _lib
+    grid = spharm.get_grid(M)
+    cfg = steppers.StepperConfig(dt=240.0, viscosity=dynamics.ViscositySpec(2, 1e5))
+    base = scenarios.gaussian_bumps(grid, batch=B)
+    rng = np.random.default_rng(M)
+    taper = torch.from_numpy((grid.n_of + 1.0) ** -2).cuda()
+    noise = torch.from_numpy(rng.standard_normal((B, grid.n_modes))).cuda() * taper
+    noise[:, : M + 1] = noise[:, : M + 1].real
+    base.data[:, 1] += 1e-6 * noise
+    outs = {}
+    for graphs in (0, 1):
+        _lib.set_option("graphs", graphs)
+        try:
+            s = base.copy()
+            for _ in range(4):
+                steppers.imex_steps_inplace(s, cfg, 2)
+            outs[graphs] = s.data.cpu()
+        finally:
+            _lib.set_option("graphs", 1)
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_step_graph_nonconvergence_raises(mods):
+    """An unconverged fixed point inside a replayed graph is caught on the device
+    and re-run on the host path, raising ImplicitSolveError with the residual."""
+    _, dynamics, steppers, _ = mods
+    g = load_golden("step_M16.npz")
+    s = _state(mods, 16, g["bumps_dt600_nu1e5_in"], g["phibar"])
+    cfg = steppers.StepperConfig(dt=600.0, implicit_max_iter=1)
+    for _ in range(3):
+        with pytest.raises(steppers.ImplicitSolveError, match="residual"):
+            steppers.imex_step(s, cfg)
