@@ -189,6 +189,32 @@ def make_states(grid, n, seed):
     return s
 
 
+def pint_cfg2(torch, iters=10):
+    """cfg2 end to end (SURVEY.md §8d "steps/s accounting"): MGRIT L=2, fine M=256
+    dt=60 nu=1e5, coarse M=51 dt=120 nu=1e5, cfactor 2, nrelax 1, N0=128, T=7680 s,
+    on this GPU (one rank).  Reference-equivalent fine steps/s = engine-accounted
+    level-0 steps per iteration x iterations / wall time of the iterations (host
+    clock with a device sync per iteration; the initial guess and the serial fine
+    reference excluded)."""
+    from paper_2306_09497_b200 import dynamics, pint, scenarios, spharm, steppers
+    lv = [pint.LevelSpec(0, 256, steppers.StepperConfig(dt=60.0, viscosity=dynamics.ViscositySpec(2, 1e5))),
+          pint.LevelSpec(1, 51, steppers.StepperConfig(dt=120.0, viscosity=dynamics.ViscositySpec(2, 1e5)))]
+    pc = pint.PintConfig(levels=tuple(lv), T=7680.0, N0=128, cfactor=2, nrelax=1, max_iters=iters)
+    prob = pint.SweProblem(pc)
+    u0 = prob.as_batch(0, scenarios.gaussian_bumps(prob.grids[0]))
+    warm = pint.PintConfig(levels=tuple(lv), T=7680.0, N0=128, cfactor=2, nrelax=1, max_iters=2)
+    pint.MgritEngine(prob, warm).run(u0, sync=torch.cuda.synchronize)     # graphs captured
+    tr = pint.MgritEngine(prob, pc).run(u0, sync=torch.cuda.synchronize)
+    wall = float(sum(tr.wall_times[1:]))
+    steps = int(sum(tr.fine_steps))
+    return {"value": steps / wall, "unit": "reference-equivalent fine steps/s",
+            "config": "cfg2: MGRIT L=2, M=256/51, dt=60/120 s, nu=1e5, cfactor 2, nrelax 1, "
+                      "N0=128, T=7680 s, gaussian_bumps",
+            "iterations": tr.iterations, "fine_steps_per_iteration": steps // max(tr.iterations, 1),
+            "ms_per_iteration": 1e3 * wall / max(tr.iterations, 1),
+            "timing": "host wall clock with a device sync per iteration (MgritEngine.run)"}
+
+
 def ncu_traffic():
     """DRAM bytes per launch of the dominant kernels from the newest committed
     `ncu --set full` capture (profiles/*_kernels.json, tools/ncu_summary.py)."""
@@ -363,6 +389,8 @@ def run_ours(args):
             "gpu_launches_note": "counted over the profiled pass (eager launches of the same "
                                  "kernels the timed pass replays as one CUDA graph per step)",
             "ms_per_step_profiled_eager": prof_ms / args.steps, "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_pint:
+        line["pint_cfg2"] = pint_cfg2(torch)
     if rank == 0 and world == 1 and not args.no_cpu:
         nproc = min(cpu_cores(), 16)
         el, done = cpu_steps(1, nproc)
@@ -384,6 +412,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--slices", type=int, default=SLICES_PER_GPU)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-pint", action="store_true", help="skip the cfg2 MGRIT leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
