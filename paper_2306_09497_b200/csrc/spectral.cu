@@ -185,9 +185,11 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 3) k_helm(int K, int B, con
                                               double *U2, const int *active, double *stats,
                                               CorOp cor, int *iters, int *counter,
                                               double tol, unsigned *hdone) {
-  // block: 32 slices x 8 mode rows; grid.x over slice tiles, grid.y over modes
-  __shared__ unsigned long long red[8][32][6];
-  const int b = blockIdx.x * 32 + threadIdx.x;
+  // block: bx slices x by mode rows (bx = 32, or the batch rounded up to a power of
+  // two when smaller, so small batches keep every lane busy); grid.x over slice
+  // tiles, grid.y over modes
+  __shared__ unsigned long long red[256][6];
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long mx[6] = {0, 0, 0, 0, 0, 0};
   const bool fused = cor.x != nullptr;
   if (counter && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
@@ -263,12 +265,12 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 3) k_helm(int K, int B, con
   }
   if (!stats) return;
 #pragma unroll
-  for (int q = 0; q < 6; ++q) red[threadIdx.y][threadIdx.x][q] = mx[q];
+  for (int q = 0; q < 6; ++q) red[threadIdx.y * blockDim.x + threadIdx.x][q] = mx[q];
   __syncthreads();
   if (threadIdx.y == 0 && act) {
     for (int q = 0; q < 6; ++q) {
-      unsigned long long v = red[0][threadIdx.x][q];
-      for (int r = 1; r < blockDim.y; ++r) v = max(v, red[r][threadIdx.x][q]);
+      unsigned long long v = red[threadIdx.x][q];
+      for (int r = 1; r < blockDim.y; ++r) v = max(v, red[r * blockDim.x + threadIdx.x][q]);
       atomicMax(reinterpret_cast<unsigned long long *>(stats) + (size_t)b * 8 + q, v);
     }
   }
@@ -547,8 +549,15 @@ int helm(int K, int B, const double *const R[3], const double *lcx, const double
          double alpha, const double *eps, const double *phibar, double *const U[3],
          const int *active, double *stats, cudaStream_t st, const CorOp *cor, int *iters,
          int *counter, double tol, unsigned *hdone) {
-  const int ybl = std::max(1, std::min((K + 7) / 8, (148 * 8) / ((B + 31) / 32)));
-  dim3 grid((B + 31) / 32, ybl), blk(32, 8);
+  int bx = 1;
+  while (bx < B && bx < 32) bx <<= 1;
+  // rows per block: at least a warp, at most 256 threads, and small enough that
+  // small problems still spread over >= 2 blocks per SM
+  int by = 256 / bx;
+  while (by > 32 / bx && by > 1 && (size_t)((K + by - 1) / by) * ((B + bx - 1) / bx) < 296) by >>= 1;
+  const int gx = (B + bx - 1) / bx;
+  const int ybl = std::max(1, std::min((K + by - 1) / by, (148 * 8) / gx));
+  dim3 grid(gx, ybl), blk(bx, by);
   CorOp c = cor ? *cor : CorOp{nullptr, nullptr, nullptr, nullptr};
   if (cor)
     k_helm<1><<<grid, blk, 0, st>>>(K, B, R[0], R[1], R[2], lcx, lcd, alpha, eps, phibar, U[0],
