@@ -273,13 +273,13 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 3) k_helm(int K, int B, con
       for (int r = 1; r < blockDim.y; ++r) v = max(v, red[r * blockDim.x + threadIdx.x][q]);
       atomicMax(reinterpret_cast<unsigned long long *>(stats) + (size_t)b * 8 + q, v);
     }
+    if (hdone) __threadfence();  // this block's statistics before its check-in
   }
   if (!hdone) return;
   // the last block to finish decides every slice (k_decide fused: one launch less
   // per fixed-point iteration); hdone returns to 0 for the next launch
   __shared__ bool last;
   __shared__ int cnt;
-  __threadfence();
   __syncthreads();
   const int tid = threadIdx.y * blockDim.x + threadIdx.x, nthr = blockDim.x * blockDim.y;
   if (tid == 0) {

@@ -499,6 +499,10 @@ int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *con
   return OK;
 }
 
+// k_decide fused into k_helm's last block pays off while launches dominate (small
+// K*B); for large batches the extra block check-in costs more than a launch
+bool fuse_decide(int K, int B) { return (size_t)K * B <= (size_t)1 << 20; }
+
 // Crank-Nicolson half step with the spectral Coriolis operator (g_fast_coriolis == 2
 // or explicit Coriolis): X = x0 + s (x1 + x2); dst = (I - a L)^-1 (I + a L) X, then
 // the viscosity factor when dtnu != 0.  One fused prologue (k_cn_start), the
@@ -554,8 +558,10 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     const double *Rc[3] = {b.R[0], b.R[1], b.R[2]};
     double *const U[3] = {dst[0], b.LC[0], b.LC[1]};
     const CorOp c{dst[1], dst[2], pl->cor_nb, pl->cor_cf};
+    unsigned *hd = fuse_decide(K, B) ? w.hdone : nullptr;
     if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, U, w.flags, w.stats,
-                   r.st2, &c, w.iters, w.counter, cfg.implicit_tol, w.hdone)) ||
+                   r.st2, &c, w.iters, w.counter, cfg.implicit_tol, hd)) ||
+        (!hd && (rc = decide(B, w.stats, w.flags, w.iters, w.counter, cfg.implicit_tol, r.st2))) ||
         (rc = loop_cond(h, w.counter, w.loop, cfg.implicit_max_iter, r.st2)))
       return rc;
     cudaGraph_t body_out;
@@ -578,9 +584,12 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
       for (int j = 0; j < n; ++j) {
         {
           ProfScope ps(3, 9.0 * 16.0 * K * B, r.st);  // rhs 3 + old 3 in, new 3 out
-          // the kernel's last block takes the per-slice decision (k_decide fused)
+          // small problems: the kernel's last block takes the per-slice decision
+          unsigned *hd = fuse_decide(K, B) ? w.hdone : nullptr;
           if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, U, w.flags,
-                         w.stats, r.st, &c, w.iters, w.counter, cfg.implicit_tol, w.hdone)))
+                         w.stats, r.st, &c, w.iters, w.counter, cfg.implicit_tol, hd)))
+            return rc;
+          if (!hd && (rc = decide(B, w.stats, w.flags, w.iters, w.counter, cfg.implicit_tol, r.st)))
             return rc;
         }
       }

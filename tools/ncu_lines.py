@@ -1,6 +1,6 @@
 """Per-source-line warp-stall samples of one kernel in an ncu report (run here).
 
-    python tools/ncu_lines.py <report.ncu-rep> <cubin> <mangled-kernel-substring> [top]
+    python tools/ncu_lines.py <report.ncu-rep> <cubin> <mangled-kernel-substring> [top] [report-name-substring]
 
 Joins ncu's SASS-level sampling (--page source --print-source sass) with the
 line table of the cubin (nvdisasm -g), because the CUDA-level source page
@@ -32,6 +32,7 @@ def line_map(cubin, kname):
 def main():
     rep, cubin, kname = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+    rname = sys.argv[5] if len(sys.argv) > 5 else kname
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -47,7 +48,7 @@ def main():
         if r and r[0] == "Address":
             hdr = r
             continue
-        if taken or hdr is None or kname not in cur or len(r) != len(hdr):
+        if taken or hdr is None or rname not in cur or len(r) != len(hdr):
             continue
         data.append(dict(zip(hdr, r)))
     base = int(data[0]["Address"], 16)
