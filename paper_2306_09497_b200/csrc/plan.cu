@@ -236,12 +236,20 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
         nb[k].x = (n - 1 >= m && n - 1 >= 1) ? row(m, n - 1) : -1;
         nb[k].y = n + 1 <= M ? row(m, n + 1) : -1;
         const double nn1 = (double)n * (n + 1.0);
-        cf[k].x = n > 0 ? w2 * epsh(m, n) * ((n + 1.0) / n) : 0.0;
-        cf[k].y = w2 * epsh(m, n + 1) * (n / (n + 1.0));
+        // absent neighbours (n-1 < m, n-1 = 0, n+1 > M) get a zero coefficient
+        cf[k].x = nb[k].x >= 0 ? w2 * epsh(m, n) * ((n + 1.0) / n) : 0.0;
+        cf[k].y = nb[k].y >= 0 ? w2 * epsh(m, n + 1) * (n / (n + 1.0)) : 0.0;
         cf[k].z = nn1 > 0 ? w2 * (m / nn1) : 0.0;
         cf[k].w = m == 0 ? 1.0 : 0.0;
       }
     if ((rc = upload(&pl->cor_nb, nb)) || (rc = upload(&pl->cor_cf, cf))) return rc;
+    // k_helm_tiled work: each m-block in chunks of 64 consecutive n (32 even + 32 odd
+    // rows of the parity-split order), largest m-blocks first
+    std::vector<int2> tiles;
+    for (int m = 0; m <= M; ++m)
+      for (int c = 0; c < (M + 1 - m + 63) / 64; ++c) tiles.push_back(make_int2(m, c));
+    pl->n_helm_tiles = (int)tiles.size();
+    if ((rc = upload(&pl->helm_tiles, tiles))) return rc;
   }
 
   // Legendre tables on the device (north pairs only)
@@ -411,6 +419,7 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->wsin2);
   cudaFree(pl->cor_scale);
   cudaFree(pl->cor_nb);
+  cudaFree(pl->helm_tiles);
   cudaFree(pl->cor_cf);
   cudaFree(pl->tw);
   cudaFree(pl->twh);

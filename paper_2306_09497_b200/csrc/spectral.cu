@@ -298,6 +298,122 @@ __global__ void __launch_bounds__(256, UN == 4 ? 1 : 3) k_helm(int K, int B, con
   }
 }
 
+// Tiled fixed-point iterate (batches of >= 32 slices): one CTA = one chunk of 64
+// consecutive n of an m-block (32 even + 32 odd rows of the parity-split order)
+// x 32 slices.  The previous iterate's xi/delta rows of the chunk plus one halo
+// row per parity are staged in shared memory with coalesced loads, so the
+// three-term Coriolis stencil reads its neighbours there; rhs and Phi stream
+// straight through.  Same arithmetic and statistics as k_helm.
+constexpr int HT_ROWS = 33;
+__global__ void __launch_bounds__(256, 3)
+    k_helm_tiled(int M, int B, const int *__restrict__ offsets, const int2 *__restrict__ tiles,
+                 const double *R0, const double *R1, const double *R2, double alpha,
+                 const double *eps, const double *phibar, double *U0, double *A1, double *A2,
+                 double *B1, double *B2, const double4 *__restrict__ cfc, const int *active,
+                 double *stats, const int *iters, int *counter) {
+  extern __shared__ double2 hsm[];  // [field xi/delta][parity][HT_ROWS][32]
+  if (counter && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+    *counter = 0;  // for the k_decide that follows
+  const int2 tl = tiles[blockIdx.x];
+  const int m = tl.x, c = tl.y;
+  const int km = M + 1 - m, ne = (km + 1) >> 1, no = km >> 1, off = offsets[m];
+  const int lane = threadIdx.x, ty = threadIdx.y;
+  const int b = blockIdx.y * 32 + lane;
+  const bool act = b < B && active[b];
+  const bool odd_it = act && (iters[b] & 1);
+  const double *X = odd_it ? B1 : A1, *D = odd_it ? B2 : A2;
+  double *WX = odd_it ? A1 : B1, *WD = odd_it ? A2 : B2;
+  auto sm = [&](int f, int p, int j) -> double2 & {
+    return hsm[((f * 2 + p) * HT_ROWS + j) * 32 + lane];
+  };
+  for (int t = ty; t < 2 * HT_ROWS; t += blockDim.y) {
+    const int p = t >= HT_ROWS, j = t - p * HT_ROWS;
+    const int gi = 32 * c + j - p;  // even rows 32c.., odd rows 32c-1..
+    double2 x = make_double2(0.0, 0.0), d = x;
+    if (act && gi >= 0 && gi < (p ? no : ne)) {
+      const size_t i = (size_t)(off + (p ? ne : 0) + gi) * B + b;
+      x = ld2(X, i);
+      d = ld2(D, i);
+    }
+    sm(0, p, j) = x;
+    sm(1, p, j) = d;
+  }
+  __syncthreads();
+  unsigned long long mx[6] = {0, 0, 0, 0, 0, 0};
+  if (act) {
+    const double pb = phibar[b], apb = alpha * pb, aap = alpha * alpha * pb;
+#pragma unroll 2
+    for (int q = 0; q < 8; ++q) {
+      const int p = q & 1, li = ty * 4 + (q >> 1), gi = 32 * c + li;
+      if (gi >= (p ? no : ne)) continue;
+      const int k = off + (p ? ne : 0) + gi;
+      const size_t i = (size_t)k * B + b;
+      const double2 rp = ld2(R0, i), r1 = ld2(R1, i), r2 = ld2(R2, i), o0 = ld2(U0, i);
+      const double e = eps[k];
+      const double4 cf = cfc[k];
+      // self row and the n-1 / n+1 rows (other parity) from shared memory
+      const int js = p ? li + 1 : li;
+      const double2 x = sm(0, p, js), d = sm(1, p, js);
+      const double2 xl = sm(0, 1 - p, li), dl = sm(1, 1 - p, li);
+      const double2 xh = sm(0, 1 - p, li + 1), dh = sm(1, 1 - p, li + 1);
+      double2 lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * x.y),
+                                -(cf.x * dl.y + cf.y * dh.y - cf.z * x.x));
+      double2 lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * d.y,
+                                cf.x * xl.y + cf.y * xh.y + cf.z * d.x);
+      if (cf.w != 0.0) {
+        lx.y = 0.0;
+        lc.y = 0.0;
+      }
+      const double2 rx = add2(r1, sc2(alpha, lx)), rd = add2(r2, sc2(alpha, lc));
+      const double denom = 1.0 + aap * e;
+      const double2 ph = make_double2((rp.x - apb * rd.x) / denom, (rp.y - apb * rd.y) / denom);
+      const double ae = alpha * e;
+      const double2 de = make_double2(rd.x + ae * ph.x, rd.y + ae * ph.y);
+      mx[0] = max(mx[0], sqmag_bits(ph.x, ph.y));
+      mx[1] = max(mx[1], sqmag_bits(rx.x, rx.y));
+      mx[2] = max(mx[2], sqmag_bits(de.x, de.y));
+      mx[3] = max(mx[3], sqmag_bits(ph.x - o0.x, ph.y - o0.y));
+      mx[4] = max(mx[4], sqmag_bits(rx.x - x.x, rx.y - x.y));
+      mx[5] = max(mx[5], sqmag_bits(de.x - d.x, de.y - d.y));
+      st2(U0, i, ph);
+      st2(WX, i, rx);
+      st2(WD, i, de);
+    }
+  }
+  // per-slice statistics: reduce over ty in shared memory (reusing the stage)
+  __syncthreads();
+  unsigned long long *red = reinterpret_cast<unsigned long long *>(hsm);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) red[(ty * 32 + lane) * 6 + q] = mx[q];
+  __syncthreads();
+  if (ty == 0 && act) {
+    for (int q = 0; q < 6; ++q) {
+      unsigned long long v = red[lane * 6 + q];
+      for (int r = 1; r < blockDim.y; ++r) v = max(v, red[(r * 32 + lane) * 6 + q]);
+      atomicMax(reinterpret_cast<unsigned long long *>(stats) + (size_t)b * 8 + q, v);
+    }
+  }
+}
+
+int helm_tiled(int M, int K, int B, const int *offsets, const int2 *tiles, int ntiles,
+               const double *const R[3], double alpha, const double *eps, const double *phibar,
+               double *U0, double *A1, double *A2, double *B1, double *B2, const double4 *cf,
+               const int *active, double *stats, const int *iters, int *counter,
+               cudaStream_t st) {
+  (void)K;
+  const int smem = 4 * HT_ROWS * 32 * (int)sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    SWE_CUDA(cudaFuncSetAttribute(k_helm_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dim3 grid(ntiles, (B + 31) / 32), blk(32, 8);
+  k_helm_tiled<<<grid, blk, smem, st>>>(M, B, offsets, tiles, R[0], R[1], R[2], alpha, eps, phibar,
+                                        U0, A1, A2, B1, B2, cf, active, stats, iters, counter);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
 // Crank-Nicolson half step prologue (steppers.py:143-152) in one pass:
 //   X   = x0 + s (x1 + x2)                  (x1, x2 nullable: the Heun combination)
 //   R   = X + alpha (L_G X + L_C X)         (L_C spectral, omitted when c.nb == null)

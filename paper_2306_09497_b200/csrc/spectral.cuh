@@ -49,6 +49,12 @@ int helm(int K, int B, const double *const R[3], const double *lcx, const double
          int *iters = nullptr, int *counter = nullptr, double tol = 0.0,
          unsigned *hdone = nullptr);
 int publish(int B, const int *counter, const int *iters, int *pub, cudaStream_t st);
+// tiled fused fixed-point iterate for batches >= 32 (see k_helm_tiled)
+int helm_tiled(int M, int K, int B, const int *offsets, const int2 *tiles, int ntiles,
+               const double *const R[3], double alpha, const double *eps, const double *phibar,
+               double *U0, double *A1, double *A2, double *B1, double *B2, const double4 *cf,
+               const int *active, double *stats, const int *iters, int *counter,
+               cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
              cudaStream_t st);

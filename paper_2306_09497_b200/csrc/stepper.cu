@@ -37,6 +37,7 @@ struct ProfRec {
 bool g_prof = false;
 bool g_capturing = false;  // a step graph is being captured: no events, no host syncs
 int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
+int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
 int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
 // Coriolis operator (eval_coriolis): 2 spectral three-term recurrence, fused into the
@@ -503,6 +504,23 @@ int cn_half(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double *con
 // K*B); for large batches the extra block check-in costs more than a launch
 bool fuse_decide(int K, int B) { return (size_t)K * B <= (size_t)1 << 20; }
 
+// one fixed-point iterate of cn_half_spec: xi/delta ping-pong per slice between
+// dst (A) and the LC buffers (B); batches >= 32 take the smem-tiled kernel
+int helm_iter(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double alpha,
+              double *const dst[3], cudaStream_t st, unsigned *hd) {
+  swe_plan *pl = r.pl;
+  Work &w = pl->ws;
+  const double *Rc[3] = {b.R[0], b.R[1], b.R[2]};
+  if (r.B >= 32 && !hd && g_helm_tiled)
+    return helm_tiled(pl->M, pl->K, r.B, pl->offsets, pl->helm_tiles, pl->n_helm_tiles, Rc, alpha,
+                      pl->eps, w.phibar, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], pl->cor_cf,
+                      w.flags, w.stats, w.iters, w.counter, st);
+  double *const U[3] = {dst[0], b.LC[0], b.LC[1]};
+  const CorOp c{dst[1], dst[2], pl->cor_nb, pl->cor_cf};
+  return helm(pl->K, r.B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, U, w.flags, w.stats, st,
+              &c, w.iters, w.counter, cfg.implicit_tol, hd);
+}
+
 // Crank-Nicolson half step with the spectral Coriolis operator (g_fast_coriolis == 2
 // or explicit Coriolis): X = x0 + s (x1 + x2); dst = (I - a L)^-1 (I + a L) X, then
 // the viscosity factor when dtnu != 0.  One fused prologue (k_cn_start), the
@@ -559,8 +577,7 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     double *const U[3] = {dst[0], b.LC[0], b.LC[1]};
     const CorOp c{dst[1], dst[2], pl->cor_nb, pl->cor_cf};
     unsigned *hd = fuse_decide(K, B) ? w.hdone : nullptr;
-    if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, U, w.flags, w.stats,
-                   r.st2, &c, w.iters, w.counter, cfg.implicit_tol, hd)) ||
+    if ((rc = helm_iter(r, cfg, b, alpha, dst, r.st2, hd)) ||
         (!hd && (rc = decide(B, w.stats, w.flags, w.iters, w.counter, cfg.implicit_tol, r.st2))) ||
         (rc = loop_cond(h, w.counter, w.loop, cfg.implicit_max_iter, r.st2)))
       return rc;
@@ -586,9 +603,7 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
           ProfScope ps(3, 9.0 * 16.0 * K * B, r.st);  // rhs 3 + old 3 in, new 3 out
           // small problems: the kernel's last block takes the per-slice decision
           unsigned *hd = fuse_decide(K, B) ? w.hdone : nullptr;
-          if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, U, w.flags,
-                         w.stats, r.st, &c, w.iters, w.counter, cfg.implicit_tol, hd)))
-            return rc;
+          if ((rc = helm_iter(r, cfg, b, alpha, dst, r.st, hd))) return rc;
           if (!hd && (rc = decide(B, w.stats, w.flags, w.iters, w.counter, cfg.implicit_tol, r.st)))
             return rc;
         }
@@ -1014,6 +1029,10 @@ long long swe_kernel_launches(void) { return g_launches; }
 int swe_set_option(const char *key, int value) {
   if (key && strcmp(key, "fft_path") == 0 && value >= 0 && value <= 2) {
     g_fft_path = value;
+    return OK;
+  }
+  if (key && strcmp(key, "helm_tiled") == 0 && (value == 0 || value == 1)) {
+    g_helm_tiled = value;
     return OK;
   }
   if (key && strcmp(key, "graphs") == 0 && (value == 0 || value == 1)) {
