@@ -28,7 +28,11 @@ namespace {
 // 8 consumer warps.  setmaxnreg moves registers from the producer warpgroup to the
 // consumers (compiled budget 65536/384 = 168 per thread -> 56 / 224).
 constexpr int V3_BN = 128, V3_NC = 8, V3_NT = 384, V3_CW0 = 4;
-constexpr int S3_KT = 16, S3_NS = 4, S3_LDA = 64 + 4, S3_LDB = V3_BN + 4;
+constexpr int S3_KT = 16, S3_NS = 4, S3_LDA = 72 + 4, S3_LDB = V3_BN + 4;
+// latitude-pair tiles are 64 wide; a remainder of <= 8 pairs (Jh = 193 at M=256)
+// joins the last tile as a fifth 8-row fragment of its upper-half warps instead
+// of costing a whole extra work unit (plan.cu synth_items_v3)
+constexpr int S3_TW = 64, S3_XTRA = 8;
 constexpr int A3_KP = 16, A3_NS = 4, A3_LDA = A3_KP + 4, A3_LDB = V3_BN + 4;
 constexpr int A3_BR = V3_ABR;  // analysis modes per parity per unit
 constexpr int A3_RW = A3_BR / 2, A3_FR = A3_RW / 8;  // rows / 8-row fragments per consumer warp
@@ -42,6 +46,7 @@ struct alignas(128) Synth3Stage {
 struct Synth3Smem {
   Synth3Stage st[S3_NS];
   unsigned long long full[S3_NS], empty[S3_NS];
+  int next;  // unit handed from producer warp 0 to warp 1
 };
 struct alignas(128) Anal3Stage {
   double A[2 * A3_BR][A3_LDA];
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
   const int nunits = args.nitems * ncol * args.nout;
   if (tid == 0) {
     for (int s = 0; s < S3_NS; ++s) {
-      mbar_init(&sm.full[s], 32);
+      mbar_init(&sm.full[s], 64);  // both producer warps' lanes
       mbar_init(&sm.empty[s], V3_NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -152,17 +157,21 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
   if (warp < V3_CW0) {
     // ------------------------------------------------------------ producer
     regs_dec();
-    if (warp != 0) return;
+    // two producer warps: warp 0 streams the table rows (A), warp 1 the spectral
+    // rows (B); each lane issues one bulk copy per stage and arrives with its bytes
+    if (warp >= 2) return;
     int it = 0;
     const int r = lane, par = r >> 4;
     while (true) {
-      int u = 0;
-      if (lane == 0) u = claim(args);
-      u = __shfl_sync(0xffffffffu, u, 0);
+      // warp 0 lane 0 claims the unit; named barrier 1 hands it to warp 1
+      asm volatile("bar.sync 1, 64;\n" ::: "memory");
+      if (warp == 0 && lane == 0) sm.next = claim(args);
+      asm volatile("bar.sync 1, 64;\n" ::: "memory");
+      const int u = sm.next;
       if (u >= nunits) {  // terminal stage: tells the consumers to stop
         const int s = it % S3_NS;
         mbar_wait(&sm.empty[s], ((it / S3_NS) & 1) ^ 1);
-        if (lane == 0) {
+        if (warp == 0 && lane == 0) {
           sm.st[s].unit = -1;
           sched_done(args);
         }
@@ -174,7 +183,8 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
       const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
       const int off = args.offsets[x.m];
       const int nch_t = (ne + S3_KT - 1) / S3_KT;
-      const unsigned abytes = (unsigned)min(64, Jp - x.tile) * 8u;
+      const bool wide = x.tile + S3_TW + S3_XTRA >= Jh;
+      const unsigned abytes = (unsigned)min(wide ? S3_TW + S3_XTRA : S3_TW, Jp - x.tile) * 8u;
       const int bcols = min(V3_BN, ld - x.c0);
       for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
         const int s = it % S3_NS;
@@ -182,20 +192,20 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
         const int term = c / nch_t, tt = (c - term * nch_t) * S3_KT + (r & 15);
         const LegTerm &T = o.t[term];
         Synth3Stage &S = sm.st[s];
-        if (lane == 0) S.unit = u;  // published by lane 0's arrive (release)
         const bool v = tt < (par ? no : ne);
         const int k = off + (par ? ne : 0) + tt;
-        S.S[r] = v ? T.sign * (T.scale ? T.scale[k] : 1.0) * (T.times_im ? (double)x.m : 1.0) : 0.0;
-        if (v) {
-          mbar_arrive_tx(&sm.full[s], abytes + (unsigned)bcols * 8u);
-          bulk_g2s(&S.A[r][0], T.tab + (size_t)k * Jp + x.tile, abytes, &sm.full[s]);
-          bulk_g2s(&S.B[r][0], T.src + (size_t)k * ld + x.c0, (unsigned)bcols * 8u, &sm.full[s]);
+        // rows past the m-block: scale 0 and A/B rows copied from a zero block (shared
+        // memory left by an earlier kernel may hold non-finite values, 0 * NaN = NaN)
+        if (warp == 0) {
+          if (lane == 0) S.unit = u;  // published by lane 0's arrive (release)
+          S.S[r] = v ? T.sign * (T.scale ? T.scale[k] : 1.0) * (T.times_im ? (double)x.m : 1.0) : 0.0;
+          mbar_arrive_tx(&sm.full[s], abytes);
+          bulk_g2s(&S.A[r][0], v ? T.tab + (size_t)k * Jp + x.tile : args.zeros, abytes,
+                   &sm.full[s]);
         } else {
-          // rows past the m-block: scale 0 and zeroed A and B rows (shared memory left
-          // by an earlier kernel may hold non-finite values, and 0 * NaN = NaN)
-          for (int q = 0; q < V3_BN; ++q) S.B[r][q] = 0.0;
-          for (int q = 0; q < 64; ++q) S.A[r][q] = 0.0;
-          mbar_arrive(&sm.full[s]);
+          mbar_arrive_tx(&sm.full[s], (unsigned)bcols * 8u);
+          bulk_g2s(&S.B[r][0], v ? T.src + (size_t)k * ld + x.c0 : args.zeros,
+                   (unsigned)bcols * 8u, &sm.full[s]);
         }
       }
     }
@@ -219,61 +229,94 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     const int km = M + 1 - x.m, ne = (km + 1) >> 1;
     const int nch_t = (ne + S3_KT - 1) / S3_KT;
     const int pw0 = x.tile + wph * 32;
-    const int nfr = max(0, min(4, (Jh - pw0 + 7) >> 3));
-    double acc[4][8][2];
+    const bool wide = x.tile + S3_TW + S3_XTRA >= Jh;  // carries the remainder pairs
+    const int tend = wide ? Jh : x.tile + S3_TW;
+    const int nfr = max(0, min(4, (tend - pw0 + 7) >> 3));
+    // remainder fragment (pairs tile+64 .. tile+71) of a wide tile, split over the
+    // four warps of this parity by 32-column quarter so the unit stays balanced
+    const int xq = wph * 2 + wch;  // this warp's column quarter of the remainder
+    const bool xtra = wide && x.tile + S3_TW < Jh;
+    double acc[4][8][2], acx[4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
-      const int s = it % S3_NS;
-      if (c > 0) mbar_wait(&sm.full[s], (it / S3_NS) & 1);
-      if (nfr > 0) {
-        const Synth3Stage &S = sm.st[s];
-        const LegTerm &T = o.t[c / nch_t];
-        const int rpar = wpar ^ T.flip;
-        const int tim = T.times_im;
-        const unsigned long long bmask = (tim && !(g & 1)) ? 0x8000000000000000ULL : 0ULL;
-        const double *Ab = &S.A[rpar * S3_KT + t][wph * 32 + g];
-        const double *Bb = &S.B[rpar * S3_KT + t][wch * 64 + (g ^ tim)];
-        const double *Sb = &S.S[rpar * S3_KT + t];
-        double a[2][4], b[2][8];
-        auto frag = [&](int kk, int q) {
-          const double sc = Sb[kk * 4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) a[q][i] = Ab[kk * 4 * S3_LDA + i * 8] * sc;
+    for (int j = 0; j < 4; ++j) acx[j][0] = acx[j][1] = 0.0;
+    // the remainder path is a separate instantiation, so ordinary units keep the
+    // lean register allocation of the plain 4 x 8 fragment loop
+    auto mainloop = [&](auto xt_tag) {
+      constexpr bool XT = decltype(xt_tag)::value;
+      for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+        const int s = it % S3_NS;
+        if (c > 0) mbar_wait(&sm.full[s], (it / S3_NS) & 1);
+        if (nfr > 0 || XT) {
+          const Synth3Stage &S = sm.st[s];
+          const LegTerm &T = o.t[c / nch_t];
+          const int rpar = wpar ^ T.flip;
+          const int tim = T.times_im;
+          const unsigned long long bmask = (tim && !(g & 1)) ? 0x8000000000000000ULL : 0ULL;
+          const double *Ab = &S.A[rpar * S3_KT + t][wph * 32 + g];
+          const double *Bb = &S.B[rpar * S3_KT + t][wch * 64 + (g ^ tim)];
+          const double *Sb = &S.S[rpar * S3_KT + t];
+          double a[2][4], b[2][8];
+          auto frag = [&](int kk, int q) {
+            const double sc = Sb[kk * 4];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * S3_LDB + j * 8], bmask);
-        };
-        frag(0, 0);
+            for (int i = 0; i < 4; ++i) a[q][i] = Ab[kk * 4 * S3_LDA + i * 8] * sc;
 #pragma unroll
-        for (int kk = 0; kk < S3_KT / 4; ++kk) {
-          const int q = kk & 1;
-          if (kk + 1 < S3_KT / 4) frag(kk + 1, q ^ 1);
+            for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * S3_LDB + j * 8], bmask);
+          };
+          frag(0, 0);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (i < nfr) {
+          for (int kk = 0; kk < S3_KT / 4; ++kk) {
+            const int q = kk & 1;
+            if (kk + 1 < S3_KT / 4) frag(kk + 1, q ^ 1);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+            for (int i = 0; i < 4; ++i)
+              if (i < nfr) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+              }
+            if constexpr (XT) {
+              const double *Ax = &S.A[rpar * S3_KT + t][S3_TW + g];
+              const double *Bx = &S.B[rpar * S3_KT + t][xq * 32 + (g ^ tim)];
+              const double ax = Ax[kk * 4 * S3_LDA] * Sb[kk * 4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                dmma(acx[j][0], acx[j][1], ax, flip_sign(Bx[kk * 4 * S3_LDB + j * 8], bmask));
             }
+          }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[s]);
-    }
+    };
+    if (xtra) mainloop(std::true_type{});
+    else mainloop(std::false_type{});
     if (o.layout == 0) {
       // E or O plane of [m][2][Jp][ld]
       double *dst = o.dst + ((size_t)x.m * 2 + wpar) * Jp * ld;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int p = pw0 + i * 8 + g;
-        if (p >= Jh) continue;
+        if (p >= tend) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
           if (col < ld)
             *reinterpret_cast<double2 *>(dst + (size_t)p * ld + col) =
                 make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);  // Im of m = 0 is dropped
+        }
+      }
+      const int px = x.tile + S3_TW + g;
+      if (xtra && px < Jh) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = x.c0 + xq * 32 + j * 8 + 2 * t;
+          if (col < ld)
+            *reinterpret_cast<double2 *>(dst + (size_t)px * ld + col) =
+                make_double2(acx[j][0], x.m ? acx[j][1] : 0.0);
         }
       }
     } else {
@@ -284,13 +327,23 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int p = pw0 + i * 8 + g;
-        if (p >= Jh) continue;
+        if (p >= tend) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
           if (col < ld)
             dst[(((size_t)p * (M + 1) + x.m) * nsl + (col >> 1)) * 2 + wpar] =
                 make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);
+        }
+      }
+      const int px = x.tile + S3_TW + g;
+      if (xtra && px < Jh) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = x.c0 + xq * 32 + j * 8 + 2 * t;
+          if (col < ld)
+            dst[(((size_t)px * (M + 1) + x.m) * nsl + (col >> 1)) * 2 + wpar] =
+                make_double2(acx[j][0], x.m ? acx[j][1] : 0.0);
         }
       }
     }

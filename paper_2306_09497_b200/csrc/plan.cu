@@ -249,6 +249,7 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
     for (int m = 0; m <= M; ++m)
       for (int c = 0; c < (M + 1 - m + 63) / 64; ++c) tiles.push_back(make_int2(m, c));
     pl->n_helm_tiles = (int)tiles.size();
+    if ((rc = upload(&pl->zeros, std::vector<double>(256, 0.0)))) return rc;
     if ((rc = upload(&pl->helm_tiles, tiles))) return rc;
   }
 
@@ -347,6 +348,12 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
       const int rt = (ne + AN_BR - 1) / AN_BR;
       for (int t = 0; t < rt; ++t) an.push_back(make_int2(m, t));
     }
+    std::vector<int2> sy3;
+    const int pt3 = std::max(1, Jh / 64 + (Jh % 64 > 8 ? 1 : 0));
+    for (int m = 0; m <= M; ++m)
+      for (int t = 0; t < pt3; ++t) sy3.push_back(make_int2(m, t));
+    pl->n_synth_items_v3 = (int)sy3.size();
+    if ((rc = upload(&pl->synth_items_v3, sy3))) return rc;
     std::vector<int2> an2;
     for (int m = 0; m <= M; ++m) {
       const int ne = (M + 2 - m) / 2;
@@ -420,12 +427,14 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->cor_scale);
   cudaFree(pl->cor_nb);
   cudaFree(pl->helm_tiles);
+  cudaFree(pl->zeros);
   cudaFree(pl->cor_cf);
   cudaFree(pl->tw);
   cudaFree(pl->twh);
   cudaFree(pl->fft_pos_z);
   cudaFree(pl->fft_pos_g);
   cudaFree(pl->synth_items);
+  cudaFree(pl->synth_items_v3);
   cudaFree(pl->anal_items);
   cudaFree(pl->anal_items_v2);
   cudaFree(pl->anal_items_v3);

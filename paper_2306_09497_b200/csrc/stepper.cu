@@ -99,6 +99,7 @@ LegArgs leg_args(const Run &r) {
   a.ld = (int)r.ld;
   a.offsets = r.pl->offsets;
   a.sched = r.pl->ws.sched;
+  a.zeros = r.pl->zeros;
   return a;
 }
 
@@ -174,7 +175,11 @@ int synth(const Run &r, LegArgs &a) {
   a.nitems = r.pl->n_synth_items;
   ProfScope ps(0, leg_flops(r, a), r.st);
   const int bn = leg_bn(r);
-  if (bn < 0) return leg_synth_v3_launch(a, r.st);
+  if (bn < 0) {
+    a.items = r.pl->synth_items_v3;
+    a.nitems = r.pl->n_synth_items_v3;
+    return leg_synth_v3_launch(a, r.st);
+  }
   if (bn) return leg_synth_v2_launch(a, bn, r.st);
   return leg_synth_launch(a, (int)((r.ld + SY_BN - 1) / SY_BN), r.st);
 }
