@@ -52,7 +52,7 @@ struct LegArgs {
   // v3 dynamic scheduling: device [ticket counter, CTAs done] (per plan / stream;
   // zero between launches)
   unsigned long long *sched;
-  const double *zeros;  // >= 256 zero doubles (v3: source of padding rows)
+  const double *zeros;  // >= 1024 zero doubles (v3: source of padding rows)
 };
 
 // Launch helpers (legendre.cu).  items/tiles are prepared by the plan.

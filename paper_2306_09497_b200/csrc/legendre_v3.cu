@@ -410,17 +410,20 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
           const size_t row = (size_t)off + (par ? ne : 0) + tt;
           cp_async16(&S.A[rr][cc], T.tab + (v ? row * Jp + q0 + cc : 0), v);
         }
+        // F+/F- rows (2 x 16 pairs, up to 1 KB each) as 32 bulk copies (TMA) instead
+        // of 2048 16-byte cp.async requests; pairs >= Jh come from the zero block
         const double *fb = T.src + (size_t)x.m * 2 * Jp * ld + x.c0;
-#pragma unroll 4
-        for (int piece = ptid; piece < 2 * A3_KP * (V3_BN / 2); piece += 128) {
-          const int rr = piece / (V3_BN / 2), cc = (piece % (V3_BN / 2)) * 2;
-          const int hs = rr / A3_KP, pr = rr % A3_KP, p = q0 + pr;
-          const bool v = (p < Jh) && (x.c0 + cc < ld);
-          cp_async16(&S.F[hs][pr][cc], fb + (v ? ((size_t)(hs ^ T.swap_pm) * Jp + p) * ld + cc : 0), v);
+        const unsigned fbytes = (unsigned)min(V3_BN, ld - x.c0) * 8u;
+        if (ptid == 0) mbar_expect_tx(&sm.full[s], 2u * A3_KP * fbytes);
+        if (ptid < 2 * A3_KP) {
+          const int hs = ptid / A3_KP, pr = ptid % A3_KP, p = q0 + pr;
+          bulk_g2s(&S.F[hs][pr][0],
+                   p < Jh ? fb + ((size_t)(hs ^ T.swap_pm) * Jp + p) * ld : args.zeros, fbytes,
+                   &sm.full[s]);
         }
         if (ptid == 0) {
           S.unit = u;
-          mbar_arrive(&sm.full[s]);  // release: publishes S.unit
+          mbar_arrive(&sm.full[s]);  // release: publishes S.unit (after the expect_tx)
         }
         cp_async_arrive(&sm.full[s]);
       }

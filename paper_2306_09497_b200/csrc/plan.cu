@@ -249,7 +249,7 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
     for (int m = 0; m <= M; ++m)
       for (int c = 0; c < (M + 1 - m + 63) / 64; ++c) tiles.push_back(make_int2(m, c));
     pl->n_helm_tiles = (int)tiles.size();
-    if ((rc = upload(&pl->zeros, std::vector<double>(256, 0.0)))) return rc;
+    if ((rc = upload(&pl->zeros, std::vector<double>(1024, 0.0)))) return rc;
     if ((rc = upload(&pl->helm_tiles, tiles))) return rc;
   }
 

@@ -58,7 +58,7 @@ struct swe_plan {
   double *cor_scale = nullptr;  // [Jp] 2 w f / ((1 - mu^2) a^2) per pair (FFT-free Coriolis)
   int2 *cor_nb = nullptr;       // [K] internal rows of modes n-1, n+1 (-1: none) (spectral Coriolis)
   double4 *cor_cf = nullptr;    // [K] (c_lo, c_hi, c_im, m == 0) of the spectral Coriolis operator
-  double *zeros = nullptr;      // 256 zero doubles (padding rows of the v3 GEMMs)
+  double *zeros = nullptr;      // 1024 zero doubles (padding rows of the v3 GEMMs)
   int2 *helm_tiles = nullptr;   // (m, chunk of 64 n) tiles of the tiled fixed-point kernel
   int n_helm_tiles = 0;
   double2 *tw = nullptr, *twh = nullptr;
