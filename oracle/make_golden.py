@@ -127,18 +127,19 @@ def gen_window_step(M, dt, nu, window=32):
 
 
 def gen_pint(name, fineM, coarseM, dt0, T, nlevels, cfactor, nrelax, iters, nu_f, nu_c,
-             cycle="F_then_V"):
+             cycle="F_then_V", coarse_scheme="imex", chunk_size=0):
     from pintswe import pint, scenarios
     from pintswe.dynamics import ViscositySpec
     from pintswe.pint import LevelSpec, PintConfig, SweProblem
     from pintswe.steppers import StepperConfig
     levels = [LevelSpec(0, fineM, StepperConfig(dt=dt0, viscosity=ViscositySpec(2, nu_f)))]
     for l in range(1, nlevels):
-        levels.append(LevelSpec(l, coarseM, StepperConfig(dt=dt0 * cfactor ** l,
+        levels.append(LevelSpec(l, coarseM, StepperConfig(scheme=coarse_scheme,
+                                                          dt=dt0 * cfactor ** l,
                                                           viscosity=ViscositySpec(2, nu_c))))
     N0 = int(round(T / dt0))
     pc = PintConfig(levels=tuple(levels), T=T, N0=N0, cfactor=cfactor, nrelax=nrelax,
-                    max_iters=iters, cycle=cycle)
+                    max_iters=iters, cycle=cycle, chunk_size=chunk_size)
     prob = SweProblem(pc)
     u0 = scenarios.gaussian_bumps(prob.grids[0])
     fine = pint.fine_serial_cpoints(prob, pc, u0)
@@ -146,8 +147,35 @@ def gen_pint(name, fineM, coarseM, dt0, T, nlevels, cfactor, nrelax, iters, nu_f
     snaps = np.stack([np.stack([_state_arrays(x) for x in snap]) for snap in tr.snapshots])
     return dict(name=name, fineM=fineM, coarseM=coarseM, dt0=dt0, T=T, nlevels=nlevels,
                 cfactor=cfactor, nrelax=nrelax, iters=iters, nu_f=nu_f, nu_c=nu_c,
-                cycle=cycle, u0=_state_arrays(u0), phibar=u0.phibar,
+                cycle=cycle, coarse_scheme=coarse_scheme, chunk_size=chunk_size,
+                u0=_state_arrays(u0), phibar=u0.phibar,
                 fine=np.stack([_state_arrays(x) for x in fine]), snapshots=snaps)
+
+
+def gen_settls(M, seed):
+    """SL-SI-SETTLS (steppers.py:171-212) and its semi-Lagrangian pieces
+    (semilag.py:25-179) on seeded inputs."""
+    from pintswe import semilag, steppers
+    from pintswe.dynamics import ViscositySpec
+    from pintswe.spharm import get_grid
+    from pintswe.steppers import StepperConfig, StepperState
+    grid = get_grid(M)
+    rng = np.random.default_rng(seed)
+    s0 = _random_state(grid, rng, 9.80616 * 29400.0, scales=(2e3, 2e-5, 2e-6))
+    cfg2 = StepperConfig(scheme="sl_si_settls", dt=1200.0, viscosity=ViscositySpec(2, 1e5))
+    cfg1 = StepperConfig(scheme="sl_si_settls", dt=1200.0, viscosity=ViscositySpec(2, 1e5),
+                         settls_mode="one_step")
+    s1 = steppers.settls_step(StepperState(s0), cfg2)          # cold start
+    s2 = steppers.settls_step(StepperState(s1, s0), cfg2)      # two-step history
+    s2o = steppers.settls_step(StepperState(s1, s0), cfg1)     # one-step ignores it
+    u = 20.0 * rng.standard_normal((grid.nlat, grid.nlon))
+    v = 10.0 * rng.standard_normal((grid.nlat, grid.nlon))
+    lam, th = semilag.departure_points(grid, u, v, 1.1 * u, 0.9 * v, 900.0)
+    vals = rng.standard_normal((grid.nlat, grid.nlon))
+    adv = semilag.advect_scalar(grid, vals, lam, th)
+    return dict(M=M, dt=1200.0, nu=1e5, phibar=s0.phibar, s0=_state_arrays(s0),
+                s1=_state_arrays(s1), s2=_state_arrays(s2), s2_one=_state_arrays(s2o),
+                u=u, v=v, dep_dt=900.0, lam=lam, th=th, vals=vals, adv=adv)
 
 
 def main():
@@ -169,6 +197,15 @@ def main():
     # 2-level MGRIT with nrelax=1 (cfg2's level structure at small M)
     np.savez_compressed(os.path.join(OUT, "pint_mgrit2_M32.npz"),
                         **gen_pint("mgrit2", 32, 16, 240.0, 7680.0, 2, 2, 1, 3, 1e5, 1e5))
+    # SL-SI-SETTLS: the stepper and a Parareal run with a SETTLS coarse level
+    # (bumps-pint-settls structure at small M), one with chunk boundaries
+    np.savez_compressed(os.path.join(OUT, "settls_M16.npz"), **gen_settls(16, 21))
+    np.savez_compressed(os.path.join(OUT, "pint_settls_M24.npz"),
+                        **gen_pint("settls", 24, 16, 300.0, 4800.0, 2, 2, 0, 3, 0.0, 1e6,
+                                   coarse_scheme="sl_si_settls"))
+    np.savez_compressed(os.path.join(OUT, "pint_settls_chunk_M24.npz"),
+                        **gen_pint("settls_chunk", 24, 16, 300.0, 4800.0, 2, 2, 1, 3, 0.0, 1e6,
+                                   coarse_scheme="sl_si_settls", chunk_size=2))
     fx = os.path.join(OUT, "fixtures")
     os.makedirs(fx, exist_ok=True)
     src = "/root/reference/pkg/frontend/fixtures"

@@ -1,8 +1,8 @@
 """Oracle FAS-MGRIT / Parareal driver and error diagnostics.
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Restates
-`/root/reference/pkg/src/pintswe/pint.py` (IMEX levels only; the SETTLS
-history policy is out of scope) and the parts of
+`/root/reference/pkg/src/pintswe/pint.py` (IMEX and SL-SI-SETTLS levels with
+the two-step history policy, pint.py:103-119) and the parts of
 `diagnostics.py` that the frozen fixtures exercise:
 
 * level sizes / validation ........ pint.py:55-95
@@ -28,6 +28,18 @@ import numpy as np
 from .sht import OracleSphere
 from .swe import OracleState, StepCfg, imex_step
 
+SETTLS, ONE_STEP, TWO_STEP = "sl_si_settls", "one_step", "two_step"
+
+
+def settls_boundary_policy(nlevels, level, nsteps, cfactor, chunk_size):   # pint.py:103-119
+    """Per-step SETTLS mode: one-step below the coarsest level; on the coarsest,
+    two-step except where the history would cross a chunk boundary."""
+    if level < nlevels - 1:
+        return [ONE_STEP] * nsteps
+    spacing = cfactor ** (nlevels - 2)
+    return [ONE_STEP if chunk_size > 0 and ((j - 1) * spacing) % chunk_size == 0 else TWO_STEP
+            for j in range(1, nsteps + 1)]
+
 
 class PintBlowUp(RuntimeError):
     def __init__(self, iteration, slice_index, trace):
@@ -50,6 +62,7 @@ class PintCfg:
     nrelax: int = 0
     max_iters: int = 10
     cycle: str = "F_then_V"
+    chunk_size: int = 0
 
     def points_on(self, level):                       # pint.py:89-90
         return self.N0 // self.cfactor ** level
@@ -68,9 +81,18 @@ class OracleProblem:
         self.cfgs = [lv.cfg for lv in pcfg.levels]
         self.step_calls = 0
 
-    def step(self, level, value):
+    def step(self, level, value, prev=None):
+        """steppers.advance (steppers.py:215-222): SETTLS uses prev unless one-step."""
         self.step_calls += 1
-        return imex_step(value, self.cfgs[level])
+        cfg = self.cfgs[level]
+        if cfg.scheme == SETTLS:
+            from .semilag import settls_step
+            return settls_step(value, None if cfg.settls_mode == ONE_STEP else prev, cfg)
+        return imex_step(value, cfg)
+
+    def tracks_history(self, level):                  # pint.py:192-194
+        cfg = self.cfgs[level]
+        return cfg.scheme == SETTLS and cfg.settls_mode == TWO_STEP
 
     def restrict(self, level, value):
         return value.to_truncation(self.spheres[level + 1])
@@ -126,16 +148,25 @@ class OracleMgrit:
             if g is not None:
                 prop = prop + g[m * i]
             res.append(prop - u[m * i])
+        modes = None                                  # pint.py:287-299
+        if self.p.tracks_history(level + 1):
+            modes = settls_boundary_policy(self.L, level + 1, n, m, self.c.chunk_size)
         gbar = [None]
         for i in range(1, n + 1):
-            tau = ubar[i] - self.p.step(level + 1, ubar[i - 1])
+            prev = ubar[i - 2] if modes and i >= 2 and modes[i - 1] == TWO_STEP else None
+            tau = ubar[i] - self.p.step(level + 1, ubar[i - 1], prev)
             gbar.append(self.p.restrict(level, res[i]) + tau)
         return ubar, gbar
 
     def coarsest(self, u, g):                         # pint.py:306-320
         lv = self.L - 1
+        modes = settls_boundary_policy(self.L, lv, len(u) - 1, self.m, self.c.chunk_size)
+        track = self.p.tracks_history(lv)
+        prev = None
         for j in range(1, len(u)):
-            v = self.p.step(lv, u[j - 1])
+            hist = prev if track and modes[j - 1] == TWO_STEP else None
+            v = self.p.step(lv, u[j - 1], hist)
+            prev = u[j - 1]
             u[j] = v if g is None else v + g[j]
 
     def cycle(self, level, u, g, kind):               # pint.py:322-337
@@ -156,8 +187,13 @@ class OracleMgrit:
     def initial_guess(self, u0):                      # pint.py:341-353
         n1 = self.c.points_on(1)
         v = [self.p.restrict(0, u0)]
+        track = self.p.tracks_history(1) and self.L == 2
+        modes = settls_boundary_policy(self.L, 1, n1, self.m, self.c.chunk_size)
+        prev = None
         for j in range(1, n1 + 1):
-            v.append(self.p.step(1, v[j - 1]))
+            hist = prev if track and modes[j - 1] == TWO_STEP else None
+            prev = v[j - 1]
+            v.append(self.p.step(1, v[j - 1], hist))
         return [self.p.prolong(1, x) for x in v]
 
     def run(self, u0: OracleState, iters=None) -> Trace:   # pint.py:355-394

@@ -111,6 +111,8 @@ class StepCfg:
     include_nonlinear: bool = True
     tol: float = 1e-12
     max_iter: int = 200
+    scheme: str = "imex"             # or "sl_si_settls" (oracle/semilag.py)
+    settls_mode: str = "two_step"
 
 
 # -- tendencies ----------------------------------------------------------------

@@ -131,19 +131,23 @@ def test_m256_step_window_matches_reference():
 def _run_pint(g):
     fine, coarse = int(g["fineM"]), int(g["coarseM"])
     dt0, nl, cf = float(g["dt0"]), int(g["nlevels"]), int(g["cfactor"])
+    scheme = str(g["coarse_scheme"]) if "coarse_scheme" in g else "imex"
     levels = [om.Level(fine, StepCfg(dt=dt0, visc_nu=float(g["nu_f"])))]
     for l in range(1, nl):
-        levels.append(om.Level(coarse, StepCfg(dt=dt0 * cf ** l, visc_nu=float(g["nu_c"]))))
+        levels.append(om.Level(coarse, StepCfg(dt=dt0 * cf ** l, visc_nu=float(g["nu_c"]),
+                                               scheme=scheme)))
     pc = om.PintCfg(levels=tuple(levels), T=float(g["T"]), N0=int(round(float(g["T"]) / dt0)),
                     cfactor=cf, nrelax=int(g["nrelax"]), max_iters=int(g["iters"]),
-                    cycle=str(g["cycle"]))
+                    cycle=str(g["cycle"]),
+                    chunk_size=int(g["chunk_size"]) if "chunk_size" in g else 0)
     prob = om.OracleProblem(pc, {fine: sphere(fine), coarse: sphere(coarse)})
     u0 = state_from(prob.spheres[0], g["u0"], g["phibar"])
     return prob, pc, u0
 
 
 @pytest.mark.parametrize("name", ["pint_fixture_M16.npz", "pint_mgrit3_M24.npz",
-                                  "pint_mgrit2_M32.npz"])
+                                  "pint_mgrit2_M32.npz", "pint_settls_M24.npz",
+                                  "pint_settls_chunk_M24.npz"])
 def test_pint_trace_matches_reference(name):
     g = load_golden(name)
     prob, pc, u0 = _run_pint(g)
@@ -189,3 +193,26 @@ def test_frozen_fixture_csvs_regenerate():
         i = int(n) - 1
         assert abs(wav[i] - float(wl)) <= 1e-15 * float(wl)
         assert abs(ener[i] - float(en)) <= 1e-10 * float(en) + 1e-30
+
+
+def test_settls_matches_reference():
+    """SL-SI-SETTLS step, departure points and bicubic interpolation vs the
+    reference (steppers.py:171-212, semilag.py:25-179)."""
+    from oracle import semilag as osl
+    g = load_golden("settls_M16.npz")
+    M = int(g["M"])
+    sph = sphere(M)
+    cfg = StepCfg(dt=float(g["dt"]), visc_nu=float(g["nu"]), scheme="sl_si_settls")
+    s0 = state_from(sph, g["s0"], g["phibar"])
+    s1 = osl.settls_step(s0, None, cfg)
+    s2 = osl.settls_step(s1, s0, cfg)
+    s2o = osl.settls_step(s1, None, cfg)
+    for st, key in ((s1, "s1"), (s2, "s2"), (s2o, "s2_one")):
+        got = np.stack([st.phi[0], st.xi[0], st.delta[0]])
+        assert rel_diff(got, g[key]) < 1e-11, key
+    lam, th = osl.departure_points(sph, g["u"], g["v"], 1.1 * g["u"], 0.9 * g["v"],
+                                   float(g["dep_dt"]))
+    assert np.abs(lam - g["lam"]).max() < 1e-12 and np.abs(th - g["th"]).max() < 1e-12
+    gi = osl.GridInterp(sph)
+    adv = gi.apply(g["vals"], gi.stencil(lam, th))
+    assert np.abs(adv - g["adv"]).max() < 1e-12 * np.abs(g["adv"]).max()
