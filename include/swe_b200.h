@@ -96,6 +96,24 @@ int swe_truncate_pad(const swe_plan *src, const swe_plan *dst, const double *in,
 int swe_state_stats(const swe_plan *plan, const double *state, int batch, double *max_abs_out,
                     int *finite_out, void *stream);
 
+/* One SL-SI-SETTLS step (steppers.py:171-212) of every slice: state [batch][3][K]
+ * advanced in place; prev [batch][3][K] is U_{n-1} (pass `state` itself for the
+ * one-step variant or a cold start); the implicit solve always includes the
+ * Coriolis term.  Returns SWE_ENOCONV (resid_out filled) like swe_imex_step and
+ * SWE_ENONFINITE when a departure point is not finite. */
+int swe_settls_step(swe_plan *plan, double *state, const double *prev, const double *phibar,
+                    int batch, const swe_stepper_cfg *cfg, double *resid_out, void *stream);
+/* Departure points (semilag.py:140-170) of every grid point for arrival winds
+ * (u_arr, v_arr) and extrapolated winds (u_ext, v_ext), grids [batch][nlat][nlon];
+ * outputs lam, th (same shape).  SWE_ENONFINITE if any is not finite. */
+int swe_departure_points(swe_plan *plan, const double *u_arr, const double *v_arr,
+                         const double *u_ext, const double *v_ext, int batch, double dt,
+                         int iterations, double *lam, double *th, void *stream);
+/* Bicubic interpolation of grids [batch][nlat][nlon] at (lam, th) of the same
+ * shape (semilag.py:82-88, advect_scalar :173-179). */
+int swe_interpolate(swe_plan *plan, const double *values, const double *lam, const double *th,
+                    int batch, double *out, void *stream);
+
 /* On-device diagnostics (diagnostics.py:46-118), deterministic reductions.
  * Kinetic-energy spectrum of states [batch][3][K]: energy[b][n-1], n = 1..M
  * (DEVICE output [batch][M]). */

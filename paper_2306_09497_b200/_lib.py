@@ -21,6 +21,7 @@ EXPORTS = (
     "swe_tendency", "swe_imex_step", "swe_truncate_pad", "swe_state_stats",
     "swe_kernel_launches", "swe_last_error", "swe_profile", "swe_profile_read",
     "swe_set_option", "swe_ke_spectrum", "swe_window_maxdiff", "swe_grid_sqdiff",
+    "swe_settls_step", "swe_departure_points", "swe_interpolate",
 )
 
 
@@ -34,6 +35,10 @@ class StepperCfgC(ctypes.Structure):
 
 
 class NoConvergence(RuntimeError):
+    pass
+
+
+class NonFinite(RuntimeError):
     pass
 
 
@@ -73,6 +78,9 @@ def load(path: str = LIB_PATH):
         "swe_ke_spectrum": (I, [P, P, I, P, P]),
         "swe_window_maxdiff": (I, [P, P, P, P, I, P, P]),
         "swe_grid_sqdiff": (I, [P, P, ctypes.c_longlong, P, P]),
+        "swe_settls_step": (I, [P, P, P, P, I, ctypes.POINTER(StepperCfgC), P, P]),
+        "swe_departure_points": (I, [P, P, P, P, P, I, D, I, P, P, P]),
+        "swe_interpolate": (I, [P, P, P, P, I, P, P]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)
@@ -96,6 +104,8 @@ def check(rc: int, what: str = ""):
         raise ValueError(msg or what)
     if rc == SWE_ENOCONV:
         raise NoConvergence(msg)
+    if rc == SWE_ENONFINITE:
+        raise NonFinite(msg)
     raise RuntimeError(f"{what}: {msg}")
 
 

@@ -250,6 +250,17 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
       for (int c = 0; c < (M + 1 - m + 63) / 64; ++c) tiles.push_back(make_int2(m, c));
     pl->n_helm_tiles = (int)tiles.size();
     if ((rc = upload(&pl->zeros, std::vector<double>(1024, 0.0)))) return rc;
+    // SETTLS: Gauss nodes and the ascending latitude list with pole ghosts
+    // (semilag.py:33-40: -pi - lat[1], -pi - lat[0], lats..., pi - lat[-1], pi - lat[-2])
+    std::vector<double> up(J), nodes(J + 4);
+    for (int j = 0; j < J; ++j) up[j] = asin(pl->mu[J - 1 - j]);
+    const double pi = 3.14159265358979323846;
+    nodes[0] = -pi - up[1];
+    nodes[1] = -pi - up[0];
+    for (int j = 0; j < J; ++j) nodes[2 + j] = up[j];
+    nodes[J + 2] = pi - up[J - 1];
+    nodes[J + 3] = pi - up[J - 2];
+    if ((rc = upload(&pl->mu_dev, pl->mu)) || (rc = upload(&pl->sl_nodes, nodes))) return rc;
     if ((rc = upload(&pl->helm_tiles, tiles))) return rc;
   }
 
@@ -398,6 +409,8 @@ void work_free(Work &w) {
   cudaFree(w.sched);
   cudaFree(w.loop);
   cudaFree(w.hdone);
+  cudaFreeHost(w.h_bad);
+  cudaFree(w.grids);
   cudaFreeHost(w.h_fail);
   cudaFree(w.phi0);
   cudaFree(w.phibar);
@@ -428,6 +441,8 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->cor_nb);
   cudaFree(pl->helm_tiles);
   cudaFree(pl->zeros);
+  cudaFree(pl->mu_dev);
+  cudaFree(pl->sl_nodes);
   cudaFree(pl->cor_cf);
   cudaFree(pl->tw);
   cudaFree(pl->twh);
@@ -462,6 +477,8 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaHostGetDevicePointer(&w.d_pub, w.h_pub, 0));
   SWE_CUDA(cudaMalloc(&w.loop, sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.hdone, sizeof(unsigned)));
+  SWE_CUDA(cudaHostAlloc(&w.h_bad, sizeof(int), cudaHostAllocMapped));
+  SWE_CUDA(cudaHostGetDevicePointer(&w.d_bad, w.h_bad, 0));
   SWE_CUDA(cudaMemset(w.hdone, 0, sizeof(unsigned)));
   SWE_CUDA(cudaHostAlloc(&w.h_fail, sizeof(int), cudaHostAllocMapped));
   SWE_CUDA(cudaHostGetDevicePointer(&w.d_fail, w.h_fail, 0));

@@ -34,6 +34,9 @@ struct Work {
   unsigned long long *sched = nullptr;  // Legendre v3 work-unit scheduler [2] (device)
   int *loop = nullptr;                  // graph mode: fixed-point iteration counter (device)
   unsigned *hdone = nullptr;            // k_helm last-block detection (device, zero between launches)
+  int *h_bad = nullptr, *d_bad = nullptr;  // SETTLS: non-finite departure point seen (mapped)
+  double *grids = nullptr;              // SETTLS grid workspace: 12 x [gcap][J][I]
+  int gcap = 0;
   int *h_fail = nullptr, *d_fail = nullptr;  // graph mode: unconverged-solve flag (mapped)
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
@@ -59,6 +62,8 @@ struct swe_plan {
   int2 *cor_nb = nullptr;       // [K] internal rows of modes n-1, n+1 (-1: none) (spectral Coriolis)
   double4 *cor_cf = nullptr;    // [K] (c_lo, c_hi, c_im, m == 0) of the spectral Coriolis operator
   double *zeros = nullptr;      // 1024 zero doubles (padding rows of the v3 GEMMs)
+  double *mu_dev = nullptr;     // [J] Gauss nodes (north -> south)
+  double *sl_nodes = nullptr;   // [J+4] ascending latitudes + 2 pole ghosts each side (SETTLS)
   int2 *helm_tiles = nullptr;   // (m, chunk of 64 n) tiles of the tiled fixed-point kernel
   int n_helm_tiles = 0;
   double2 *tw = nullptr, *twh = nullptr;

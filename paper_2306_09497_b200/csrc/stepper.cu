@@ -14,6 +14,7 @@
 #include "../../include/swe_b200.h"
 #include "plan.cuh"
 #include "spectral.cuh"
+#include "settls.cuh"
 
 namespace swe {
 
@@ -535,14 +536,21 @@ int helm_iter(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double al
 int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
                  const double *const x0[3], const double *const x1[3],
                  const double *const x2[3], double s, double *const dst[3], double alpha,
-                 double dtnu, int *iters_host, double *resid_host) {
+                 double dtnu, int *iters_host, double *resid_host, bool rhs_given = false) {
   swe_plan *pl = r.pl;
   const int K = pl->K, B = r.B;
   const bool impl = cfg.coriolis_implicit != 0 && pl->omega != 0.0;
   Work &w = pl->ws;
   int rc;
   const CorOp cor{nullptr, nullptr, impl ? pl->cor_nb : nullptr, impl ? pl->cor_cf : nullptr};
-  {
+  if (rhs_given) {
+    // implicit_linear_solve of a given right-hand side (steppers.py:74-118): b.R
+    // already holds it; the first iterate is its Helmholtz solve
+    const double *Rc[3] = {b.R[0], b.R[1], b.R[2]};
+    if ((rc = helm(K, B, Rc, nullptr, nullptr, alpha, pl->eps, w.phibar, dst, nullptr, nullptr,
+                   r.st)))
+      return rc;
+  } else {
     ProfScope ps(3, (x1 ? 12.0 : 6.0) * 16.0 * K * B, r.st);
     Ptr3C X0 = {{x0[0], x0[1], x0[2]}}, X1 = {{nullptr, nullptr, nullptr}}, X2 = X1;
     if (x1) {
@@ -708,6 +716,125 @@ int imex_internal(const Run &r, const swe_stepper_cfg &cfg, int *iters_host, dou
     if ((rc = visc(pl->K, r.B, u, pl->eps, dt * cfg.visc_nu, cfg.visc_order / 2.0, r.st))) return rc;
   }
   return OK;
+}
+
+// ---- SL-SI-SETTLS (steppers.py:171-212) -----------------------------------------
+// grids [B][J][I] of the semi-Lagrangian step: 12 per slice, in the plan
+int grid_reserve(swe_plan *pl, int B) {
+  Work &w = pl->ws;
+  if (B <= w.gcap) return OK;
+  cudaFree(w.grids);
+  w.grids = nullptr;
+  SWE_CUDA(cudaMalloc(&w.grids, (size_t)12 * B * pl->J * pl->I * sizeof(double)));
+  w.gcap = B;
+  return OK;
+}
+
+// (u, v) grids of internal-layout (xi, delta) (spharm.py:296-313)
+int winds_internal(const Run &r, const double *xi, const double *de, double *u, double *v) {
+  swe_plan *pl = r.pl;
+  const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
+  LegArgs a = leg_args(r);
+  a.nout = 2;
+  LegTerm hu = term(H, xi, -1.0, 0, il), hv = term(H, de, 1.0, 0, il);
+  set_out(a, 0, r.half(0), term(P, de, 1.0, 1, il), &hu, H);
+  set_out(a, 1, r.half(1), term(P, xi, 1.0, 1, il), &hv, H);
+  int rc;
+  if ((rc = synth(r, a))) return rc;
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.in[0] = r.half(0);
+  f.in[1] = r.half(1);
+  f.gout[0] = u;
+  f.gout[1] = v;
+  return fft(r, FOP_SYNTH2_GRID, f);
+}
+
+// grid of one internal-layout spectral field (spharm.py:249-257)
+int synth_grid_internal(const Run &r, const double *c, double *g) {
+  LegArgs a = leg_args(r);
+  a.nout = 1;
+  set_out(a, 0, r.half(0), term(r.pl->P, c), nullptr, r.pl->H);
+  int rc;
+  if ((rc = synth(r, a))) return rc;
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.in[0] = r.half(0);
+  f.gout[0] = g;
+  f.scale_mode = 0;
+  return fft(r, FOP_SYNTH_GRID, f);
+}
+
+// internal-layout spectral field of a grid, times sign (spharm.py:238-247)
+int analysis_internal(const Run &r, const double *g, double *c, double sign = 1.0) {
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.gin[0] = g;
+  f.out[0] = r.fsp(0);
+  int rc;
+  if ((rc = fft(r, FOP_ANALYSIS, f))) return rc;
+  LegArgs a = leg_args(r);
+  a.nout = 1;
+  set_out(a, 0, c, term(r.pl->P, r.fsp(0), sign), nullptr, r.pl->H);
+  return anal(r, a);
+}
+
+// phi component of nonlinear_rest: -analysis(Phi' delta) (dynamics.py:154-160);
+// g0, g1, g2 grid scratch
+int nonlinear_rest_internal(const Run &r, const double *phi, const double *de, double *g0,
+                            double *g1, double *g2, double *out) {
+  swe_plan *pl = r.pl;
+  int rc;
+  if ((rc = synth_grid_internal(r, phi, g0)) || (rc = synth_grid_internal(r, de, g1))) return rc;
+  if ((rc = phiprime_mul(r.B, (size_t)pl->J * pl->I, g0, g1, pl->ws.phibar, g2, r.st))) return rc;
+  return analysis_internal(r, g2, out, -1.0);
+}
+
+// one SETTLS step of every slice: U (spec 0-2) in/out, history P (spec 21-23)
+int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host) {
+  swe_plan *pl = r.pl;
+  const int K = pl->K, B = r.B;
+  const Bufs b = bufs(r);
+  Work &w = pl->ws;
+  const double dt = cfg.dt, half = 0.5 * dt;
+  int rc;
+  if ((rc = grid_reserve(pl, B))) return rc;
+  const size_t gsz = (size_t)B * pl->J * pl->I;
+  double *G[12];
+  for (int i = 0; i < 12; ++i) G[i] = w.grids + i * gsz;
+  double *const P[3] = {r.spec(21), r.spec(22), r.spec(23)};
+  // winds at t_n and t_{n-1}, departure points (semilag.py:140-170, two iterations)
+  if ((rc = winds_internal(r, b.U[1], b.U[2], G[0], G[1])) ||
+      (rc = winds_internal(r, P[1], P[2], G[2], G[3])))
+    return rc;
+  SetArgs sa{B, pl->J, pl->I, pl->mu_dev, pl->coslat, pl->sl_nodes, pl->a, G[0], G[1], G[2], G[3],
+             0};
+  if ((rc = departure_points(sa, 2, dt, G[4], G[5], w.d_bad, r.st))) return rc;
+  // L U = L_G U + L_C U (spectral Coriolis) -> K1; N_R(U) -> K2[0], N_R(prev) -> K2[1]
+  if ((rc = coriolis_spec(K, B, CorOp{b.U[1], b.U[2], pl->cor_nb, pl->cor_cf}, b.LC[0], b.LC[1],
+                          r.st)) ||
+      (rc = lin_tend(K, B, b.U[0], b.U[2], b.LC[0], b.LC[1], pl->eps, w.phibar, b.K1, r.st)) ||
+      (rc = nonlinear_rest_internal(r, b.U[0], b.U[2], G[6], G[7], G[8], b.K2[0])) ||
+      (rc = nonlinear_rest_internal(r, P[0], P[2], G[6], G[7], G[8], b.K2[1])))
+    return rc;
+  // G = U + dt/2 (L U + 2 N_R(U) - N_R(prev)) -> MID, taken at the departure points
+  if ((rc = settls_g(K, B, b.U, b.K1, b.K2[0], b.K2[1], half, b.MID, r.st))) return rc;
+  for (int f = 0; f < 3; ++f)
+    if ((rc = synth_grid_internal(r, b.MID[f], G[6 + f]))) return rc;
+  GridPtrs gp;
+  for (int f = 0; f < 4; ++f) {
+    gp.in[f] = f < 3 ? G[6 + f] : nullptr;
+    gp.out[f] = f < 3 ? G[9 + f] : nullptr;
+  }
+  if ((rc = interp_fields(sa, G[4], G[5], 3, gp, r.st))) return rc;
+  for (int f = 0; f < 3; ++f)
+    if ((rc = analysis_internal(r, G[9 + f], b.R[f]))) return rc;
+  // + dt/2 N_R(U) at arrival, then (I - dt/2 L) U_new = RHS and the viscosity factor
+  if ((rc = spec_axpy(K, B, b.R[0], b.K2[0], half, r.st))) return rc;
+  swe_stepper_cfg c2 = cfg;
+  c2.coriolis_implicit = 1;  // implicit_linear_solve(..., include_coriolis=True)
+  return cn_half_spec(r, c2, b, nullptr, nullptr, nullptr, 0.0, b.U, half, dt * cfg.visc_nu,
+                      nullptr, resid_host, true);
 }
 
 int options_key() { return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8); }
@@ -1010,6 +1137,71 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
     }
   SpecPtrsC s = {{b.U[0], b.U[1], b.U[2]}};
   return to_boundary(s, state, batch, 3, pl->K, pl->perm, r.st);
+}
+
+int swe_settls_step(swe_plan *pl, double *state, const double *prev, const double *phibar,
+                    int batch, const swe_stepper_cfg *cfg, double *resid_out, void *stream) {
+  int rc;
+  if ((rc = check_cfg(cfg))) return rc;
+  if (!phibar || !prev) {
+    set_error("phibar / prev is NULL");
+    return E_SHAPE;
+  }
+  if ((rc = prepare(pl, batch, phibar, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  const Bufs b = bufs(r);
+  SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}}, p = {{r.spec(21), r.spec(22), r.spec(23)}};
+  if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st)) ||
+      (rc = to_internal(prev, p, batch, 3, pl->K, pl->perm, r.st)))
+    return rc;
+  SWE_CUDA(cudaMemsetAsync(pl->ws.d_bad, 0, sizeof(int), r.st));
+  if ((rc = settls_internal(r, *cfg, resid_out))) return rc;
+  SWE_CUDA(cudaStreamSynchronize(r.st));
+  if (*reinterpret_cast<volatile int *>(pl->ws.h_bad)) {
+    set_error("departure-point iteration diverged");
+    return E_NONFINITE;
+  }
+  SpecPtrsC s = {{b.U[0], b.U[1], b.U[2]}};
+  return to_boundary(s, state, batch, 3, pl->K, pl->perm, r.st);
+}
+
+int swe_departure_points(swe_plan *pl, const double *u_arr, const double *v_arr,
+                         const double *u_ext, const double *v_ext, int batch, double dt,
+                         int iterations, double *lam, double *th, void *stream) {
+  int rc;
+  if (!u_arr || !v_arr || !u_ext || !v_ext || !lam || !th || iterations < 0) {
+    set_error("swe_departure_points: null argument or iterations < 0");
+    return E_SHAPE;
+  }
+  if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  SetArgs sa{batch, pl->J, pl->I, pl->mu_dev, pl->coslat, pl->sl_nodes, pl->a,
+             u_arr, v_arr, u_ext, v_ext, 1};
+  SWE_CUDA(cudaMemsetAsync(pl->ws.d_bad, 0, sizeof(int), st));
+  if ((rc = departure_points(sa, iterations, dt, lam, th, pl->ws.d_bad, st))) return rc;
+  SWE_CUDA(cudaStreamSynchronize(st));
+  if (*reinterpret_cast<volatile int *>(pl->ws.h_bad)) {
+    set_error("departure-point iteration diverged");
+    return E_NONFINITE;
+  }
+  return OK;
+}
+
+int swe_interpolate(swe_plan *pl, const double *values, const double *lam, const double *th,
+                    int batch, double *out, void *stream) {
+  int rc;
+  if (!values || !lam || !th || !out) {
+    set_error("swe_interpolate: null argument");
+    return E_SHAPE;
+  }
+  if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
+  SetArgs sa{batch, pl->J, pl->I, pl->mu_dev, pl->coslat, pl->sl_nodes, pl->a,
+             nullptr, nullptr, nullptr, nullptr, 1};
+  GridPtrs gp;
+  memset(&gp, 0, sizeof(gp));
+  gp.in[0] = values;
+  gp.out[0] = out;
+  return interp_fields(sa, lam, th, 1, gp, (cudaStream_t)stream);
 }
 
 int swe_truncate_pad(const swe_plan *src, const swe_plan *dst, const double *in, double *out,

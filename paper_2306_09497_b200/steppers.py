@@ -103,11 +103,44 @@ def imex_step(state: PrognosticState, cfg: StepperConfig) -> PrognosticState:
     return imex_steps_inplace(state.copy(), cfg, 1)
 
 
+def settls_step_inplace(state: PrognosticState, cfg: StepperConfig,
+                        prev: Optional[PrognosticState] = None) -> PrognosticState:
+    """One SL-SI-SETTLS step IN PLACE (steppers.py:171-212); prev = U_{n-1} of the
+    same batch, ignored in one-step mode (None = cold start)."""
+    from .semilag import DeparturePointError
+    if cfg.settls_mode == ONE_STEP or prev is None:
+        prev = state
+    if prev.batch != state.batch or prev.grid is not state.grid:
+        raise ValueError("SETTLS history must match the state's batch and grid")
+    grid = state.grid
+    c = cfg.to_c()
+    resid = np.zeros(state.batch)
+    rc = grid._lib.swe_settls_step(grid.plan, _ptr(state.data), _ptr(prev.data),
+                                   _ptr(state.phibar_t), state.batch, ctypes.byref(c),
+                                   resid.ctypes.data_as(ctypes.c_void_p), _stream())
+    try:
+        _lib.check(rc, "swe_settls_step")
+    except _lib.NoConvergence as exc:
+        raise ImplicitSolveError(str(exc)) from None
+    except _lib.NonFinite as exc:
+        raise DeparturePointError(str(exc)) from None
+    return state
+
+
+def settls_step(sstate: StepperState, cfg: StepperConfig) -> PrognosticState:
+    """One SL-SI-SETTLS step; the input state is untouched (steppers.py:171-212)."""
+    return settls_step_inplace(sstate.current.copy(), cfg, sstate.previous)
+
+
 def advance(sstate: StepperState, cfg: StepperConfig) -> StepperState:
-    """One step of the configured scheme (steppers.py:215-222)."""
+    """One step of the configured scheme, maintaining the SETTLS history
+    (steppers.py:215-222)."""
     if cfg.scheme == IMEX:
         return StepperState(imex_step(sstate.current, cfg), None)
-    raise NotImplementedError("SL-SI-SETTLS is a coarse-level scheme outside the GPU path")
+    new = settls_step(sstate, cfg)
+    if cfg.settls_mode == TWO_STEP:
+        return StepperState(new, sstate.current)
+    return StepperState(new, None)
 
 
 def propagate(sstate: StepperState, t0: float, t1: float, cfg: StepperConfig) -> StepperState:
@@ -119,11 +152,13 @@ def propagate(sstate: StepperState, t0: float, t1: float, cfg: StepperConfig) ->
     nsteps = int(round(steps_f))
     if abs(steps_f - nsteps) > 1e-9:
         raise ValueError(f"slice [{t0}, {t1}] is not an integral number of dt")
-    if cfg.scheme != IMEX:
-        raise NotImplementedError("SL-SI-SETTLS is a coarse-level scheme outside the GPU path")
-    if nsteps == 0:
-        return StepperState(sstate.current.copy(), None)
-    return StepperState(imex_steps_inplace(sstate.current.copy(), cfg, nsteps), None)
+    if cfg.scheme == IMEX:
+        if nsteps == 0:
+            return StepperState(sstate.current.copy(), None)
+        return StepperState(imex_steps_inplace(sstate.current.copy(), cfg, nsteps), None)
+    for _ in range(nsteps):
+        sstate = advance(sstate, cfg)
+    return sstate
 
 
 class HostPipeline:
