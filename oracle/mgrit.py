@@ -113,6 +113,13 @@ class OracleMgrit:
     def __init__(self, problem: OracleProblem, pcfg: PintCfg):
         self.p, self.c, self.m, self.L = problem, pcfg, pcfg.cfactor, len(pcfg.levels)
 
+    def tracks(self, level):
+        f = getattr(self.p, "tracks_history", None)
+        return bool(f(level)) if f is not None else False
+
+    def step(self, level, value, prev=None):
+        return self.p.step(level, value) if prev is None else self.p.step(level, value, prev)
+
     def f_sweep(self, level, u, g):                   # pint.py:223-241
         m = self.m
         for i in range(1, len(u) // m + 1):
@@ -149,23 +156,23 @@ class OracleMgrit:
                 prop = prop + g[m * i]
             res.append(prop - u[m * i])
         modes = None                                  # pint.py:287-299
-        if self.p.tracks_history(level + 1):
+        if self.tracks(level + 1):
             modes = settls_boundary_policy(self.L, level + 1, n, m, self.c.chunk_size)
         gbar = [None]
         for i in range(1, n + 1):
             prev = ubar[i - 2] if modes and i >= 2 and modes[i - 1] == TWO_STEP else None
-            tau = ubar[i] - self.p.step(level + 1, ubar[i - 1], prev)
+            tau = ubar[i] - self.step(level + 1, ubar[i - 1], prev)
             gbar.append(self.p.restrict(level, res[i]) + tau)
         return ubar, gbar
 
     def coarsest(self, u, g):                         # pint.py:306-320
         lv = self.L - 1
         modes = settls_boundary_policy(self.L, lv, len(u) - 1, self.m, self.c.chunk_size)
-        track = self.p.tracks_history(lv)
+        track = self.tracks(lv)
         prev = None
         for j in range(1, len(u)):
             hist = prev if track and modes[j - 1] == TWO_STEP else None
-            v = self.p.step(lv, u[j - 1], hist)
+            v = self.step(lv, u[j - 1], hist)
             prev = u[j - 1]
             u[j] = v if g is None else v + g[j]
 
@@ -187,13 +194,13 @@ class OracleMgrit:
     def initial_guess(self, u0):                      # pint.py:341-353
         n1 = self.c.points_on(1)
         v = [self.p.restrict(0, u0)]
-        track = self.p.tracks_history(1) and self.L == 2
+        track = self.tracks(1) and self.L == 2
         modes = settls_boundary_policy(self.L, 1, n1, self.m, self.c.chunk_size)
         prev = None
         for j in range(1, n1 + 1):
             hist = prev if track and modes[j - 1] == TWO_STEP else None
             prev = v[j - 1]
-            v.append(self.p.step(1, v[j - 1], hist))
+            v.append(self.step(1, v[j - 1], hist))
         return [self.p.prolong(1, x) for x in v]
 
     def run(self, u0: OracleState, iters=None) -> Trace:   # pint.py:355-394

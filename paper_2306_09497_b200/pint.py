@@ -31,6 +31,19 @@ import numpy as np
 import torch
 
 F_THEN_V = "F_then_V"
+SL_SI_SETTLS, ONE_STEP, TWO_STEP = "sl_si_settls", "one_step", "two_step"
+
+
+def settls_boundary_policy(nlevels: int, level_index: int, nsteps: int, cfactor: int,
+                           chunk_size: int):
+    """Per-step SETTLS mode of one level (pint.py:103-119): one-step below the
+    coarsest level; on the coarsest, two-step except where the step's history
+    would sit in another chunk of `chunk_size` fine C-point slices."""
+    if level_index < nlevels - 1:
+        return [ONE_STEP] * nsteps
+    spacing = cfactor ** (nlevels - 2)
+    return [ONE_STEP if chunk_size > 0 and ((j - 1) * spacing) % chunk_size == 0 else TWO_STEP
+            for j in range(1, nsteps + 1)]
 V_CYCLE = "V"
 
 
@@ -229,10 +242,17 @@ class MgritEngine:
         S = n // self.G
         return self.g * S + 1, (self.g + 1) * S
 
-    def _step(self, level, x):
+    def _tracks(self, level) -> bool:
+        """Problem keeps SETTLS two-step history on `level` (optional protocol)."""
+        f = getattr(self.problem, "tracks_history", None)
+        return bool(f(level)) if f is not None else False
+
+    def _step(self, level, x, prev=None):
         if level == 0:
             self.fine_steps += x.shape[0]
-        return self.problem.step_batch(level, x)
+        if prev is None:
+            return self.problem.step_batch(level, x)
+        return self.problem.step_batch(level, x, prev)
 
     def _exchange_halo(self, level, u):
         if self.G == 1:
@@ -289,7 +309,20 @@ class MgritEngine:
         cps = torch.arange(m * (lo - 1), m * hi + 1, m, device=u.device)   # halo + owned
         ub_local = pr.restrict_batch(level, u[cps])
         r = self._residual(level, u, g, lo, hi)
-        tau = ub_local[1:] - self._step(level + 1, ub_local[:-1])
+        prev = None
+        if self._tracks(level + 1):
+            # the coarse operator sees the coarse sweep's history pattern
+            # (pint.py:287-299): slice i >= 2 in two-step mode uses ubar[i-2]
+            modes = settls_boundary_policy(self.L, level + 1, n, m, self.cfg.chunk_size)
+            prev = ub_local[:-1].clone()
+            for i in range(lo, hi + 1):
+                if i >= 2 and modes[i - 1] == TWO_STEP:
+                    if i - 2 < lo - 1:
+                        raise NotImplementedError(
+                            "SETTLS history across rank blocks: set chunk_size to a "
+                            "multiple of the slices per rank")
+                    prev[i - lo] = ub_local[i - 2 - (lo - 1)]
+        tau = ub_local[1:] - self._step(level + 1, ub_local[:-1], prev)
         gb_local = pr.restrict_batch(level, r) + tau
         ubar = pr.zeros(level + 1, n + 1)
         gbar = pr.zeros(level + 1, n + 1)
@@ -309,10 +342,15 @@ class MgritEngine:
         if self.G > 1:
             lo, hi = self._own_points(lv, n)
             g = torch.cat([g[:1], self.comm.all_gather(g[lo:hi + 1])])
+        modes = settls_boundary_policy(self.L, lv, n, self.m, self.cfg.chunk_size)
+        track = self._tracks(lv)
+        prev = None
         for j in range(1, n + 1):
-            new = self._step(lv, u[j - 1:j])
+            hist = prev if track and modes[j - 1] == TWO_STEP else None
+            new = self._step(lv, u[j - 1:j], hist)
             if g is not None:
                 new = new + g[j:j + 1]
+            prev = u[j - 1:j].clone()
             u[j:j + 1] = new
 
     def _own_points(self, level, npts):
@@ -344,8 +382,11 @@ class MgritEngine:
         pr = self.problem
         v = pr.zeros(1, n1 + 1)
         v[0:1] = pr.restrict_batch(0, u0)
+        track = self._tracks(1) and self.L == 2
+        modes = settls_boundary_policy(self.L, 1, n1, self.m, self.cfg.chunk_size)
         for j in range(1, n1 + 1):
-            v[j:j + 1] = self._step(1, v[j - 1:j])
+            hist = v[j - 2:j - 1] if track and j >= 2 and modes[j - 1] == TWO_STEP else None
+            v[j:j + 1] = self._step(1, v[j - 1:j], hist)
         return pr.prolong_batch(1, v)
 
     def _cpoints(self, u):
@@ -454,9 +495,6 @@ class SweProblem:
         self.geometry = geometry or SphereGeometry()
         self.grids = [get_grid(spec.M, self.geometry) for spec in config.levels]
         self.level_cfgs = [spec.stepper for spec in config.levels]
-        for c in self.level_cfgs:
-            if c.scheme != IMEX:
-                raise NotImplementedError("GPU SweProblem supports IMEX levels only")
         self.phibar = phibar
         self.step_calls = 0
 
@@ -482,11 +520,17 @@ class SweProblem:
         g = self.grids[level]
         return torch.zeros((n, 3, g.n_modes), dtype=torch.complex128, device=f"cuda:{g.device}")
 
-    def step_batch(self, level, x):
-        from .steppers import imex_steps_inplace
+    def step_batch(self, level, x, prev=None):
+        """One step of every point of x; prev (SETTLS two-step history, same shape)
+        or None.  For SETTLS a point's own value as its prev means no history."""
+        from .steppers import IMEX, imex_steps_inplace, settls_step_inplace
         st = self.wrap(level, x.clone())
         self.step_calls += x.shape[0]
-        imex_steps_inplace(st, self.level_cfgs[level], 1)
+        cfg = self.level_cfgs[level]
+        if cfg.scheme == IMEX:
+            imex_steps_inplace(st, cfg, 1)
+        else:
+            settls_step_inplace(st, cfg, None if prev is None else self.wrap(level, prev))
         return st.data
 
     def restrict_batch(self, level, x):
@@ -524,4 +568,7 @@ class SweProblem:
         return value.is_finite()
 
     def tracks_history(self, level) -> bool:
-        return False
+        """pint.py:192-194."""
+        from .steppers import SL_SI_SETTLS, TWO_STEP as TS
+        cfg = self.level_cfgs[level]
+        return cfg.scheme == SL_SI_SETTLS and cfg.settls_mode == TS

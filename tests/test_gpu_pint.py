@@ -18,14 +18,17 @@ def _setup(g):
     from paper_2306_09497_b200 import dynamics, pint, spharm, steppers
     fine, coarse = int(g["fineM"]), int(g["coarseM"])
     dt0, nl, cf = float(g["dt0"]), int(g["nlevels"]), int(g["cfactor"])
+    scheme = str(g["coarse_scheme"]) if "coarse_scheme" in g else "imex"
     levels = [pint.LevelSpec(0, fine, steppers.StepperConfig(
         dt=dt0, viscosity=dynamics.ViscositySpec(2, float(g["nu_f"]))))]
     for lv in range(1, nl):
         levels.append(pint.LevelSpec(lv, coarse, steppers.StepperConfig(
-            dt=dt0 * cf ** lv, viscosity=dynamics.ViscositySpec(2, float(g["nu_c"])))))
+            scheme=scheme, dt=dt0 * cf ** lv,
+            viscosity=dynamics.ViscositySpec(2, float(g["nu_c"])))))
     pc = pint.PintConfig(levels=tuple(levels), T=float(g["T"]),
                          N0=int(round(float(g["T"]) / dt0)), cfactor=cf,
-                         nrelax=int(g["nrelax"]), max_iters=int(g["iters"]), cycle=str(g["cycle"]))
+                         nrelax=int(g["nrelax"]), max_iters=int(g["iters"]), cycle=str(g["cycle"]),
+                         chunk_size=int(g["chunk_size"]) if "chunk_size" in g else 0)
     prob = pint.SweProblem(pc)
     u0 = g["u0"]
     st = dynamics.PrognosticState.from_fields(prob.grids[0], u0[0], u0[1], u0[2],
@@ -34,7 +37,8 @@ def _setup(g):
 
 
 @pytest.mark.parametrize("name", ["pint_fixture_M16.npz", "pint_mgrit3_M24.npz",
-                                  "pint_mgrit2_M32.npz"])
+                                  "pint_mgrit2_M32.npz", "pint_settls_M24.npz",
+                                  "pint_settls_chunk_M24.npz"])
 def test_gpu_engine_matches_reference_trace(name):
     g = load_golden(name)
     pint, prob, pc, u0 = _setup(g)
