@@ -64,6 +64,7 @@ def build_stepper(section: dict, dt=None) -> steppers.StepperConfig:
             dt=float(dt if dt is not None else section["dt"]),
             viscosity=ViscositySpec(order_q=int(v.get("order", 2)),
                                     coeff_nu=float(v.get("coeff", 0.0))),
+            settls_mode=section.get("settls_mode", "two_step"),
             coriolis_treatment=section.get("coriolis_treatment", "implicit"))
     except (KeyError, ValueError) as exc:
         raise ConfigError(f"bad stepper section: {exc}") from exc
