@@ -136,8 +136,9 @@ SWE_DEV void put_z(const LCtx &c, int row, int k, int k2, double2 Xk, double2 Xc
 }
 
 // fields a.in[0..nf-1]: E/O half spectra [m][2][Jp][ld] of pair p -> Z of their north
-// and south rows.  One flattened loop over (field, k pair, slice) keeps many loads in
-// flight; field `subf` has phisub subtracted from E at m = 0 (phi_prime,
+// and south rows.  One flattened loop over (k pair, slice, field), field fastest: the
+// lanes of a warp store to the same slot of different rows (one 256-byte line, no
+// bank conflicts) and keep many loads in flight; field `subf` has phisub subtracted from E at m = 0 (phi_prime,
 // dynamics.py:52-56).  With a.dlam, field 2 is i m times field 5 (d_lambda Phi).
 SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1, S = c.S;
@@ -151,7 +152,7 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
-      const int f = idx / per, r = idx - f * per, k = r / S, s = r - k * S;
+      const int r = idx / nf, f = idx - r * nf, k = r / S, s = r - k * S;
       const bool ok = idx < total && s < c.nsl;
       const int k2 = k == 0 ? N2 : N2 - k;
       const double2 z = make_double2(0.0, 0.0);
@@ -184,7 +185,7 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
-      const int f = idx / per, r = idx - f * per, k = r / S, s = r - k * S;
+      const int r = idx / nf, f = idx - r * nf, k = r / S, s = r - k * S;
       if (idx >= total || s >= c.nsl) continue;
       if (f == subf && k == 0) e[u].x -= a.phisub[c.b0 + s];
       const int k2 = N2 - k;
@@ -249,7 +250,7 @@ SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, int nf, double w01, d
   const int M = a.M, S = c.S, N2 = a.N2, per = (M + 1) * S;
   const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
   for (int idx = c.tid; idx < nf * per; idx += c.nthr) {
-    const int f = idx / per, r = idx - f * per, k = r / S, s = r - k * S;
+    const int r = idx / nf, f = idx - r * nf, k = r / S, s = r - k * S;
     if (s >= c.nsl) continue;
     const int z1 = __ldg(a.pos_z + k), z2 = __ldg(a.pos_z + (k == 0 ? 0 : N2 - k));
     double2 w = __ldg(a.twh + k);
