@@ -474,6 +474,246 @@ __global__ void __launch_bounds__(256) k_cn_start(int K, int B, Ptr3C x0, Ptr3C 
   }
 }
 
+// Whole Crank-Nicolson half step for small truncations (coarse levels): one CTA
+// per slice runs prologue (as k_cn_start), the complete Coriolis fixed point (as
+// k_helm + k_decide, the slice's own convergence loop) and the epilogue (as
+// k_cn_finish) in one launch, with the iterate (Phi and two xi/delta buffers) in
+// shared memory and block-level reductions for the statistics.  Same arithmetic
+// as the multi-kernel path, so results are identical; it removes ~12 launches
+// per half step where launch latency dominates.  rhs_given: R = X (the SETTLS
+// implicit solve).  Not converged after max_iter: the residual of
+// steppers.py:113-118 goes to resid[b], *counter counts such slices.
+constexpr int CS_NT = 1024;
+SWE_DEV unsigned long long blk_max_u64(unsigned long long v, unsigned long long *red) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? red[l] : 0ULL;
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (l == 0) red[32] = v;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__global__ void __launch_bounds__(CS_NT) k_cn_small(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2,
+                                                  double s, double alpha, const double *eps,
+                                                  const double *phibar, const int2 *nbt,
+                                                  const double4 *cft, int rhs_given, Ptr3 R,
+                                                  Ptr3 dst, int max_iter, double tol, double dtnu,
+                                                  double halfq, int *iters, int *flags,
+                                                  int *counter, double *resid, int *fail) {
+  extern __shared__ double2 csm[];  // [Phi][xi A][xi B][de A][de B], K each
+  double2 *P = csm, *XA = csm + K, *XB = csm + 2 * K, *DA = csm + 3 * K, *DB = csm + 4 * K;
+  __shared__ unsigned long long red[33];
+  __shared__ int sdone;
+  const int b = blockIdx.x;
+  const bool cor = nbt != nullptr;
+  const double pb = phibar[b], apb = alpha * pb, aap = alpha * alpha * pb;
+  auto at = [&](int k) { return (size_t)k * B + b; };
+  // ---- prologue: stage X's xi/delta, then rhs R and the first iterate
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    XB[k] = comb(x0, x1, x2, s, 1, at(k));
+    DB[k] = comb(x0, x1, x2, s, 2, at(k));
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const double2 ph = comb(x0, x1, x2, s, 0, at(k)), xi = XB[k], de = DB[k];
+    const double e = eps[k];
+    double2 r0, r1, r2;
+    if (rhs_given) {
+      r0 = ph;
+      r1 = xi;
+      r2 = de;
+    } else {
+      double2 lx = make_double2(0.0, 0.0), lc = lx;
+      if (cor) {
+        const int2 nb = nbt[k];
+        const double4 cf = cft[k];
+        double2 xl = lx, dl = lx, xh = lx, dh = lx;
+        if (nb.x >= 0) {
+          xl = XB[nb.x];
+          dl = DB[nb.x];
+        }
+        if (nb.y >= 0) {
+          xh = XB[nb.y];
+          dh = DB[nb.y];
+        }
+        lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * xi.y),
+                          -(cf.x * dl.y + cf.y * dh.y - cf.z * xi.x));
+        lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * de.y,
+                          cf.x * xl.y + cf.y * xh.y + cf.z * de.x);
+        if (cf.w != 0.0) {
+          lx.y = 0.0;
+          lc.y = 0.0;
+        }
+      }
+      const double2 lphi = make_double2(-pb * de.x, -pb * de.y);
+      const double2 lde = add2(sc2(e, ph), lc);
+      r0 = add2(ph, sc2(alpha, lphi));
+      r1 = add2(xi, sc2(alpha, lx));
+      r2 = add2(de, sc2(alpha, lde));
+    }
+    st2(R.p[0], at(k), r0);
+    st2(R.p[1], at(k), r1);
+    st2(R.p[2], at(k), r2);
+    const double denom = 1.0 + aap * e;
+    const double2 nph = make_double2((r0.x - apb * r2.x) / denom, (r0.y - apb * r2.y) / denom);
+    const double ae = alpha * e;
+    P[k] = nph;
+    XA[k] = r1;
+    DA[k] = make_double2(r2.x + ae * nph.x, r2.y + ae * nph.y);
+  }
+  __syncthreads();
+  // ---- fixed point (steppers.py:96-112), the slice's own loop
+  int it = 0, done = !cor;
+  double2 *cx = XA, *cd = DA, *nx = XB, *nd = DB;
+  for (; !done && it < max_iter; ++it) {
+    unsigned long long mx[6] = {0, 0, 0, 0, 0, 0};
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      const int2 nb = nbt[k];
+      const double4 cf = cft[k];
+      const double2 rp = ld2(R.p[0], at(k)), r1 = ld2(R.p[1], at(k)), r2 = ld2(R.p[2], at(k));
+      const double e = eps[k];
+      const double2 x = cx[k], d = cd[k];
+      double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
+      if (nb.x >= 0) {
+        xl = cx[nb.x];
+        dl = cd[nb.x];
+      }
+      if (nb.y >= 0) {
+        xh = cx[nb.y];
+        dh = cd[nb.y];
+      }
+      double2 lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * x.y),
+                                -(cf.x * dl.y + cf.y * dh.y - cf.z * x.x));
+      double2 lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * d.y,
+                                cf.x * xl.y + cf.y * xh.y + cf.z * d.x);
+      if (cf.w != 0.0) {
+        lx.y = 0.0;
+        lc.y = 0.0;
+      }
+      const double2 rx = add2(r1, sc2(alpha, lx)), rd = add2(r2, sc2(alpha, lc));
+      const double denom = 1.0 + aap * e;
+      const double2 ph = make_double2((rp.x - apb * rd.x) / denom, (rp.y - apb * rd.y) / denom);
+      const double ae = alpha * e;
+      const double2 de = make_double2(rd.x + ae * ph.x, rd.y + ae * ph.y);
+      const double2 o0 = P[k];
+      mx[0] = max(mx[0], sqmag_bits(ph.x, ph.y));
+      mx[1] = max(mx[1], sqmag_bits(rx.x, rx.y));
+      mx[2] = max(mx[2], sqmag_bits(de.x, de.y));
+      mx[3] = max(mx[3], sqmag_bits(ph.x - o0.x, ph.y - o0.y));
+      mx[4] = max(mx[4], sqmag_bits(rx.x - x.x, rx.y - x.y));
+      mx[5] = max(mx[5], sqmag_bits(de.x - d.x, de.y - d.y));
+      P[k] = ph;
+      nx[k] = rx;
+      nd[k] = de;
+    }
+    double st[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) st[q] = __longlong_as_double((long long)blk_max_u64(mx[q], red));
+    if (threadIdx.x == 0) {
+      double v[6];
+      for (int q = 0; q < 6; ++q) v[q] = sqrt(st[q]);  // as decide_slice
+      double overall = fmax(fmax(v[0], v[1]), v[2]);
+      if (isnan(v[0]) || isnan(v[1]) || isnan(v[2])) overall = nan("");
+      overall = (overall > 1e-300 || isnan(overall)) ? overall : 1e-300;
+      bool ok = true;
+      for (int f = 0; f < 3; ++f) {
+        const double tiny = 1e-13 * overall;
+        const double scale = (v[f] >= tiny || isnan(v[f])) ? v[f] : tiny;
+        if (v[3 + f] > tol * scale) ok = false;
+      }
+      sdone = ok;
+    }
+    __syncthreads();
+    done = sdone;
+    double2 *t = cx;
+    cx = nx;
+    nx = t;
+    t = cd;
+    cd = nd;
+    nd = t;
+  }
+  if (threadIdx.x == 0) {
+    iters[b] = it;
+    flags[b] = !done;
+    resid[b] = 0.0;
+  }
+  if (!done) {
+    // residual |u - alpha (L_G + L_C) u - rhs| (steppers.py:113-118)
+    double rmax = 0.0;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      const int2 nb = nbt[k];
+      const double4 cf = cft[k];
+      const double2 x = cx[k], d = cd[k], ph = P[k];
+      double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
+      if (nb.x >= 0) {
+        xl = cx[nb.x];
+        dl = cd[nb.x];
+      }
+      if (nb.y >= 0) {
+        xh = cx[nb.y];
+        dh = cd[nb.y];
+      }
+      double2 lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * x.y),
+                                -(cf.x * dl.y + cf.y * dh.y - cf.z * x.x));
+      double2 lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * d.y,
+                                cf.x * xl.y + cf.y * xh.y + cf.z * d.x);
+      if (cf.w != 0.0) {
+        lx.y = 0.0;
+        lc.y = 0.0;
+      }
+      const double2 lph = make_double2(-pb * d.x, -pb * d.y);
+      const double2 lde = add2(sc2(eps[k], ph), lc);
+      const double2 v[3] = {ph, x, d}, l[3] = {lph, lx, lde};
+      for (int f = 0; f < 3; ++f) {
+        const double2 rr = ld2(R.p[f], at(k));
+        rmax = fmax(rmax, hypot(v[f].x - alpha * l[f].x - rr.x, v[f].y - alpha * l[f].y - rr.y));
+      }
+    }
+    const double r = __longlong_as_double(
+        (long long)blk_max_u64((unsigned long long)__double_as_longlong(rmax), red));
+    if (threadIdx.x == 0) {
+      resid[b] = r;
+      atomicAdd(counter, 1);
+      if (fail) *fail = 1;
+    }
+  }
+  // ---- epilogue: viscosity factor (dynamics.py:191-200) and the result
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double bh = 1.0;
+    if (dtnu != 0.0 && done) bh = 1.0 / (1.0 + dtnu * pow(eps[k], halfq));
+    const double2 ph = P[k], x = cx[k], d = cd[k];
+    st2(dst.p[0], at(k), dtnu != 0.0 && done ? sc2(bh, ph) : ph);
+    st2(dst.p[1], at(k), dtnu != 0.0 && done ? sc2(bh, x) : x);
+    st2(dst.p[2], at(k), dtnu != 0.0 && done ? sc2(bh, d) : d);
+  }
+}
+
+int cn_small_ok(int K) { return K <= 2800; }
+
+int cn_small(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+             const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
+             int rhs_given, Ptr3 R, Ptr3 dst, int max_iter, double tol, double dtnu,
+             double halfq, int *iters, int *flags, int *counter, double *resid, int *fail,
+             cudaStream_t st) {
+  const int smem = 5 * K * (int)sizeof(double2);
+  static int attr = 0;
+  if (smem > attr) {
+    SWE_CUDA(cudaFuncSetAttribute(k_cn_small, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
+  }
+  k_cn_small<<<B, CS_NT, smem, st>>>(K, B, x0, x1, x2, s, alpha, eps, phibar, nb, cf, rhs_given,
+                                     R, dst, max_iter, tol, dtnu, halfq, iters, flags, counter,
+                                     resid, fail);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
 // Fixed-point epilogue: slices whose iterate ended in the B buffers (odd iteration
 // count) copy xi/delta back to A = u[1], u[2]; with dtnu != 0 the viscosity
 // factor (dynamics.py:191-200) is applied to every slice on the way.

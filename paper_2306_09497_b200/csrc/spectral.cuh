@@ -55,6 +55,13 @@ int helm_tiled(int M, int K, int B, const int *offsets, const int2 *tiles, int n
                double *U0, double *A1, double *A2, double *B1, double *B2, const double4 *cf,
                const int *active, double *stats, const int *iters, int *counter,
                cudaStream_t st);
+// whole CN half step for K <= 2800 modes (coarse levels), one CTA per slice
+int cn_small_ok(int K);
+int cn_small(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+             const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
+             int rhs_given, Ptr3 R, Ptr3 dst, int max_iter, double tol, double dtnu,
+             double halfq, int *iters, int *flags, int *counter, double *resid, int *fail,
+             cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
              cudaStream_t st);

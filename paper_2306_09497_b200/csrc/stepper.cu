@@ -39,6 +39,7 @@ bool g_prof = false;
 bool g_capturing = false;  // a step graph is being captured: no events, no host syncs
 int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
+int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
 int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
 // Coriolis operator (eval_coriolis): 2 spectral three-term recurrence, fused into the
@@ -543,6 +544,52 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
   Work &w = pl->ws;
   int rc;
   const CorOp cor{nullptr, nullptr, impl ? pl->cor_nb : nullptr, impl ? pl->cor_cf : nullptr};
+  if (g_cn_small && cn_small_ok(K)) {
+    // coarse levels: the whole half step in one launch, one CTA per slice
+    Ptr3C X0 = {{nullptr, nullptr, nullptr}}, X1 = X0, X2 = X0;
+    if (rhs_given) {
+      X0 = {{b.R[0], b.R[1], b.R[2]}};
+    } else {
+      X0 = {{x0[0], x0[1], x0[2]}};
+      if (x1) {
+        X1 = {{x1[0], x1[1], x1[2]}};
+        X2 = {{x2[0], x2[1], x2[2]}};
+      }
+    }
+    Ptr3 R = {{b.R[0], b.R[1], b.R[2]}}, D = {{dst[0], dst[1], dst[2]}};
+    SWE_CUDA(cudaMemsetAsync(w.counter, 0, sizeof(int), r.st));
+    {
+      ProfScope ps(3, (x1 ? 12.0 : 6.0) * 16.0 * K * B, r.st);
+      if ((rc = cn_small(K, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, cor.nb, cor.cf,
+                         rhs_given ? 1 : 0, R, D, cfg.implicit_max_iter, cfg.implicit_tol, dtnu,
+                         cfg.visc_order / 2.0, w.iters, w.flags, w.counter, w.stats,
+                         r.graph ? w.d_fail : nullptr, r.st)))
+        return rc;
+    }
+    if (r.graph) return OK;
+    if ((rc = publish(B, w.counter, w.iters, w.d_pub, r.st))) return rc;
+    SWE_CUDA(cudaStreamSynchronize(r.st));
+    const int active = reinterpret_cast<volatile int *>(w.h_pub)[0];
+    if (iters_host)
+      for (int i = 0; i < B; ++i) iters_host[2 * i] = reinterpret_cast<volatile int *>(w.h_pub)[1 + i];
+    if (active > 0) {
+      std::vector<double> res(B);
+      SWE_CUDA(cudaMemcpyAsync(res.data(), w.stats, sizeof(double) * B, cudaMemcpyDeviceToHost,
+                               r.st));
+      std::vector<int> fl(B);
+      SWE_CUDA(cudaMemcpyAsync(fl.data(), w.flags, sizeof(int) * B, cudaMemcpyDeviceToHost, r.st));
+      SWE_CUDA(cudaStreamSynchronize(r.st));
+      double worst = 0.0;
+      for (int i = 0; i < B; ++i) {
+        if (!fl[i]) res[i] = 0.0;
+        worst = std::max(worst, res[i]);
+        if (resid_host) resid_host[i] = res[i];
+      }
+      set_error("Coriolis iteration did not converge; residual %.3e", worst);
+      return E_NOCONV;
+    }
+    return OK;
+  }
   if (rhs_given) {
     // implicit_linear_solve of a given right-hand side (steppers.py:74-118): b.R
     // already holds it; the first iterate is its Helmholtz solve
@@ -837,7 +884,10 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
                       nullptr, resid_host, true);
 }
 
-int options_key() { return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8); }
+int options_key() {
+  return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
+         (g_helm_tiled << 13);
+}
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
 // capture stream on the second call with a given key (the first runs eagerly:
@@ -1226,6 +1276,10 @@ long long swe_kernel_launches(void) { return g_launches; }
 int swe_set_option(const char *key, int value) {
   if (key && strcmp(key, "fft_path") == 0 && value >= 0 && value <= 2) {
     g_fft_path = value;
+    return OK;
+  }
+  if (key && strcmp(key, "cn_small") == 0 && (value == 0 || value == 1)) {
+    g_cn_small = value;
     return OK;
   }
   if (key && strcmp(key, "helm_tiled") == 0 && (value == 0 || value == 1)) {
