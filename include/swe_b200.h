@@ -96,6 +96,11 @@ int swe_truncate_pad(const swe_plan *src, const swe_plan *dst, const double *in,
 int swe_state_stats(const swe_plan *plan, const double *state, int batch, double *max_abs_out,
                     int *finite_out, void *stream);
 
+/* Serial IMEX sweep (the coarsest-level solve, pint.py:306-320): u [n+1][3][K]
+ * device states, u[j] = step(u[j-1]) + g[j] for j = 1..n with g [n+1][3][K]
+ * (nullable; g[0] unused); one CUDA-graph step per point and one host check. */
+int swe_imex_sweep(swe_plan *plan, double *u, const double *g, int n, const double *phibar,
+                   const swe_stepper_cfg *cfg, double *resid_out, void *stream);
 /* One SL-SI-SETTLS step (steppers.py:171-212) of every slice: state [batch][3][K]
  * advanced in place; prev [batch][3][K] is U_{n-1} (pass `state` itself for the
  * one-step variant or a cold start); the implicit solve always includes the

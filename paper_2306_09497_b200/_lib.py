@@ -21,7 +21,7 @@ EXPORTS = (
     "swe_tendency", "swe_imex_step", "swe_truncate_pad", "swe_state_stats",
     "swe_kernel_launches", "swe_last_error", "swe_profile", "swe_profile_read",
     "swe_set_option", "swe_ke_spectrum", "swe_window_maxdiff", "swe_grid_sqdiff",
-    "swe_settls_step", "swe_departure_points", "swe_interpolate",
+    "swe_settls_step", "swe_departure_points", "swe_interpolate", "swe_imex_sweep",
 )
 
 
@@ -81,6 +81,7 @@ def load(path: str = LIB_PATH):
         "swe_settls_step": (I, [P, P, P, P, I, ctypes.POINTER(StepperCfgC), P, P]),
         "swe_departure_points": (I, [P, P, P, P, P, I, D, I, P, P, P]),
         "swe_interpolate": (I, [P, P, P, P, I, P, P]),
+        "swe_imex_sweep": (I, [P, P, P, I, P, ctypes.POINTER(StepperCfgC), P, P]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

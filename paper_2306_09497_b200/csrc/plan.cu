@@ -411,6 +411,7 @@ void work_free(Work &w) {
   cudaFree(w.hdone);
   cudaFreeHost(w.h_bad);
   cudaFree(w.grids);
+  cudaFree(w.sweep_g);
   cudaFreeHost(w.h_fail);
   cudaFree(w.phi0);
   cudaFree(w.phibar);

@@ -36,6 +36,8 @@ struct Work {
   unsigned *hdone = nullptr;            // k_helm last-block detection (device, zero between launches)
   int *h_bad = nullptr, *d_bad = nullptr;  // SETTLS: non-finite departure point seen (mapped)
   double *grids = nullptr;              // SETTLS grid workspace: 12 x [gcap][J][I]
+  double *sweep_g = nullptr;            // serial-sweep forcing, internal layout 3 x [K][2 scap]
+  int scap = 0;
   int gcap = 0;
   int *h_fail = nullptr, *d_fail = nullptr;  // graph mode: unconverged-solve flag (mapped)
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift

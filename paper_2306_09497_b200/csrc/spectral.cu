@@ -950,6 +950,23 @@ int loop_cond(cudaGraphConditionalHandle h, const int *counter, int *loop, int m
   return OK;
 }
 
+// y[k] += g[k][col] for one batch-1 spectral field set (3 fields, [K][2]) from a
+// batch-n set ([K][2n]) (serial coarse sweep forcing)
+__global__ void k_add_col(int K, int n, int col, Ptr3 y, Ptr3C g) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const double2 a = ld2(y.p[f], k), b = ld2(g.p[f], (size_t)k * n + col);
+      st2(y.p[f], k, add2(a, b));
+    }
+}
+
+int add_col(int K, int n, int col, Ptr3 y, Ptr3C g, cudaStream_t st) {
+  k_add_col<<<(K + 255) / 256, 256, 0, st>>>(K, n, col, y, g);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
 // copy the active count and the iteration counts to mapped host memory
 __global__ void k_publish(int B, const int *counter, const int *iters, volatile int *pub) {
   for (int i = threadIdx.x; i <= B; i += blockDim.x) pub[i] = i == 0 ? *counter : iters[i - 1];

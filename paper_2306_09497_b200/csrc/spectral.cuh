@@ -62,6 +62,7 @@ int cn_small(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              int rhs_given, Ptr3 R, Ptr3 dst, int max_iter, double tol, double dtnu,
              double halfq, int *iters, int *flags, int *counter, double *resid, int *fail,
              cudaStream_t st);
+int add_col(int K, int n, int col, Ptr3 y, Ptr3C g, cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
              cudaStream_t st);

@@ -1189,6 +1189,60 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
   return to_boundary(s, state, batch, 3, pl->K, pl->perm, r.st);
 }
 
+int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double *phibar,
+                   const swe_stepper_cfg *cfg, double *resid_out, void *stream) {
+  int rc;
+  if ((rc = check_cfg(cfg))) return rc;
+  if (!u || !phibar || n < 0) {
+    set_error("swe_imex_sweep: null argument or n < 0");
+    return E_SHAPE;
+  }
+  if (n == 0) return OK;
+  if ((rc = prepare(pl, 1, phibar, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, 1, stream);
+  const Bufs b = bufs(r);
+  const int K = pl->K;
+  Work &w = pl->ws;
+  Ptr3C G = {{nullptr, nullptr, nullptr}};
+  if (g) {
+    if (n > w.scap) {
+      cudaFree(w.sweep_g);
+      w.sweep_g = nullptr;
+      SWE_CUDA(cudaMalloc(&w.sweep_g, (size_t)3 * K * 2 * n * sizeof(double)));
+      w.scap = n;
+    }
+    SpecPtrs gi = {{w.sweep_g, w.sweep_g + (size_t)K * 2 * n, w.sweep_g + (size_t)2 * K * 2 * n}};
+    if ((rc = to_internal(g + (size_t)3 * K * 2, gi, n, 3, K, pl->perm, r.st))) return rc;
+    G = {{gi.p[0], gi.p[1], gi.p[2]}};
+  }
+  const size_t stride = (size_t)3 * K * 2;  // doubles per state
+  SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
+  SpecPtrsC sc = {{b.U[0], b.U[1], b.U[2]}};
+  Ptr3 U = {{b.U[0], b.U[1], b.U[2]}};
+  cudaGraphExec_t exec = nullptr;
+  if (g_graphs && !g_prof && (rc = step_graph(r, *cfg, &exec))) return rc;
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool graph = pass == 0 && exec;
+    if ((rc = to_internal(u, d, 1, 3, K, pl->perm, r.st))) return rc;
+    if (graph) SWE_CUDA(cudaMemsetAsync(w.d_fail, 0, sizeof(int), r.st));
+    for (int j = 1; j <= n; ++j) {
+      if (graph) {
+        SWE_CUDA(cudaGraphLaunch(exec, r.st));
+      } else if ((rc = imex_internal(r, *cfg, nullptr, resid_out))) {
+        return rc;
+      }
+      if (g && (rc = add_col(K, n, j - 1, U, G, r.st))) return rc;
+      if ((rc = to_boundary(sc, u + (size_t)j * stride, 1, 3, K, pl->perm, r.st))) return rc;
+    }
+    if (!graph) return OK;
+    SWE_CUDA(cudaStreamSynchronize(r.st));
+    if (!*reinterpret_cast<volatile int *>(w.h_fail)) return OK;
+    // an unconverged solve inside the graph: redo the sweep on the host-driven path,
+    // which raises at the failing step with the residual like steppers.py
+  }
+  return OK;
+}
+
 int swe_settls_step(swe_plan *pl, double *state, const double *prev, const double *phibar,
                     int batch, const swe_stepper_cfg *cfg, double *resid_out, void *stream) {
   int rc;

@@ -30,6 +30,9 @@ from typing import Optional, Sequence
 import numpy as np
 import torch
 
+from ._lib import NoConvergence as _NoConv
+from ._lib import check as _lib_check
+
 F_THEN_V = "F_then_V"
 SL_SI_SETTLS, ONE_STEP, TWO_STEP = "sl_si_settls", "one_step", "two_step"
 
@@ -344,6 +347,9 @@ class MgritEngine:
             g = torch.cat([g[:1], self.comm.all_gather(g[lo:hi + 1])])
         modes = settls_boundary_policy(self.L, lv, n, self.m, self.cfg.chunk_size)
         track = self._tracks(lv)
+        sweep = getattr(self.problem, "sweep_batch", None)
+        if sweep is not None and sweep(lv, u, g):   # whole chain on the device
+            return
         prev = None
         for j in range(1, n + 1):
             hist = prev if track and modes[j - 1] == TWO_STEP else None
@@ -532,6 +538,30 @@ class SweProblem:
         else:
             settls_step_inplace(st, cfg, None if prev is None else self.wrap(level, prev))
         return st.data
+
+    def sweep_batch(self, level, u, g) -> bool:
+        """u[j] = step(u[j-1]) + g[j], j = 1..n, in place on the device
+        (swe_imex_sweep); False when the level is not a plain IMEX level."""
+        import ctypes
+        from .spharm import _ptr, _stream
+        from .steppers import IMEX, ImplicitSolveError
+        cfg = self.level_cfgs[level]
+        if cfg.scheme != IMEX or u.shape[0] < 2:
+            return False
+        grid = self.grids[level]
+        n = u.shape[0] - 1
+        self.step_calls += n
+        pb = self._pb(1, u.device)
+        c = cfg.to_c()
+        resid = np.zeros(1)
+        rc = grid._lib.swe_imex_sweep(grid.plan, _ptr(u), None if g is None else _ptr(g), n,
+                                      _ptr(pb), ctypes.byref(c),
+                                      resid.ctypes.data_as(ctypes.c_void_p), _stream())
+        try:
+            _lib_check(rc, "swe_imex_sweep")
+        except _NoConv as exc:
+            raise ImplicitSolveError(str(exc)) from None
+        return True
 
     def restrict_batch(self, level, x):
         from .spharm import truncate_pad

@@ -86,3 +86,36 @@ def test_gpu_blowup_raises():
     with pytest.raises(pint.PintBlowUpError) as ei:
         pint.mgrit_run(prob, pc, bad)
     assert ei.value.trace.blowup is not None
+
+
+def test_device_sweep_matches_stepwise():
+    """swe_imex_sweep (the coarsest solve on the device) equals stepping point by
+    point and adding the forcing, bitwise; an unconverged solve still raises."""
+    import torch
+    from paper_2306_09497_b200 import dynamics, pint, scenarios, steppers
+    g = load_golden("pint_mgrit2_M32.npz")
+    _, prob, pc, u0 = _setup(g)
+    lv = 1
+    grid = prob.grids[lv]
+    n = 6
+    u = prob.zeros(lv, n + 1)
+    u[0:1] = prob.restrict_batch(0, prob.as_batch(0, u0))
+    rng = np.random.default_rng(1)
+    taper = (grid.n_of + 1.0) ** -2
+    f = torch.zeros_like(u)
+    f[:, 0] = torch.from_numpy(rng.standard_normal((n + 1, grid.n_modes)) * taper).to(u.device)
+    f[:, 1] = torch.from_numpy(rng.standard_normal((n + 1, grid.n_modes)) * 1e-9 * taper).to(u.device)
+    ref = u.clone()
+    for j in range(1, n + 1):
+        ref[j:j + 1] = prob.step_batch(lv, ref[j - 1:j]) + f[j:j + 1]
+    assert prob.sweep_batch(lv, u, f)
+    assert bool(torch.isfinite(ref).all()) and torch.equal(u, ref)
+    bad = pint.SweProblem(pint.PintConfig(
+        levels=(pc.levels[0], pint.LevelSpec(1, grid.M, steppers.StepperConfig(
+            dt=pc.levels[1].stepper.dt, implicit_max_iter=1))),
+        T=pc.T, N0=pc.N0, cfactor=pc.cfactor))
+    bad.phibar = prob.phibar
+    for _ in range(2):   # second call replays the captured graph
+        w = u.clone()
+        with pytest.raises(steppers.ImplicitSolveError, match="residual"):
+            bad.sweep_batch(1, w, None)
