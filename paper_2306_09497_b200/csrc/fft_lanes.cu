@@ -1,18 +1,27 @@
-// Longitude FFT stage, "lane = row" variant for small-radix lengths.
+// Longitude FFT stage, "lane = row" variant.
 //
 // One CTA owns one latitude PAIR p (north row p, south row J-1-p) and S
-// slices; its 16 transform rows are (field, hemisphere, slice), row index
-// (f*2 + h)*S + s.  Shared memory holds X[slot][16]: the 16 rows of one slot
-// form one 256-byte line, half-warp lane r works on row r, every butterfly
-// access is a conflict-free full line and a half-warp shares its twiddles.
+// slices; its LW (16 or 8) transform rows are (field, hemisphere, slice), row
+// index (f*2 + h)*S + s.  Shared memory holds X[slot][LW]: the rows of one slot
+// form one line, lane r of a row group works on row r, every butterfly access
+// is a conflict-free full line and the row group shares its twiddles.
+// Radices 2..13 run unrolled per thread; any other prime (29 and 53 for
+// M = 1024, N2 = 1537) runs as a CTA-wide "generic" stage whose thread items
+// are (butterfly, GT output pairs, row).
 // Inputs are the parity-split Legendre outputs E/O ([m][2][Jp][ld]):
 // north = E + O, south = E - O.  Outputs are the folded analysis inputs
 // F+- = w (f_north +- f_south) ([m][2][Jp][ld]); on the equator (J odd) the
 // south row coincides with the north row and F+ = F- = w f_north.
 // Transform algebra (real packing, Cooley-Tukey / prime-factor, slot maps) is
 // shared with fft.cu.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "fft.cuh"
 #include "fft_core.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace swe {
 
@@ -20,18 +29,23 @@ using namespace fftcore;
 
 namespace {
 
-constexpr int LW = 16;  // rows per CTA: a half-warp covers them, so each warp runs two
-                        // butterflies per instruction and two CTAs fit on an SM
+// LW rows per CTA.  16: a half-warp covers them, each warp runs two butterflies per
+// instruction and two CTAs fit on an SM (N2 <= 907).  8: longer rows (N2 <= 1815,
+// e.g. M = 1024), one 512-thread CTA per SM; the 14-row nonlinear pass is then split
+// by hemisphere over a two-CTA cluster that combines F+- through distributed shared
+// memory.
+constexpr int GT = 4;  // generic radix: output pairs (t, R - t) per thread item
 
 // Shared-memory position of (slot, row): the 16 rows of a slot stay one 256-byte
 // line, permuted by the slot (XOR swizzle), so that accesses to one row across
 // consecutive slots (put_z, the grid products, extraction) spread over the banks
 // while a butterfly's 16 (or 8) rows of one slot remain a conflict-free line.
+template <int LW>
 SWE_DEV int xs(int slot, int row) { return slot * LW + (row ^ ((slot << 1) & (LW - 1))); }
 
 // MODE 0 DIT, 1 DIF, 2 prime-factor (no twiddles); see fft.cu.  RW rows take part
 // (RW lanes per butterfly, 32/RW butterflies per warp instruction).
-template <int R, int MODE, int RW>
+template <int R, int MODE, int RW, int LW>
 SWE_DEV void lane_stage(double2 *X, int N2, int Lp, double dir, const double2 *tw, int warp,
                         int nw, int lane) {
   constexpr int H = (R - 1) / 2, BW = 32 / RW;
@@ -52,94 +66,194 @@ SWE_DEV void lane_stage(double2 *X, int N2, int Lp, double dir, const double2 *t
     double2 v[R], y[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      v[q] = X[xs(base + q * Lp, row)];
+      v[q] = X[xs<LW>(base + q * Lp, row)];
       if (MODE == 0 && q && k) v[q] = cm(v[q], twd(tw, q * k * tws, dir));
     }
     dft<R>(v, dir, cr, sr, y);
 #pragma unroll
     for (int t = 0; t < R; ++t)
-      X[xs(base + t * Lp, row)] = (MODE == 1 && t && k) ? cm(y[t], twd(tw, t * k * tws, dir)) : y[t];
+      X[xs<LW>(base + t * Lp, row)] =
+          (MODE == 1 && t && k) ? cm(y[t], twd(tw, t * k * tws, dir)) : y[t];
   }
 }
 
-template <int MODE, int RW>
-SWE_DEV void lane_run_stage(double2 *X, int N2, int Lp, int R, double dir, const double2 *tw,
-                            int warp, int nw, int lane) {
-  switch (R) {
-    case 2: lane_stage<2, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 3: lane_stage<3, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 4: lane_stage<4, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 5: lane_stage<5, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 7: lane_stage<7, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 11: lane_stage<11, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    default: lane_stage<13, MODE, RW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-  }
-}
-
-struct LCtx {
-  double2 *X;
-  int p, jn, js, eq, b0, nsl, S, tid, nthr, warp, lane, nw;
-};
-
-SWE_DEV int lrow(const LCtx &c, int f, int h, int s) { return (f * 2 + h) * c.S + s; }
-
-SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
-  int Lp = 1;
-  for (int s = 0; s < a.nst; ++s) {
-    if (a.pfa) lane_run_stage<2, LW>(c.X, a.N2, Lp, a.radix[s], 1.0, a.tw, c.warp, c.nw, c.lane);
-    else lane_run_stage<0, LW>(c.X, a.N2, Lp, a.radix[s], 1.0, a.tw, c.warp, c.nw, c.lane);
-    Lp *= a.radix[s];
+// Any odd radix R, CTA-wide (call with every thread, between barriers).  The same
+// sums as dft<R>: with S_q = v_q + v_{R-q}, D_q = v_q - v_{R-q} (q = 1..H),
+//   y_t, y_{R-t} = v_0 + sum_q S_q cos(2 pi q t / R) -+ dir i sum_q D_q sin(...)
+// Thread item (butterfly, group of GT consecutive t in 0..H, row): a round takes as
+// many whole butterflies as the CTA holds items for, reads their inputs, then (after
+// a barrier) overwrites them in place.  ct = shared (cos, sin)(2 pi e / R), e < R.
+template <int MODE, int RW, int LW>
+SWE_DEV void lane_stage_gen(double2 *X, double2 *ct, int N2, int Lp, int R, double dir,
+                            const double2 *tw, int tid, int nthr) {
+  for (int e = tid; e < R; e += nthr) ct[e] = __ldg(tw + e * (N2 / R));
+  __syncthreads();
+  const int H = (R - 1) / 2, G = (H + GT) / GT;
+  const int L = Lp * R, nbf = N2 / R, tws = N2 / L;
+  const int row = tid % RW, item = tid / RW, bpr = (nthr / RW) / G;
+  const int bl = item / G, grp = item - bl * G;
+  for (int b0 = 0; b0 < nbf; b0 += bpr) {
+    const int bf = b0 + bl;
+    const bool act = bl < bpr && bf < nbf;
+    double re[GT], im[GT], sx[GT], sy[GT];
+    int e[GT];
+    int base = 0, k = 0;
+    if (act) {
+      const int g = bf / Lp;
+      k = bf - g * Lp;
+      base = g * L + k;
+      const double2 v0 = X[xs<LW>(base, row)];
+#pragma unroll
+      for (int j = 0; j < GT; ++j) {
+        re[j] = v0.x;
+        im[j] = v0.y;
+        sx[j] = 0.0;
+        sy[j] = 0.0;
+        e[j] = 0;
+      }
+      for (int q = 1; q <= H; ++q) {
+        double2 p = X[xs<LW>(base + q * Lp, row)], m = X[xs<LW>(base + (R - q) * Lp, row)];
+        if (MODE == 0 && k) {
+          p = cm(p, twd(tw, q * k * tws, dir));
+          m = cm(m, twd(tw, (R - q) * k * tws, dir));
+        }
+        const double Sx = p.x + m.x, Sy = p.y + m.y, Dx = p.x - m.x, Dy = p.y - m.y;
+#pragma unroll
+        for (int j = 0; j < GT; ++j) {
+          e[j] += grp * GT + j;
+          if (e[j] >= R) e[j] -= R;
+          const double2 w = ct[e[j]];
+          re[j] = fma(Sx, w.x, re[j]);
+          im[j] = fma(Sy, w.x, im[j]);
+          sx[j] = fma(Dx, w.y, sx[j]);
+          sy[j] = fma(Dy, w.y, sy[j]);
+        }
+      }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < GT; ++j) {
+        const int t = grp * GT + j;
+        if (t > H) break;
+        double2 y = make_double2(re[j] - dir * sy[j], im[j] + dir * sx[j]);
+        if (MODE == 1 && t && k) y = cm(y, twd(tw, t * k * tws, dir));
+        X[xs<LW>(base + t * Lp, row)] = y;
+        if (t) {
+          double2 y2 = make_double2(re[j] + dir * sy[j], im[j] - dir * sx[j]);
+          if (MODE == 1 && k) y2 = cm(y2, twd(tw, (R - t) * k * tws, dir));
+          X[xs<LW>(base + (R - t) * Lp, row)] = y2;
+        }
+      }
+    }
     __syncthreads();
   }
 }
 
+// one stage over rows 0..RW-1, ends with a CTA barrier.  GEN: the length has a
+// non-unrolled radix (kernels without it keep the small-radix register budget)
+template <int MODE, int RW, int LW, bool GEN>
+SWE_DEV void lane_run_stage(double2 *X, double2 *ct, int N2, int Lp, int R, double dir,
+                            const double2 *tw, int tid, int nthr) {
+  const int warp = tid >> 5, nw = nthr >> 5, lane = tid & 31;
+  switch (R) {
+    case 2: lane_stage<2, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 3: lane_stage<3, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 4: lane_stage<4, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 5: lane_stage<5, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 7: lane_stage<7, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    // (with a generic radix in the length, 11 and 13 go generic too: their unrolled
+    // register footprint next to the generic stage would spill)
+    case 11:
+      if constexpr (!GEN) {
+        lane_stage<11, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane);
+        break;
+      }
+    case 13:
+      if constexpr (!GEN) {
+        lane_stage<13, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane);
+        break;
+      }
+    default:
+      if constexpr (GEN) {
+        lane_stage_gen<MODE, RW, LW>(X, ct, N2, Lp, R, dir, tw, tid, nthr);
+        return;
+      }
+      break;
+  }
+  __syncthreads();
+}
+
+struct LCtx {
+  double2 *X, *ct;
+  int p, jn, js, eq, b0, nsl, S, tid, nthr;
+  int split, hem;  // split: this CTA holds only hemisphere hem's rows (row = f*S + s)
+};
+
+SWE_DEV int lrow(const LCtx &c, int f, int h, int s) {
+  return c.split ? f * c.S + s : (f * 2 + h) * c.S + s;
+}
+
+template <int LW, bool GEN>
+SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
+  int Lp = 1;
+  for (int s = 0; s < a.nst; ++s) {
+    if (a.pfa)
+      lane_run_stage<2, LW, LW, GEN>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
+    else
+      lane_run_stage<0, LW, LW, GEN>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
+    Lp *= a.radix[s];
+  }
+}
+
 // forward transform of rows 0..RW-1
-template <int RW = LW>
+template <int RW, int LW, bool GEN>
 SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
   if (a.pfa) {
     int Lp = 1;
     for (int s = 0; s < a.nst; ++s) {
-      lane_run_stage<2, RW>(c.X, a.N2, Lp, a.radix[s], -1.0, a.tw, c.warp, c.nw, c.lane);
+      lane_run_stage<2, RW, LW, GEN>(c.X, c.ct, a.N2, Lp, a.radix[s], -1.0, a.tw, c.tid, c.nthr);
       Lp *= a.radix[s];
-      __syncthreads();
     }
     return;
   }
   int L = a.N2;
   for (int s = a.nst - 1; s >= 0; --s) {
     const int R = a.radix[s];
-    lane_run_stage<1, RW>(c.X, a.N2, L / R, R, -1.0, a.tw, c.warp, c.nw, c.lane);
+    lane_run_stage<1, RW, LW, GEN>(c.X, c.ct, a.N2, L / R, R, -1.0, a.tw, c.tid, c.nthr);
     L /= R;
-    __syncthreads();
   }
 }
 
 // Z of one hemisphere row from its half spectrum X (see fft.cu build comment):
 //   Z[k] = (X[k] + conj X[N2-k]) + i w^k (X[k] - conj X[N2-k])
 // (w1, w2) = twh[k], twh[N2-k] and (z1, z2) = pos_z[k], pos_z[N2-k], prefetched
+template <int LW>
 SWE_DEV void put_z(const LCtx &c, int row, int k, int k2, double2 Xk, double2 Xc, double2 w1,
                    double2 w2, int z1, int z2) {
   if (k == 0) {
-    c.X[xs(z1, row)] = make_double2(Xk.x, Xk.x);
+    c.X[xs<LW>(z1, row)] = make_double2(Xk.x, Xk.x);
     return;
   }
   const double2 A = make_double2(Xk.x + Xc.x, Xk.y - Xc.y);
   const double2 D = make_double2(Xk.x - Xc.x, Xk.y + Xc.y);
   const double2 Bk = cm(D, w1);
-  c.X[xs(z1, row)] = make_double2(A.x - Bk.y, A.y + Bk.x);
+  c.X[xs<LW>(z1, row)] = make_double2(A.x - Bk.y, A.y + Bk.x);
   if (k2 != k) {
     const double2 A2 = make_double2(Xc.x + Xk.x, Xc.y - Xk.y);
     const double2 D2 = make_double2(Xc.x - Xk.x, Xc.y + Xk.y);
     const double2 B2 = cm(D2, w2);
-    c.X[xs(z2, row)] = make_double2(A2.x - B2.y, A2.y + B2.x);
+    c.X[xs<LW>(z2, row)] = make_double2(A2.x - B2.y, A2.y + B2.x);
   }
 }
 
 // fields a.in[0..nf-1]: E/O half spectra [m][2][Jp][ld] of pair p -> Z of their north
-// and south rows.  One flattened loop over (k pair, slice, field), field fastest: the
-// lanes of a warp store to the same slot of different rows (one 256-byte line, no
-// bank conflicts) and keep many loads in flight; field `subf` has phisub subtracted from E at m = 0 (phi_prime,
-// dynamics.py:52-56).  With a.dlam, field 2 is i m times field 5 (d_lambda Phi).
+// and south rows (only hemisphere c.hem when split).  One flattened loop over (k pair,
+// slice, field), field fastest: the lanes of a warp store to the same slot of
+// different rows (one line, no bank conflicts) and keep many loads in flight; field
+// `subf` has phisub subtracted from E at m = 0 (phi_prime, dynamics.py:52-56).  With
+// a.dlam, field 2 is i m times field 5 (d_lambda Phi).
+template <int LW>
 SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1, S = c.S;
   const size_t eo = (size_t)a.Jp * a.ld / 2;  // E -> O offset (double2)
@@ -196,60 +310,74 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
         e2[u] = make_double2(-mk2 * e2[u].y, mk2 * e2[u].x);
         o2[u] = make_double2(-mk2 * o2[u].y, mk2 * o2[u].x);
       }
-      put_z(c, lrow(c, f, 0, s), k, k2, make_double2(e[u].x + o[u].x, e[u].y + o[u].y),
-            make_double2(e2[u].x + o2[u].x, e2[u].y + o2[u].y), w1[u], w2[u], z1[u], z2[u]);
-      put_z(c, lrow(c, f, 1, s), k, k2, make_double2(e[u].x - o[u].x, e[u].y - o[u].y),
-            make_double2(e2[u].x - o2[u].x, e2[u].y - o2[u].y), w1[u], w2[u], z1[u], z2[u]);
+      if (!c.split || c.hem == 0)
+        put_z<LW>(c, lrow(c, f, 0, s), k, k2, make_double2(e[u].x + o[u].x, e[u].y + o[u].y),
+                  make_double2(e2[u].x + o2[u].x, e2[u].y + o2[u].y), w1[u], w2[u], z1[u],
+                  z2[u]);
+      if (!c.split || c.hem == 1)
+        put_z<LW>(c, lrow(c, f, 1, s), k, k2, make_double2(e[u].x - o[u].x, e[u].y - o[u].y),
+                  make_double2(e2[u].x - o2[u].x, e2[u].y - o2[u].y), w1[u], w2[u], z1[u],
+                  z2[u]);
     }
   }
 }
 
 // grid sample n of row r lives in X[pos_g[n/2]][r].{x,y}
+template <int LW>
 SWE_DEV double &gval(const FftArgs &a, const LCtx &c, int n, int row) {
-  double *p = reinterpret_cast<double *>(c.X + xs(__ldg(a.pos_g + (n >> 1)), row));
+  double *p = reinterpret_cast<double *>(c.X + xs<LW>(__ldg(a.pos_g + (n >> 1)), row));
   return p[n & 1];
 }
+template <int LW>
 SWE_DEV double &gslot(const LCtx &c, int p, int h, int row) {
-  return reinterpret_cast<double *>(c.X + xs(p, row))[h];
+  return reinterpret_cast<double *>(c.X + xs<LW>(p, row))[h];
 }
 
+template <int LW>
 SWE_DEV void lane_load_grid(const FftArgs &a, const LCtx &c, const double *src, int f) {
   for (int h = 0; h < 2; ++h) {
     const int j = (h && !c.eq) ? c.js : c.jn;
     for (int s = 0; s < c.nsl; ++s) {
       const double *g = src + ((size_t)(c.b0 + s) * a.J + j) * a.I;
-      for (int n = c.tid; n < a.I; n += c.nthr) gval(a, c, n, lrow(c, f, h, s)) = __ldg(g + n);
+      for (int n = c.tid; n < a.I; n += c.nthr) gval<LW>(a, c, n, lrow(c, f, h, s)) = __ldg(g + n);
     }
   }
 }
 
+template <int LW>
 SWE_DEV void lane_store_grid(const FftArgs &a, const LCtx &c, double *dst, int f, double scale) {
   for (int h = 0; h < 2 - c.eq; ++h) {
     const int j = h ? c.js : c.jn;
     for (int s = 0; s < c.nsl; ++s) {
       double *g = dst + ((size_t)(c.b0 + s) * a.J + j) * a.I;
-      for (int n = c.tid; n < a.I; n += c.nthr) g[n] = gval(a, c, n, lrow(c, f, h, s)) * scale;
+      for (int n = c.tid; n < a.I; n += c.nthr) g[n] = gval<LW>(a, c, n, lrow(c, f, h, s)) * scale;
     }
   }
 }
 
-// fm[k] (k = 0..M) of rows (f, h, s): fm = (Ge + w^{-k} Go) / I, see fft.cu;
-// F+ = scale (fm_N + fm_S), F- = scale (fm_N - fm_S)  ->  a.out[f] [m][2][Jp][ld]
-// (z1, z2) = slots of Z[k], Z[N2-k]; w = conj twh[k]
-SWE_DEV double2 row_fm(const LCtx &c, int row, int z1, int z2, double2 w) {
-  const double2 zk = c.X[xs(z1, row)];
-  const double2 zc = c.X[xs(z2, row)];
+// fm[k] (k = 0..M) of row `row` of the buffer X: fm = (Ge + w^{-k} Go) / I, see
+// fft.cu; (z1, z2) = slots of Z[k], Z[N2-k]; w = conj twh[k].  X may be a peer
+// CTA's shared memory (cluster address).
+template <int LW>
+SWE_DEV double2 row_fm(const double2 *X, int row, int z1, int z2, double2 w) {
+  const double2 zk = X[xs<LW>(z1, row)];
+  const double2 zc = X[xs<LW>(z2, row)];
   const double2 Sg = make_double2(zk.x + zc.x, zk.y - zc.y);
   const double2 D = make_double2(zk.y + zc.y, -(zk.x - zc.x));
   const double2 t = cm(w, D);
   return make_double2(Sg.x + t.x, Sg.y + t.y);  // 2 * I * fm
 }
 
-// fields 0..nf-1 -> a.out[f], scaled by w01 (fields 0, 1) or w23 (2, 3); one flattened loop
-SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, int nf, double w01, double w23) {
+// fields 0..nf-1 -> a.out[f] as F+ = scale (fm_N + fm_S), F- = scale (fm_N - fm_S)
+// ([m][2][Jp][ld]), scaled by w01 (fields 0, 1) or w23 (2, 3); one flattened loop.
+// XN / XS hold the north / south rows (the same buffer unless split); items
+// i0, i0 + istep, ... of the (k, slice, field) range.
+template <int LW>
+SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, const double2 *XN, const double2 *XS,
+                          int nf, double w01, double w23, int i0, int istep) {
   const int M = a.M, S = c.S, N2 = a.N2, per = (M + 1) * S;
   const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
-  for (int idx = c.tid; idx < nf * per; idx += c.nthr) {
+  for (int idx = i0; idx < nf * per; idx += istep) {
     const int r = idx / nf, f = idx - r * nf, k = r / S, s = r - k * S;
     if (s >= c.nsl) continue;
     const int z1 = __ldg(a.pos_z + k), z2 = __ldg(a.pos_z + (k == 0 ? 0 : N2 - k));
@@ -258,53 +386,66 @@ SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, int nf, double w01, d
     const double h = 0.5 * (f < 2 ? w01 : w23);
     double2 *d = reinterpret_cast<double2 *>(a.out[f] + (size_t)c.p * a.ld) + c.b0 +
                  (size_t)k * 2 * pm + s;
-    const double2 fn = row_fm(c, lrow(c, f, 0, s), z1, z2, w);
+    const double2 fn = row_fm<LW>(XN, lrow(c, f, 0, s), z1, z2, w);
     if (c.eq) {
       const double2 v = make_double2(fn.x * h, fn.y * h);
       d[0] = v;
       d[pm] = v;
     } else {
-      const double2 fs = row_fm(c, lrow(c, f, 1, s), z1, z2, w);
+      const double2 fs = row_fm<LW>(XS, lrow(c, f, 1, s), z1, z2, w);
       d[0] = make_double2((fn.x + fs.x) * h, (fn.y + fs.y) * h);
       d[pm] = make_double2((fn.x - fs.x) * h, (fn.y - fs.y) * h);
     }
   }
 }
 
+template <int LW>
+constexpr int lane_threads() { return LW == 16 ? 256 : 512; }
+
+// slices per CTA (rows = fields x 2 hemispheres x slices; the LW = 8 nonlinear pass
+// holds one hemisphere of one slice per CTA)
+__host__ __device__ constexpr int lane_slices(int op, int lw) {
+  return lw == 16 ? fft_lane_slices(op) : (op == FOP_NONLINEAR ? 1 : fft_lane_slices(op) / 2);
+}
+
 }  // namespace
 
-template <int OP>
-__global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant__ FftArgs a) {
+template <int OP, int LW, bool GEN>
+__global__ void __launch_bounds__(lane_threads<LW>(), 512 / lane_threads<LW>())
+    fft_lanes_kernel(const __grid_constant__ FftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool SPLIT = OP == FOP_NONLINEAR && LW == 8;
   LCtx c;
   c.X = reinterpret_cast<double2 *>(smem_raw);
-  c.S = fft_lane_slices(OP);
+  c.ct = c.X + (size_t)a.N2 * LW;
+  c.S = lane_slices(OP, LW);
+  c.split = SPLIT;
   // consecutive CTAs take consecutive slice groups of one pair: they share the
-  // 32-byte sectors of the [m][2][Jp][ld] rows, which then hit in L2
+  // 32-byte sectors of the [m][2][Jp][ld] rows, which then hit in L2.  Split: the
+  // two CTAs of a cluster are the two hemispheres of one slice.
+  c.hem = SPLIT ? (int)(blockIdx.x & 1) : 0;
+  const int grp = SPLIT ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   c.p = blockIdx.y;
   c.jn = c.p;
   c.js = a.J - 1 - c.p;
   c.eq = c.js == c.jn;
-  c.b0 = blockIdx.x * c.S;
+  c.b0 = grp * c.S;
   c.nsl = min(c.S, a.nslices - c.b0);
   c.tid = threadIdx.x;
   c.nthr = blockDim.x;
-  c.warp = threadIdx.x >> 5;
-  c.lane = threadIdx.x & 31;
-  c.nw = blockDim.x >> 5;
   const int p = c.p, I = a.I, S = c.S;
   const double ia = a.inv_acos[p];
 
   if constexpr (OP == FOP_SYNTH_GRID || OP == FOP_SYNTH2_GRID) {
     constexpr int NF = OP == FOP_SYNTH_GRID ? 1 : 2;
-    lane_load_eo(a, c, NF, -1);
+    lane_load_eo<LW>(a, c, NF, -1);
     __syncthreads();
-    lane_ifft(a, c);
+    lane_ifft<LW, GEN>(a, c);
     const double sc = (OP == FOP_SYNTH2_GRID || a.scale_mode) ? ia : 1.0;
-    for (int f = 0; f < NF; ++f) lane_store_grid(a, c, a.gout[f], f, sc);
+    for (int f = 0; f < NF; ++f) lane_store_grid<LW>(a, c, a.gout[f], f, sc);
   } else if constexpr (OP == FOP_ANALYSIS || OP == FOP_VORTDIV) {
     constexpr int NF = OP == FOP_ANALYSIS ? 1 : 2;
-    for (int f = 0; f < NF; ++f) lane_load_grid(a, c, a.gin[f], f);
+    for (int f = 0; f < NF; ++f) lane_load_grid<LW>(a, c, a.gin[f], f);
     __syncthreads();
     if constexpr (OP == FOP_VORTDIV) {
       const double cs = a.coslat[p];
@@ -314,14 +455,14 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
       }
       __syncthreads();
     }
-    lane_fft(a, c);
+    lane_fft<LW, LW, GEN>(a, c);
     const double w = OP == FOP_ANALYSIS ? a.wq[p] * a.inv_I : a.wsin2[p] * a.inv_I * a.inv_a;
-    lane_extract(a, c, NF, w, w);
+    lane_extract<LW>(a, c, c.X, c.X, NF, w, w, c.tid, c.nthr);
   } else if constexpr (OP == FOP_CORIOLIS) {
     // linear_coriolis (dynamics.py:129-135): f u, f v -> vortdiv_from_uv; f = -f on the south row
-    lane_load_eo(a, c, 2, -1);
+    lane_load_eo<LW>(a, c, 2, -1);
     __syncthreads();
-    lane_ifft(a, c);
+    lane_ifft<LW, GEN>(a, c);
     const double cs = a.coslat[p], fc = a.fcor[p];
     for (int idx = c.tid; idx < a.N2 * LW; idx += c.nthr) {
       const int row = (idx & (LW - 1)) ^ (((idx / LW) << 1) & (LW - 1));  // undo xs()
@@ -330,21 +471,22 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
       c.X[idx] = make_double2((fr * (z.x * ia)) * cs, (fr * (z.y * ia)) * cs);
     }
     __syncthreads();
-    lane_fft(a, c);
+    lane_fft<LW, LW, GEN>(a, c);
     const double w = a.wsin2[p] * a.inv_I * a.inv_a;
-    lane_extract(a, c, 2, w, w);
+    lane_extract<LW>(a, c, c.X, c.X, 2, w, w, c.tid, c.nthr);
   } else if constexpr (OP == FOP_NONLINEAR) {
     // nonlinear_advection + nonlinear_rest (dynamics.py:142-160)
     // in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi, 5 Phi (phi_prime applied here), 6 delta
-    lane_load_eo(a, c, 7, 5);
+    lane_load_eo<LW>(a, c, 7, 5);
     __syncthreads();
-    lane_ifft(a, c);
+    lane_ifft<LW, GEN>(a, c);
     const double cs = a.coslat[p];
+    constexpr int NH = SPLIT ? 1 : 2;  // hemispheres held by this CTA
     // lanes: (slot, hemisphere, x/y) fastest, so a half-warp reads one bank each
-    for (int idx = c.tid; idx < I * 2 * S; idx += c.nthr) {
-      const int s = idx / (2 * I), r = idx - s * 2 * I;
-      const int pp = r >> 2, h = (r >> 1) & 1, hh = r & 1;
-      auto R = [&](int f) -> double & { return gslot(c, pp, hh, lrow(c, f, h, s)); };
+    for (int idx = c.tid; idx < I * NH * S; idx += c.nthr) {
+      const int s = idx / (NH * I), r = idx - s * NH * I;
+      const int pp = r / (2 * NH), h = SPLIT ? c.hem : (r >> 1) & 1, hh = r & 1;
+      auto R = [&](int f) -> double & { return gslot<LW>(c, pp, hh, lrow(c, f, h, s)); };
       const double u = R(0) * ia, v = R(1) * ia, gx = R(2) * ia, gy = R(3) * ia;
       const double xi = R(4), ph = R(5), de = R(6);
       R(0) = -(u * gx + v * gy) - ph * de;   // -(V.grad Phi) - Phi' delta
@@ -353,46 +495,97 @@ __global__ void __launch_bounds__(256, 2) fft_lanes_kernel(const __grid_constant
       R(3) = (xi * v) * cs;                  // (xi v) cos
     }
     __syncthreads();
-    lane_fft<8>(a, c);  // only the 4 product fields x 2 hemispheres (rows 0..7, S = 1)
+    // only the 4 product fields (x 2 hemispheres unless split; S = 1)
+    lane_fft<SPLIT ? 4 : 8, LW, GEN>(a, c);
     const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
-    lane_extract(a, c, 4, w, wv);
+    if constexpr (SPLIT) {
+      // F+- needs both hemispheres: each CTA of the pair folds half of the (k, field)
+      // items, reading the peer's rows through distributed shared memory
+      cg::cluster_group cl = cg::this_cluster();
+      cl.sync();
+      const double2 *XN = cl.map_shared_rank(c.X, 0), *XS = cl.map_shared_rank(c.X, 1);
+      lane_extract<LW>(a, c, XN, XS, 4, w, wv, c.hem * c.nthr + c.tid, 2 * c.nthr);
+      cl.sync();  // keep this CTA's rows alive until the peer is done reading them
+    } else {
+      lane_extract<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr);
+    }
   }
 }
 
-template <int OP>
-static int launch_lanes(const FftArgs &a, int smem, int nthreads, cudaStream_t st) {
+namespace {
+
+int lane_width(const FftArgs &a, int *rgen) {
+  int g = 0;
+  for (int s = 0; s < a.nst; ++s)
+    if (!fft_small_radix(a.radix[s])) g = std::max(g, a.radix[s]);
+  if (g) g = std::max(g, 13);  // 11 and 13 then run generic as well
+  if (rgen) *rgen = g;
+  const int G = (g - 1) / 2 / GT + 1;  // thread items per row of one generic butterfly
+  for (int lw : {16, 8}) {
+    const size_t smem = ((size_t)a.N2 * lw + g) * sizeof(double2);
+    const int items = lane_threads<16>() * (lw == 16 ? 1 : 2) / lw;
+    if (smem <= 227 * 1024 && (g == 0 || (g % 2 == 1 && G <= items))) return lw;
+  }
+  return 0;
+}
+
+template <int OP, int LW, bool GEN>
+int launch_lanes(const FftArgs &a, int smem, cudaStream_t st) {
   static int attr = 0;
   if (smem > attr) {
-    SWE_CUDA(cudaFuncSetAttribute(fft_lanes_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
+    SWE_CUDA(cudaFuncSetAttribute(fft_lanes_kernel<OP, LW, GEN>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = smem;
   }
-  const int S = fft_lane_slices(OP);
-  dim3 grid((a.nslices + S - 1) / S, a.Jh);
-  fft_lanes_kernel<OP><<<grid, nthreads, smem, st>>>(a);
+  const int S = lane_slices(OP, LW);
+  const bool split = OP == FOP_NONLINEAR && LW == 8;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3((a.nslices + S - 1) / S * (split ? 2 : 1), a.Jh);
+  cfg.blockDim = dim3(lane_threads<LW>());
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  if (split) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  SWE_CUDA(cudaLaunchKernelEx(&cfg, fft_lanes_kernel<OP, LW, GEN>, a));
   SWE_LAUNCH_CHECK();
   return OK;
 }
 
-int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
-  const int smem = a.N2 * LW * (int)sizeof(double2);
-  const int nthr = 256;
+template <int LW, bool GEN>
+int launch_width(int op, const FftArgs &a, int smem, cudaStream_t st) {
   switch (op) {
-    case FOP_SYNTH_GRID: return launch_lanes<FOP_SYNTH_GRID>(a, smem, nthr, st);
-    case FOP_SYNTH2_GRID: return launch_lanes<FOP_SYNTH2_GRID>(a, smem, nthr, st);
-    case FOP_ANALYSIS: return launch_lanes<FOP_ANALYSIS>(a, smem, nthr, st);
-    case FOP_VORTDIV: return launch_lanes<FOP_VORTDIV>(a, smem, nthr, st);
-    case FOP_CORIOLIS: return launch_lanes<FOP_CORIOLIS>(a, smem, nthr, st);
-    case FOP_NONLINEAR: return launch_lanes<FOP_NONLINEAR>(a, smem, nthr, st);
+    case FOP_SYNTH_GRID: return launch_lanes<FOP_SYNTH_GRID, LW, GEN>(a, smem, st);
+    case FOP_SYNTH2_GRID: return launch_lanes<FOP_SYNTH2_GRID, LW, GEN>(a, smem, st);
+    case FOP_ANALYSIS: return launch_lanes<FOP_ANALYSIS, LW, GEN>(a, smem, st);
+    case FOP_VORTDIV: return launch_lanes<FOP_VORTDIV, LW, GEN>(a, smem, st);
+    case FOP_CORIOLIS: return launch_lanes<FOP_CORIOLIS, LW, GEN>(a, smem, st);
+    case FOP_NONLINEAR: return launch_lanes<FOP_NONLINEAR, LW, GEN>(a, smem, st);
   }
   set_error("unknown fft op %d", op);
   return E_SHAPE;
 }
 
-bool fft_lanes_ok(const FftArgs &a) {
-  for (int s = 0; s < a.nst; ++s)
-    if (!fft_small_radix(a.radix[s])) return false;
-  return (size_t)a.N2 * LW * sizeof(double2) <= 227 * 1024;
+}  // namespace
+
+int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
+  int g = 0;
+  const int lw = lane_width(a, &g);
+  if (!lw) {
+    set_error("internal: lane FFT does not fit N2=%d", a.N2);
+    return E_SHAPE;
+  }
+  const int smem = (int)(((size_t)a.N2 * lw + g) * sizeof(double2));
+  if (g) return lw == 16 ? launch_width<16, true>(op, a, smem, st) : launch_width<8, true>(op, a, smem, st);
+  return lw == 16 ? launch_width<16, false>(op, a, smem, st) : launch_width<8, false>(op, a, smem, st);
 }
+
+bool fft_lanes_ok(const FftArgs &a) { return lane_width(a, nullptr) != 0; }
 
 }  // namespace swe

@@ -78,7 +78,9 @@ def test_wide_batches_match_oracle(gpu, B):
     assert rel_diff(xi, xo) < TOL and rel_diff(de, do) < TOL
 
 
-@pytest.mark.parametrize("M", [1, 2, 5, 8, 13, 16, 31, 32, 51, 64, 100, 256])
+# 56 (N2 = 85 = 5*17) and 63 (95 = 5*19) take the generic-radix lane stage at 16
+# rows per CTA, 100 (N2 = 151, prime) the 8-row lane kernel
+@pytest.mark.parametrize("M", [1, 2, 5, 8, 13, 16, 31, 32, 51, 56, 63, 64, 100, 256])
 def test_batched_transforms_match_oracle(gpu, fft_path, M):
     from oracle.sht import random_bandlimited
     grid = gpu.get_grid(M)
@@ -97,6 +99,32 @@ def test_batched_transforms_match_oracle(gpu, fft_path, M):
     xi, de = grid.vortdiv_from_uv(gi[:3], gi[2:5])
     xo, do = sph.vortdiv_from_uv(gi[:3], gi[2:5])
     assert rel_diff(xi, xo) < TOL and rel_diff(de, do) < TOL
+
+
+def test_m1024_lane_kernel_matches_row_kernel(gpu):
+    """M = 1024 (N2 = 1537 = 29*53: generic radices, 8 rows per CTA): every lane-kernel
+    transform agrees with the warp-per-row kernel and the round trip closes."""
+    from paper_2306_09497_b200 import _lib
+    g = gpu.get_grid(1024)
+    rng = np.random.default_rng(1024)
+    B = 3
+    c = (g.n_of + 1.0) ** -1.5 * np.exp(2j * np.pi * rng.uniform(size=(B, g.n_modes)))
+    c[:, : g.M + 1] = c[:, : g.M + 1].real
+    out = {}
+    for path in (1, 2):
+        _lib.set_option("fft_path", path)
+        try:
+            gr = g.synthesis(c)
+            u, v = g.uv_from_vortdiv(c, c[::-1].copy())
+            out[path] = (gr, u, v, g.analysis(gr), g.vortdiv_from_uv(u, v))
+        finally:
+            _lib.set_option("fft_path", 0)
+    a, b = out[1], out[2]
+    for x, y in zip(a[:4], b[:4]):
+        assert rel_diff(y, x) < 1e-12
+    for x, y in zip(a[4], b[4]):
+        assert rel_diff(y, x) < 1e-12
+    assert np.abs(b[3] - c).max() <= 1e-11 * np.abs(c).max()
 
 
 @pytest.mark.parametrize("M", [16, 64, 256])

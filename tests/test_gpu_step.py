@@ -236,13 +236,15 @@ def test_host_pipeline_matches_inplace(mods):
         assert torch.equal(outs[i], want[i]), i
 
 
-@pytest.mark.parametrize("M,B", [(51, 3), (51, 40), (256, 3)])
+@pytest.mark.parametrize("M,B", [(51, 3), (51, 40), (256, 3), (56, 3), (100, 3), (100, 40)])
 @pytest.mark.parametrize("path", [1, 2], ids=["fft_rows", "fft_lanes"])
 def test_nonlinear_prime_factor_sizes(mods, M, B, path):
     """Nonlinear tendency on prime-factor FFT lengths (N2 = 77 = 7*11 at M=51,
     385 = 5*7*11 at M=256, the benchmark size) on both FFT kernels, batched,
     against the oracle.  B = 40 takes the warp-specialised synthesis, which on
-    the lane kernel hands over in the pair-major layout."""
+    the lane kernel hands over in the pair-major layout.  M = 56 (N2 = 85 = 5*17)
+    runs a generic-radix lane stage; M = 100 (N2 = 151, prime) the 8-row lane
+    kernel whose nonlinear pass splits the hemispheres over a two-CTA cluster."""
     spharm, dynamics, _, _ = mods
     from paper_2306_09497_b200 import _lib
     from oracle.sht import OracleSphere, random_bandlimited
@@ -265,6 +267,36 @@ def test_nonlinear_prime_factor_sizes(mods, M, B, path):
     for f in range(3):
         g = got[f].cpu().numpy()
         assert np.abs(g - want[f]).max() <= 1e-11 * np.abs(want[f]).max(), f
+
+
+def test_nonlinear_m1024_lanes_match_rows(mods):
+    """M = 1024 (configs 4/5): the 8-row, cluster-split lane kernel with generic
+    radices 29 and 53 gives the warp-per-row kernel's nonlinear tendency."""
+    spharm, dynamics, _, _ = mods
+    from paper_2306_09497_b200 import _lib
+    grid = spharm.get_grid(1024)
+    rng = np.random.default_rng(1024)
+    B = 2
+    c = []
+    for _ in range(3):
+        x = (grid.n_of + 1.0) ** -1.5 * np.exp(2j * np.pi * rng.uniform(size=(B, grid.n_modes)))
+        x[:, : grid.M + 1] = x[:, : grid.M + 1].real
+        c.append(x)
+    phi = 3e5 * c[0]
+    phi[:, 0] += 9.80616 * 29400.0 * np.sqrt(2.0)
+    s = dynamics.PrognosticState.from_fields(grid, phi, 1e-5 * c[1], 1e-6 * c[2],
+                                             np.full(B, 9.80616 * 29400.0))
+    got = {}
+    for path in (1, 2):
+        _lib.set_option("fft_path", path)
+        try:
+            got[path] = [t.cpu().numpy() for t in dynamics.nonlinear(s)]
+        finally:
+            _lib.set_option("fft_path", 0)
+    for f in range(3):
+        a, b = got[1][f], got[2][f]
+        assert np.isfinite(b).all()
+        assert np.abs(b - a).max() <= 1e-11 * np.abs(a).max(), f  # as vs the oracle
 
 
 @pytest.mark.parametrize("M,B", [(32, 3), (51, 40)])
