@@ -215,6 +215,66 @@ def pint_cfg2(torch, iters=10):
             "timing": "host wall clock with a device sync per iteration (MgritEngine.run)"}
 
 
+def sht_cfg4(torch, Ms=(256, 1024)):
+    """cfg4: batched SHT round trip, 3 fields x 256 slices, c_mn =
+    (n+1)^-1.5 e^{i phi}, phi ~ U[0, 2 pi) from default_rng(230609497) drawn as
+    (3, 256, K), m = 0 entries real (cos phi).  One synthesis + one analysis per
+    field-slice, one field (256 slices) per call, coefficients resident on the GPU;
+    CUDA events around the 3 fields after a warm-up pass."""
+    import numpy as np
+    from paper_2306_09497_b200 import spharm
+    out = {}
+    for M in Ms:
+        g = spharm.get_grid(M)
+        rng = np.random.default_rng(230609497)
+        ph = rng.uniform(0.0, 2.0 * np.pi, size=(3, 256, g.n_modes))
+        amp = (g.n_of + 1.0) ** -1.5
+        c = amp * np.exp(1j * ph)
+        c[..., : M + 1] = amp[: M + 1] * np.cos(ph[..., : M + 1])
+        ct = torch.from_numpy(c).cuda()
+        del c, ph
+        back = g.analysis(g.synthesis(ct[0]))  # warm-up (plans, workspaces)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        backs = [g.analysis(g.synthesis(ct[f])) for f in range(3)]
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        err = max(float((backs[f] - ct[f]).abs().max()) for f in range(3))
+        del backs
+        out[f"M{M}"] = {"field_slices_per_s": 768 / (ms * 1e-3), "ms": ms,
+                        "round_trip_max_abs_err": err}
+        del ct, back
+        torch.cuda.empty_cache()
+    out["note"] = "3 fields x 256 slices, synthesis + analysis per field-slice"
+    return out
+
+
+def fine_cfg5(torch, slices=64, steps=5):
+    """cfg5: M=1024, dt=2 s, nu=0, gaussian_bumps, 64 independent
+    intervals per GPU (512 over 8 GPUs) advanced by the fine IMEX step; CUDA
+    events around `steps` steps after 2 warm-up steps."""
+    from paper_2306_09497_b200 import dynamics, scenarios, spharm, steppers
+    g = spharm.get_grid(1024)
+    s = scenarios.gaussian_bumps(g, batch=slices)
+    cfg = steppers.StepperConfig(dt=2.0, viscosity=dynamics.ViscositySpec(2, 0.0))
+    steppers.imex_steps_inplace(s, cfg, 2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    steppers.imex_steps_inplace(s, cfg, steps)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    rate = slices / (ms * 1e-3)
+    return {"value": rate, "unit": "fine slice-steps/s per GPU", "ms_per_step": ms,
+            "slices_per_gpu": slices, "finite": bool(s.is_finite()),
+            "cfg5_seconds_at_8_gpus": 15360 / (8 * rate),
+            "config": "cfg5: gaussian_bumps M=1024, dt=2 s, nu=0, IMEX, 512 intervals x 30 steps "
+                      "(64 per GPU at 8 GPUs)"}
+
+
 def ncu_traffic():
     """DRAM bytes per launch of the dominant kernels from the newest committed
     `ncu --set full` capture (profiles/*_kernels.json, tools/ncu_summary.py)."""
@@ -400,6 +460,9 @@ def run_ours(args):
             "ms_per_step_profiled_eager": prof_ms / args.steps, "clocks": clk}
     if rank == 0 and world == 1 and not args.no_pint:
         line["pint_cfg2"] = pint_cfg2(torch)
+    if rank == 0 and world == 1 and not args.no_extra:
+        line["sht_cfg4"] = sht_cfg4(torch)
+        line["fine_cfg5"] = fine_cfg5(torch)
     if rank == 0 and world == 1 and not args.no_cpu:
         nproc = min(cpu_cores(), 16)
         el, done = cpu_steps(1, nproc)
@@ -422,6 +485,7 @@ def main():
     ap.add_argument("--slices", type=int, default=SLICES_PER_GPU)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-pint", action="store_true", help="skip the cfg2 MGRIT leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg4 / cfg5 (M=1024) legs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
