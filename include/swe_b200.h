@@ -146,8 +146,12 @@ int swe_profile(int enable);
  * "leg_path": 0 auto, 1 small-batch Legendre kernels, 2 / 3 wide-tile kernels
  * with 128 / 64 columns per CTA, 4 warp-specialised persistent kernels.
  * "fast_coriolis": 2 (default) spectral three-term recurrence, 1 FFT-free
- * Legendre pair, 0 pseudospectral FFT round trip.  Results agree to roundoff
- * on every path (within 1e-12 relative between the fast_coriolis modes). */
+ * Legendre pair, 0 pseudospectral FFT round trip.  "graphs": 1 (default)
+ * replay one CUDA graph per IMEX step.  "helm_tiled", "cn_small", "cn_cluster":
+ * 1 / 0 enable / disable the tiled fixed-point kernel, the one-CTA-per-slice half
+ * step (K <= 2800) and the one-cluster-per-slice half step (K up to ~38k modes;
+ * default 0, the other two default 1).  Results agree to roundoff on every path (bitwise between the
+ * half-step paths; within 1e-12 relative between the fast_coriolis modes). */
 int swe_set_option(const char *key, int value);
 int swe_profile_read(double *ms_out, double *work_out, long long *count_out);
 const char *swe_last_error(void);

@@ -62,6 +62,13 @@ int cn_small(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              int rhs_given, Ptr3 R, Ptr3 dst, int max_iter, double tol, double dtnu,
              double halfq, int *iters, int *flags, int *counter, double *resid, int *fail,
              cudaStream_t st);
+// the same for K up to ~38k modes (the fine level M = 256): one thread-block
+// cluster per slice; cn_cluster_size(M) = CTAs per cluster, 0 when not applicable
+int cn_cluster_size(int M);
+int cn_cluster(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+               const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
+               int rhs_given, Ptr3 dst, int max_iter, double tol, double dtnu, double halfq,
+               int *iters, int *flags, int *counter, double *resid, int *fail, cudaStream_t st);
 int add_col(int K, int n, int col, Ptr3 y, Ptr3C g, cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,

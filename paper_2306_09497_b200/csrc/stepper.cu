@@ -40,6 +40,8 @@ bool g_capturing = false;  // a step graph is being captured: no events, no host
 int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
+int g_cn_cluster = 0;      // one-launch CN half step, one thread-block cluster per slice
+                           // (correct, but latency-bound at M = 256: off by default)
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
 int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
 // Coriolis operator (eval_coriolis): 2 spectral three-term recurrence, fused into the
@@ -544,8 +546,10 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
   Work &w = pl->ws;
   int rc;
   const CorOp cor{nullptr, nullptr, impl ? pl->cor_nb : nullptr, impl ? pl->cor_cf : nullptr};
-  if (g_cn_small && cn_small_ok(K)) {
-    // coarse levels: the whole half step in one launch, one CTA per slice
+  const bool small = g_cn_small && cn_small_ok(K);
+  if (small || (g_cn_cluster && cn_cluster_size(pl->M))) {
+    // the whole half step in one launch: one CTA per slice (coarse levels) or one
+    // thread-block cluster per slice (the fine level)
     Ptr3C X0 = {{nullptr, nullptr, nullptr}}, X1 = X0, X2 = X0;
     if (rhs_given) {
       X0 = {{b.R[0], b.R[1], b.R[2]}};
@@ -560,11 +564,17 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     SWE_CUDA(cudaMemsetAsync(w.counter, 0, sizeof(int), r.st));
     {
       ProfScope ps(3, (x1 ? 12.0 : 6.0) * 16.0 * K * B, r.st);
-      if ((rc = cn_small(K, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, cor.nb, cor.cf,
-                         rhs_given ? 1 : 0, R, D, cfg.implicit_max_iter, cfg.implicit_tol, dtnu,
-                         cfg.visc_order / 2.0, w.iters, w.flags, w.counter, w.stats,
-                         r.graph ? w.d_fail : nullptr, r.st)))
-        return rc;
+      if (small)
+        rc = cn_small(K, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, cor.nb, cor.cf,
+                      rhs_given ? 1 : 0, R, D, cfg.implicit_max_iter, cfg.implicit_tol, dtnu,
+                      cfg.visc_order / 2.0, w.iters, w.flags, w.counter, w.stats,
+                      r.graph ? w.d_fail : nullptr, r.st);
+      else
+        rc = cn_cluster(pl->M, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, cor.nb, cor.cf,
+                        rhs_given ? 1 : 0, D, cfg.implicit_max_iter, cfg.implicit_tol, dtnu,
+                        cfg.visc_order / 2.0, w.iters, w.flags, w.counter, w.stats,
+                        r.graph ? w.d_fail : nullptr, r.st);
+      if (rc) return rc;
     }
     if (r.graph) return OK;
     if ((rc = publish(B, w.counter, w.iters, w.d_pub, r.st))) return rc;
@@ -886,7 +896,7 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
-         (g_helm_tiled << 13);
+         (g_helm_tiled << 13) | (g_cn_cluster << 14);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1334,6 +1344,10 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "cn_small") == 0 && (value == 0 || value == 1)) {
     g_cn_small = value;
+    return OK;
+  }
+  if (key && strcmp(key, "cn_cluster") == 0 && (value == 0 || value == 1)) {
+    g_cn_cluster = value;
     return OK;
   }
   if (key && strcmp(key, "helm_tiled") == 0 && (value == 0 || value == 1)) {

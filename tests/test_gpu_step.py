@@ -368,3 +368,55 @@ def test_tiled_fixed_point_matches_untiled(mods):
     assert np.array_equal(its[0], its[1])
     for b in range(B):
         assert rel_diff(outs[1][b], outs[0][b]) < 1e-13, b
+
+
+@pytest.mark.parametrize("M,B", [(100, 3), (256, 3), (256, 40)])
+@pytest.mark.parametrize("graphs", [0, 1])
+def test_cluster_half_step_matches_multikernel(mods, M, B, graphs):
+    """The one-cluster-per-slice Crank-Nicolson half step (whole fixed point in
+    distributed shared memory) gives the multi-kernel path's iteration counts and
+    states (M = 100: 3-CTA clusters, M = 256: 16-CTA clusters)."""
+    spharm, dynamics, steppers, scenarios = mods
+    import torch
+    from paper_2306_09497_b200 import _lib
+    grid = spharm.get_grid(M)
+    cfg = steppers.StepperConfig(dt=240.0, viscosity=dynamics.ViscositySpec(2, 1e5))
+    base = scenarios.gaussian_bumps(grid, batch=B)
+    rng = np.random.default_rng(M + B)
+    taper = torch.from_numpy((grid.n_of + 1.0) ** -2).cuda()
+    noise = torch.from_numpy(rng.standard_normal((B, grid.n_modes))).cuda() * taper
+    noise[:, : M + 1] = noise[:, : M + 1].real
+    base.data[:, 1] += 1e-6 * noise
+    base.data[:, 2] += 1e-7 * noise
+    outs, its = {}, {}
+    _lib.set_option("graphs", graphs)
+    try:
+        for cl in (0, 1):
+            _lib.set_option("cn_cluster", cl)
+            s = base.copy()
+            it = np.zeros((3, B, 2), dtype=np.int32)
+            steppers.imex_steps_inplace(s, cfg, 3, None if graphs else it)
+            outs[cl], its[cl] = s.data.cpu().numpy(), it
+    finally:
+        _lib.set_option("cn_cluster", 0)
+        _lib.set_option("graphs", 1)
+    assert np.array_equal(its[0], its[1])
+    for b in range(B):
+        assert rel_diff(outs[1][b], outs[0][b]) < 1e-13, b
+
+
+def test_cluster_half_step_nonconvergence_raises(mods):
+    """An unconverged fixed point on the cluster path raises ImplicitSolveError
+    with the residual (eager and under graphs)."""
+    spharm, dynamics, steppers, scenarios = mods
+    from paper_2306_09497_b200 import _lib
+    grid = spharm.get_grid(256)
+    s = scenarios.gaussian_bumps(grid, batch=2)
+    cfg = steppers.StepperConfig(dt=600.0, implicit_max_iter=1)
+    _lib.set_option("cn_cluster", 1)
+    try:
+        for _ in range(3):
+            with pytest.raises(steppers.ImplicitSolveError, match="residual"):
+                steppers.imex_step(s, cfg)
+    finally:
+        _lib.set_option("cn_cluster", 0)
