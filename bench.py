@@ -275,6 +275,40 @@ def fine_cfg5(torch, slices=64, steps=5):
                       "(64 per GPU at 8 GPUs)"}
 
 
+def direct_leg(torch, steppers, cfg, state, steps, flush):
+    """Same workload with StepperConfig.implicit_solver="direct" (per-m tridiagonal
+    solve of the CN implicit system instead of the reference's fixed point,
+    SURVEY.md §8f row 4): device-timed like the main leg, plus its max relative
+    difference from the fixed-point step on the same input (Phi' and xi/delta)."""
+    import dataclasses
+    cfg_d = dataclasses.replace(cfg, implicit_solver="direct")
+    st = state.copy()
+    for _ in range(3):
+        steppers.imex_steps_inplace(st, cfg_d, 1)
+    torch.cuda.synchronize()
+    total = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record()
+        steppers.imex_steps_inplace(st, cfg_d, 1)
+        e_ev.record()
+        e_ev.synchronize()
+        total += s_ev.elapsed_time(e_ev)
+    a, d = state.copy(), state.copy()
+    steppers.imex_steps_inplace(a, cfg, 1)
+    steppers.imex_steps_inplace(d, cfg_d, 1)
+    x, y = a.data.clone(), d.data.clone()
+    x[:, 0, 0] = 0.0   # Phi': the mean mode dominates Phi
+    y[:, 0, 0] = 0.0
+    rel = float(((x - y).abs().amax(dim=-1) / x.abs().amax(dim=-1)).max())
+    B = state.batch
+    return {"value": B * steps / (total * 1e-3), "unit": "fine slice-steps/s",
+            "ms_per_step": total / steps, "max_rel_diff_vs_fixed_point": rel,
+            "note": "opt-in solver (implicit_solver='direct'); the headline value uses the "
+                    "reference's fixed point"}
+
+
 def ncu_traffic():
     """DRAM bytes per launch of the dominant kernels from the newest committed
     `ncu --set full` capture (profiles/*_kernels.json, tools/ncu_summary.py)."""
@@ -381,6 +415,8 @@ def run_ours(args):
     total_ms = float(t[0])
     value = world * B * args.steps / (total_ms * 1e-3)
 
+    direct = direct_leg(torch, steppers, cfg, state, args.steps, flush) if not args.no_extra else None
+
     # e2e through the public API with pinned host buffers: every step copies its
     # batch in (H2D) and its result out (D2H); steppers.HostPipeline overlaps the
     # copies of neighbouring steps with the compute of the current one
@@ -460,6 +496,8 @@ def run_ours(args):
             "ms_per_step_profiled_eager": prof_ms / args.steps, "clocks": clk}
     if rank == 0 and world == 1 and not args.no_pint:
         line["pint_cfg2"] = pint_cfg2(torch)
+    if direct is not None:
+        line["direct_solve"] = direct
     if rank == 0 and world == 1 and not args.no_extra:
         line["sht_cfg4"] = sht_cfg4(torch)
         line["fine_cfg5"] = fine_cfg5(torch)

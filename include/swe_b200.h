@@ -46,6 +46,9 @@ typedef struct {
   int include_nonlinear;   /* 1 (default) */
   double implicit_tol;     /* 1e-12 */
   int implicit_max_iter;   /* 200 */
+  int implicit_solver;     /* 0: the reference fixed point (default); 1: direct per-m
+                              tridiagonal solve of the same system,
+                              no iterations (iters_out = 0), never SWE_ENOCONV */
 } swe_stepper_cfg;
 
 /* SphereGrid(Truncation.for_wavenumber(M), SphereGeometry(a, omega, g))

@@ -31,7 +31,7 @@ class StepperCfgC(ctypes.Structure):
     _fields_ = [("dt", ctypes.c_double), ("visc_order", ctypes.c_int),
                 ("visc_nu", ctypes.c_double), ("coriolis_implicit", ctypes.c_int),
                 ("include_nonlinear", ctypes.c_int), ("implicit_tol", ctypes.c_double),
-                ("implicit_max_iter", ctypes.c_int)]
+                ("implicit_max_iter", ctypes.c_int), ("implicit_solver", ctypes.c_int)]
 
 
 class NoConvergence(RuntimeError):

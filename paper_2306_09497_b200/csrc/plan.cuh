@@ -44,7 +44,7 @@ struct Work {
   double *phibar = nullptr; // [cap]
 };
 
-constexpr int NSPEC = 25;  // 21-23: input backup of a graph-mode call
+constexpr int NSPEC = 30;  // 21-23: input backup of a graph-mode call
 constexpr int NHALF = 7;
 constexpr int NF = 4;
 
@@ -87,7 +87,7 @@ struct swe_plan {
   struct StepGraph {
     int B;
     double dt, nu, tol;
-    int order, cor_impl, nonlin, max_iter, opts;
+    int order, cor_impl, nonlin, max_iter, opts, solver;
     cudaGraph_t graph;
     cudaGraphExec_t exec;
   };

@@ -1089,6 +1089,193 @@ int cn_cluster(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alph
   return OK;
 }
 
+// Direct solve of the Crank-Nicolson implicit system (I - a (L_G + L_C)) U = R,
+// SURVEY.md §8f row 4 (the reference iterates it to tol, steppers.py:74-118; the
+// converged iterate and this solution agree to ~tol).  Eliminating
+// Phi = r0 - a Pb delta leaves, per order m and slice, two decoupled complex
+// tridiagonal chains in n: xi_n couples to delta_{n-+1} and delta_n to xi_{n-+1}, so
+// chain c = 0 holds xi at even n-m and delta at odd n-m, chain 1 the others:
+//   xi_n:    (1 - i a cz_n) xi_n + a cx_n d_{n-1} + a cy_n d_{n+1} = r1_n
+//   delta_n: (1 + a^2 Pb eps_n - i a cz_n) d_n - a cx_n x_{n-1} - a cy_n x_{n+1}
+//            = r2_n + a eps_n r0_n
+// (cx, cy, cz = plan.cu cor_cf).  m = 0 keeps real parts only in L_C, so there the
+// imaginary parts decouple.  Thomas elimination, one thread per (m, chain, slice),
+// slices fastest (coalesced rows of the [K][B] layout), longest chains (m = 0)
+// first.  Forward pass: R from X = x0 + s (x1 + x2) on the fly (or R = X), the
+// modified coefficients c'_j, d'_j and r0 to scratch; backward pass (a second
+// launch, since dst may alias x0): back substitution, Phi, viscosity -> dst.
+// The chains are diagonally dominant for the CN step sizes (|a cx|, |a cy| << 1).
+SWE_DEV int cd_row(int M, int m, int n) {
+  const int d = n - m, ne = (M + 2 - m) / 2, off = m * (M + 1) - m * (m - 1) / 2;
+  return off + ((d & 1) ? ne + (d >> 1) : (d >> 1));
+}
+SWE_DEV double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+SWE_DEV double2 cdiv(double2 a, double2 b) {
+  const double inv = 1.0 / (b.x * b.x + b.y * b.y);
+  return make_double2((a.x * b.x + a.y * b.y) * inv, (a.y * b.x - a.x * b.y) * inv);
+}
+
+// pass 1 (one thread per mode and slice, fully parallel): the right-hand sides of
+// both chain rows of mode k -- the xi row r1 and the delta row r2 + a eps r0 -- and
+// r0, from X = x0 + s (x1 + x2) (or R = X given)
+__global__ void __launch_bounds__(256) k_cn_direct_rhs(int K, int B, Ptr3C x0, Ptr3C x1,
+                                                       Ptr3C x2, double s, double alpha,
+                                                       const double *eps, const double *phibar,
+                                                       const int2 *nbt, const double4 *cft,
+                                                       int rhs_given, Ptr3 sc) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
+    auto at = [&](int kk) { return (size_t)kk * B + b; };
+    const double a = alpha, e = eps[k], pb = phibar[b];
+    const double2 ph = comb(x0, x1, x2, s, 0, _i), xi = comb(x0, x1, x2, s, 1, _i),
+                  de = comb(x0, x1, x2, s, 2, _i);
+    double2 r0, r1, r2;
+    if (rhs_given) {
+      r0 = ph;
+      r1 = xi;
+      r2 = de;
+    } else {
+      const int2 nb = nbt[k];
+      const double4 cf = cft[k];
+      double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
+      if (nb.x >= 0) {
+        xl = comb(x0, x1, x2, s, 1, at(nb.x));
+        dl = comb(x0, x1, x2, s, 2, at(nb.x));
+      }
+      if (nb.y >= 0) {
+        xh = comb(x0, x1, x2, s, 1, at(nb.y));
+        dh = comb(x0, x1, x2, s, 2, at(nb.y));
+      }
+      double2 lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * xi.y),
+                                -(cf.x * dl.y + cf.y * dh.y - cf.z * xi.x));
+      double2 lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * de.y,
+                                cf.x * xl.y + cf.y * xh.y + cf.z * de.x);
+      if (cf.w != 0.0) {
+        lx.y = 0.0;
+        lc.y = 0.0;
+      }
+      r0 = add2(ph, sc2(a, make_double2(-pb * de.x, -pb * de.y)));
+      r1 = add2(xi, sc2(a, lx));
+      r2 = add2(de, sc2(a, add2(sc2(e, ph), lc)));
+    }
+    st2(sc.p[0], _i, r0);
+    st2(sc.p[1], _i, r1);
+    st2(sc.p[2], _i, add2(r2, sc2(a * e, r0)));
+  }
+}
+
+// pass 2: Thomas elimination and back substitution of one chain (m, c) of slice b.
+// The chain's inputs are independent of the recurrence, so they are fetched CD_U
+// rows at a time ahead of the dependent arithmetic (latency, not bandwidth, bounds
+// a 257-row chain).  d' overwrites d in place, c' goes to cp[f]; dst may alias the
+// step input (pass 1 has consumed it).
+constexpr int CD_U = 8;
+__global__ void __launch_bounds__(128) k_cn_direct_chain(
+    int M, int B, double alpha, const double *__restrict__ eps, const double *__restrict__ phibar,
+    const double4 *__restrict__ cft, const double *__restrict__ r0s, double *__restrict__ dxs,
+    double *__restrict__ dds, double *__restrict__ cpx, double *__restrict__ cpd, Ptr3 dst,
+    double dtnu, double halfq) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (M + 1) * 2 * B) return;
+  const int b = t % B, q = t / B, c = q & 1, m = q >> 1;
+  const double a = alpha, aap = alpha * alpha * phibar[b], apb = alpha * phibar[b];
+  auto at = [&](int k) { return (size_t)k * B + b; };
+  double2 cprev = make_double2(0.0, 0.0), dprev = cprev;
+  for (int n0 = m; n0 <= M; n0 += CD_U) {
+    double2 dv[CD_U];
+    double4 cfv[CD_U];
+    double ev[CD_U];
+#pragma unroll
+    for (int u = 0; u < CD_U; ++u) {
+      const int n = n0 + u;
+      if (n > M) break;
+      const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
+      dv[u] = __ldg(reinterpret_cast<const double2 *>(f ? dds : dxs) + at(k));
+      cfv[u] = cft[k];
+      ev[u] = __ldg(eps + k);
+    }
+#pragma unroll
+    for (int u = 0; u < CD_U; ++u) {
+      const int n = n0 + u;
+      if (n > M) break;
+      const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
+      const double4 cf = cfv[u];
+      const double2 d = dv[u];
+      // row coefficients: xi rows (f = 0) / delta rows (f = 1)
+      const double sg = f ? -a : a;
+      const double ax = sg * cf.x, cy = sg * cf.y;
+      const double2 bb = make_double2(f ? 1.0 + aap * ev[u] : 1.0, -a * cf.z);
+      double2 cj, dj;
+      if (m == 0) {  // real coefficients; imaginary parts decoupled (no L_C at m = 0)
+        const double den = bb.x - ax * cprev.x;
+        cj = make_double2(cy / den, 0.0);
+        dj = make_double2((d.x - ax * dprev.x) / den, d.y / bb.x);
+      } else {
+        const double2 den = make_double2(bb.x - ax * cprev.x, bb.y - ax * cprev.y);
+        cj = cdiv(make_double2(cy, 0.0), den);
+        dj = cdiv(make_double2(d.x - ax * dprev.x, d.y - ax * dprev.y), den);
+      }
+      reinterpret_cast<double2 *>(f ? cpd : cpx)[at(k)] = cj;
+      reinterpret_cast<double2 *>(f ? dds : dxs)[at(k)] = dj;
+      cprev = cj;
+      dprev = dj;
+    }
+  }
+  // back substitution u_j = d'_j - c'_j u_{j+1}, Phi = r0 - a Pb delta, viscosity
+  double2 uu = make_double2(0.0, 0.0);
+  for (int n0 = M; n0 >= m; n0 -= CD_U) {
+    double2 cv[CD_U], dv[CD_U], rv[CD_U];
+    double ev[CD_U];
+#pragma unroll
+    for (int u = 0; u < CD_U; ++u) {
+      const int n = n0 - u;
+      if (n < m) break;
+      const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
+      cv[u] = reinterpret_cast<const double2 *>(f ? cpd : cpx)[at(k)];
+      dv[u] = reinterpret_cast<const double2 *>(f ? dds : dxs)[at(k)];
+      rv[u] = f ? __ldg(reinterpret_cast<const double2 *>(r0s) + at(k)) : make_double2(0.0, 0.0);
+      ev[u] = __ldg(eps + k);
+    }
+#pragma unroll
+    for (int u = 0; u < CD_U; ++u) {
+      const int n = n0 - u;
+      if (n < m) break;
+      const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
+      const double2 cj = cv[u], dj = dv[u];
+      if (m == 0)
+        uu = make_double2(dj.x - cj.x * uu.x, dj.y);
+      else
+        uu = make_double2(dj.x - (cj.x * uu.x - cj.y * uu.y), dj.y - (cj.x * uu.y + cj.y * uu.x));
+      double bh = 1.0;
+      if (dtnu != 0.0) bh = 1.0 / (1.0 + dtnu * pow(ev[u], halfq));
+      st2(dst.p[f ? 2 : 1], at(k), dtnu != 0.0 ? sc2(bh, uu) : uu);
+      if (f) {
+        const double2 ph = make_double2(rv[u].x - apb * uu.x, rv[u].y - apb * uu.y);
+        st2(dst.p[0], at(k), dtnu != 0.0 ? sc2(bh, ph) : ph);
+      }
+    }
+  }
+}
+
+int cn_direct(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+              const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
+              int rhs_given, double *const scratch[5], Ptr3 dst, double dtnu, double halfq,
+              cudaStream_t st) {
+  const int K = (M + 1) * (M + 2) / 2;
+  Ptr3 sc = {{scratch[0], scratch[1], scratch[2]}};
+  k_cn_direct_rhs<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, x0, x1, x2, s, alpha, eps, phibar, nb, cf,
+                                                 rhs_given, sc);
+  SWE_LAUNCH_CHECK();
+  const int n = (M + 1) * 2 * B, nt = 128;
+  k_cn_direct_chain<<<(n + nt - 1) / nt, nt, 0, st>>>(M, B, alpha, eps, phibar, cf, scratch[0],
+                                                      scratch[1], scratch[2], scratch[3],
+                                                      scratch[4], dst, dtnu, halfq);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
 // Fixed-point epilogue: slices whose iterate ended in the B buffers (odd iteration
 // count) copy xi/delta back to A = u[1], u[2]; with dtnu != 0 the viscosity
 // factor (dynamics.py:191-200) is applied to every slice on the way.

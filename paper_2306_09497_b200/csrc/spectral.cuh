@@ -69,6 +69,12 @@ int cn_cluster(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alph
                const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
                int rhs_given, Ptr3 dst, int max_iter, double tol, double dtnu, double halfq,
                int *iters, int *flags, int *counter, double *resid, int *fail, cudaStream_t st);
+// direct (block-tridiagonal) solve of the same implicit system instead of the fixed
+// point (StepperConfig.implicit_solver = "direct"); scratch = 5 spectral arrays
+int cn_direct(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+              const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
+              int rhs_given, double *const scratch[5], Ptr3 dst, double dtnu, double halfq,
+              cudaStream_t st);
 int add_col(int K, int n, int col, Ptr3 y, Ptr3C g, cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,

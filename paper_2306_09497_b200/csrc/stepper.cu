@@ -546,6 +546,31 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
   Work &w = pl->ws;
   int rc;
   const CorOp cor{nullptr, nullptr, impl ? pl->cor_nb : nullptr, impl ? pl->cor_cf : nullptr};
+  if (impl && cfg.implicit_solver == 1) {
+    // direct per-m tridiagonal solve of the implicit system (no fixed-point loop)
+    Ptr3C X0 = {{b.R[0], b.R[1], b.R[2]}}, X1 = {{nullptr, nullptr, nullptr}}, X2 = X1;
+    if (!rhs_given) {
+      X0 = {{x0[0], x0[1], x0[2]}};
+      if (x1) {
+        X1 = {{x1[0], x1[1], x1[2]}};
+        X2 = {{x2[0], x2[1], x2[2]}};
+      }
+    }
+    double *const scr[5] = {r.spec(25), r.spec(26), r.spec(27), r.spec(28), r.spec(29)};
+    Ptr3 D = {{dst[0], dst[1], dst[2]}};
+    {
+      ProfScope ps(3, (x1 ? 9.0 : 3.0) * 16.0 * K * B + 13.0 * 16.0 * K * B, r.st);
+      if ((rc = cn_direct(pl->M, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, pl->cor_nb,
+                          pl->cor_cf, rhs_given ? 1 : 0, scr, D, dtnu, cfg.visc_order / 2.0,
+                          r.st)))
+        return rc;
+    }
+    if (iters_host)
+      for (int i = 0; i < B; ++i) iters_host[2 * i] = 0;
+    if (resid_host)
+      for (int i = 0; i < B; ++i) resid_host[i] = 0.0;
+    return OK;
+  }
   const bool small = g_cn_small && cn_small_ok(K);
   if (small || (g_cn_cluster && cn_cluster_size(pl->M))) {
     // the whole half step in one launch: one CTA per slice (coarse levels) or one
@@ -912,7 +937,7 @@ int step_graph(const Run &r, const swe_stepper_cfg &cfg, cudaGraphExec_t *exec) 
     if (g.B == r.B && g.dt == cfg.dt && g.nu == cfg.visc_nu && g.tol == cfg.implicit_tol &&
         g.order == cfg.visc_order && g.cor_impl == cfg.coriolis_implicit &&
         g.nonlin == cfg.include_nonlinear && g.max_iter == cfg.implicit_max_iter &&
-        g.opts == opts) {
+        g.opts == opts && g.solver == cfg.implicit_solver) {
       if (!g.exec) {  // seen once: capture now
         Run rr = r;
         for (auto &c : pl->cap)
@@ -948,6 +973,7 @@ int step_graph(const Run &r, const swe_stepper_cfg &cfg, cudaGraphExec_t *exec) 
   g.nonlin = cfg.include_nonlinear;
   g.max_iter = cfg.implicit_max_iter;
   g.opts = opts;
+  g.solver = cfg.implicit_solver;
   g.graph = nullptr;
   g.exec = nullptr;
   pl->graphs.push_back(g);

@@ -45,6 +45,11 @@ class StepperConfig:
     include_nonlinear: bool = True
     implicit_tol: float = 1e-12
     implicit_max_iter: int = 200
+    # "fixed_point": the reference's iteration (steppers.py:74-118, iteration counts
+    # and ImplicitSolveError as there); "direct": the same implicit system solved
+    # exactly per order m, agreeing with the converged iterate
+    # to ~implicit_tol; GPU-only extension
+    implicit_solver: str = "fixed_point"
 
     def __post_init__(self):
         if self.dt <= 0:
@@ -55,12 +60,15 @@ class StepperConfig:
             raise ValueError(f"unknown SETTLS mode {self.settls_mode!r}")
         if self.coriolis_treatment not in ("implicit", "explicit"):
             raise ValueError("coriolis_treatment must be implicit or explicit")
+        if self.implicit_solver not in ("fixed_point", "direct"):
+            raise ValueError("implicit_solver must be fixed_point or direct")
 
     def to_c(self) -> _lib.StepperCfgC:
         return _lib.StepperCfgC(self.dt, self.viscosity.order_q, self.viscosity.coeff_nu,
                                 1 if self.coriolis_treatment == "implicit" else 0,
                                 1 if self.include_nonlinear else 0, self.implicit_tol,
-                                self.implicit_max_iter)
+                                self.implicit_max_iter,
+                                1 if self.implicit_solver == "direct" else 0)
 
 
 @dataclasses.dataclass

@@ -222,3 +222,16 @@ def test_two_rank_gloo_bitwise(name, factors, c):
         assert p.exitcode == 0
     for r in range(2):
         assert np.array_equal(out[r][0], ref), (name, r)
+
+
+def test_stepper_config_implicit_solver():
+    """StepperConfig keeps the reference fields and defaults; the GPU-only
+    implicit_solver extension defaults to the reference fixed point and is
+    validated and passed through the C struct."""
+    from paper_2306_09497_b200 import steppers
+    c = steppers.StepperConfig()
+    assert c.implicit_solver == "fixed_point" and c.implicit_max_iter == 200
+    assert c.to_c().implicit_solver == 0
+    assert steppers.StepperConfig(implicit_solver="direct").to_c().implicit_solver == 1
+    with pytest.raises(ValueError):
+        steppers.StepperConfig(implicit_solver="lu")

@@ -420,3 +420,90 @@ def test_cluster_half_step_nonconvergence_raises(mods):
                 steppers.imex_step(s, cfg)
     finally:
         _lib.set_option("cn_cluster", 0)
+
+
+@pytest.mark.parametrize("M,B,dt", [(32, 6, 240.0), (51, 40, 960.0), (256, 3, 60.0), (256, 64, 60.0)])
+def test_direct_implicit_solve_matches_fixed_point(mods, M, B, dt):
+    """implicit_solver="direct" (per-m tridiagonal solve of (I - a L) U = R, SURVEY.md
+    §8f row 4) agrees with the reference fixed point converged to tol = 1e-12."""
+    spharm, dynamics, steppers, scenarios = mods
+    import dataclasses
+    import torch
+    grid = spharm.get_grid(M)
+    cfg = steppers.StepperConfig(dt=dt, viscosity=dynamics.ViscositySpec(2, 1e5))
+    base = scenarios.gaussian_bumps(grid, batch=B)
+    rng = np.random.default_rng(M + B)
+    taper = torch.from_numpy((grid.n_of + 1.0) ** -2).cuda()
+    noise = torch.from_numpy(rng.standard_normal((B, grid.n_modes))
+                             + 1j * rng.standard_normal((B, grid.n_modes))).cuda() * taper
+    noise[:, : M + 1] = noise[:, : M + 1].real
+    base.data[:, 1] += 1e-6 * noise
+    base.data[:, 2] += 1e-7 * noise
+    out = {}
+    for solver in ("fixed_point", "direct"):
+        s = base.copy()
+        it = np.zeros((4, B, 2), dtype=np.int32)
+        steppers.imex_steps_inplace(s, dataclasses.replace(cfg, implicit_solver=solver), 4, it)
+        out[solver] = (s.data.cpu().numpy(), it)
+    a, ia = out["fixed_point"]
+    d, idd = out["direct"]
+    assert (ia > 0).all() and (idd == 0).all()
+    for b in range(B):
+        for f in range(3):
+            ref = a[b, f] - (a[b, f, 0] if f == 0 else 0.0)   # Phi': the mean mode dominates Phi
+            got = d[b, f] - (d[b, f, 0] if f == 0 else 0.0)
+            assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max(), (b, f)
+
+
+def test_direct_implicit_solve_matches_oracle(mods):
+    """The direct solve against the oracle's fixed-point step (6 slices at different
+    perturbation levels, the per-slice oracle check of the batched step)."""
+    spharm, dynamics, steppers, _ = mods
+    from oracle.sht import OracleSphere
+    from oracle.swe import StepCfg, imex_step, gaussian_bumps, OracleState
+    M = 32
+    sph = OracleSphere(M)
+    rng = np.random.default_rng(5)
+    base = gaussian_bumps(sph)
+    states = []
+    for b in range(6):
+        s = base.copy()
+        noise = (rng.standard_normal(sph.n_modes) + 1j * rng.standard_normal(sph.n_modes))
+        noise[: M + 1] = noise[: M + 1].real
+        noise *= (sph.n_of + 1.0) ** -3
+        s.xi = s.xi + 1e-6 * 10.0 ** (b - 3) * noise[None]
+        s.delta = s.delta + 1e-7 * 10.0 ** (b - 3) * noise[None]
+        states.append(s)
+    ob = OracleState.stack(states)
+    ref = imex_step(ob, StepCfg(dt=240.0, visc_nu=1e5), [])
+    grid = spharm.get_grid(M)
+    gs = dynamics.PrognosticState.from_fields(grid, ob.phi, ob.xi, ob.delta, ob.phibar)
+    cfg = steppers.StepperConfig(dt=240.0, viscosity=dynamics.ViscositySpec(2, 1e5),
+                                 implicit_solver="direct")
+    steppers.imex_steps_inplace(gs, cfg, 1)
+    phi, xi, de, _ = gs.to_numpy()
+    for b in range(6):
+        got = np.stack([phi[b], xi[b], de[b]])
+        want = np.stack([ref.phi[b], ref.xi[b], ref.delta[b]])
+        assert rel_diff(got, want) < 1e-10, b
+
+
+def test_direct_implicit_solve_settls(mods):
+    """The SETTLS implicit solve (given right-hand side) through the direct solver."""
+    spharm, dynamics, steppers, scenarios = mods
+    import dataclasses
+    grid = spharm.get_grid(51)
+    cfg = steppers.StepperConfig(scheme=steppers.SL_SI_SETTLS, dt=960.0,
+                                 viscosity=dynamics.ViscositySpec(2, 1e5))
+    s0 = scenarios.gaussian_bumps(grid, batch=2)
+    out = {}
+    for solver in ("fixed_point", "direct"):
+        st = steppers.StepperState(s0.copy())
+        for _ in range(3):
+            st = steppers.advance(st, dataclasses.replace(cfg, implicit_solver=solver))
+        out[solver] = st.current.data.cpu().numpy()
+    a, d = out["fixed_point"], out["direct"]
+    for f in range(3):
+        ref = a[:, f] - (a[:, f, :1] if f == 0 else 0.0)
+        got = d[:, f] - (d[:, f, :1] if f == 0 else 0.0)
+        assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max(), f
