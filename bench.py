@@ -314,7 +314,7 @@ def ncu_traffic():
     `ncu --set full` capture (profiles/*_kernels.json, tools/ncu_summary.py)."""
     import glob
     files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
-                                          "profiles", "*_kernels.json")), key=os.path.getmtime)
+                                          "profiles", "r*_kernels.json")))  # round tags sort
     if not files:
         return {}
     try:
@@ -328,7 +328,9 @@ def ncu_traffic():
         return ((r.get("dram__bytes_read.sum") or 0) + (r.get("dram__bytes_write.sum") or 0)) * u
 
     leg = [dram(r) for r in recs if r["kernel"].startswith(("leg_synth_v3", "leg_anal_v3"))]
-    fft = [dram(r) for r in recs if "fft_lanes_kernel" in r["kernel"]]
+    # the bench configuration's FFT kernel (16-row lanes; M=1024 captures use 8 rows)
+    fft = [dram(r) for r in recs
+           if "fft_lanes_kernel" in r["kernel"] and ", 8," not in r["kernel"]]
     out = {"source": "profiles/" + os.path.basename(files[-1])}
     if leg:
         out["legendre"] = sum(leg) / len(leg)
