@@ -513,6 +513,7 @@ __global__ void __launch_bounds__(CS_NT) k_cn_small(int K, int B, Ptr3C x0, Ptr3
   extern __shared__ double2 csm[];  // [Phi][xi A][xi B][de A][de B], K each
   double2 *P = csm, *XA = csm + K, *XB = csm + 2 * K, *DA = csm + 3 * K, *DB = csm + 4 * K;
   __shared__ unsigned long long red[33];
+  __shared__ unsigned long long red6[6][CS_NT / 32];
   __shared__ int sdone;
   const int b = blockIdx.x;
   const bool cor = nbt != nullptr;
@@ -616,12 +617,22 @@ __global__ void __launch_bounds__(CS_NT) k_cn_small(int K, int B, Ptr3C x0, Ptr3
       nx[k] = rx;
       nd[k] = de;
     }
-    double st[6];
+    // the 6 block maxima in one pass: warp shuffles, one staging barrier, warp 0
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int q = 0; q < 6; ++q) st[q] = __longlong_as_double((long long)blk_max_u64(mx[q], red));
-    if (threadIdx.x == 0) {
+    for (int q = 0; q < 6; ++q) {
+      for (int o = 16; o > 0; o >>= 1) mx[q] = max(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], o));
+      if (lane == 0) red6[q][warp] = mx[q];
+    }
+    __syncthreads();
+    if (warp == 0) {
       double v[6];
-      for (int q = 0; q < 6; ++q) v[q] = sqrt(st[q]);  // as decide_slice
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        unsigned long long x = lane < (int)(blockDim.x >> 5) ? red6[q][lane] : 0ULL;
+        for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+        v[q] = sqrt(__longlong_as_double((long long)x));  // as decide_slice
+      }
       double overall = fmax(fmax(v[0], v[1]), v[2]);
       if (isnan(v[0]) || isnan(v[1]) || isnan(v[2])) overall = nan("");
       overall = (overall > 1e-300 || isnan(overall)) ? overall : 1e-300;
@@ -631,7 +642,7 @@ __global__ void __launch_bounds__(CS_NT) k_cn_small(int K, int B, Ptr3C x0, Ptr3
         const double scale = (v[f] >= tiny || isnan(v[f])) ? v[f] : tiny;
         if (v[3 + f] > tol * scale) ok = false;
       }
-      sdone = ok;
+      if (lane == 0) sdone = ok;
     }
     __syncthreads();
     done = sdone;
