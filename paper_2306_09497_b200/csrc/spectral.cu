@@ -1177,72 +1177,137 @@ __global__ void __launch_bounds__(256) k_cn_direct_rhs(int K, int B, Ptr3C x0, P
   }
 }
 
-// pass 2: Thomas elimination and back substitution of one chain (m, c) of slice b.
+// pass 2: one chain (m, c) of slice b solved from both ends at once ("twisted"
+// factorization): lane l < 16 of a warp eliminates rows 0..p-1 downwards
+// (u_j = d'_j - c'_j u_{j+1}), lane l + 16 rows L-1..p+1 upwards
+// (u_j = e'_j - a'_j u_{j-1}) for the same slice; they meet at the middle row p
+// through a shuffle, then back-substitute outwards.  Half the sequential depth of a
+// one-sided Thomas sweep (the chains are latency-bound: up to 257 dependent rows).
 // The chain's inputs are independent of the recurrence, so they are fetched CD_U
-// rows at a time ahead of the dependent arithmetic (latency, not bandwidth, bounds
-// a 257-row chain).  d' overwrites d in place, c' goes to cp[f]; dst may alias the
-// step input (pass 1 has consumed it).
+// rows at a time ahead of the dependent arithmetic.  d' / e' overwrite d in place,
+// c' / a' go to cp[f]; dst may alias the step input (pass 1 has consumed it).
+// m = 0: real coefficients, the imaginary parts are decoupled (u.y = d.y / b).
 constexpr int CD_U = 8;
+struct CdRow {
+  double2 d;
+  double ax, cy;  // coefficients of u_{j-1}, u_{j+1}
+  double2 b;      // diagonal
+  double e;       // eps (viscosity)
+};
+SWE_DEV CdRow cd_load(int M, int m, int c, int n, int B, int b, double a, double aap,
+                      const double *__restrict__ eps, const double4 *__restrict__ cft,
+                      const double *__restrict__ dxs, const double *__restrict__ dds) {
+  const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
+  const double4 cf = cft[k];
+  CdRow r;
+  r.d = __ldg(reinterpret_cast<const double2 *>(f ? dds : dxs) + (size_t)k * B + b);
+  r.e = __ldg(eps + k);
+  const double sg = f ? -a : a;  // xi rows (f = 0) / delta rows (f = 1)
+  r.ax = sg * cf.x;
+  r.cy = sg * cf.y;
+  r.b = make_double2(f ? 1.0 + aap * r.e : 1.0, -a * cf.z);
+  return r;
+}
+
 __global__ void __launch_bounds__(128) k_cn_direct_chain(
     int M, int B, double alpha, const double *__restrict__ eps, const double *__restrict__ phibar,
     const double4 *__restrict__ cft, const double *__restrict__ r0s, double *__restrict__ dxs,
     double *__restrict__ dds, double *__restrict__ cpx, double *__restrict__ cpd, Ptr3 dst,
     double dtnu, double halfq) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (M + 1) * 2 * B) return;
-  const int b = t % B, q = t / B, c = q & 1, m = q >> 1;
-  const double a = alpha, aap = alpha * alpha * phibar[b], apb = alpha * phibar[b];
-  auto at = [&](int k) { return (size_t)k * B + b; };
-  double2 cprev = make_double2(0.0, 0.0), dprev = cprev;
-  for (int n0 = m; n0 <= M; n0 += CD_U) {
-    double2 dv[CD_U];
-    double4 cfv[CD_U];
-    double ev[CD_U];
+  const int nbg = (B + 15) / 16;
+  const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wi >= (M + 1) * 2 * nbg) return;  // whole warps leave together
+  const int mc = wi / nbg, bg = wi - mc * nbg, m = mc >> 1, c = mc & 1;
+  const int b = bg * 16 + (lane & 15), up = lane >> 4;  // up: the lower half of the chain
+  const bool act = b < B;
+  const int bb = act ? b : 0;
+  const double a = alpha, aap = alpha * alpha * phibar[bb], apb = alpha * phibar[bb];
+  const int L = M + 1 - m, p = L >> 1;  // middle row (local index)
+  auto at = [&](int k) { return (size_t)k * B + bb; };
+  auto put = [&](double *base, int k, double2 v) {
+    if (act) reinterpret_cast<double2 *>(base)[at(k)] = v;
+  };
+  // ---- elimination towards the middle
+  double2 cprev = make_double2(0.0, 0.0), dprev = cprev;  // (c', d') or (a', e') of the last row
+  const int nrow = up ? L - 1 - p : p;  // rows this lane eliminates
+  for (int r0 = 0; r0 < nrow; r0 += CD_U) {
+    CdRow rv[CD_U];
 #pragma unroll
     for (int u = 0; u < CD_U; ++u) {
-      const int n = n0 + u;
-      if (n > M) break;
-      const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
-      dv[u] = __ldg(reinterpret_cast<const double2 *>(f ? dds : dxs) + at(k));
-      cfv[u] = cft[k];
-      ev[u] = __ldg(eps + k);
+      const int r = r0 + u;
+      if (r >= nrow) break;
+      const int j = up ? L - 1 - r : r;
+      rv[u] = cd_load(M, m, c, m + j, B, bb, a, aap, eps, cft, dxs, dds);
     }
 #pragma unroll
     for (int u = 0; u < CD_U; ++u) {
-      const int n = n0 + u;
-      if (n > M) break;
+      const int r = r0 + u;
+      if (r >= nrow) break;
+      const int j = up ? L - 1 - r : r, n = m + j;
       const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
-      const double4 cf = cfv[u];
-      const double2 d = dv[u];
-      // row coefficients: xi rows (f = 0) / delta rows (f = 1)
-      const double sg = f ? -a : a;
-      const double ax = sg * cf.x, cy = sg * cf.y;
-      const double2 bb = make_double2(f ? 1.0 + aap * ev[u] : 1.0, -a * cf.z);
+      const CdRow &w = rv[u];
+      // downwards: den = b - ax c'_{j-1}, c' = cy / den; upwards: den = b - cy a'_{j+1}, a' = ax / den
+      const double lo = up ? w.cy : w.ax, hi = up ? w.ax : w.cy;
       double2 cj, dj;
-      if (m == 0) {  // real coefficients; imaginary parts decoupled (no L_C at m = 0)
-        const double den = bb.x - ax * cprev.x;
-        cj = make_double2(cy / den, 0.0);
-        dj = make_double2((d.x - ax * dprev.x) / den, d.y / bb.x);
+      if (m == 0) {
+        const double den = w.b.x - lo * cprev.x;
+        cj = make_double2(hi / den, 0.0);
+        dj = make_double2((w.d.x - lo * dprev.x) / den, w.d.y / w.b.x);
       } else {
-        const double2 den = make_double2(bb.x - ax * cprev.x, bb.y - ax * cprev.y);
-        cj = cdiv(make_double2(cy, 0.0), den);
-        dj = cdiv(make_double2(d.x - ax * dprev.x, d.y - ax * dprev.y), den);
+        const double2 den = make_double2(w.b.x - lo * cprev.x, w.b.y - lo * cprev.y);
+        cj = cdiv(make_double2(hi, 0.0), den);
+        dj = cdiv(make_double2(w.d.x - lo * dprev.x, w.d.y - lo * dprev.y), den);
       }
-      reinterpret_cast<double2 *>(f ? cpd : cpx)[at(k)] = cj;
-      reinterpret_cast<double2 *>(f ? dds : dxs)[at(k)] = dj;
+      put(f ? cpd : cpx, k, cj);
+      put(f ? dds : dxs, k, dj);
       cprev = cj;
       dprev = dj;
     }
   }
-  // back substitution u_j = d'_j - c'_j u_{j+1}, Phi = r0 - a Pb delta, viscosity
-  double2 uu = make_double2(0.0, 0.0);
-  for (int n0 = M; n0 >= m; n0 -= CD_U) {
+  // ---- middle row p: a u_{p-1} + b u_p + c u_{p+1} = d with u_{p-1} = d' - c' u_p
+  // (upper lane) and u_{p+1} = e' - a' u_p (lower lane)
+  const double2 ca = make_double2(__shfl_xor_sync(0xffffffffu, cprev.x, 16),
+                                  __shfl_xor_sync(0xffffffffu, cprev.y, 16));
+  const double2 de = make_double2(__shfl_xor_sync(0xffffffffu, dprev.x, 16),
+                                  __shfl_xor_sync(0xffffffffu, dprev.y, 16));
+  double2 uu;
+  {
+    const CdRow w = cd_load(M, m, c, m + p, B, bb, a, aap, eps, cft, dxs, dds);
+    // (c'_{p-1}, d'_{p-1}) live in the upper lane, (a'_{p+1}, e'_{p+1}) in the lower one
+    const double2 cu = up ? ca : cprev, du = up ? de : dprev;
+    const double2 al = up ? cprev : ca, el = up ? dprev : de;
+    if (m == 0) {
+      const double den = w.b.x - w.ax * cu.x - w.cy * al.x;
+      uu = make_double2((w.d.x - w.ax * du.x - w.cy * el.x) / den, w.d.y / w.b.x);
+    } else {
+      const double2 den = make_double2(w.b.x - w.ax * cu.x - w.cy * al.x,
+                                       w.b.y - w.ax * cu.y - w.cy * al.y);
+      uu = cdiv(make_double2(w.d.x - w.ax * du.x - w.cy * el.x, w.d.y - w.ax * du.y - w.cy * el.y),
+                den);
+    }
+    if (!up) {  // the upper lane writes the middle row
+      const int n = m + p, f = ((n - m) + c) & 1, k = cd_row(M, m, n);
+      double bh = 1.0;
+      if (dtnu != 0.0) bh = 1.0 / (1.0 + dtnu * pow(w.e, halfq));
+      if (act) {
+        st2(dst.p[f ? 2 : 1], at(k), dtnu != 0.0 ? sc2(bh, uu) : uu);
+        if (f) {
+          const double2 r0 = ld2(r0s, at(k));
+          const double2 ph = make_double2(r0.x - apb * uu.x, r0.y - apb * uu.y);
+          st2(dst.p[0], at(k), dtnu != 0.0 ? sc2(bh, ph) : ph);
+        }
+      }
+    }
+  }
+  // ---- back substitution outwards from the middle, Phi = r0 - a Pb delta, viscosity
+  for (int r0 = nrow - 1; r0 >= 0; r0 -= CD_U) {
     double2 cv[CD_U], dv[CD_U], rv[CD_U];
     double ev[CD_U];
 #pragma unroll
     for (int u = 0; u < CD_U; ++u) {
-      const int n = n0 - u;
-      if (n < m) break;
+      const int r = r0 - u;
+      if (r < 0) break;
+      const int j = up ? L - 1 - r : r, n = m + j;
       const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
       cv[u] = reinterpret_cast<const double2 *>(f ? cpd : cpx)[at(k)];
       dv[u] = reinterpret_cast<const double2 *>(f ? dds : dxs)[at(k)];
@@ -1251,8 +1316,9 @@ __global__ void __launch_bounds__(128) k_cn_direct_chain(
     }
 #pragma unroll
     for (int u = 0; u < CD_U; ++u) {
-      const int n = n0 - u;
-      if (n < m) break;
+      const int r = r0 - u;
+      if (r < 0) break;
+      const int j = up ? L - 1 - r : r, n = m + j;
       const int f = ((n - m) + c) & 1, k = cd_row(M, m, n);
       const double2 cj = cv[u], dj = dv[u];
       if (m == 0)
@@ -1261,10 +1327,12 @@ __global__ void __launch_bounds__(128) k_cn_direct_chain(
         uu = make_double2(dj.x - (cj.x * uu.x - cj.y * uu.y), dj.y - (cj.x * uu.y + cj.y * uu.x));
       double bh = 1.0;
       if (dtnu != 0.0) bh = 1.0 / (1.0 + dtnu * pow(ev[u], halfq));
-      st2(dst.p[f ? 2 : 1], at(k), dtnu != 0.0 ? sc2(bh, uu) : uu);
-      if (f) {
-        const double2 ph = make_double2(rv[u].x - apb * uu.x, rv[u].y - apb * uu.y);
-        st2(dst.p[0], at(k), dtnu != 0.0 ? sc2(bh, ph) : ph);
+      if (act) {
+        st2(dst.p[f ? 2 : 1], at(k), dtnu != 0.0 ? sc2(bh, uu) : uu);
+        if (f) {
+          const double2 ph = make_double2(rv[u].x - apb * uu.x, rv[u].y - apb * uu.y);
+          st2(dst.p[0], at(k), dtnu != 0.0 ? sc2(bh, ph) : ph);
+        }
       }
     }
   }
@@ -1279,7 +1347,7 @@ int cn_direct(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha
   k_cn_direct_rhs<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, x0, x1, x2, s, alpha, eps, phibar, nb, cf,
                                                  rhs_given, sc);
   SWE_LAUNCH_CHECK();
-  const int n = (M + 1) * 2 * B, nt = 128;
+  const int n = (M + 1) * 2 * ((B + 15) / 16) * 32, nt = 128;
   k_cn_direct_chain<<<(n + nt - 1) / nt, nt, 0, st>>>(M, B, alpha, eps, phibar, cf, scratch[0],
                                                       scratch[1], scratch[2], scratch[3],
                                                       scratch[4], dst, dtnu, halfq);
