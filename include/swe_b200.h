@@ -151,9 +151,10 @@ int swe_profile(int enable);
  * "fast_coriolis": 2 (default) spectral three-term recurrence, 1 FFT-free
  * Legendre pair, 0 pseudospectral FFT round trip.  "graphs": 1 (default)
  * replay one CUDA graph per IMEX step.  "helm_tiled", "cn_small", "cn_cluster":
- * 1 / 0 enable / disable the tiled fixed-point kernel, the one-CTA-per-slice half
- * step (K <= 2800) and the one-cluster-per-slice half step (K up to ~38k modes;
- * default 0, the other two default 1).  Results agree to roundoff on every path (bitwise between the
+ * 1 / 0 enable / disable the tiled fixed-point kernel and the one-CTA-per-slice
+ * half step (K <= 2800); "cn_cluster" 1 (default) runs the shared-memory-resident
+ * half step when one CTA holds a slice (K <= 2400), 2 also as a cluster of CTAs
+ * per slice (K up to ~38k modes), 0 never.  Results agree to roundoff on every path (bitwise between the
  * half-step paths; within 1e-12 relative between the fast_coriolis modes). */
 int swe_set_option(const char *key, int value);
 int swe_profile_read(double *ms_out, double *work_out, long long *count_out);

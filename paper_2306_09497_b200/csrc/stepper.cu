@@ -40,8 +40,9 @@ bool g_capturing = false;  // a step graph is being captured: no events, no host
 int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
-int g_cn_cluster = 0;      // one-launch CN half step, one thread-block cluster per slice
-                           // (correct, but latency-bound at M = 256: off by default)
+int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 only
+                           // when one CTA holds a slice (coarse levels, default), 2 also
+                           // as a multi-CTA cluster per slice (latency-bound at M = 256)
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
 int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
 // Coriolis operator (eval_coriolis): 2 spectral three-term recurrence, fused into the
@@ -571,8 +572,10 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
       for (int i = 0; i < B; ++i) resid_host[i] = 0.0;
     return OK;
   }
-  const bool small = g_cn_small && cn_small_ok(K);
-  if (small || (g_cn_cluster && cn_cluster_size(pl->M))) {
+  const int ccs = g_cn_cluster ? cn_cluster_size(pl->M) : 0;
+  const bool clus = ccs == 1 || (g_cn_cluster == 2 && ccs > 1);
+  const bool small = !clus && g_cn_small && cn_small_ok(K);
+  if (small || clus) {
     // the whole half step in one launch: one CTA per slice (coarse levels) or one
     // thread-block cluster per slice (the fine level)
     Ptr3C X0 = {{nullptr, nullptr, nullptr}}, X1 = X0, X2 = X0;
@@ -1372,7 +1375,7 @@ int swe_set_option(const char *key, int value) {
     g_cn_small = value;
     return OK;
   }
-  if (key && strcmp(key, "cn_cluster") == 0 && (value == 0 || value == 1)) {
+  if (key && strcmp(key, "cn_cluster") == 0 && value >= 0 && value <= 2) {
     g_cn_cluster = value;
     return OK;
   }

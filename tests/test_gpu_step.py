@@ -391,18 +391,56 @@ def test_cluster_half_step_matches_multikernel(mods, M, B, graphs):
     outs, its = {}, {}
     _lib.set_option("graphs", graphs)
     try:
-        for cl in (0, 1):
+        for cl in (0, 2):
             _lib.set_option("cn_cluster", cl)
             s = base.copy()
             it = np.zeros((3, B, 2), dtype=np.int32)
             steppers.imex_steps_inplace(s, cfg, 3, None if graphs else it)
             outs[cl], its[cl] = s.data.cpu().numpy(), it
     finally:
-        _lib.set_option("cn_cluster", 0)
+        _lib.set_option("cn_cluster", 1)
         _lib.set_option("graphs", 1)
-    assert np.array_equal(its[0], its[1])
+    assert np.array_equal(its[0], its[2])
     for b in range(B):
-        assert rel_diff(outs[1][b], outs[0][b]) < 1e-13, b
+        assert rel_diff(outs[2][b], outs[0][b]) < 1e-13, b
+
+
+@pytest.mark.parametrize("M,B", [(16, 1), (51, 1), (51, 40)])
+@pytest.mark.parametrize("graphs", [0, 1])
+def test_coarse_half_step_variants_agree(mods, M, B, graphs):
+    """Coarse levels: the shared-memory-resident half step (one CTA per slice, rhs in
+    shared memory; the default), the one-CTA k_cn_small and the multi-kernel path
+    give the same iteration counts and states."""
+    spharm, dynamics, steppers, scenarios = mods
+    import torch
+    from paper_2306_09497_b200 import _lib
+    grid = spharm.get_grid(M)
+    cfg = steppers.StepperConfig(dt=480.0, viscosity=dynamics.ViscositySpec(2, 1e5))
+    base = scenarios.gaussian_bumps(grid, batch=B)
+    rng = np.random.default_rng(M * B)
+    taper = torch.from_numpy((grid.n_of + 1.0) ** -2).cuda()
+    noise = torch.from_numpy(rng.standard_normal((B, grid.n_modes))).cuda() * taper
+    noise[:, : M + 1] = noise[:, : M + 1].real
+    base.data[:, 1] += 1e-6 * noise
+    base.data[:, 2] += 1e-7 * noise
+    outs, its = {}, {}
+    _lib.set_option("graphs", graphs)
+    try:
+        for name, cl, sm in (("cluster", 1, 1), ("small", 0, 1), ("multi", 0, 0)):
+            _lib.set_option("cn_cluster", cl)
+            _lib.set_option("cn_small", sm)
+            s = base.copy()
+            it = np.zeros((3, B, 2), dtype=np.int32)
+            steppers.imex_steps_inplace(s, cfg, 3, None if graphs else it)
+            outs[name], its[name] = s.data.cpu().numpy(), it
+    finally:
+        _lib.set_option("cn_cluster", 1)
+        _lib.set_option("cn_small", 1)
+        _lib.set_option("graphs", 1)
+    for name in ("small", "multi"):
+        assert np.array_equal(its[name], its["cluster"]), name
+        for b in range(B):
+            assert rel_diff(outs[name][b], outs["cluster"][b]) < 1e-13, (name, b)
 
 
 def test_cluster_half_step_nonconvergence_raises(mods):
@@ -413,13 +451,13 @@ def test_cluster_half_step_nonconvergence_raises(mods):
     grid = spharm.get_grid(256)
     s = scenarios.gaussian_bumps(grid, batch=2)
     cfg = steppers.StepperConfig(dt=600.0, implicit_max_iter=1)
-    _lib.set_option("cn_cluster", 1)
+    _lib.set_option("cn_cluster", 2)
     try:
         for _ in range(3):
             with pytest.raises(steppers.ImplicitSolveError, match="residual"):
                 steppers.imex_step(s, cfg)
     finally:
-        _lib.set_option("cn_cluster", 0)
+        _lib.set_option("cn_cluster", 1)
 
 
 @pytest.mark.parametrize("M,B,dt", [(32, 6, 240.0), (51, 40, 960.0), (256, 3, 60.0), (256, 64, 60.0)])
