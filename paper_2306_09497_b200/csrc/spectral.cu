@@ -921,20 +921,23 @@ __global__ void __launch_bounds__(CC_NT, 1) k_cn_cluster(
         for (int o = 16; o > 0; o >>= 1) v[q] = max(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
       }
       const int par = it & 1;
-      if (lane == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                         cc_smem(&sh.mbar[par])),
-                     "r"(48 * C)
-                     : "memory");
-      }
-      if (lane < C)
+      if (C > 1) {  // a one-CTA "cluster" (coarse levels) already holds the slice maxima
+        if (lane == 0) {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           cc_smem(&sh.mbar[par])),
+                       "r"(48 * C)
+                       : "memory");
+        }
+        if (lane < C)
 #pragma unroll
-        for (int q = 0; q < 6; q += 2) cc_send16(&sh.inbox[par][c][q], &sh.mbar[par], lane, v[q], v[q + 1]);
-      cc_wait(&sh.mbar[par], (it >> 1) & 1);
+          for (int q = 0; q < 6; q += 2)
+            cc_send16(&sh.inbox[par][c][q], &sh.mbar[par], lane, v[q], v[q + 1]);
+        cc_wait(&sh.mbar[par], (it >> 1) & 1);
 #pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        v[q] = lane < C ? sh.inbox[par][lane][q] : 0ULL;
-        for (int o = 16; o > 0; o >>= 1) v[q] = max(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+        for (int q = 0; q < 6; ++q) {
+          v[q] = lane < C ? sh.inbox[par][lane][q] : 0ULL;
+          for (int o = 16; o > 0; o >>= 1) v[q] = max(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+        }
       }
       if (lane == 0) {
         double w[6];
