@@ -365,6 +365,9 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    for kv in args.opt:
+        k, v = kv.split("=")
+        _lib.set_option(k, int(v))
     B = args.slices
     grid = spharm.get_grid(M)
     cfg = steppers.StepperConfig(dt=DT, viscosity=dynamics.ViscositySpec(2, NU))
@@ -529,6 +532,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-pint", action="store_true", help="skip the cfg2 MGRIT leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg4 / cfg5 (M=1024) legs")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library tuning switch key=value (swe_set_option), for experiments")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -253,6 +253,23 @@ SWE_DEV void put_z(const LCtx &c, int row, int k, int k2, double2 Xk, double2 Xc
 // different rows (one line, no bank conflicts) and keep many loads in flight; field
 // `subf` has phisub subtracted from E at m = 0 (phi_prime, dynamics.py:52-56).  With
 // a.dlam, field 2 is i m times field 5 (d_lambda Phi).
+// flattened (k, slice, field) item -> (k, s, f): field fastest, or with SF slice
+// fastest (adjacent slices share 32-byte sectors of the [..][m][slice] layouts)
+template <bool SF>
+SWE_DEV void item_ksf(int idx, int nf, int S, int &k, int &s, int &f) {
+  if constexpr (SF) {
+    const int r = idx / S;
+    s = idx - r * S;
+    k = r / nf;
+    f = r - k * nf;
+  } else {
+    const int r = idx / nf;
+    f = idx - r * nf;
+    k = r / S;
+    s = r - k * S;
+  }
+}
+
 template <int LW>
 SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1, S = c.S;
@@ -266,7 +283,8 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
-      const int r = idx / nf, f = idx - r * nf, k = r / S, s = r - k * S;
+      int k, s, f;
+      item_ksf<LW == 32>(idx, nf, S, k, s, f);
       const bool ok = idx < total && s < c.nsl;
       const int k2 = k == 0 ? N2 : N2 - k;
       const double2 z = make_double2(0.0, 0.0);
@@ -299,7 +317,8 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
-      const int r = idx / nf, f = idx - r * nf, k = r / S, s = r - k * S;
+      int k, s, f;
+      item_ksf<LW == 32>(idx, nf, S, k, s, f);
       if (idx >= total || s >= c.nsl) continue;
       if (f == subf && k == 0) e[u].x -= a.phisub[c.b0 + s];
       const int k2 = N2 - k;
@@ -378,7 +397,8 @@ SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, const double2 *XN, co
   const int M = a.M, S = c.S, N2 = a.N2, per = (M + 1) * S;
   const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
   for (int idx = i0; idx < nf * per; idx += istep) {
-    const int r = idx / nf, f = idx - r * nf, k = r / S, s = r - k * S;
+    int k, s, f;
+    item_ksf<LW == 32>(idx, nf, S, k, s, f);
     if (s >= c.nsl) continue;
     const int z1 = __ldg(a.pos_z + k), z2 = __ldg(a.pos_z + (k == 0 ? 0 : N2 - k));
     double2 w = __ldg(a.twh + k);
@@ -400,12 +420,14 @@ SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, const double2 *XN, co
 }
 
 template <int LW>
-constexpr int lane_threads() { return LW == 16 ? 256 : 512; }
+constexpr int lane_threads() { return LW == 16 ? 256 : 512; }  // 8 and 32 rows: one CTA per SM
 
 // slices per CTA (rows = fields x 2 hemispheres x slices; the LW = 8 nonlinear pass
 // holds one hemisphere of one slice per CTA)
 __host__ __device__ constexpr int lane_slices(int op, int lw) {
-  return lw == 16 ? fft_lane_slices(op) : (op == FOP_NONLINEAR ? 1 : fft_lane_slices(op) / 2);
+  return lw == 16   ? fft_lane_slices(op)
+         : lw == 32 ? 2 * fft_lane_slices(op)
+                    : (op == FOP_NONLINEAR ? 1 : fft_lane_slices(op) / 2);
 }
 
 }  // namespace
@@ -496,7 +518,7 @@ __global__ void __launch_bounds__(lane_threads<LW>(), 512 / lane_threads<LW>())
     }
     __syncthreads();
     // only the 4 product fields (x 2 hemispheres unless split; S = 1)
-    lane_fft<SPLIT ? 4 : 8, LW, GEN>(a, c);
+    lane_fft<SPLIT ? 4 : 8 * lane_slices(OP, LW), LW, GEN>(a, c);
     const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
     if constexpr (SPLIT) {
       // F+- needs both hemispheres: each CTA of the pair folds half of the (k, field)
@@ -582,6 +604,9 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
     return E_SHAPE;
   }
   const int smem = (int)(((size_t)a.N2 * lw + g) * sizeof(double2));
+  if (a.lw32 && op == FOP_NONLINEAR && !g && lw == 16 &&
+      (size_t)a.N2 * 32 * sizeof(double2) <= 227 * 1024)
+    return launch_lanes<FOP_NONLINEAR, 32, false>(a, a.N2 * 32 * (int)sizeof(double2), st);
   if (g) return lw == 16 ? launch_width<16, true>(op, a, smem, st) : launch_width<8, true>(op, a, smem, st);
   return lw == 16 ? launch_width<16, false>(op, a, smem, st) : launch_width<8, false>(op, a, smem, st);
 }

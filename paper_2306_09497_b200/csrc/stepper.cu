@@ -40,6 +40,7 @@ bool g_capturing = false;  // a step graph is being captured: no events, no host
 int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
+int g_fft_lw32 = 0;        // nonlinear lane FFT with 32 rows (2 slices) per CTA
 int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 only
                            // when one CTA holds a slice (coarse levels, default), 2 also
                            // as a multi-CTA cluster per slice (latency-bound at M = 256)
@@ -386,6 +387,7 @@ int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], d
     for (int i = 0; i < 4; ++i) f.out[i] = r.fsp(i);
     f.dlam = 1;
     f.in_pm = pm;
+    f.lw32 = g_fft_lw32;
     if ((rc = fft(r, FOP_NONLINEAR, f))) return rc;
   }
   {
@@ -924,7 +926,7 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
-         (g_helm_tiled << 13) | (g_cn_cluster << 14);
+         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1373,6 +1375,10 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "cn_small") == 0 && (value == 0 || value == 1)) {
     g_cn_small = value;
+    return OK;
+  }
+  if (key && strcmp(key, "fft_lw32") == 0 && (value == 0 || value == 1)) {
+    g_fft_lw32 = value;
     return OK;
   }
   if (key && strcmp(key, "cn_cluster") == 0 && value >= 0 && value <= 2) {
