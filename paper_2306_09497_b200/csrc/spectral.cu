@@ -8,6 +8,7 @@
 #include "spectral.cuh"
 
 #include <cooperative_groups.h>
+#include <vector>
 
 namespace cg = cooperative_groups;
 
@@ -1034,24 +1035,30 @@ static int cc_ranges(int M, int C, CcRanges &rg) {
 
 // cluster size for truncation M (0: the cluster path does not apply or cannot be
 // scheduled)
-int cn_cluster_size(int M) {
-  static int cached_M = -1, cached_C = 0;
-  if (cached_M == M) return cached_C;
+int cn_cluster_size(int M, int want) {
+  static std::vector<int3> cache;  // (M, want, C)
+  static int attr_smem = 0;
+  for (const int3 &e : cache)
+    if (e.x == M && e.y == want) return e.z;
   const int K = (M + 1) * (M + 2) / 2;
   int C = 0, cap = 0;
   CcRanges rg;
-  for (int c = std::max(1, (K + CC_CHUNK - 1) / CC_CHUNK); c <= CC_MAXC && !cap; ++c) {
-    const int cc = c > 8 ? CC_MAXC : c;  // non-portable sizes: the smallest ranges
+  const int c0 = std::max(std::max(1, want), (K + CC_CHUNK - 1) / CC_CHUNK);
+  for (int c = std::min(c0, CC_MAXC); c <= CC_MAXC && !cap; ++c) {
+    const int cc = (c > 8 && want <= 8) ? CC_MAXC : c;  // non-portable sizes: the smallest ranges
     if ((cap = cc_ranges(M, cc, rg))) C = cc;
   }
   int ok = 0;
   if (C) {
+    // the attribute only grows: graphs captured for another truncation keep launching
     const int smem = 6 * cap * (int)sizeof(double2);
-    if (cudaFuncSetAttribute(k_cn_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
-            cudaSuccess &&
+    if ((smem <= attr_smem ||
+         cudaFuncSetAttribute(k_cn_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
+             cudaSuccess) &&
         (C <= 8 || cudaFuncSetAttribute(k_cn_cluster,
                                         cudaFuncAttributeNonPortableClusterSizeAllowed,
                                         1) == cudaSuccess)) {
+      attr_smem = std::max(attr_smem, smem);
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute at[1];
       cfg.gridDim = dim3(C);
@@ -1068,16 +1075,15 @@ int cn_cluster_size(int M) {
     }
     cudaGetLastError();  // a refused configuration is not an error: the multi-kernel path runs
   }
-  cached_M = M;
-  cached_C = ok ? C : 0;
-  return cached_C;
+  cache.push_back(make_int3(M, want, ok ? C : 0));
+  return ok ? C : 0;
 }
 
-int cn_cluster(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+int cn_cluster(int M, int want, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
                const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
                int rhs_given, Ptr3 dst, int max_iter, double tol, double dtnu, double halfq,
                int *iters, int *flags, int *counter, double *resid, int *fail, cudaStream_t st) {
-  const int C = cn_cluster_size(M), K = (M + 1) * (M + 2) / 2;
+  const int C = cn_cluster_size(M, want), K = (M + 1) * (M + 2) / 2;
   CcRanges rg;
   const int cap = C ? cc_ranges(M, C, rg) : 0;
   if (!cap) {

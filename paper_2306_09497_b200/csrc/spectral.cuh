@@ -63,9 +63,10 @@ int cn_small(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              double halfq, int *iters, int *flags, int *counter, double *resid, int *fail,
              cudaStream_t st);
 // the same for K up to ~38k modes (the fine level M = 256): one thread-block
-// cluster per slice; cn_cluster_size(M) = CTAs per cluster, 0 when not applicable
-int cn_cluster_size(int M);
-int cn_cluster(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+// cluster per slice; cn_cluster_size(M, want) = CTAs per cluster (at least `want`
+// when the m-blocks allow), 0 when not applicable
+int cn_cluster_size(int M, int want);
+int cn_cluster(int M, int want, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
                const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
                int rhs_given, Ptr3 dst, int max_iter, double tol, double dtnu, double halfq,
                int *iters, int *flags, int *counter, double *resid, int *fail, cudaStream_t st);

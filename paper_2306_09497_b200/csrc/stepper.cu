@@ -40,7 +40,8 @@ bool g_capturing = false;  // a step graph is being captured: no events, no host
 int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
-int g_fft_lw32 = 0;        // nonlinear lane FFT with 32 rows (2 slices) per CTA
+int g_fft_lw32 = 0;
+int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: fewest)        // nonlinear lane FFT with 32 rows (2 slices) per CTA
 int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 only
                            // when one CTA holds a slice (coarse levels, default), 2 also
                            // as a multi-CTA cluster per slice (latency-bound at M = 256)
@@ -574,8 +575,14 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
       for (int i = 0; i < B; ++i) resid_host[i] = 0.0;
     return OK;
   }
-  const int ccs = g_cn_cluster ? cn_cluster_size(pl->M) : 0;
-  const bool clus = ccs == 1 || (g_cn_cluster == 2 && ccs > 1);
+  // CTAs per slice: small batches spread a slice over several SMs (the fixed point
+  // of one slice on one SM is instruction-bound), B >= 32 keeps one CTA per slice
+  int want = g_cc_ctas ? g_cc_ctas : (B >= 32 ? 1 : std::min(16, std::max(1, 64 / B)));
+  int ccs = 0;
+  if (g_cn_cluster)
+    for (; want >= 1 && !(ccs = cn_cluster_size(pl->M, want)); want /= 2) {
+    }
+  const bool clus = ccs >= 1 && (ccs <= want || g_cn_cluster == 2);
   const bool small = !clus && g_cn_small && cn_small_ok(K);
   if (small || clus) {
     // the whole half step in one launch: one CTA per slice (coarse levels) or one
@@ -600,7 +607,7 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
                       cfg.visc_order / 2.0, w.iters, w.flags, w.counter, w.stats,
                       r.graph ? w.d_fail : nullptr, r.st);
       else
-        rc = cn_cluster(pl->M, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, cor.nb, cor.cf,
+        rc = cn_cluster(pl->M, want, B, X0, X1, X2, s, alpha, pl->eps, w.phibar, cor.nb, cor.cf,
                         rhs_given ? 1 : 0, D, cfg.implicit_max_iter, cfg.implicit_tol, dtnu,
                         cfg.visc_order / 2.0, w.iters, w.flags, w.counter, w.stats,
                         r.graph ? w.d_fail : nullptr, r.st);
@@ -926,7 +933,7 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
-         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16);
+         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16) | (g_cc_ctas << 17);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1375,6 +1382,10 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "cn_small") == 0 && (value == 0 || value == 1)) {
     g_cn_small = value;
+    return OK;
+  }
+  if (key && strcmp(key, "cn_cluster_ctas") == 0 && value >= 0 && value <= 16) {
+    g_cc_ctas = value;
     return OK;
   }
   if (key && strcmp(key, "fft_lw32") == 0 && (value == 0 || value == 1)) {
