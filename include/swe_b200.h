@@ -153,8 +153,10 @@ int swe_profile(int enable);
  * replay one CUDA graph per IMEX step.  "helm_tiled", "cn_small", "cn_cluster":
  * 1 / 0 enable / disable the tiled fixed-point kernel and the one-CTA-per-slice
  * half step (K <= 2800); "cn_cluster" 1 (default) runs the shared-memory-resident
- * half step when one CTA holds a slice (K <= 2400), 2 also as a cluster of CTAs
- * per slice (K up to ~38k modes), 0 never.  Results agree to roundoff on every path (bitwise between the
+ * half step when its cluster of CTAs per slice is no larger than the batch asks
+ * for (one CTA per slice from 32 slices, up to 16 for one slice; K up to ~38k
+ * modes), 2 at any cluster size, 0 never; "cn_cluster_ctas" forces the CTAs per
+ * slice (0 = by batch size).  "fft_lw32" 1: 32-row nonlinear lane FFT (default 0).  Results agree to roundoff on every path (bitwise between the
  * half-step paths; within 1e-12 relative between the fast_coriolis modes). */
 int swe_set_option(const char *key, int value);
 int swe_profile_read(double *ms_out, double *work_out, long long *count_out);
