@@ -571,3 +571,33 @@ def test_nonlinear_lw32_matches_lw16(mods, M, B):
             _lib.set_option("fft_lw32", 0)
     for f in range(3):
         assert np.array_equal(out[0][f], out[1][f]), f
+
+
+@pytest.mark.parametrize("B", [65, 130])
+def test_odd_and_wide_batches_match_single_slice(mods, B):
+    """M=256 batches past the 64/128-column GEMM tiles and the 32-slice CN tiles
+    (odd remainders): selected slices equal their own single-slice steps (which
+    take the small-batch kernels and the per-slice cluster half step) with the
+    same fixed-point iteration counts."""
+    spharm, dynamics, steppers, scenarios = mods
+    import torch
+    M = 256
+    grid = spharm.get_grid(M)
+    cfg = steppers.StepperConfig(dt=60.0, viscosity=dynamics.ViscositySpec(2, 1e5))
+    base = scenarios.gaussian_bumps(grid, batch=B)
+    rng = np.random.default_rng(B)
+    taper = torch.from_numpy((grid.n_of + 1.0) ** -2).cuda()
+    noise = torch.from_numpy(rng.standard_normal((B, grid.n_modes))).cuda() * taper
+    noise[:, : M + 1] = noise[:, : M + 1].real
+    base.data[:, 1] += 1e-6 * noise
+    base.data[:, 2] += 1e-7 * noise
+    s = base.copy()
+    it = np.zeros((2, B, 2), dtype=np.int32)
+    steppers.imex_steps_inplace(s, cfg, 2, it)
+    got = s.data.cpu().numpy()
+    for b in (0, 31, 32, B // 2, B - 1):
+        one = dynamics.PrognosticState(grid, base.data[b:b + 1].clone(), base.phibar_t[b:b + 1].clone())
+        it1 = np.zeros((2, 1, 2), dtype=np.int32)
+        steppers.imex_steps_inplace(one, cfg, 2, it1)
+        assert np.array_equal(it1[:, 0], it[:, b]), b
+        assert rel_diff(one.data[0].cpu().numpy(), got[b]) < 1e-12, b
