@@ -147,7 +147,9 @@ int swe_profile(int enable);
 /* Tuning switches.  "fft_path": 0 auto, 1 warp-per-row FFT kernel, 2 lane=row
  * FFT kernel (falls back to 1 where its radix/size limits do not hold).
  * "leg_path": 0 auto, 1 small-batch Legendre kernels, 2 / 3 wide-tile kernels
- * with 128 / 64 columns per CTA, 4 warp-specialised persistent kernels.
+ * with 128 / 64 columns per CTA, 4 warp-specialised persistent kernels, 5 the
+ * 8-lane dot-product kernels for 1..4 slices ("gemv_max_b": the auto path's
+ * largest batch for them, default 3).
  * "fast_coriolis": 2 (default) spectral three-term recurrence, 1 FFT-free
  * Legendre pair, 0 pseudospectral FFT round trip.  "graphs": 1 (default)
  * replay one CUDA graph per IMEX step.  "helm_tiled", "cn_small", "cn_cluster":

@@ -58,6 +58,9 @@ struct LegArgs {
 // Launch helpers (legendre.cu).  items/tiles are prepared by the plan.
 int leg_synth_launch(const LegArgs &a, int ncoltiles, cudaStream_t st);
 int leg_anal_launch(const LegArgs &a, int ncoltiles, cudaStream_t st);
+// few-slice variants (8-lane dot products) over the first nslice complex columns
+int leg_synth_gemv_launch(const LegArgs &a, int nslice, cudaStream_t st);
+int leg_anal_gemv_launch(const LegArgs &a, int nslice, int K, cudaStream_t st);
 // wide-tile variants (legendre_v2.cu): column tile bn = 64 (4 warps) or 128 (8 warps)
 int leg_synth_v2_launch(const LegArgs &a, int bn, cudaStream_t st);
 int leg_anal_v2_launch(const LegArgs &a, int bn, cudaStream_t st);

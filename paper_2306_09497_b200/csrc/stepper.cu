@@ -41,6 +41,7 @@ int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per 
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
 int g_fft_lw32 = 0;
+int g_gemv_max_b = 3;      // batches up to this size take the dot-product Legendre kernels
 int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: fewest)        // nonlinear lane FFT with 32 rows (2 slices) per CTA
 int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 only
                            // when one CTA holds a slice (coarse levels, default), 2 also
@@ -181,6 +182,8 @@ int synth(const Run &r, LegArgs &a) {
   a.items = r.pl->synth_items;
   a.nitems = r.pl->n_synth_items;
   ProfScope ps(0, leg_flops(r, a), r.st);
+  if ((g_leg_path == 5 && r.B <= 4) || (g_leg_path == 0 && r.B <= g_gemv_max_b))
+    return leg_synth_gemv_launch(a, r.B, r.st);
   const int bn = leg_bn(r);
   if (bn < 0) {
     a.items = r.pl->synth_items_v3;
@@ -193,6 +196,8 @@ int synth(const Run &r, LegArgs &a) {
 
 int anal(const Run &r, LegArgs &a) {
   ProfScope ps(1, leg_flops(r, a), r.st);
+  if ((g_leg_path == 5 && r.B <= 4) || (g_leg_path == 0 && r.B <= g_gemv_max_b))
+    return leg_anal_gemv_launch(a, r.B, r.pl->K, r.st);
   const int bn = leg_bn(r);
   if (bn) {
     if (bn < 0) {
@@ -933,7 +938,7 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
-         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16) | (g_cc_ctas << 17);
+         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16) | (g_cc_ctas << 17) | (g_gemv_max_b << 22);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1408,7 +1413,11 @@ int swe_set_option(const char *key, int value) {
     g_fast_coriolis = value;
     return OK;
   }
-  if (key && strcmp(key, "leg_path") == 0 && value >= 0 && value <= 4) {
+  if (key && strcmp(key, "gemv_max_b") == 0 && value >= 0 && value <= 4) {
+    g_gemv_max_b = value;
+    return OK;
+  }
+  if (key && strcmp(key, "leg_path") == 0 && value >= 0 && value <= 5) {
     g_leg_path = value;
     return OK;
   }

@@ -47,8 +47,9 @@ def test_transforms_match_reference_goldens(gpu, name):
     assert rel_diff(xi, g["vd_xi"]) < TOL and rel_diff(de, g["vd_delta"]) < TOL
 
 
-@pytest.fixture(params=[(1, 1), (2, 2), (1, 2), (2, 3), (1, 4), (2, 4)],
-                ids=["rows_v1", "lanes_v2w128", "rows_v2w128", "lanes_v2w64", "rows_v3", "lanes_v3"])
+@pytest.fixture(params=[(1, 1), (2, 2), (1, 2), (2, 3), (1, 4), (2, 4), (2, 5)],
+                ids=["rows_v1", "lanes_v2w128", "rows_v2w128", "lanes_v2w64", "rows_v3", "lanes_v3",
+                     "lanes_gemv"])
 def fft_path(request):
     """Force each FFT kernel (warp-per-row / lane=row) and Legendre tiling
     (64- / 128-column) so every code path is parity-checked at every M."""
@@ -138,14 +139,26 @@ def test_round_trip(gpu, M):
 
 
 def test_batch_independence_bitwise(gpu):
-    """A slice's result must not depend on which batch it rides in."""
+    """A slice's result must not depend on which batch it rides in (bitwise within
+    one kernel generation: the small-batch, tiled and persistent GEMMs accumulate
+    in different orders, so the batch-size switch is pinned here)."""
     from oracle.sht import random_bandlimited
+    from paper_2306_09497_b200 import _lib
     grid = gpu.get_grid(32)
     rng = np.random.default_rng(9)
     c = random_bandlimited(oracle(32), rng, batch=(7,))
+    _lib.set_option("leg_path", 1)
+    try:
+        full = grid.synthesis(c)
+        for b in (0, 3, 6):
+            assert np.array_equal(grid.synthesis(c[b]), full[b])
+    finally:
+        _lib.set_option("leg_path", 0)
+    # across generations (here: 8-lane dot products at B=1 vs DMMA tiles at B=7)
     full = grid.synthesis(c)
     for b in (0, 3, 6):
-        assert np.array_equal(grid.synthesis(c[b]), full[b])
+        one = grid.synthesis(c[b])
+        assert np.abs(one - full[b]).max() <= 1e-14 * np.abs(full[b]).max()
 
 
 def test_shape_errors(gpu):
