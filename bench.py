@@ -429,7 +429,8 @@ def run_ours(args):
     # cfg2 end to end right after the main leg (before the legs that add plans,
     # graphs and pinned buffers)
     pint = pint_cfg2(torch) if rank == 0 and world == 1 and not args.no_pint else None
-    direct = direct_leg(torch, steppers, cfg, state, args.steps, flush) if not args.no_extra else None
+    direct = (direct_leg(torch, steppers, cfg, state, args.steps, flush)
+              if not args.no_extra and world == 1 else None)
 
     # e2e through the public API with pinned host buffers: every step copies its
     # batch in (H2D) and its result out (D2H); steppers.HostPipeline overlaps the
