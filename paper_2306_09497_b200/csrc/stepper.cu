@@ -40,12 +40,12 @@ bool g_capturing = false;  // a step graph is being captured: no events, no host
 int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
-int g_fft_lw32 = 0;
+int g_fft_lw32 = 0;        // nonlinear lane FFT with 32 rows (2 slices) per CTA
 int g_gemv_max_b = 3;      // batches up to this size take the dot-product Legendre kernels
-int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: fewest)        // nonlinear lane FFT with 32 rows (2 slices) per CTA
-int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 only
-                           // when one CTA holds a slice (coarse levels, default), 2 also
-                           // as a multi-CTA cluster per slice (latency-bound at M = 256)
+int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: by batch)
+int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 when
+                           // its CTAs per slice fit the batch's ask (default), 2 at any
+                           // size (latency-bound at M = 256 x 64 slices), 0 never
 int g_fft_path = 0;  // 0 auto, 1 warp-per-row, 2 lane = row
 int g_leg_path = 0;  // 0 auto, 1 legendre.cu, 2 v2 with 128 columns, 3 v2 with 64 columns
 // Coriolis operator (eval_coriolis): 2 spectral three-term recurrence, fused into the

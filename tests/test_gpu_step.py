@@ -601,3 +601,29 @@ def test_odd_and_wide_batches_match_single_slice(mods, B):
         steppers.imex_steps_inplace(one, cfg, 2, it1)
         assert np.array_equal(it1[:, 0], it[:, b]), b
         assert rel_diff(one.data[0].cpu().numpy(), got[b]) < 1e-12, b
+
+
+@pytest.mark.parametrize("implicit,nonlin", [(True, False), (False, False)])
+def test_linear_only_steps_match_oracle(mods, implicit, nonlin):
+    """include_nonlinear=False (linear dynamics only, steppers.py:121-140), with the
+    Coriolis term implicit or explicit, against the oracle step."""
+    spharm, dynamics, steppers, _ = mods
+    from oracle.sht import OracleSphere
+    from oracle.swe import StepCfg, imex_step, gaussian_bumps
+    M, B = 32, 2
+    sph = OracleSphere(M)
+    s0 = gaussian_bumps(sph, batch=B)
+    s0.xi[1] += 1e-6 * (sph.n_of + 1.0) ** -2
+    tr = "implicit" if implicit else "explicit"
+    ref = imex_step(s0, StepCfg(dt=240.0, visc_nu=1e5, coriolis_treatment=tr,
+                                include_nonlinear=nonlin), [])
+    grid = spharm.get_grid(M)
+    st = dynamics.PrognosticState.from_fields(grid, s0.phi, s0.xi, s0.delta, s0.phibar)
+    cfg = steppers.StepperConfig(dt=240.0, viscosity=dynamics.ViscositySpec(2, 1e5),
+                                 coriolis_treatment=tr, include_nonlinear=nonlin)
+    out = steppers.imex_step(st, cfg)
+    phi, xi, de, _ = out.to_numpy()
+    for b in range(B):
+        got = np.stack([phi[b], xi[b], de[b]])
+        want = np.stack([ref.phi[b], ref.xi[b], ref.delta[b]])
+        assert rel_diff(got, want) < 1e-10, b
