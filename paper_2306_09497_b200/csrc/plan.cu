@@ -7,6 +7,7 @@
 #include <algorithm>
 
 #include "plan.cuh"
+#include "spectral.cuh"
 
 namespace swe {
 
@@ -400,6 +401,8 @@ void work_free(Work &w) {
   cudaFree(w.half);
   cudaFree(w.fspec);
   cudaFree(w.stats);
+  cudaFree(w.fstats);
+  cudaFree(w.target2);
   cudaFree(w.flags);
   cudaFree(w.iters);
   cudaFree(w.counter);
@@ -469,6 +472,9 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaMalloc(&w.half, NHALF * half * sizeof(double)));
   SWE_CUDA(cudaMalloc(&w.fspec, NF * half * sizeof(double)));
   SWE_CUDA(cudaMalloc(&w.stats, (size_t)B * 8 * sizeof(double)));
+  SWE_CUDA(cudaMalloc(&w.fstats, (size_t)B * cn_fused_kmax() * 6 * sizeof(unsigned long long)));
+  SWE_CUDA(cudaMemset(w.fstats, 0, (size_t)B * cn_fused_kmax() * 6 * sizeof(unsigned long long)));
+  SWE_CUDA(cudaMalloc(&w.target2, (size_t)B * sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.flags, (size_t)B * sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.iters, (size_t)B * sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.counter, sizeof(int)));

@@ -23,6 +23,8 @@ struct Work {
   double *half = nullptr;   // NHALF half-spectrum arrays [M+1][J][2*cap]
   double *fspec = nullptr;  // NF analysis-input arrays  [M+1][J][2*cap]
   double *stats = nullptr;  // [cap][8]
+  unsigned long long *fstats = nullptr;  // [cap][cn_fused_kmax()][6] (k_cn_fused)
+  int *target2 = nullptr;   // [cap] k_cn_fused recompute targets
   int *flags = nullptr;     // [cap] active / converged flags, iteration counts
   int *iters = nullptr;     // [cap]
   int *counter = nullptr;   // device counter (active slices)

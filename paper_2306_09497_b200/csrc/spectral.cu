@@ -1364,6 +1364,299 @@ int cn_direct(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha
   return OK;
 }
 
+// Speculative fused Crank-Nicolson fixed point for the fine level (batches of
+// slices, M + 2 <= CF_MAXROW): one CTA = one pair of m-blocks (m, M - m), i.e.
+// M + 2 rows, x CF_S slices, with Phi, xi, delta and the rhs of all its modes
+// resident in shared memory.  L_C couples (m, n -+ 1) inside an m-block only, so
+// the CTA runs every fixed-point iteration without leaving the SM; what it cannot
+// know is when the slice converges (a max over all m).  It therefore runs a
+// GUESSED number of iterations G (the last observed count), records the per-slice
+// convergence maxima of EVERY iteration 1..G ([slice][iteration][6] ordered-bit
+// atomics) and stores the iterate reached at each slice's target.  k_cn_decide
+// then finds each slice's true first converged iteration k*: k* = G is the common
+// case (done); k* < G re-runs this kernel for those slices only with target k*;
+// no convergence by G leaves the slice active for the ordinary k_helm_tiled loop,
+// which continues from iterate G (xi/delta in A or B by iteration parity, as
+// k_helm_tiled expects).  Per-mode arithmetic is k_cn_start's and k_helm_tiled's,
+// so iterates, iteration counts and results are bitwise those of the
+// multi-kernel path (steppers.py:74-118, :143-152).
+constexpr int CF_S = 4, CF_EPT = 3, CF_NTMAX = 352, CF_MAXROW = CF_NTMAX * CF_EPT / CF_S,
+              CF_KS = 16;
+// local n-1 / n+1 rows of local row r in the parity-split m-block [base, base + km)
+// (the rows cor_nb points at; -1: none)
+SWE_DEV void cf_nbrs(int r, int base, int km, int &lo, int &hi) {
+  const int ne = (km + 1) >> 1, no = km >> 1, li = r - base;
+  if (li < ne) {  // n = m + 2 li: odd rows li - 1 and li
+    lo = li >= 1 ? base + ne + li - 1 : -1;
+    hi = li < no ? base + ne + li : -1;
+  } else {  // n = m + 1 + 2 (li - ne): even rows li - ne and li - ne + 1
+    lo = base + li - ne;
+    hi = li - ne + 1 < ne ? base + li - ne + 1 : -1;
+  }
+}
+__global__ void __launch_bounds__(CF_NTMAX, 2)
+    k_cn_fused(int M, int B, const int *__restrict__ offsets, const double4 *__restrict__ cft,
+               const double *__restrict__ eps, const double *__restrict__ phibar, Ptr3C x0,
+               Ptr3C x1, Ptr3C x2, double s, double alpha, Ptr3 R, int write_r, double *U0,
+               double *A1, double *A2, double *B1, double *B2, const int *__restrict__ target,
+               int G, unsigned long long *__restrict__ fst) {
+  extern __shared__ double2 fsm[];
+  const int m1 = blockIdx.x, m2 = M - m1;
+  const int km1 = M + 1 - m1, km2 = m2 > m1 ? M + 1 - m2 : 0, nrow = km1 + km2;
+  const int n = nrow * CF_S, NT = blockDim.x, tid = threadIdx.x;
+  // xi/delta iterates ping-pong between the A and B copies (iterate k lives in A
+  // when k is even, as in global memory); the rhs xi/delta rows in Q1/Q2; Phi and
+  // the rhs Phi have no stencil and stay in registers (pv, q0)
+  double2 *XA = fsm, *DA = XA + n, *XB = DA + n, *DB = XB + n, *Q1 = DB + n, *Q2 = Q1 + n;
+  double4 *rcf = reinterpret_cast<double4 *>(Q2 + n);
+  double *re = reinterpret_cast<double *>(rcf + nrow);
+  __shared__ unsigned long long sst[CF_KS][CF_S][6];
+  __shared__ int tgt[CF_S];
+  const int sl = tid % CF_S, b = blockIdx.y * CF_S + sl;
+  if (tid < CF_S) {
+    const int bb = blockIdx.y * CF_S + tid;
+    tgt[tid] = bb < B ? (target ? target[bb] : G) : 0;
+  }
+  for (int q = tid; q < CF_KS * CF_S * 6; q += NT) (&sst[0][0][0])[q] = 0ULL;
+  const int off1 = offsets[m1], off2 = km2 ? offsets[m2] : 0;
+  auto grow = [&](int r) { return r < km1 ? off1 + r : off2 + r - km1; };
+  for (int r = tid; r < nrow; r += NT) {
+    const int k = grow(r);
+    rcf[r] = cft[k];
+    re[r] = eps[k];
+  }
+  __syncthreads();
+  const int mytgt = tgt[sl];
+  int kmax = 0;
+#pragma unroll
+  for (int q = 0; q < CF_S; ++q) kmax = max(kmax, tgt[q]);
+  if (kmax == 0) return;  // no slice of this CTA needs work (uniform)
+  const bool act = mytgt > 0;
+  const double pb = act ? phibar[b] : 0.0, apb = alpha * pb, aap = alpha * alpha * pb;
+  int lo[CF_EPT], hi[CF_EPT];
+  double2 pv[CF_EPT], q0[CF_EPT];
+  // ---- prologue (as k_cn_start): X staged in the B copies
+#pragma unroll
+  for (int j = 0; j < CF_EPT; ++j) {
+    const int e = tid + j * NT, r = e / CF_S;
+    lo[j] = hi[j] = -1;
+    if (e < n && act) {
+      if (r < km1) cf_nbrs(r, 0, km1, lo[j], hi[j]);
+      else cf_nbrs(r, km1, km2, lo[j], hi[j]);
+      const size_t i = (size_t)grow(r) * B + b;
+      pv[j] = comb(x0, x1, x2, s, 0, i);
+      XB[e] = comb(x0, x1, x2, s, 1, i);
+      DB[e] = comb(x0, x1, x2, s, 2, i);
+    }
+  }
+  __syncthreads();
+  // rhs R = X + alpha (L_G X + L_C X), then the first iterate helm(R) into A
+#pragma unroll
+  for (int j = 0; j < CF_EPT; ++j) {
+    const int e = tid + j * NT, r = e / CF_S;
+    if (e < n && act) {
+      const double2 ph = pv[j], xi = XB[e], de = DB[e];
+      const double e_ = re[r];
+      const double4 cf = rcf[r];
+      double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
+      if (lo[j] >= 0) {
+        xl = XB[lo[j] * CF_S + sl];
+        dl = DB[lo[j] * CF_S + sl];
+      }
+      if (hi[j] >= 0) {
+        xh = XB[hi[j] * CF_S + sl];
+        dh = DB[hi[j] * CF_S + sl];
+      }
+      double2 lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * xi.y),
+                                -(cf.x * dl.y + cf.y * dh.y - cf.z * xi.x));
+      double2 lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * de.y,
+                                cf.x * xl.y + cf.y * xh.y + cf.z * de.x);
+      if (cf.w != 0.0) {
+        lx.y = 0.0;
+        lc.y = 0.0;
+      }
+      const double2 lphi = make_double2(-pb * de.x, -pb * de.y);
+      const double2 lde = add2(sc2(e_, ph), lc);
+      const double2 r0 = add2(ph, sc2(alpha, lphi)), r1 = add2(xi, sc2(alpha, lx)),
+                    r2 = add2(de, sc2(alpha, lde));
+      q0[j] = r0;
+      Q1[e] = r1;
+      Q2[e] = r2;
+      if (write_r) {
+        const size_t i = (size_t)grow(r) * B + b;
+        st2(R.p[0], i, r0);
+        st2(R.p[1], i, r1);
+        st2(R.p[2], i, r2);
+      }
+      const double apb_ = alpha * pb, denom = 1.0 + alpha * alpha * pb * e_;
+      const double2 nph =
+          make_double2((r0.x - apb_ * r2.x) / denom, (r0.y - apb_ * r2.y) / denom);
+      const double ae = alpha * e_;
+      pv[j] = nph;
+      XA[e] = r1;
+      DA[e] = make_double2(r2.x + ae * nph.x, r2.y + ae * nph.y);
+    }
+  }
+  __syncthreads();
+  // ---- fixed-point iterations 1..kmax (as k_helm_tiled), one barrier each
+  const int lane = tid & 31;
+  for (int it = 1; it <= kmax; ++it) {
+    const double2 *X = (it & 1) ? XA : XB, *D = (it & 1) ? DA : DB;
+    double2 *NX = (it & 1) ? XB : XA, *ND = (it & 1) ? DB : DA;
+    const bool out = it == mytgt;
+    unsigned long long mx[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < CF_EPT; ++j) {
+      const int e = tid + j * NT, r = e / CF_S;
+      if (e < n && act) {
+        const double2 rp = q0[j], r1 = Q1[e], r2 = Q2[e], o0 = pv[j];
+        const double e_ = re[r];
+        const double4 cf = rcf[r];
+        const double2 x = X[e], d = D[e];
+        double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
+        if (lo[j] >= 0) {
+          xl = X[lo[j] * CF_S + sl];
+          dl = D[lo[j] * CF_S + sl];
+        }
+        if (hi[j] >= 0) {
+          xh = X[hi[j] * CF_S + sl];
+          dh = D[hi[j] * CF_S + sl];
+        }
+        double2 lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * x.y),
+                                  -(cf.x * dl.y + cf.y * dh.y - cf.z * x.x));
+        double2 lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * d.y,
+                                  cf.x * xl.y + cf.y * xh.y + cf.z * d.x);
+        if (cf.w != 0.0) {
+          lx.y = 0.0;
+          lc.y = 0.0;
+        }
+        const double2 rx = add2(r1, sc2(alpha, lx)), rd = add2(r2, sc2(alpha, lc));
+        const double denom = 1.0 + aap * e_;
+        const double2 ph = make_double2((rp.x - apb * rd.x) / denom, (rp.y - apb * rd.y) / denom);
+        const double ae = alpha * e_;
+        const double2 de = make_double2(rd.x + ae * ph.x, rd.y + ae * ph.y);
+        mx[0] = max(mx[0], sqmag_bits(ph.x, ph.y));
+        mx[1] = max(mx[1], sqmag_bits(rx.x, rx.y));
+        mx[2] = max(mx[2], sqmag_bits(de.x, de.y));
+        mx[3] = max(mx[3], sqmag_bits(ph.x - o0.x, ph.y - o0.y));
+        mx[4] = max(mx[4], sqmag_bits(rx.x - x.x, rx.y - x.y));
+        mx[5] = max(mx[5], sqmag_bits(de.x - d.x, de.y - d.y));
+        pv[j] = ph;
+        NX[e] = rx;
+        ND[e] = de;
+        if (out) {
+          const size_t i = (size_t)grow(r) * B + b;
+          st2(U0, i, ph);
+          st2((it & 1) ? B1 : A1, i, rx);
+          st2((it & 1) ? B2 : A2, i, de);
+        }
+      }
+      asm volatile("" ::: "memory");  // one element's loads in flight at a time (registers)
+    }
+    // per-slice maxima: lanes of one slice differ in bits 2..4
+    if (fst && it <= CF_KS) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+#pragma unroll
+        for (int o = CF_S; o < 32; o <<= 1) mx[q] = max(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], o));
+        if (lane < CF_S && mx[q]) atomicMax(&sst[it - 1][lane][q], mx[q]);
+      }
+    }
+    __syncthreads();
+  }
+  if (fst) {
+    const int nk = min(kmax, CF_KS);
+    for (int q = tid; q < nk * CF_S * 6; q += NT) {
+      const int it = q / (CF_S * 6), ss = (q / 6) % CF_S, f = q % 6;
+      const int bb = blockIdx.y * CF_S + ss;
+      const unsigned long long v = sst[it][ss][f];
+      if (bb < B && tgt[ss] > 0 && v) atomicMax(fst + ((size_t)bb * CF_KS + it) * 6 + f, v);
+    }
+  }
+}
+
+int cn_fused_ok(int M, int B) { return M + 2 <= CF_MAXROW && B >= 1; }  // M <= 262
+int cn_fused_kmax() { return CF_KS; }
+
+int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *eps,
+             const double *phibar, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+             Ptr3 R, int write_r, double *U0, double *A1, double *A2, double *B1, double *B2,
+             const int *target, int G, unsigned long long *fst, cudaStream_t st) {
+  const int nrow = M + 2, n = nrow * CF_S;
+  const int NT = std::min(CF_NTMAX, ((n + CF_EPT - 1) / CF_EPT + 31) / 32 * 32);
+  const int smem = 6 * n * (int)sizeof(double2) + nrow * (int)(sizeof(double4) + sizeof(double));
+  static int attr = 0;
+  if (smem > attr) {
+    SWE_CUDA(cudaFuncSetAttribute(k_cn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
+  }
+  dim3 grid(M / 2 + 1, (B + CF_S - 1) / CF_S);
+  k_cn_fused<<<grid, NT, smem, st>>>(M, B, offsets, cf, eps, phibar, x0, x1, x2, s, alpha, R,
+                                     write_r, U0, A1, A2, B1, B2, target, G, fst);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
+// Per-slice decision after k_cn_fused (one block): first converged iteration k*
+// of each slice from the recorded maxima (decide_slice's test, steppers.py:100-112),
+// k* < G -> target2 = k* (recompute pass), none -> still active after G
+// iterations.  Sets counter = active slices, loop = G and, in a graph, the WHILE
+// node's condition; zeroes the maxima for the next call.
+SWE_DEV bool cf_converged(const unsigned long long *q6, double tol) {
+  double v[6];
+  for (int q = 0; q < 6; ++q) v[q] = sqrt(__longlong_as_double((long long)q6[q]));
+  double overall = fmax(fmax(v[0], v[1]), v[2]);
+  if (isnan(v[0]) || isnan(v[1]) || isnan(v[2])) overall = nan("");
+  overall = (overall > 1e-300 || isnan(overall)) ? overall : 1e-300;
+  for (int f = 0; f < 3; ++f) {
+    const double tiny = 1e-13 * overall;
+    const double scale = (v[f] >= tiny || isnan(v[f])) ? v[f] : tiny;
+    if (v[3 + f] > tol * scale) return false;
+  }
+  return true;
+}
+__global__ void k_cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters,
+                            int *target2, int *counter, int *loop, double tol,
+                            cudaGraphConditionalHandle h, int has_h, int max_iter) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    unsigned long long *q = fst + (size_t)b * CF_KS * 6;
+    int ks = 0;
+    for (int k = 1; k <= G && !ks; ++k)
+      if (cf_converged(q + (k - 1) * 6, tol)) ks = k;
+    for (int k = 0; k < G * 6; ++k) q[k] = 0ULL;
+    if (ks) {
+      flags[b] = 0;
+      iters[b] = ks;
+      target2[b] = ks < G ? ks : 0;
+    } else {
+      flags[b] = 1;
+      iters[b] = G;
+      target2[b] = 0;
+      ++mine;
+    }
+  }
+  if (mine) atomicAdd(&cnt, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *counter = cnt;
+    *loop = G;
+    if (has_h) cudaGraphSetConditional(h, (cnt > 0 && G < max_iter) ? 1u : 0u);
+  }
+}
+
+int cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters, int *target2,
+              int *counter, int *loop, double tol, const cudaGraphConditionalHandle *h,
+              int max_iter, cudaStream_t st) {
+  k_cn_decide<<<1, 1024, 0, st>>>(B, G, fst, flags, iters, target2, counter, loop, tol,
+                                  h ? *h : cudaGraphConditionalHandle(0), h != nullptr, max_iter);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
 // Fixed-point epilogue: slices whose iterate ended in the B buffers (odd iteration
 // count) copy xi/delta back to A = u[1], u[2]; with dtnu != 0 the viscosity
 // factor (dynamics.py:191-200) is applied to every slice on the way.

@@ -76,6 +76,18 @@ int cn_direct(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha
               const double *eps, const double *phibar, const int2 *nb, const double4 *cf,
               int rhs_given, double *const scratch[5], Ptr3 dst, double dtnu, double halfq,
               cudaStream_t st);
+// speculative fused fixed point (fine level, M <= 262; see k_cn_fused): G guessed
+// iterations with per-iteration maxima in fst [B][cn_fused_kmax()][6]; target
+// (nullable: all G) = the iteration whose iterate is stored per slice, 0 = skip
+int cn_fused_ok(int M, int B);
+int cn_fused_kmax();
+int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *eps,
+             const double *phibar, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
+             Ptr3 R, int write_r, double *U0, double *A1, double *A2, double *B1, double *B2,
+             const int *target, int G, unsigned long long *fst, cudaStream_t st);
+int cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters, int *target2,
+              int *counter, int *loop, double tol, const cudaGraphConditionalHandle *h,
+              int max_iter, cudaStream_t st);
 int add_col(int K, int n, int col, Ptr3 y, Ptr3C g, cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,

@@ -40,6 +40,7 @@ bool g_capturing = false;  // a step graph is being captured: no events, no host
 int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per step
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
+int g_cn_fused = 1;        // speculative smem-resident fixed point (k_cn_fused) on the fine level
 int g_fft_lw32 = 0;        // nonlinear lane FFT with 32 rows (2 slices) per CTA
 int g_gemv_max_b = 3;      // batches up to this size take the dot-product Legendre kernels
 int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: by batch)
@@ -642,7 +643,35 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     }
     return OK;
   }
-  if (rhs_given) {
+  // speculative fused fixed point (k_cn_fused): prologue plus the first G iterations
+  // in one pass, a decision, a recompute pass for slices that converged earlier
+  const bool fused = impl && !rhs_given && g_cn_fused && cfg.implicit_max_iter > 0 &&
+                     cn_fused_ok(pl->M, B);
+  const int G = std::max(1, std::min(std::min(pl->iter_guess, cfg.implicit_max_iter),
+                                     cn_fused_kmax()));
+  auto fused_passes = [&](const cudaGraphConditionalHandle *h) -> int {
+    Ptr3C X0 = {{x0[0], x0[1], x0[2]}}, X1 = {{nullptr, nullptr, nullptr}}, X2 = X1;
+    if (x1) {
+      X1 = {{x1[0], x1[1], x1[2]}};
+      X2 = {{x2[0], x2[1], x2[2]}};
+    }
+    Ptr3 R = {{b.R[0], b.R[1], b.R[2]}};
+    int rc2;
+    ProfScope ps(3, ((x1 ? 9.0 : 3.0) + 6.0) * 16.0 * K * B, r.st);
+    if ((rc2 = cn_fused(pl->M, B, pl->offsets, pl->cor_cf, pl->eps, w.phibar, X0, X1,
+                        X2, s, alpha, R, 1, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], nullptr, G,
+                        w.fstats, r.st)) ||
+        (rc2 = cn_decide(B, G, w.fstats, w.flags, w.iters, w.target2, w.counter, w.loop,
+                         cfg.implicit_tol, h, cfg.implicit_max_iter, r.st)) ||
+        (rc2 = cn_fused(pl->M, B, pl->offsets, pl->cor_cf, pl->eps, w.phibar, X0, X1,
+                        X2, s, alpha, R, 0, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], w.target2,
+                        G, nullptr, r.st)))
+      return rc2;
+    return OK;
+  };
+  if (fused) {
+    // the graph branch below launches the passes once its condition handle exists
+  } else if (rhs_given) {
     // implicit_linear_solve of a given right-hand side (steppers.py:74-118): b.R
     // already holds it; the first iterate is its Helmholtz solve
     const double *Rc[3] = {b.R[0], b.R[1], b.R[2]};
@@ -664,10 +693,12 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     // CUDA graph: the iteration loop is a conditional WHILE node whose body (Helmholtz
     // with inline L_C, decision, condition update) runs until no slice is active or
     // max_iter is reached; an unconverged exit raises *d_fail in the epilogue
-    if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
     SWE_CUDA(cudaMemsetAsync(w.stats, 0, sizeof(double) * 8 * B, r.st));
-    SWE_CUDA(cudaMemsetAsync(w.loop, 0, sizeof(int), r.st));
-    SWE_CUDA(cudaMemsetAsync(w.counter, 0, sizeof(int), r.st));
+    if (!fused) {
+      if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
+      SWE_CUDA(cudaMemsetAsync(w.loop, 0, sizeof(int), r.st));
+      SWE_CUDA(cudaMemsetAsync(w.counter, 0, sizeof(int), r.st));
+    }
     cudaStreamCaptureStatus cst;
     cudaGraph_t g;
     const cudaGraphNode_t *deps = nullptr;
@@ -676,6 +707,10 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     cudaGraphConditionalHandle h;
     SWE_CUDA(cudaGraphConditionalHandleCreate(&h, g, cfg.implicit_max_iter > 0 ? 1u : 0u,
                                               cudaGraphCondAssignDefault));
+    if (fused) {  // k_cn_decide sets the WHILE condition for the remaining iterations
+      if ((rc = fused_passes(&h))) return rc;
+      SWE_CUDA(cudaStreamGetCaptureInfo(r.st, &cst, nullptr, &g, &deps, &nd));
+    }
     cudaGraphNodeParams np = {cudaGraphNodeTypeConditional};
     np.conditional.handle = h;
     np.conditional.type = cudaGraphCondTypeWhile;
@@ -708,6 +743,14 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     const CorOp c{dst[1], dst[2], pl->cor_nb, pl->cor_cf};
     int launched = 0, batch = std::max(1, pl->iter_guess), maxit = 0;
     active = B;
+    if (fused) {
+      if ((rc = fused_passes(nullptr))) return rc;
+      launched = G;
+      batch = 1;
+      if ((rc = publish(B, w.counter, w.iters, w.d_pub, r.st))) return rc;
+      SWE_CUDA(cudaStreamSynchronize(r.st));
+      active = reinterpret_cast<volatile int *>(w.h_pub)[0];
+    }
     while (launched < cfg.implicit_max_iter && active > 0) {
       const int n = std::min(batch, cfg.implicit_max_iter - launched);
       for (int j = 0; j < n; ++j) {
@@ -938,7 +981,8 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
-         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16) | (g_cc_ctas << 17) | (g_gemv_max_b << 22);
+         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16) | (g_cc_ctas << 17) | (g_gemv_max_b << 22) |
+         (g_cn_fused << 25);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1399,6 +1443,10 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "cn_cluster") == 0 && value >= 0 && value <= 2) {
     g_cn_cluster = value;
+    return OK;
+  }
+  if (key && strcmp(key, "cn_fused") == 0 && (value == 0 || value == 1)) {
+    g_cn_fused = value;
     return OK;
   }
   if (key && strcmp(key, "helm_tiled") == 0 && (value == 0 || value == 1)) {

@@ -443,6 +443,64 @@ def test_coarse_half_step_variants_agree(mods, M, B, graphs):
             assert rel_diff(outs[name][b], outs["cluster"][b]) < 1e-13, (name, b)
 
 
+@pytest.mark.parametrize("M,B", [(256, 40), (101, 6), (64, 33)])
+@pytest.mark.parametrize("graphs", [0, 1])
+def test_fused_fixed_point_matches_multikernel(mods, M, B, graphs):
+    """The speculative shared-memory fixed point (k_cn_fused: guessed iteration count,
+    per-iteration maxima, recompute of early-converged slices, k_helm_tiled loop for
+    late ones) gives the multi-kernel path's iteration counts and bitwise states.
+    The dt sequence moves the guess above and below the true count (5 <-> 9)."""
+    spharm, dynamics, steppers, scenarios = mods
+    import torch
+    from paper_2306_09497_b200 import _lib
+    grid = spharm.get_grid(M)
+    base = scenarios.gaussian_bumps(grid, batch=B)
+    rng = np.random.default_rng(M + 7 * B)
+    taper = torch.from_numpy((grid.n_of + 1.0) ** -2).cuda()
+    noise = torch.from_numpy(rng.standard_normal((B, grid.n_modes))).cuda() * taper
+    noise[:, : M + 1] = noise[:, : M + 1].real
+    base.data[:, 1] += 1e-6 * noise
+    base.data[:, 2] += 1e-7 * noise
+    outs, its = {}, {}
+    _lib.set_option("graphs", graphs)
+    _lib.set_option("cn_cluster", 0)
+    try:
+        for fused in (0, 1):
+            _lib.set_option("cn_fused", fused)
+            s = base.copy()
+            seq = []
+            for dt in (60.0, 960.0, 60.0, 240.0):
+                cfg = steppers.StepperConfig(dt=dt, viscosity=dynamics.ViscositySpec(2, 1e5))
+                it = np.zeros((2, B, 2), dtype=np.int32)
+                steppers.imex_steps_inplace(s, cfg, 2, None if graphs else it)
+                seq.append(it)
+            outs[fused], its[fused] = s.data.cpu().numpy(), np.stack(seq)
+    finally:
+        _lib.set_option("cn_fused", 1)
+        _lib.set_option("cn_cluster", 1)
+        _lib.set_option("graphs", 1)
+    assert np.array_equal(its[0], its[1])
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_fused_fixed_point_nonconvergence_raises(mods):
+    """max_iter below the needed count on the fused path raises ImplicitSolveError
+    with the residual, eager and under graphs."""
+    spharm, dynamics, steppers, scenarios = mods
+    from paper_2306_09497_b200 import _lib
+    grid = spharm.get_grid(256)
+    s = scenarios.gaussian_bumps(grid, batch=36)
+    _lib.set_option("cn_cluster", 0)
+    try:
+        for mi in (1, 2):
+            cfg = steppers.StepperConfig(dt=600.0, implicit_max_iter=mi)
+            for _ in range(3):
+                with pytest.raises(steppers.ImplicitSolveError, match="residual"):
+                    steppers.imex_step(s, cfg)
+    finally:
+        _lib.set_option("cn_cluster", 1)
+
+
 def test_cluster_half_step_nonconvergence_raises(mods):
     """An unconverged fixed point on the cluster path raises ImplicitSolveError
     with the residual (eager and under graphs)."""
