@@ -1401,7 +1401,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
                double *A1, double *A2, double *B1, double *B2, const int *__restrict__ target,
                int G, unsigned long long *__restrict__ fst) {
   extern __shared__ double2 fsm[];
-  const int m1 = blockIdx.x, m2 = M - m1;
+  const int m1 = blockIdx.y, m2 = M - m1;  // slice groups fastest: CTAs in flight cover whole rows
   const int km1 = M + 1 - m1, km2 = m2 > m1 ? M + 1 - m2 : 0, nrow = km1 + km2;
   const int n = nrow * CF_S, NT = blockDim.x, tid = threadIdx.x;
   // xi/delta iterates ping-pong between the A and B copies (iterate k lives in A
@@ -1412,9 +1412,9 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
   double *re = reinterpret_cast<double *>(rcf + nrow);
   __shared__ unsigned long long sst[CF_KS][CF_S][6];
   __shared__ int tgt[CF_S];
-  const int sl = tid % CF_S, b = blockIdx.y * CF_S + sl;
+  const int sl = tid % CF_S, b = blockIdx.x * CF_S + sl;
   if (tid < CF_S) {
-    const int bb = blockIdx.y * CF_S + tid;
+    const int bb = blockIdx.x * CF_S + tid;
     tgt[tid] = bb < B ? (target ? target[bb] : G) : 0;
   }
   for (int q = tid; q < CF_KS * CF_S * 6; q += NT) (&sst[0][0][0])[q] = 0ULL;
@@ -1568,7 +1568,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
     const int nk = min(kmax, CF_KS);
     for (int q = tid; q < nk * CF_S * 6; q += NT) {
       const int it = q / (CF_S * 6), ss = (q / 6) % CF_S, f = q % 6;
-      const int bb = blockIdx.y * CF_S + ss;
+      const int bb = blockIdx.x * CF_S + ss;
       const unsigned long long v = sst[it][ss][f];
       if (bb < B && tgt[ss] > 0 && v) atomicMax(fst + ((size_t)bb * CF_KS + it) * 6 + f, v);
     }
@@ -1590,7 +1590,7 @@ int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *
     SWE_CUDA(cudaFuncSetAttribute(k_cn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = smem;
   }
-  dim3 grid(M / 2 + 1, (B + CF_S - 1) / CF_S);
+  dim3 grid((B + CF_S - 1) / CF_S, M / 2 + 1);
   k_cn_fused<<<grid, NT, smem, st>>>(M, B, offsets, cf, eps, phibar, x0, x1, x2, s, alpha, R,
                                      write_r, U0, A1, A2, B1, B2, target, G, fst);
   SWE_LAUNCH_CHECK();
