@@ -1417,7 +1417,14 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
     const int bb = blockIdx.x * CF_S + tid;
     tgt[tid] = bb < B ? (target ? target[bb] : G) : 0;
   }
-  for (int q = tid; q < CF_KS * CF_S * 6; q += NT) (&sst[0][0][0])[q] = 0ULL;
+  __syncthreads();
+  const int mytgt = tgt[sl];
+  int kmax = 0;
+#pragma unroll
+  for (int q = 0; q < CF_S; ++q) kmax = max(kmax, tgt[q]);
+  if (kmax == 0) return;  // no slice of this CTA needs work (uniform; recompute pass)
+  if (fst)
+    for (int q = tid; q < CF_KS * CF_S * 6; q += NT) (&sst[0][0][0])[q] = 0ULL;
   const int off1 = offsets[m1], off2 = km2 ? offsets[m2] : 0;
   auto grow = [&](int r) { return r < km1 ? off1 + r : off2 + r - km1; };
   for (int r = tid; r < nrow; r += NT) {
@@ -1426,16 +1433,15 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
     re[r] = eps[k];
   }
   __syncthreads();
-  const int mytgt = tgt[sl];
-  int kmax = 0;
-#pragma unroll
-  for (int q = 0; q < CF_S; ++q) kmax = max(kmax, tgt[q]);
-  if (kmax == 0) return;  // no slice of this CTA needs work (uniform)
   const bool act = mytgt > 0;
   const double pb = act ? phibar[b] : 0.0, apb = alpha * pb, aap = alpha * alpha * pb;
   int lo[CF_EPT], hi[CF_EPT];
   double2 pv[CF_EPT], q0[CF_EPT];
-  // ---- prologue (as k_cn_start): X staged in the B copies
+  // ---- prologue (as k_cn_start): X staged in the B copies.  The xi/delta inputs go
+  // global -> shared by cp.async (no registers, all loads of a thread in flight):
+  // a single input straight into XB/DB; with the Heun terms x0 -> XA/DA, x1 ->
+  // Q1/Q2, x2 -> XB/DB, combined as comb() does once they have landed.
+  const bool heun = x1.p[0] != nullptr;
 #pragma unroll
   for (int j = 0; j < CF_EPT; ++j) {
     const int e = tid + j * NT, r = e / CF_S;
@@ -1444,12 +1450,44 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
       if (r < km1) cf_nbrs(r, 0, km1, lo[j], hi[j]);
       else cf_nbrs(r, km1, km2, lo[j], hi[j]);
       const size_t i = (size_t)grow(r) * B + b;
+      if (heun) {
+        cp_async16(&XA[e], x0.p[1] + 2 * i, true);
+        cp_async16(&DA[e], x0.p[2] + 2 * i, true);
+        cp_async16(&Q1[e], x1.p[1] + 2 * i, true);
+        cp_async16(&Q2[e], x1.p[2] + 2 * i, true);
+        cp_async16(&XB[e], x2.p[1] + 2 * i, true);
+        cp_async16(&DB[e], x2.p[2] + 2 * i, true);
+      } else {
+        cp_async16(&XB[e], x0.p[1] + 2 * i, true);
+        cp_async16(&DB[e], x0.p[2] + 2 * i, true);
+      }
       pv[j] = comb(x0, x1, x2, s, 0, i);
-      XB[e] = comb(x0, x1, x2, s, 1, i);
-      DB[e] = comb(x0, x1, x2, s, 2, i);
     }
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
+  if (heun) {
+    double2 cx[CF_EPT], cd[CF_EPT];
+#pragma unroll
+    for (int j = 0; j < CF_EPT; ++j) {
+      const int e = tid + j * NT;
+      if (e < n && act) {
+        const double2 ax = Q1[e], bx = XB[e], ad = Q2[e], bd = DB[e];
+        cx[j] = add2(XA[e], sc2(s, make_double2(ax.x + bx.x, ax.y + bx.y)));
+        cd[j] = add2(DA[e], sc2(s, make_double2(ad.x + bd.x, ad.y + bd.y)));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CF_EPT; ++j) {
+      const int e = tid + j * NT;
+      if (e < n && act) {  // own elements only: no barrier needed between
+        XB[e] = cx[j];
+        DB[e] = cd[j];
+      }
+    }
+    __syncthreads();
+  }
   // rhs R = X + alpha (L_G X + L_C X), then the first iterate helm(R) into A
 #pragma unroll
   for (int j = 0; j < CF_EPT; ++j) {
