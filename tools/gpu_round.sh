@@ -5,5 +5,4 @@ timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&
 tail -3 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/ncu_one.py > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fft_lanes|leg_synth_v3|leg_anal_v3|k_helm_tiled|k_cn_start|k_cn_finish" -c 8 -o gpurun_out/full python tools/ncu_one.py > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
+bash tools/gpu_ncu.sh

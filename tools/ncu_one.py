@@ -1,4 +1,5 @@
-"""Minimal driver for ncu: one warm cfg2 fine step (M=256, 64 slices)."""
+"""Minimal driver for ncu: one cfg2 fine step (M=256, 64 slices) after a warm-up step
+(steady-state iteration guess); run ncu with --profile-from-start off."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -12,4 +13,8 @@ cfg = steppers.StepperConfig(dt=60.0, viscosity=dynamics.ViscositySpec(2, 1e5))
 st = bench.make_states(grid, 64, 0)
 steppers.imex_steps_inplace(st, cfg, 1)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()
+steppers.imex_steps_inplace(st, cfg, 1)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok")
