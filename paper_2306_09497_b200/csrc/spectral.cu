@@ -1399,7 +1399,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
                const double *__restrict__ eps, const double *__restrict__ phibar, Ptr3C x0,
                Ptr3C x1, Ptr3C x2, double s, double alpha, Ptr3 R, int write_r, double *U0,
                double *A1, double *A2, double *B1, double *B2, const int *__restrict__ target,
-               int G, unsigned long long *__restrict__ fst) {
+               int G, unsigned long long *__restrict__ fst, double dtnu, double halfq) {
   extern __shared__ double2 fsm[];
   const int m1 = blockIdx.y, m2 = M - m1;  // slice groups fastest: CTAs in flight cover whole rows
   const int km1 = M + 1 - m1, km2 = m2 > m1 ? M + 1 - m2 : 0, nrow = km1 + km2;
@@ -1409,7 +1409,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
   // the rhs Phi have no stencil and stay in registers (pv, q0)
   double2 *XA = fsm, *DA = XA + n, *XB = DA + n, *DB = XB + n, *Q1 = DB + n, *Q2 = Q1 + n;
   double4 *rcf = reinterpret_cast<double4 *>(Q2 + n);
-  double *re = reinterpret_cast<double *>(rcf + nrow);
+  double *re = reinterpret_cast<double *>(rcf + nrow), *rbh = re + nrow;
   __shared__ unsigned long long sst[CF_KS][CF_S][6];
   __shared__ int tgt[CF_S];
   const int sl = tid % CF_S, b = blockIdx.x * CF_S + sl;
@@ -1421,7 +1421,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
   const int mytgt = tgt[sl];
   int kmax = 0;
 #pragma unroll
-  for (int q = 0; q < CF_S; ++q) kmax = max(kmax, tgt[q]);
+  for (int q = 0; q < CF_S; ++q) kmax = max(kmax, abs(tgt[q]));
   if (kmax == 0) return;  // no slice of this CTA needs work (uniform; recompute pass)
   if (fst)
     for (int q = tid; q < CF_KS * CF_S * 6; q += NT) (&sst[0][0][0])[q] = 0ULL;
@@ -1431,9 +1431,14 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
     const int k = grow(r);
     rcf[r] = cft[k];
     re[r] = eps[k];
+    rbh[r] = dtnu != 0.0 ? 1.0 / (1.0 + dtnu * pow(eps[k], halfq)) : 1.0;  // as k_cn_finish
   }
   __syncthreads();
-  const bool act = mytgt > 0;
+  // target > 0: final result at that iteration (viscosity applied, xi/delta in A,
+  // as k_cn_finish would leave it); < 0: the raw iterate -target in its parity
+  // buffer for the k_helm_tiled loop to continue from; 0: nothing to do
+  const bool act = mytgt != 0, fin = mytgt > 0;
+  const int kout = abs(mytgt);
   const double pb = act ? phibar[b] : 0.0, apb = alpha * pb, aap = alpha * alpha * pb;
   int lo[CF_EPT], hi[CF_EPT];
   double2 pv[CF_EPT], q0[CF_EPT];
@@ -1541,7 +1546,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
   for (int it = 1; it <= kmax; ++it) {
     const double2 *X = (it & 1) ? XA : XB, *D = (it & 1) ? DA : DB;
     double2 *NX = (it & 1) ? XB : XA, *ND = (it & 1) ? DB : DA;
-    const bool out = it == mytgt;
+    const bool out = it == kout;
     unsigned long long mx[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int j = 0; j < CF_EPT; ++j) {
@@ -1584,9 +1589,20 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
         ND[e] = de;
         if (out) {
           const size_t i = (size_t)grow(r) * B + b;
-          st2(U0, i, ph);
-          st2((it & 1) ? B1 : A1, i, rx);
-          st2((it & 1) ? B2 : A2, i, de);
+          if (!fin) {
+            st2(U0, i, ph);
+            st2((it & 1) ? B1 : A1, i, rx);
+            st2((it & 1) ? B2 : A2, i, de);
+          } else if (dtnu != 0.0) {
+            const double bh = rbh[r];
+            st2(U0, i, sc2(bh, ph));
+            st2(A1, i, sc2(bh, rx));
+            st2(A2, i, sc2(bh, de));
+          } else {
+            st2(U0, i, ph);
+            st2(A1, i, rx);
+            st2(A2, i, de);
+          }
         }
       }
       asm volatile("" ::: "memory");  // one element's loads in flight at a time (registers)
@@ -1608,7 +1624,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
       const int it = q / (CF_S * 6), ss = (q / 6) % CF_S, f = q % 6;
       const int bb = blockIdx.x * CF_S + ss;
       const unsigned long long v = sst[it][ss][f];
-      if (bb < B && tgt[ss] > 0 && v) atomicMax(fst + ((size_t)bb * CF_KS + it) * 6 + f, v);
+      if (bb < B && tgt[ss] != 0 && v) atomicMax(fst + ((size_t)bb * CF_KS + it) * 6 + f, v);
     }
   }
 }
@@ -1619,10 +1635,11 @@ int cn_fused_kmax() { return CF_KS; }
 int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *eps,
              const double *phibar, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              Ptr3 R, int write_r, double *U0, double *A1, double *A2, double *B1, double *B2,
-             const int *target, int G, unsigned long long *fst, cudaStream_t st) {
+             const int *target, int G, unsigned long long *fst, double dtnu, double halfq,
+             cudaStream_t st) {
   const int nrow = M + 2, n = nrow * CF_S;
   const int NT = std::min(CF_NTMAX, ((n + CF_EPT - 1) / CF_EPT + 31) / 32 * 32);
-  const int smem = 6 * n * (int)sizeof(double2) + nrow * (int)(sizeof(double4) + sizeof(double));
+  const int smem = 6 * n * (int)sizeof(double2) + nrow * (int)(sizeof(double4) + 2 * sizeof(double));
   static int attr = 0;
   if (smem > attr) {
     SWE_CUDA(cudaFuncSetAttribute(k_cn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1630,7 +1647,7 @@ int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *
   }
   dim3 grid((B + CF_S - 1) / CF_S, M / 2 + 1);
   k_cn_fused<<<grid, NT, smem, st>>>(M, B, offsets, cf, eps, phibar, x0, x1, x2, s, alpha, R,
-                                     write_r, U0, A1, A2, B1, B2, target, G, fst);
+                                     write_r, U0, A1, A2, B1, B2, target, G, fst, dtnu, halfq);
   SWE_LAUNCH_CHECK();
   return OK;
 }
@@ -1669,11 +1686,11 @@ __global__ void k_cn_decide(int B, int G, unsigned long long *fst, int *flags, i
     if (ks) {
       flags[b] = 0;
       iters[b] = ks;
-      target2[b] = ks < G ? ks : 0;
+      target2[b] = ks < G ? ks : 0;  // recompute the final result at k*
     } else {
       flags[b] = 1;
       iters[b] = G;
-      target2[b] = 0;
+      target2[b] = -G;  // pass 1 stored a final result: recompute the raw iterate G
       ++mine;
     }
   }
@@ -1700,10 +1717,11 @@ int cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters, int
 // factor (dynamics.py:191-200) is applied to every slice on the way.
 __global__ void k_cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2,
                             const int *iters, const double *nn1a2, double dtnu, double halfq,
-                            const int *counter, int *fail) {
+                            const int *counter, int *fail, const int *skip) {
   if (fail && blockIdx.x == 0 && threadIdx.x == 0 && *counter > 0) *fail = 1;
   FOR_KB(K, B) {
     const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
+    if (skip && skip[b] >= 0) continue;  // finished by k_cn_fused
     const bool odd = iters && (iters[b] & 1);
     if (dtnu != 0.0) {
       const double bh = 1.0 / (1.0 + dtnu * pow(nn1a2[k], halfq));
@@ -1917,9 +1935,9 @@ int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
 
 int cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2, const int *iters,
               const double *nn1a2, double dtnu, double halfq, cudaStream_t st,
-              const int *counter, int *fail) {
+              const int *counter, int *fail, const int *skip) {
   k_cn_finish<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, u, b1, b2, iters, nn1a2, dtnu, halfq,
-                                                      counter, fail);
+                                                      counter, fail, skip);
   SWE_LAUNCH_CHECK();
   return OK;
 }

@@ -78,13 +78,15 @@ int cn_direct(int M, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha
               cudaStream_t st);
 // speculative fused fixed point (fine level, M <= 262; see k_cn_fused): G guessed
 // iterations with per-iteration maxima in fst [B][cn_fused_kmax()][6]; target
-// (nullable: all G) = the iteration whose iterate is stored per slice, 0 = skip
+// (nullable: all G) per slice: > 0 the final (viscosity-applied) result of that
+// iteration, < 0 the raw iterate -target for the k_helm_tiled loop, 0 skip
 int cn_fused_ok(int M, int B);
 int cn_fused_kmax();
 int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *eps,
              const double *phibar, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              Ptr3 R, int write_r, double *U0, double *A1, double *A2, double *B1, double *B2,
-             const int *target, int G, unsigned long long *fst, cudaStream_t st);
+             const int *target, int G, unsigned long long *fst, double dtnu, double halfq,
+             cudaStream_t st);
 int cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters, int *target2,
               int *counter, int *loop, double tol, const cudaGraphConditionalHandle *h,
               int max_iter, cudaStream_t st);
@@ -92,10 +94,11 @@ int add_col(int K, int n, int col, Ptr3 y, Ptr3C g, cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
              cudaStream_t st);
-// counter/fail (nullable): graph mode records an unconverged fixed point in *fail
+// counter/fail (nullable): graph mode records an unconverged fixed point in *fail;
+// skip (nullable): slices with skip[b] >= 0 were finished by k_cn_fused
 int cn_finish(int K, int B, Ptr3 u, const double *b1, const double *b2, const int *iters,
               const double *nn1a2, double dtnu, double halfq, cudaStream_t st,
-              const int *counter = nullptr, int *fail = nullptr);
+              const int *counter = nullptr, int *fail = nullptr, const int *skip = nullptr);
 int loop_cond(cudaGraphConditionalHandle h, const int *counter, int *loop, int max_iter,
               cudaStream_t st);
 int decide(int B, double *stats, int *active, int *iters, int *counter, double tol,

@@ -660,12 +660,12 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     ProfScope ps(3, ((x1 ? 9.0 : 3.0) + 6.0) * 16.0 * K * B, r.st);
     if ((rc2 = cn_fused(pl->M, B, pl->offsets, pl->cor_cf, pl->eps, w.phibar, X0, X1,
                         X2, s, alpha, R, 1, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], nullptr, G,
-                        w.fstats, r.st)) ||
+                        w.fstats, dtnu, cfg.visc_order / 2.0, r.st)) ||
         (rc2 = cn_decide(B, G, w.fstats, w.flags, w.iters, w.target2, w.counter, w.loop,
                          cfg.implicit_tol, h, cfg.implicit_max_iter, r.st)) ||
         (rc2 = cn_fused(pl->M, B, pl->offsets, pl->cor_cf, pl->eps, w.phibar, X0, X1,
                         X2, s, alpha, R, 0, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], w.target2,
-                        G, nullptr, r.st)))
+                        G, nullptr, dtnu, cfg.visc_order / 2.0, r.st)))
       return rc2;
     return OK;
   };
@@ -733,7 +733,7 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     SWE_CUDA(cudaStreamUpdateCaptureDependencies(r.st, &node, 1, cudaStreamSetCaptureDependencies));
     Ptr3 u = {{dst[0], dst[1], dst[2]}};
     return cn_finish(K, B, u, b.LC[0], b.LC[1], w.iters, pl->eps, dtnu, cfg.visc_order / 2.0, r.st,
-                     w.counter, w.d_fail);
+                     w.counter, w.d_fail, fused ? w.target2 : nullptr);
   }
   if (impl) {
     if ((rc = fill_int(w.flags, B, 1, r.st)) || (rc = fill_int(w.iters, B, 0, r.st))) return rc;
@@ -784,7 +784,8 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     ProfScope ps(3, (dtnu != 0.0 ? 6.0 : 4.0) * 16.0 * K * B, r.st);
     Ptr3 u = {{dst[0], dst[1], dst[2]}};
     if ((rc = cn_finish(K, B, u, b.LC[0], b.LC[1], impl ? w.iters : nullptr, pl->eps,
-                        active > 0 ? 0.0 : dtnu, cfg.visc_order / 2.0, r.st)))
+                        active > 0 ? 0.0 : dtnu, cfg.visc_order / 2.0, r.st, nullptr, nullptr,
+                        fused ? w.target2 : nullptr)))
       return rc;
   }
   if (active > 0) {
