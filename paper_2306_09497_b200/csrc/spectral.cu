@@ -1525,7 +1525,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
       q0[j] = r0;
       Q1[e] = r1;
       Q2[e] = r2;
-      if (write_r) {
+      if (write_r && mytgt < 0) {  // rhs only for slices the tiled loop continues
         const size_t i = (size_t)grow(r) * B + b;
         st2(R.p[0], i, r0);
         st2(R.p[1], i, r1);

@@ -657,14 +657,14 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     }
     Ptr3 R = {{b.R[0], b.R[1], b.R[2]}};
     int rc2;
-    ProfScope ps(3, ((x1 ? 9.0 : 3.0) + 6.0) * 16.0 * K * B, r.st);
+    ProfScope ps(3, ((x1 ? 9.0 : 3.0) + 3.0) * 16.0 * K * B, r.st);
     if ((rc2 = cn_fused(pl->M, B, pl->offsets, pl->cor_cf, pl->eps, w.phibar, X0, X1,
-                        X2, s, alpha, R, 1, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], nullptr, G,
+                        X2, s, alpha, R, 0, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], nullptr, G,
                         w.fstats, dtnu, cfg.visc_order / 2.0, r.st)) ||
         (rc2 = cn_decide(B, G, w.fstats, w.flags, w.iters, w.target2, w.counter, w.loop,
                          cfg.implicit_tol, h, cfg.implicit_max_iter, r.st)) ||
         (rc2 = cn_fused(pl->M, B, pl->offsets, pl->cor_cf, pl->eps, w.phibar, X0, X1,
-                        X2, s, alpha, R, 0, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], w.target2,
+                        X2, s, alpha, R, 1, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], w.target2,
                         G, nullptr, dtnu, cfg.visc_order / 2.0, r.st)))
       return rc2;
     return OK;
