@@ -49,7 +49,17 @@ typedef struct {
   int implicit_solver;     /* 0: the reference fixed point (default); 1: direct per-m
                               tridiagonal solve of the same system,
                               no iterations (iters_out = 0), never SWE_ENOCONV */
+  int select_batch;        /* 0 (default): kernels chosen for `batch`; n > 0: chosen as for
+                              a batch of n slices, whatever `batch` is.  A slice's result
+                              is bitwise a function of (its input, select_batch) only, so a
+                              sharded engine that passes the GLOBAL slice count reproduces
+                              the one-rank trace bitwise (SPEC.md:330 worker invariance) */
 } swe_stepper_cfg;
+
+/* sizeof(swe_stepper_cfg) as compiled into the library: bindings check it
+ * against their own struct before the first call (the struct is passed by
+ * pointer, so a short binding struct would be read past its end). */
+int swe_stepper_cfg_size(void);
 
 /* SphereGrid(Truncation.for_wavenumber(M), SphereGeometry(a, omega, g))
  * -- spharm.py:154-202, get_grid spharm.py:346-349. */

@@ -178,9 +178,136 @@ def gen_settls(M, seed):
                 u=u, v=v, dep_dt=900.0, lam=lam, th=th, vals=vals, adv=adv)
 
 
+# --------------------------------------------------------------------------- round 2
+# Compact PinT goldens for the BASELINE configs at their real parameters: every
+# C-point of every iteration on the modes n <= window (the modes the coarse
+# level corrects), full states at the middle and last C-point, per-field max|.|
+# of every C-point, and the reference's own run-pint outputs (errors.csv /
+# spectrum.csv written by runner._pint_outputs from the same trace).
+
+# acceptance C10 configs (/root/reference/pkg/tests/test_acceptance.py:251-275)
+AC10_CONFIG = {
+    "scenario": "gaussian_bumps", "T": 6 * 3600.0,
+    "fine": {"M": 64, "dt": 240.0, "scheme": "imex", "viscosity": {"order": 2, "coeff": 0.0}},
+    "pint": {"nlevels": 2, "cfactor": 2, "nrelax": 0, "max_iters": 5, "chunk_size": 0,
+             "coarse": {"M": 32, "scheme": "imex", "viscosity": {"order": 2, "coeff": 1.0e5}}},
+    "diagnostics": {"rnorms": [8, 32], "spectrum_iterations": [0, 5], "l2": False},
+}
+AC10_AGGRESSIVE = {
+    "scenario": "gaussian_bumps", "T": 48 * 240.0,
+    "fine": {"M": 64, "dt": 240.0, "scheme": "imex", "viscosity": {"order": 2, "coeff": 0.0}},
+    "pint": {"nlevels": 3, "cfactor": 4, "nrelax": 0, "max_iters": 5, "chunk_size": 0,
+             "coarse": {"M": 32, "scheme": "imex", "viscosity": {"order": 2, "coeff": 1.0e5}}},
+    "diagnostics": {"rnorms": [8, 32], "spectrum_iterations": [0], "l2": False},
+}
+
+
+def _with(cfg, **pint_over):
+    import copy
+    out = copy.deepcopy(cfg)
+    for k, v in pint_over.items():
+        if k in ("T",):
+            out[k] = v
+        else:
+            out["pint"][k] = v
+    return out
+
+
+# cfg1 (BASELINE configs[0]): the bumps-pint-desk preset
+# (config.py:113-124) on 8 intervals x 4 fine steps = N0 32 (T = 7680 s),
+# Parareal (nrelax 0, cfactor 2), 5 iterations
+CFG1 = _with(AC10_CONFIG, T=32 * 240.0)
+# cfg3's level structure (3 levels, cfactor 4, nrelax 2, F_then_V) at M=64/32
+CFG3_STRUCT = _with(AC10_AGGRESSIVE, nrelax=2, max_iters=4)
+
+
+def gen_pint_run(name, cfg, window=32):
+    """Reference trace of runner.cmd_run_pint's computation for `cfg`
+    (runner.py:215-257), stored compactly, plus its errors.csv/spectrum.csv."""
+    import tempfile
+    from pintswe import pint, runner
+    pcfg = runner.build_pint_config(cfg)
+    geometry = runner.build_geometry(cfg)
+    prob = pint.SweProblem(pcfg, geometry)
+    u0 = runner.initial_state(cfg, pcfg.levels[0].M, geometry)
+    fine = pint.fine_serial_cpoints(prob, pcfg, u0)
+    tr = pint.mgrit_run(prob, pcfg, u0, fine_reference=fine)
+    g0 = prob.grids[0]
+    sel = np.flatnonzero(g0.n_of <= window)
+    snaps = np.stack([np.stack([_state_arrays(x) for x in snap]) for snap in tr.snapshots])
+    fine_a = np.stack([_state_arrays(x) for x in fine])
+    n1 = snaps.shape[1] - 1
+    full_idx = np.array(sorted({n1 // 2, n1}))
+    with tempfile.TemporaryDirectory() as td:
+        runner._pint_outputs(td, cfg, tr, fine[-1], None, 0.0, "ok", 1)
+        errors = open(os.path.join(td, "errors.csv")).read()
+        spectrum = open(os.path.join(td, "spectrum.csv")).read()
+    lv = pcfg.levels
+    return dict(name=name, config_json=json.dumps(cfg, sort_keys=True), window=window, sel=sel,
+                fineM=lv[0].M, coarseM=lv[1].M, dt0=lv[0].dt, T=pcfg.T, N0=pcfg.N0,
+                nlevels=pcfg.nlevels, cfactor=pcfg.cfactor, nrelax=pcfg.nrelax,
+                iters=pcfg.max_iters, nu_f=lv[0].stepper.viscosity.coeff_nu,
+                nu_c=lv[1].stepper.viscosity.coeff_nu, cycle=pcfg.cycle,
+                u0=_state_arrays(u0), phibar=u0.phibar,
+                snap_window=snaps[..., sel], snap_full_idx=full_idx,
+                snap_full=snaps[:, full_idx], snap_maxabs=np.abs(snaps).max(axis=-1),
+                fine_window=fine_a[..., sel], fine_final=fine_a[-1],
+                errors_csv=np.array(errors), spectrum_csv=np.array(spectrum))
+
+
+def gen_m1024_step(window=64):
+    """cfg5's step (M=1024, dt=2 s, nu=0, gaussian_bumps, steppers.py:155-168) on
+    the modes n <= window, with per-field max|.| of the whole output."""
+    out = gen_window_step(1024, 2.0, 0.0, window=window)
+    return out
+
+
+def gen_m1024_sht(seed=230609497, nfs=2, rows=(0, 1, 383, 768, 1536)):
+    """cfg4's transforms at M=1024 on `nfs` field-slices drawn with cfg4's law
+    (amplitude (n+1)^-1.5, random phase, m = 0 real): synthesis on a few latitude
+    rows, analysis of a seeded random grid on n <= 64 plus max|.|."""
+    from pintswe.spharm import get_grid
+    M = 1024
+    g = get_grid(M)
+    rng = np.random.default_rng(seed)
+    ph = rng.uniform(0.0, 2.0 * np.pi, size=(nfs, g.n_modes))
+    amp = (g.n_of + 1.0) ** -1.5
+    c = amp * np.exp(1j * ph)
+    c[:, : M + 1] = amp[: M + 1] * np.cos(ph[:, : M + 1])
+    rows = np.array(rows)
+    syn = np.stack([g.synthesis(x)[rows] for x in c])
+    rng2 = np.random.default_rng(seed + 1)
+    gin = rng2.standard_normal((nfs, g.nlat, g.nlon))
+    an = np.stack([g.analysis(x) for x in gin])
+    sel = np.flatnonzero(g.n_of <= 64)
+    # the coefficients are regenerated from `seed` by the tests (cfg4's law above)
+    return dict(M=M, seed=seed, nfs=nfs, rows=rows, synthesis_rows=syn,
+                synthesis_maxabs=np.array([np.abs(g.synthesis(x)).max() for x in c]),
+                grid_seed=seed + 1, analysis_window=an[:, sel], sel=sel,
+                analysis_maxabs=np.abs(an).max(axis=-1))
+
+
+def main_r2(which):
+    """Round-2 goldens: `python oracle/make_golden.py cfg1 ac10 cfg3s m1024 m1024sht`."""
+    jobs = {
+        "cfg1": ("pint_cfg1_M64.npz", lambda: gen_pint_run("cfg1", CFG1)),
+        "ac10": ("pint_ac10_M64.npz", lambda: gen_pint_run("ac10", AC10_CONFIG)),
+        "ac10agg": ("pint_ac10agg_M64.npz", lambda: gen_pint_run("ac10agg", AC10_AGGRESSIVE)),
+        "cfg3s": ("pint_cfg3s_M64.npz", lambda: gen_pint_run("cfg3s", CFG3_STRUCT)),
+        "m1024": ("step_window_M1024.npz", gen_m1024_step),
+        "m1024sht": ("sht_M1024.npz", gen_m1024_sht),
+    }
+    for w in which:
+        fn, job = jobs[w]
+        np.savez_compressed(os.path.join(OUT, fn), **job())
+        print("wrote", fn, flush=True)
+
+
 def main():
     sys.path.insert(0, REF)
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1:
+        return main_r2(sys.argv[1:])
     np.savez_compressed(os.path.join(OUT, "sht_M16.npz"), **gen_sht(16, 230609497))
     np.savez_compressed(os.path.join(OUT, "sht_M32.npz"), **gen_sht(32, 230609498))
     np.savez_compressed(os.path.join(OUT, "tend_M24.npz"), **gen_tendencies(24, 7))

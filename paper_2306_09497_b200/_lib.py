@@ -22,6 +22,7 @@ EXPORTS = (
     "swe_kernel_launches", "swe_last_error", "swe_profile", "swe_profile_read",
     "swe_set_option", "swe_ke_spectrum", "swe_window_maxdiff", "swe_grid_sqdiff",
     "swe_settls_step", "swe_departure_points", "swe_interpolate", "swe_imex_sweep",
+    "swe_stepper_cfg_size",
 )
 
 
@@ -31,7 +32,8 @@ class StepperCfgC(ctypes.Structure):
     _fields_ = [("dt", ctypes.c_double), ("visc_order", ctypes.c_int),
                 ("visc_nu", ctypes.c_double), ("coriolis_implicit", ctypes.c_int),
                 ("include_nonlinear", ctypes.c_int), ("implicit_tol", ctypes.c_double),
-                ("implicit_max_iter", ctypes.c_int), ("implicit_solver", ctypes.c_int)]
+                ("implicit_max_iter", ctypes.c_int), ("implicit_solver", ctypes.c_int),
+                ("select_batch", ctypes.c_int)]
 
 
 class NoConvergence(RuntimeError):
@@ -82,11 +84,15 @@ def load(path: str = LIB_PATH):
         "swe_departure_points": (I, [P, P, P, P, P, I, D, I, P, P, P]),
         "swe_interpolate": (I, [P, P, P, P, I, P, P]),
         "swe_imex_sweep": (I, [P, P, P, I, P, ctypes.POINTER(StepperCfgC), P, P]),
+        "swe_stepper_cfg_size": (I, []),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.swe_stepper_cfg_size() != ctypes.sizeof(StepperCfgC):
+        raise RuntimeError(f"{path}: swe_stepper_cfg is {lib.swe_stepper_cfg_size()} bytes, "
+                           f"the binding's is {ctypes.sizeof(StepperCfgC)} (stale library?)")
     _lib = lib
     return lib
 

@@ -87,7 +87,7 @@ struct swe_plan {
   // CUDA graphs of one IMEX step (stepper.cu), keyed by batch, stepper config and
   // tuning switches; invalidated when the workspace is reallocated
   struct StepGraph {
-    int B;
+    int B, Bsel;
     double dt, nu, tol;
     int order, cor_impl, nonlin, max_iter, opts, solver;
     cudaGraph_t graph;

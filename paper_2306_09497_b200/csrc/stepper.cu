@@ -87,6 +87,11 @@ struct ProfScope {
 struct Run {
   swe_plan *pl;
   int B;
+  // batch the kernel generation is chosen for (swe_stepper_cfg.select_batch; = B
+  // by default): a slice's arithmetic depends only on Bsel, never on how many
+  // slices share the call, so any split of slices over calls or ranks that keeps
+  // Bsel gives bitwise identical results
+  int Bsel;
   size_t ld;
   cudaStream_t st;
   bool graph = false;          // capturing a step graph (cn_half_spec builds a WHILE node)
@@ -175,7 +180,7 @@ int leg_bn(const Run &r) {
     case 2: return 128;
     case 3: return 64;
     case 4: return -1;
-    default: return r.ld >= 64 ? -1 : (r.ld > 32 ? 64 : 0);
+    default: return 2 * r.Bsel >= 64 ? -1 : (2 * r.Bsel > 32 ? 64 : 0);
   }
 }
 
@@ -183,7 +188,7 @@ int synth(const Run &r, LegArgs &a) {
   a.items = r.pl->synth_items;
   a.nitems = r.pl->n_synth_items;
   ProfScope ps(0, leg_flops(r, a), r.st);
-  if ((g_leg_path == 5 && r.B <= 4) || (g_leg_path == 0 && r.B <= g_gemv_max_b))
+  if ((g_leg_path == 5 && r.Bsel <= 4) || (g_leg_path == 0 && r.Bsel <= g_gemv_max_b))
     return leg_synth_gemv_launch(a, r.B, r.st);
   const int bn = leg_bn(r);
   if (bn < 0) {
@@ -197,7 +202,7 @@ int synth(const Run &r, LegArgs &a) {
 
 int anal(const Run &r, LegArgs &a) {
   ProfScope ps(1, leg_flops(r, a), r.st);
-  if ((g_leg_path == 5 && r.B <= 4) || (g_leg_path == 0 && r.B <= g_gemv_max_b))
+  if ((g_leg_path == 5 && r.Bsel <= 4) || (g_leg_path == 0 && r.Bsel <= g_gemv_max_b))
     return leg_anal_gemv_launch(a, r.B, r.pl->K, r.st);
   const int bn = leg_bn(r);
   if (bn) {
@@ -278,7 +283,7 @@ int fft(const Run &r, int op, FftArgs &a) {
                                  r.st));
   // path: lane = row kernel for small-radix lengths with enough slices, else warp-per-row
   const bool lanes =
-      g_fft_path == 2 || (g_fft_path == 0 && (r.B >= 8 || op == FOP_NONLINEAR));
+      g_fft_path == 2 || (g_fft_path == 0 && (r.Bsel >= 8 || op == FOP_NONLINEAR));
   if (lanes && fft_lanes_ok(a)) {
     ProfScope ps(2, bytes, r.st);
     return fft_lanes_launch(op, a, r.st);
@@ -530,7 +535,7 @@ int helm_iter(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b, double al
   swe_plan *pl = r.pl;
   Work &w = pl->ws;
   const double *Rc[3] = {b.R[0], b.R[1], b.R[2]};
-  if (r.B >= 32 && !hd && g_helm_tiled)
+  if (r.Bsel >= 32 && !hd && g_helm_tiled)
     return helm_tiled(pl->M, pl->K, r.B, pl->offsets, pl->helm_tiles, pl->n_helm_tiles, Rc, alpha,
                       pl->eps, w.phibar, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], pl->cor_cf,
                       w.flags, w.stats, w.iters, w.counter, st);
@@ -583,7 +588,8 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
   }
   // CTAs per slice: small batches spread a slice over several SMs (the fixed point
   // of one slice on one SM is instruction-bound), B >= 32 keeps one CTA per slice
-  int want = g_cc_ctas ? g_cc_ctas : (B >= 32 ? 1 : std::min(16, std::max(1, 64 / B)));
+  const int Bs = r.Bsel;
+  int want = g_cc_ctas ? g_cc_ctas : (Bs >= 32 ? 1 : std::min(16, std::max(1, 64 / Bs)));
   int ccs = 0;
   if (g_cn_cluster)
     for (; want >= 1 && !(ccs = cn_cluster_size(pl->M, want)); want /= 2) {
@@ -996,7 +1002,7 @@ int step_graph(const Run &r, const swe_stepper_cfg &cfg, cudaGraphExec_t *exec) 
   if (g_fast_coriolis != 2 && cfg.coriolis_implicit) return OK;
   const int opts = options_key();
   for (auto &g : pl->graphs)
-    if (g.B == r.B && g.dt == cfg.dt && g.nu == cfg.visc_nu && g.tol == cfg.implicit_tol &&
+    if (g.B == r.B && g.Bsel == r.Bsel && g.dt == cfg.dt && g.nu == cfg.visc_nu && g.tol == cfg.implicit_tol &&
         g.order == cfg.visc_order && g.cor_impl == cfg.coriolis_implicit &&
         g.nonlin == cfg.include_nonlinear && g.max_iter == cfg.implicit_max_iter &&
         g.opts == opts && g.solver == cfg.implicit_solver) {
@@ -1027,6 +1033,7 @@ int step_graph(const Run &r, const swe_stepper_cfg &cfg, cudaGraphExec_t *exec) 
     }
   swe_plan::StepGraph g;
   g.B = r.B;
+  g.Bsel = r.Bsel;
   g.dt = cfg.dt;
   g.nu = cfg.visc_nu;
   g.tol = cfg.implicit_tol;
@@ -1047,6 +1054,10 @@ int check_cfg(const swe_stepper_cfg *cfg) {
     set_error("dt must be positive");
     return E_SHAPE;
   }
+  if (cfg->select_batch < 0) {
+    set_error("select_batch must be >= 0");
+    return E_SHAPE;
+  }
   if (cfg->visc_order < 2 || cfg->visc_order % 2 || cfg->visc_nu < 0) {
     set_error("viscosity order must be an even integer >= 2 and coefficient >= 0");
     return E_SHAPE;
@@ -1062,6 +1073,7 @@ Run make_run(swe_plan *pl, int B, void *stream) {
   Run r;
   r.pl = pl;
   r.B = B;
+  r.Bsel = B;
   r.ld = 2 * (size_t)B;
   r.st = (cudaStream_t)stream;
   return r;
@@ -1253,6 +1265,7 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
   }
   if ((rc = prepare(pl, batch, phibar, (cudaStream_t)stream))) return rc;
   Run r = make_run(pl, batch, stream);
+  r.Bsel = cfg->select_batch > 0 ? cfg->select_batch : r.B;
   const Bufs b = bufs(r);
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
   if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st))) return rc;
@@ -1298,6 +1311,7 @@ int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double
   if (n == 0) return OK;
   if ((rc = prepare(pl, 1, phibar, (cudaStream_t)stream))) return rc;
   Run r = make_run(pl, 1, stream);
+  r.Bsel = cfg->select_batch > 0 ? cfg->select_batch : r.B;
   const Bufs b = bufs(r);
   const int K = pl->K;
   Work &w = pl->ws;
@@ -1351,6 +1365,7 @@ int swe_settls_step(swe_plan *pl, double *state, const double *prev, const doubl
   }
   if ((rc = prepare(pl, batch, phibar, (cudaStream_t)stream))) return rc;
   Run r = make_run(pl, batch, stream);
+  r.Bsel = cfg->select_batch > 0 ? cfg->select_batch : r.B;
   const Bufs b = bufs(r);
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}}, p = {{r.spec(21), r.spec(22), r.spec(23)}};
   if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st)) ||
@@ -1424,6 +1439,8 @@ int swe_state_stats(const swe_plan *pl, const double *state, int batch, double *
 }
 
 long long swe_kernel_launches(void) { return g_launches; }
+
+int swe_stepper_cfg_size(void) { return (int)sizeof(swe_stepper_cfg); }
 
 int swe_set_option(const char *key, int value) {
   if (key && strcmp(key, "fft_path") == 0 && value >= 0 && value <= 2) {

@@ -15,10 +15,14 @@ Differences are in execution only, never in the iterates:
   every F-sweep (the only data dependence between slices, pint.py:229-231),
   the coarsest serial sweep (pint.py:306-320) runs redundantly on every rank
   after an all-gather of its forcing, and blow-up flags are all-reduced.
-Each slice's arithmetic does not depend on the batch it rides in, so traces
-are bitwise identical for any batch composition and any number of ranks
-(the reference's worker-count contract).
-The SL-SI-SETTLS history policy (pint.py:103-119) is out of scope (IMEX only).
+Rank-count determinism (the reference's worker-count contract):
+a rank's share of a sweep is stepped with the kernels chosen for the sweep's
+GLOBAL point count (`select_batch`, see steppers.py), and the serial sweeps
+(coarsest level, initial guess) run one point per call on every rank, so each
+point's arithmetic is the same for any number of ranks and the traces are
+bitwise identical (tests/test_gpu_multirank.py).
+The SL-SI-SETTLS history policy (pint.py:103-119) is followed in the FAS tau,
+the coarsest sweep and the initial guess.
 """
 
 from __future__ import annotations
@@ -172,7 +176,13 @@ def speedup_report(trace: IterationTrace, t_ref: float):
 
 
 class Comm:
-    """Slice-block exchange over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    """Slice-block exchange over torch.distributed.
+
+    NCCL (one rank per GPU): device buffers go over NVLink directly.  Any other
+    backend (gloo: CPU tests, or several ranks sharing one GPU in the multi-rank
+    parity test) stages device tensors through host memory, so no kernel of one
+    rank ever waits on another rank's kernels.
+    """
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -180,16 +190,22 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
+        self.stage = dist.get_backend(group) != "nccl"
+
+    def _wire(self, t: torch.Tensor) -> torch.Tensor:
+        t = t.contiguous()
+        return t.cpu() if self.stage and t.is_cuda else t
 
     def halo(self, send: torch.Tensor, recv: torch.Tensor):
         """send -> rank+1, recv <- rank-1 (first/last rank skip)."""
         d = self.dist
         ops = []
         if self.rank + 1 < self.size:
-            ops.append(d.P2POp(d.isend, send.contiguous(), self.rank + 1, self.group))
+            ops.append(d.P2POp(d.isend, self._wire(send), self.rank + 1, self.group))
         buf = None
         if self.rank > 0:
-            buf = torch.empty_like(recv)
+            buf = torch.empty(recv.shape, dtype=recv.dtype,
+                              device="cpu" if self.stage else recv.device)
             ops.append(d.P2POp(d.irecv, buf, self.rank - 1, self.group))
         if ops:
             for req in d.batch_isend_irecv(ops):
@@ -198,14 +214,15 @@ class Comm:
             recv.copy_(buf)
 
     def all_gather(self, local: torch.Tensor) -> torch.Tensor:
+        src = self._wire(local)
         out = torch.empty((self.size * local.shape[0],) + tuple(local.shape[1:]),
-                          dtype=local.dtype, device=local.device)
+                          dtype=local.dtype, device=src.device)
         if out.is_complex():
-            self.dist.all_gather_into_tensor(torch.view_as_real(out),
-                                             torch.view_as_real(local.contiguous()), group=self.group)
+            self.dist.all_gather_into_tensor(torch.view_as_real(out), torch.view_as_real(src),
+                                             group=self.group)
         else:
-            self.dist.all_gather_into_tensor(out, local.contiguous(), group=self.group)
-        return out
+            self.dist.all_gather_into_tensor(out, src, group=self.group)
+        return out.to(local.device)
 
     def min_int(self, v: int) -> int:
         t = torch.tensor([v], dtype=torch.int64,
@@ -250,12 +267,20 @@ class MgritEngine:
         f = getattr(self.problem, "tracks_history", None)
         return bool(f(level)) if f is not None else False
 
-    def _step(self, level, x, prev=None):
+    def _step(self, level, x, prev=None, sharded=True):
+        """One step of every point of x.  sharded: x is this rank's share of a sweep
+        over G * len(x) points; the problem then picks its kernels for the global
+        count (select_batch), so every rank count runs the same arithmetic per
+        point.  Serial calls (coarsest sweep, initial guess) run on every rank
+        alike and pass no hint."""
         if level == 0:
             self.fine_steps += x.shape[0]
+        kw = {}
+        if getattr(self.problem, "supports_select_batch", False):
+            kw["select_batch"] = x.shape[0] * self.G if sharded else 0
         if prev is None:
-            return self.problem.step_batch(level, x)
-        return self.problem.step_batch(level, x, prev)
+            return self.problem.step_batch(level, x, **kw)
+        return self.problem.step_batch(level, x, prev, **kw)
 
     def _exchange_halo(self, level, u):
         if self.G == 1:
@@ -353,7 +378,7 @@ class MgritEngine:
         prev = None
         for j in range(1, n + 1):
             hist = prev if track and modes[j - 1] == TWO_STEP else None
-            new = self._step(lv, u[j - 1:j], hist)
+            new = self._step(lv, u[j - 1:j], hist, sharded=False)
             if g is not None:
                 new = new + g[j:j + 1]
             prev = u[j - 1:j].clone()
@@ -392,7 +417,7 @@ class MgritEngine:
         modes = settls_boundary_policy(self.L, 1, n1, self.m, self.cfg.chunk_size)
         for j in range(1, n1 + 1):
             hist = v[j - 2:j - 1] if track and j >= 2 and modes[j - 1] == TWO_STEP else None
-            v[j:j + 1] = self._step(1, v[j - 1:j], hist)
+            v[j:j + 1] = self._step(1, v[j - 1:j], hist, sharded=False)
         return pr.prolong_batch(1, v)
 
     def _cpoints(self, u):
@@ -500,7 +525,11 @@ class SweProblem:
         self.config = config
         self.geometry = geometry or SphereGeometry()
         self.grids = [get_grid(spec.M, self.geometry) for spec in config.levels]
-        self.level_cfgs = [spec.stepper for spec in config.levels]
+        # SETTLS below the coarsest level runs one-step (pint.py:164-170)
+        L = config.nlevels
+        self.level_cfgs = [dataclasses.replace(spec.stepper, settls_mode=ONE_STEP)
+                           if spec.stepper.scheme == SL_SI_SETTLS and lv < L - 1 else spec.stepper
+                           for lv, spec in enumerate(config.levels)]
         self.phibar = phibar
         self.step_calls = 0
 
@@ -526,17 +555,21 @@ class SweProblem:
         g = self.grids[level]
         return torch.zeros((n, 3, g.n_modes), dtype=torch.complex128, device=f"cuda:{g.device}")
 
-    def step_batch(self, level, x, prev=None):
+    supports_select_batch = True
+
+    def step_batch(self, level, x, prev=None, select_batch=0):
         """One step of every point of x; prev (SETTLS two-step history, same shape)
-        or None.  For SETTLS a point's own value as its prev means no history."""
+        or None.  For SETTLS a point's own value as its prev means no history.
+        select_batch: kernel-selection batch (steppers module docstring)."""
         from .steppers import IMEX, imex_steps_inplace, settls_step_inplace
         st = self.wrap(level, x.clone())
         self.step_calls += x.shape[0]
         cfg = self.level_cfgs[level]
         if cfg.scheme == IMEX:
-            imex_steps_inplace(st, cfg, 1)
+            imex_steps_inplace(st, cfg, 1, select_batch=select_batch)
         else:
-            settls_step_inplace(st, cfg, None if prev is None else self.wrap(level, prev))
+            settls_step_inplace(st, cfg, None if prev is None else self.wrap(level, prev),
+                                select_batch=select_batch)
         return st.data
 
     def sweep_batch(self, level, u, g) -> bool:

@@ -6,10 +6,14 @@ Mirror of `/root/reference/pkg/src/pintswe/steppers.py`: StepperConfig
 slice of a batched PrognosticState through libswe_b200.so's swe_imex_step;
 the implicit Coriolis fixed point keeps per-slice convergence (each slice
 stops at its own iteration, exactly as a serial call would).
+settls_step / advance / propagate also run the SL-SI-SETTLS scheme (:171-212,
+swe_settls_step) with the reference's one-step / two-step history.
 
-The SL-SI-SETTLS scheme (:171-212) is a coarse-level-only scheme and is out of
-scope for the GPU path; configuring it raises
-NotImplementedError at step time.
+`select_batch` (imex_steps_inplace, settls_step_inplace): the kernel generation
+of a call is chosen for that many slices instead of the call's own batch, so a
+slice's result is bitwise a function of its input and select_batch alone; the
+sharded MGRIT engine passes the global slice count of the sweep and gets the
+one-rank trace bitwise on any number of ranks.
 """
 
 from __future__ import annotations
@@ -63,12 +67,13 @@ class StepperConfig:
         if self.implicit_solver not in ("fixed_point", "direct"):
             raise ValueError("implicit_solver must be fixed_point or direct")
 
-    def to_c(self) -> _lib.StepperCfgC:
+    def to_c(self, select_batch: int = 0) -> _lib.StepperCfgC:
         return _lib.StepperCfgC(self.dt, self.viscosity.order_q, self.viscosity.coeff_nu,
                                 1 if self.coriolis_treatment == "implicit" else 0,
                                 1 if self.include_nonlinear else 0, self.implicit_tol,
                                 self.implicit_max_iter,
-                                1 if self.implicit_solver == "direct" else 0)
+                                1 if self.implicit_solver == "direct" else 0,
+                                int(select_batch))
 
 
 @dataclasses.dataclass
@@ -80,16 +85,18 @@ class StepperState:
 
 
 def imex_steps_inplace(state: PrognosticState, cfg: StepperConfig, nsteps: int = 1,
-                       iters: Optional[np.ndarray] = None) -> PrognosticState:
+                       iters: Optional[np.ndarray] = None,
+                       select_batch: int = 0) -> PrognosticState:
     """Advance `state` by `nsteps` IMEX steps IN PLACE (device data mutated).
 
     iters, if given, is an int32 array [nsteps, B, 2] receiving the fixed-point
     iteration counts of the two Crank-Nicolson solves of every step.
+    select_batch > 0 picks the kernels as for that batch size (module docstring).
     """
     if cfg.scheme != IMEX:
-        raise NotImplementedError("the GPU propagator implements the IMEX scheme only")
+        raise ValueError("imex_steps_inplace needs scheme='imex' (use advance/settls_step)")
     grid = state.grid
-    c = cfg.to_c()
+    c = cfg.to_c(select_batch)
     resid = np.zeros(state.batch)
     ip = None
     if iters is not None:
@@ -112,7 +119,8 @@ def imex_step(state: PrognosticState, cfg: StepperConfig) -> PrognosticState:
 
 
 def settls_step_inplace(state: PrognosticState, cfg: StepperConfig,
-                        prev: Optional[PrognosticState] = None) -> PrognosticState:
+                        prev: Optional[PrognosticState] = None,
+                        select_batch: int = 0) -> PrognosticState:
     """One SL-SI-SETTLS step IN PLACE (steppers.py:171-212); prev = U_{n-1} of the
     same batch, ignored in one-step mode (None = cold start)."""
     from .semilag import DeparturePointError
@@ -121,7 +129,7 @@ def settls_step_inplace(state: PrognosticState, cfg: StepperConfig,
     if prev.batch != state.batch or prev.grid is not state.grid:
         raise ValueError("SETTLS history must match the state's batch and grid")
     grid = state.grid
-    c = cfg.to_c()
+    c = cfg.to_c(select_batch)
     resid = np.zeros(state.batch)
     rc = grid._lib.swe_settls_step(grid.plan, _ptr(state.data), _ptr(prev.data),
                                    _ptr(state.phibar_t), state.batch, ctypes.byref(c),
@@ -185,7 +193,11 @@ class HostPipeline:
     def __init__(self, grid: SphereGrid, cfg: StepperConfig, batch: int, nsteps: int = 1,
                  depth: int = 3):
         if cfg.scheme != IMEX:
-            raise NotImplementedError("the GPU propagator implements the IMEX scheme only")
+            raise ValueError("HostPipeline runs the IMEX scheme")
+        if depth < 2:
+            # submit(i) copies into slot i % depth before the deferred batch i-1
+            # has launched; with one slot that copy would overwrite its input
+            raise ValueError("HostPipeline needs depth >= 2")
         self.grid, self.cfg, self.batch, self.nsteps = grid, cfg, int(batch), int(nsteps)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.compute = torch.cuda.current_stream()

@@ -227,3 +227,31 @@ def test_stale_nonfinite_workspace(gpu, leg):
     finally:
         _lib.set_option("leg_path", 0)
         _lib.set_option("fast_coriolis", 2)
+
+
+def test_m1024_transforms_match_reference():
+    """cfg4's transforms at M=1024 against the REFERENCE (oracle/make_golden.py
+    m1024sht): synthesis of cfg4-law coefficients (regenerated from the seed) on 5
+    latitude rows plus max|.|, analysis of a seeded random grid on n <= 64 plus
+    max|.|; 1e-12 relative to the field's max."""
+    import torch
+    from paper_2306_09497_b200 import spharm
+    g = load_golden("sht_M1024.npz")
+    M, nfs = int(g["M"]), int(g["nfs"])
+    grid = spharm.get_grid(M)
+    rng = np.random.default_rng(int(g["seed"]))
+    ph = rng.uniform(0.0, 2.0 * np.pi, size=(nfs, grid.n_modes))
+    amp = (grid.n_of + 1.0) ** -1.5
+    c = amp * np.exp(1j * ph)
+    c[:, : M + 1] = amp[: M + 1] * np.cos(ph[:, : M + 1])
+    syn = grid.synthesis(torch.from_numpy(c).cuda()).cpu().numpy()
+    for b in range(nfs):
+        mx = g["synthesis_maxabs"][b]
+        assert abs(np.abs(syn[b]).max() - mx) <= 1e-12 * mx
+        assert np.abs(syn[b][g["rows"]] - g["synthesis_rows"][b]).max() <= 1e-12 * mx
+    gin = np.random.default_rng(int(g["grid_seed"])).standard_normal((nfs, grid.nlat, grid.nlon))
+    an = grid.analysis(torch.from_numpy(gin).cuda()).cpu().numpy()
+    for b in range(nfs):
+        mx = g["analysis_maxabs"][b]
+        assert abs(np.abs(an[b]).max() - mx) <= 1e-12 * mx
+        assert np.abs(an[b][g["sel"]] - g["analysis_window"][b]).max() <= 1e-12 * mx

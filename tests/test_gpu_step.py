@@ -685,3 +685,82 @@ def test_linear_only_steps_match_oracle(mods, implicit, nonlin):
         got = np.stack([phi[b], xi[b], de[b]])
         want = np.stack([ref.phi[b], ref.xi[b], ref.delta[b]])
         assert rel_diff(got, want) < 1e-10, b
+
+
+@pytest.mark.parametrize("M,dt,B,nsteps", [(256, 60.0, 64, 2), (51, 120.0, 64, 2)])
+def test_headline_path_full_state_matches_oracle(mods, M, dt, B, nsteps):
+    """The bench's default path (M=256 x 64 slices: v3 DMMA GEMMs, the 16-row lane
+    FFT, k_cn_fused + its WHILE-node graph; M=51 x 64: the coarse-level path) against
+    the oracle's imex_step on full states: 4 slices spread over the batch, every
+    field and Phi' to 1e-10 relative sup-norm, identical fixed-point iteration
+    counts, and the graph replay bitwise equal to the eager launches."""
+    spharm, dynamics, steppers, scenarios = mods
+    import torch
+    from oracle.sht import OracleSphere
+    from oracle.swe import OracleState, StepCfg, imex_step as o_step
+    grid = spharm.get_grid(M)
+    cfg = steppers.StepperConfig(dt=dt, viscosity=dynamics.ViscositySpec(2, 1e5))
+    base = scenarios.gaussian_bumps(grid, batch=B)
+    rng = np.random.default_rng(M)
+    taper = torch.from_numpy((grid.n_of + 1.0) ** -2).cuda()
+    noise = torch.from_numpy(rng.standard_normal((B, grid.n_modes))
+                             + 1j * rng.standard_normal((B, grid.n_modes))).cuda() * taper
+    noise[:, : M + 1] = noise[:, : M + 1].real
+    amp = torch.logspace(-9, -5, B, dtype=torch.float64).cuda()[:, None]
+    base.data[:, 1] += amp * noise
+    base.data[:, 2] += 0.1 * amp * noise
+    # eager launches with iteration counts, then the graph path (the second call with
+    # the same key captures, the third replays)
+    eager = base.copy()
+    its = np.zeros((nsteps, B, 2), dtype=np.int32)
+    steppers.imex_steps_inplace(eager, cfg, nsteps, its)
+    for _ in range(2):
+        graph = base.copy()
+        steppers.imex_steps_inplace(graph, cfg, nsteps)
+    assert torch.equal(graph.data, eager.data)
+    got = graph.data.cpu().numpy()
+    pick = [0, B // 3, 2 * B // 3, B - 1]
+    sph = OracleSphere(M)
+    x = base.data[pick].cpu().numpy()
+    s = OracleState(sph, x[:, 0].copy(), x[:, 1].copy(), x[:, 2].copy(),
+                    base.phibar_t[pick].cpu().numpy())
+    o_its = []
+    for k in range(nsteps):
+        stats = []
+        s = o_step(s, StepCfg(dt=dt, visc_nu=1e5), stats)
+        o_its.append(np.stack(stats, axis=-1))
+    assert np.array_equal(its[:, pick], np.stack(o_its)), (its[:, pick], o_its)
+    worst = 0.0
+    for j, b in enumerate(pick):
+        want = np.stack([s.phi[j], s.xi[j], s.delta[j]])
+        d = rel_diff(got[b], want)
+        pa, pw = got[b][0].copy(), want[0].copy()
+        pa[0] = pw[0] = 0.0
+        dp = float(np.abs(pa - pw).max() / np.abs(pw).max())
+        worst = max(worst, d, dp)
+        assert d < 1e-10 and dp < 1e-10, (b, d, dp)
+    print(f"[PARITY] M={M} B={B} default path vs oracle: worst {worst:.2e}, "
+          f"iterations {sorted(set(its.ravel().tolist()))}")
+
+
+def test_m1024_step_window_matches_reference(mods):
+    """cfg5's fine step (M=1024, dt=2 s, nu=0, gaussian_bumps) on the
+    default path against the REFERENCE's own step (oracle/make_golden.py m1024) on
+    the modes n <= 64, per field relative to the field's max."""
+    spharm, dynamics, steppers, scenarios = mods
+    g = load_golden("step_window_M1024.npz")
+    grid = spharm.get_grid(1024)
+    s = scenarios.gaussian_bumps(grid, batch=2)
+    cfg = steppers.StepperConfig(dt=float(g["dt"]),
+                                 viscosity=dynamics.ViscositySpec(2, float(g["nu"])))
+    steppers.imex_steps_inplace(s, cfg, 1)
+    full = s.data[0].cpu().numpy()
+    out = full[:, g["sel"]]
+    worst = 0.0
+    for f in range(3):
+        mx = float(np.abs(full[f]).max())
+        assert abs(mx - g["out_maxabs"][f]) <= 1e-10 * g["out_maxabs"][f], f
+        e = np.abs(out[f] - g["out_window"][f]).max() / g["out_maxabs"][f]
+        worst = max(worst, e)
+        assert e <= 1e-10, (f, e)
+    print(f"[PARITY] M=1024 cfg5 step vs reference (n <= 64): worst {worst:.2e}")

@@ -163,6 +163,26 @@ def test_pint_trace_matches_reference(name):
             assert rel_diff(got, snaps[k, i]) < 1e-10, (k, i)
 
 
+@pytest.mark.slow
+def test_pint_cfg1_trace_matches_reference():
+    """BASELINE cfg1 (bumps-pint-desk, M=64/32, Parareal, N0 32, 5 iterations): the
+    oracle engine against the reference's compact golden (every C-point on n <= 32,
+    max|.| per field, full states at the middle and last C-point)."""
+    g = load_golden("pint_cfg1_M64.npz")
+    prob, pc, u0 = _run_pint(g)
+    tr = om.OracleMgrit(prob, pc).run(u0)
+    sel, win, mx = g["sel"], g["snap_window"], g["snap_maxabs"]
+    assert len(tr.snapshots) == win.shape[0]
+    full = {int(i): j for j, i in enumerate(g["snap_full_idx"])}
+    for k, snap in enumerate(tr.snapshots):
+        for i, st in enumerate(snap):
+            got = np.stack([st.phi[0], st.xi[0], st.delta[0]])
+            assert (np.abs(np.abs(got).max(axis=-1) - mx[k, i]) <= 1e-10 * mx[k, i]).all()
+            assert (np.abs(got[:, sel] - win[k, i]).max(axis=-1) <= 1e-10 * mx[k, i]).all()
+            if i in full:
+                assert rel_diff(got, g["snap_full"][k, full[i]]) < 1e-10, (k, i)
+
+
 def _read_csv(path):
     with open(path) as fh:
         rows = list(csv.reader(fh))
