@@ -77,6 +77,13 @@ long long swe_plan_bytes(const swe_plan *plan);
 int swe_synthesis(swe_plan *plan, const double *spec, double *grid, int batch, void *stream);
 /* SphereGrid.analysis (spharm.py:238-247): grid -> spec */
 int swe_analysis(swe_plan *plan, const double *grid, double *spec, int batch, void *stream);
+/* SphereGrid._synthesis_pair (spharm.py:259-267): sum_m (P cp_m + H ch_m) e^{i m lambda};
+ * cp, ch [batch][K] -> grid [batch][nlat][nlon] */
+int swe_synthesis_pair(swe_plan *plan, const double *cp, const double *ch, double *grid,
+                       int batch, void *stream);
+/* SphereGrid.grad_grid (spharm.py:282-294): gx = d/dlambda / (a cos), gy = d/dtheta / a */
+int swe_grad_grid(swe_plan *plan, const double *spec, double *gx, double *gy, int batch,
+                  void *stream);
 /* SphereGrid.uv_from_vortdiv (spharm.py:296-313) */
 int swe_uv_from_vortdiv(swe_plan *plan, const double *xi, const double *delta, double *u,
                         double *v, int batch, void *stream);
@@ -86,7 +93,8 @@ int swe_vortdiv_from_uv(swe_plan *plan, const double *u, const double *v, double
 
 /* Tendencies of a state batch (dynamics.py:121-165).  kind:
  *   0 linear_gravity, 1 linear_coriolis, 2 nonlinear_advection + nonlinear_rest,
- *   3 full_rhs.  state/out: [batch][3][K]; phibar: [batch] (device). */
+ *   3 full_rhs, 4 nonlinear_advection, 5 nonlinear_rest.
+ *   state/out: [batch][3][K]; phibar: [batch] (device). */
 int swe_tendency(swe_plan *plan, int kind, const double *state, const double *phibar,
                  double *out, int batch, void *stream);
 

@@ -207,7 +207,9 @@ class OracleMgrit:
         m, n0, n1 = self.m, self.c.N0, self.c.points_on(1)
         guess = self.initial_guess(u0)
         trace = Trace(snapshots=[guess])
-        limit = 1e10 * max(float(u0.max_abs()[0]), 1e-300)
+        # np.atleast_1d: the oracle's batched states return arrays, a per-state
+        # problem's states (the reference protocol, pint.py:185-189) plain scalars
+        limit = 1e10 * max(float(np.atleast_1d(u0.max_abs())[0]), 1e-300)
         self.check(trace, 0, guess, limit)
         u = [None] * (n0 + 1)
         u[0] = u0.copy()
@@ -226,7 +228,8 @@ class OracleMgrit:
     @staticmethod
     def check(trace, k, snap, limit):                 # pint.py:396-400
         for i, v in enumerate(snap):
-            if not bool(v.is_finite()[0]) or float(v.max_abs()[0]) > limit:
+            if (not bool(np.atleast_1d(v.is_finite())[0])
+                    or float(np.atleast_1d(v.max_abs())[0]) > limit):
                 trace.blowup = {"iteration": k, "slice": i}
                 raise PintBlowUp(k, i, trace)
 

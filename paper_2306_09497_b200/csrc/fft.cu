@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(256) fft_kernel(const __grid_constant__ FftArg
       __syncthreads();
       c2r_fields(a, c, 4, 2);
       __syncthreads();
-      pointwise([&](int s, int n) { rd(2, s)[n] -= rd(4, s)[n] * rd(5, s)[n]; });
+      if (!a.no_rest) pointwise([&](int s, int n) { rd(2, s)[n] -= rd(4, s)[n] * rd(5, s)[n]; });
       __syncthreads();
       const int f[4] = {2, 3, 0, 1};
       const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;

@@ -48,6 +48,7 @@ struct FftArgs {
   int lw32;                     // FOP_NONLINEAR, lane kernel: 32 rows = 2 slices per CTA
   int dlam;                     // FOP_NONLINEAR: field 2 (d_lambda Phi) is i m times field 5's
                                 // half spectrum (in[2] unused): saves one synthesis term
+  int no_rest;                  // FOP_NONLINEAR: omit -Phi' delta (nonlinear_advection alone)
   const double *in[FFT_MAXF];   // E/O half spectra      [m][2][Jp][ld]
   double *out[FFT_MAXF];        // F+/F- analysis inputs [m][2][Jp][ld]
   const double *gin[2];         // grids [slice][J][I]

@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(lane_threads<LW>(), 512 / lane_threads<LW>())
       const int pp = r / (2 * NH), h = SPLIT ? c.hem : (r >> 1) & 1, hh = r & 1;
       auto R = [&](int f) -> double & { return gslot<LW>(c, pp, hh, lrow(c, f, h, s)); };
       const double u = R(0) * ia, v = R(1) * ia, gx = R(2) * ia, gy = R(3) * ia;
-      const double xi = R(4), ph = R(5), de = R(6);
+      const double xi = R(4), ph = a.no_rest ? 0.0 : R(5), de = R(6);
       R(0) = -(u * gx + v * gy) - ph * de;   // -(V.grad Phi) - Phi' delta
       R(1) = 0.5 * (u * u + v * v);          // kinetic energy
       R(2) = (xi * u) * cs;                  // (xi u) cos

@@ -371,7 +371,8 @@ int eval_coriolis(const Run &r, const double *xi, const double *de, double *oxi,
 }
 
 // N = N_A + N_R (dynamics.py:142-160) into k[3]; ke uses scratch spectral array `tmp`
-int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], double *tmp) {
+int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], double *tmp,
+                   bool no_rest = false) {
   swe_plan *pl = r.pl;
   const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
   const bool pm = leg_bn(r) < 0 && fft_uses_lanes(r);
@@ -398,6 +399,7 @@ int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], d
     for (int i = 0; i < 7; ++i) f.in[i] = i == 2 ? nullptr : r.half(i);
     for (int i = 0; i < 4; ++i) f.out[i] = r.fsp(i);
     f.dlam = 1;
+    f.no_rest = no_rest ? 1 : 0;
     f.in_pm = pm;
     f.lw32 = g_fft_lw32;
     if ((rc = fft(r, FOP_NONLINEAR, f))) return rc;
@@ -1190,6 +1192,50 @@ int swe_uv_from_vortdiv(swe_plan *pl, const double *xi, const double *delta, dou
   return fft(r, FOP_SYNTH2_GRID, f);
 }
 
+int swe_synthesis_pair(swe_plan *pl, const double *cp, const double *ch, double *grid, int batch,
+                       void *stream) {
+  int rc;
+  if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  SpecPtrs d0 = {{r.spec(0)}}, d1 = {{r.spec(1)}};
+  if ((rc = to_internal(cp, d0, batch, 1, pl->K, pl->perm, r.st)) ||
+      (rc = to_internal(ch, d1, batch, 1, pl->K, pl->perm, r.st)))
+    return rc;
+  LegArgs a = leg_args(r);
+  a.nout = 1;
+  LegTerm th = term(pl->H, r.spec(1));
+  set_out(a, 0, r.half(0), term(pl->P, r.spec(0)), &th, pl->H);
+  if ((rc = synth(r, a))) return rc;
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.in[0] = r.half(0);
+  f.gout[0] = grid;
+  f.scale_mode = 0;
+  return fft(r, FOP_SYNTH_GRID, f);
+}
+
+int swe_grad_grid(swe_plan *pl, const double *spec, double *gx, double *gy, int batch,
+                  void *stream) {
+  int rc;
+  if ((rc = prepare(pl, batch, nullptr, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  SpecPtrs d0 = {{r.spec(0)}};
+  if ((rc = to_internal(spec, d0, batch, 1, pl->K, pl->perm, r.st))) return rc;
+  LegArgs a = leg_args(r);
+  a.nout = 2;
+  // gx = synth(i m c) / (a cos), gy = pair(0, c) / (a cos)   (spharm.py:282-294)
+  set_out(a, 0, r.half(0), term(pl->P, r.spec(0), 1.0, 1), nullptr, pl->H);
+  set_out(a, 1, r.half(1), term(pl->H, r.spec(0)), nullptr, pl->H);
+  if ((rc = synth(r, a))) return rc;
+  FftArgs f;
+  memset(&f, 0, sizeof(f));
+  f.in[0] = r.half(0);
+  f.in[1] = r.half(1);
+  f.gout[0] = gx;
+  f.gout[1] = gy;
+  return fft(r, FOP_SYNTH2_GRID, f);
+}
+
 int swe_vortdiv_from_uv(swe_plan *pl, const double *u, const double *v, double *xi, double *delta,
                         int batch, void *stream) {
   int rc;
@@ -1218,7 +1264,7 @@ int swe_vortdiv_from_uv(swe_plan *pl, const double *u, const double *v, double *
 int swe_tendency(swe_plan *pl, int kind, const double *state, const double *phibar, double *out,
                  int batch, void *stream) {
   int rc;
-  if (kind < 0 || kind > 3) {
+  if (kind < 0 || kind > 5) {
     set_error("unknown tendency kind %d", kind);
     return E_SHAPE;
   }
@@ -1241,8 +1287,15 @@ int swe_tendency(swe_plan *pl, int kind, const double *state, const double *phib
                        pl->eps, pl->ws.phibar, b.K1, r.st)))
       return rc;
   }
-  if (kind == 2 || kind == 3) {
-    if ((rc = eval_nonlinear(r, Uc, b.K2, b.TMP))) return rc;
+  if (kind == 5) {  // nonlinear_rest alone: (-Phi' delta, 0, 0)
+    if ((rc = grid_reserve(pl, batch))) return rc;
+    const size_t gsz = (size_t)batch * pl->J * pl->I;
+    double *G = pl->ws.grids;
+    if ((rc = nonlinear_rest_internal(r, b.U[0], b.U[2], G, G + gsz, G + 2 * gsz, b.K1[0])))
+      return rc;
+  }
+  if (kind == 2 || kind == 3 || kind == 4) {
+    if ((rc = eval_nonlinear(r, Uc, b.K2, b.TMP, kind == 4))) return rc;
     if ((rc = tend_finish(K, batch, b.K2[2], b.TMP, pl->lap_eig, b.K2[1], nullptr, nullptr, r.st)))
       return rc;
     Ptr3C k1c = {{b.K1[0], b.K1[1], b.K1[2]}}, k2c = {{b.K2[0], b.K2[1], b.K2[2]}},

@@ -174,6 +174,7 @@ class ViscositySpec:
 
 
 TEND_GRAVITY, TEND_CORIOLIS, TEND_NONLINEAR, TEND_FULL = 0, 1, 2, 3
+TEND_ADVECTION, TEND_REST = 4, 5
 
 
 def _tendency(state: PrognosticState, kind: int) -> Tendency:
@@ -204,6 +205,17 @@ def nonlinear(state: PrognosticState) -> Tendency:
     return _tendency(state, TEND_NONLINEAR)
 
 
+def nonlinear_advection(state: PrognosticState) -> Tendency:
+    """(-V.grad Phi, -div(xi V), -lap(V.V/2) + curl(xi V)) (dynamics.py:142-151):
+    the fused grid pass without the -Phi' delta product."""
+    return _tendency(state, TEND_ADVECTION)
+
+
+def nonlinear_rest(state: PrognosticState) -> Tendency:
+    """(-Phi' delta, 0, 0) via a dealiased grid product (dynamics.py:154-160)."""
+    return _tendency(state, TEND_REST)
+
+
 def full_rhs(state: PrognosticState) -> Tendency:
     """L_G + L_C + N_A + N_R (dynamics.py:163-165)."""
     return _tendency(state, TEND_FULL)
@@ -223,3 +235,15 @@ def viscosity_damping(grid: SphereGrid, vspec: ViscositySpec, dt: float) -> np.n
     """b(n) = 1/(1 + dt nu (n(n+1)/a^2)^(q/2)) per packed mode (dynamics.py:181-188)."""
     nn1 = grid.n_of * (grid.n_of + 1.0) / grid.geometry.radius_a ** 2
     return 1.0 / (1.0 + dt * vspec.coeff_nu * nn1 ** (vspec.order_q / 2.0))
+
+
+def viscosity_step(state: PrognosticState, vspec: ViscositySpec, dt: float) -> PrognosticState:
+    """Backward-Euler damping of Phi', xi, delta (dynamics.py:191-200); b(0) = 1
+    keeps the mean geopotential.  (The IMEX step applies it fused in k_cn_fused /
+    k_cn_finish; this is the standalone API call.)"""
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    if vspec.coeff_nu == 0.0:
+        return state.copy()
+    b = torch.from_numpy(viscosity_damping(state.grid, vspec, dt)).to(state.data.device)
+    return PrognosticState(state.grid, state.data * b, state.phibar_t.clone())

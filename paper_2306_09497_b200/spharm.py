@@ -192,6 +192,33 @@ class SphereGrid:
                    "swe_analysis")
         return self._out(c, tt, single)
 
+    def _synthesis_pair(self, cp, ch):
+        """sum_m (P cp_m + H ch_m) e^{i m lambda} on the grid (spharm.py:259-267)."""
+        self._check_spec(cp)
+        self._check_spec(ch)
+        p, tt = self._to_dev(cp, torch.complex128)
+        h, _ = self._to_dev(ch, torch.complex128)
+        single = p.ndim == 1
+        p, h = p.reshape(-1, self.n_modes), h.reshape(-1, self.n_modes)
+        if p.shape != h.shape:
+            raise ValueError("cp and ch must have the same shape")
+        g = torch.empty((p.shape[0], self.nlat, self.nlon), dtype=torch.float64, device=p.device)
+        _lib.check(self._lib.swe_synthesis_pair(self._plan, _ptr(p), _ptr(h), _ptr(g), p.shape[0],
+                                                _stream()), "swe_synthesis_pair")
+        return self._out(g, tt, single)
+
+    def grad_grid(self, coeffs):
+        """(gx, gy) = (1/(a cos) d/dlambda, 1/a d/dtheta) on the grid (spharm.py:282-294)."""
+        self._check_spec(coeffs)
+        c, tt = self._to_dev(coeffs, torch.complex128)
+        single = c.ndim == 1
+        c = c.reshape(-1, self.n_modes)
+        gx = torch.empty((c.shape[0], self.nlat, self.nlon), dtype=torch.float64, device=c.device)
+        gy = torch.empty_like(gx)
+        _lib.check(self._lib.swe_grad_grid(self._plan, _ptr(c), _ptr(gx), _ptr(gy), c.shape[0],
+                                           _stream()), "swe_grad_grid")
+        return self._out(gx, tt, single), self._out(gy, tt, single)
+
     def laplacian(self, coeffs):
         self._check_spec(coeffs)
         return coeffs * self._eig("lap", self.laplacian_eig, coeffs)
@@ -241,6 +268,34 @@ class SphereGrid:
 
     def device_bytes(self) -> int:
         return int(self._lib.swe_plan_bytes(self._plan))
+
+
+@dataclasses.dataclass
+class SpectralField:
+    """Packed complex coefficients of one real scalar field (spharm.py:374-386)."""
+
+    grid: SphereGrid
+    coeffs: object
+
+    def __post_init__(self):
+        self.grid._check_spec(self.coeffs)
+
+    def to_grid(self) -> "GridField":
+        return GridField(self.grid, self.grid.synthesis(self.coeffs))
+
+
+@dataclasses.dataclass
+class GridField:
+    """Real values on the Gaussian grid, latitudes north first (spharm.py:389-399)."""
+
+    grid: SphereGrid
+    values: object
+
+    def __post_init__(self):
+        self.grid._check_grid(self.values)
+
+    def to_spectral(self) -> SpectralField:
+        return SpectralField(self.grid, self.grid.analysis(self.values))
 
 
 @functools.lru_cache(maxsize=64)
