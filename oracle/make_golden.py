@@ -255,6 +255,49 @@ def gen_pint_run(name, cfg, window=32):
                 errors_csv=np.array(errors), spectrum_csv=np.array(spectrum))
 
 
+# cfg3's real horizon (N0 1024, dt0 60 s, 3 levels, cfactor 4, nrelax 2, coarse
+# M=51) with the fine level at M=64 (the reference runs it in ~1 h): the engine
+# diverges; the golden records the reference's blow-up iteration / slice and the
+# trace up to it
+CFG3_BLOWUP = {
+    "scenario": "gaussian_bumps", "T": 1024 * 60.0,
+    "fine": {"M": 64, "dt": 60.0, "scheme": "imex", "viscosity": {"order": 2, "coeff": 1.0e5}},
+    "pint": {"nlevels": 3, "cfactor": 4, "nrelax": 2, "max_iters": 4, "chunk_size": 0,
+             "coarse": {"M": 51, "scheme": "imex", "viscosity": {"order": 2, "coeff": 1.0e5}}},
+    "diagnostics": {"rnorms": [8, 32], "spectrum_iterations": [0], "l2": False},
+}
+
+
+def gen_pint_blowup(name, cfg, window=32):
+    """Reference mgrit_run until PintBlowUpError (pint.py:396-400): blow-up record
+    plus the compact trace of the iterations before it."""
+    from pintswe import pint, runner
+    pcfg = runner.build_pint_config(cfg)
+    geometry = runner.build_geometry(cfg)
+    prob = pint.SweProblem(pcfg, geometry)
+    u0 = runner.initial_state(cfg, pcfg.levels[0].M, geometry)
+    try:
+        tr = pint.mgrit_run(prob, pcfg, u0)
+        blow = None
+    except pint.PintBlowUpError as exc:
+        tr = exc.trace
+        blow = (exc.iteration, exc.slice_index)
+    g0 = prob.grids[0]
+    sel = np.flatnonzero(g0.n_of <= window)
+    k_ok = len(tr.snapshots) if blow is None else blow[0]
+    snaps = np.stack([np.stack([_state_arrays(x) for x in snap]) for snap in tr.snapshots[:k_ok]])
+    lv = pcfg.levels
+    return dict(name=name, config_json=json.dumps(cfg, sort_keys=True), window=window, sel=sel,
+                fineM=lv[0].M, coarseM=lv[1].M, dt0=lv[0].dt, T=pcfg.T, N0=pcfg.N0,
+                nlevels=pcfg.nlevels, cfactor=pcfg.cfactor, nrelax=pcfg.nrelax,
+                iters=pcfg.max_iters, nu_f=lv[0].stepper.viscosity.coeff_nu,
+                nu_c=lv[1].stepper.viscosity.coeff_nu, cycle=pcfg.cycle,
+                u0=_state_arrays(u0), phibar=u0.phibar,
+                blowup=np.array(blow if blow else (-1, -1)),
+                snap_window=snaps[..., sel], snap_maxabs=np.abs(snaps).max(axis=-1),
+                snap_full_idx=np.array([snaps.shape[1] - 1]), snap_full=snaps[:, -1:])
+
+
 def gen_m1024_step(window=64):
     """cfg5's step (M=1024, dt=2 s, nu=0, gaussian_bumps, steppers.py:155-168) on
     the modes n <= window, with per-field max|.| of the whole output."""
@@ -295,6 +338,7 @@ def main_r2(which):
         "ac10agg": ("pint_ac10agg_M64.npz", lambda: gen_pint_run("ac10agg", AC10_AGGRESSIVE)),
         "cfg3s": ("pint_cfg3s_M64.npz", lambda: gen_pint_run("cfg3s", CFG3_STRUCT)),
         "m1024": ("step_window_M1024.npz", gen_m1024_step),
+        "cfg3blow": ("pint_cfg3blow_M64.npz", lambda: gen_pint_blowup("cfg3blow", CFG3_BLOWUP)),
         "m1024sht": ("sht_M1024.npz", gen_m1024_sht),
     }
     for w in which:

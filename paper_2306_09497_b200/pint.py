@@ -431,8 +431,11 @@ class MgritEngine:
         return torch.cat([u[0:1], self.comm.all_gather(mine)])
 
     def run(self, u0, fine_reference=None, initial_cpoints=None, keep_snapshots=True,
-            sync=None) -> IterationTrace:
-        """u0: tensor [1, ...] on level 0.  sync(): device barrier for wall times."""
+            sync=None, clock=None) -> IterationTrace:
+        """u0: tensor [1, ...] on level 0.  sync(): device barrier for wall times.
+        clock: optional object with start() / stop() -> seconds timing each
+        iteration's cycle (default: host perf_counter between sync() calls, the
+        reference's per-iteration wall time, pint.py:384-390)."""
         cfg = self.cfg
         m = self.m
         n0, n1 = cfg.N0, cfg.points_on(1)
@@ -460,12 +463,17 @@ class MgritEngine:
         for s in range(1, m):
             u[m * (idx - 1) + s] = guess[:-1]
         for k in range(1, cfg.max_iters + 1):
-            sync()
-            t0 = time.perf_counter()
             f0 = self.fine_steps
-            self._cycle(0, u, None, cfg.cycle)
-            sync()
-            trace.wall_times.append(time.perf_counter() - t0)
+            if clock is not None:
+                clock.start()
+                self._cycle(0, u, None, cfg.cycle)
+                trace.wall_times.append(clock.stop())
+            else:
+                sync()
+                t0 = time.perf_counter()
+                self._cycle(0, u, None, cfg.cycle)
+                sync()
+                trace.wall_times.append(time.perf_counter() - t0)
             trace.fine_steps.append(self.fine_steps - f0)
             snap = self._cpoints(u)
             trace.snapshots.append(SnapshotList(self.problem, snap) if keep_snapshots else None)
