@@ -49,6 +49,8 @@ struct FftArgs {
   int dlam;                     // FOP_NONLINEAR: field 2 (d_lambda Phi) is i m times field 5's
                                 // half spectrum (in[2] unused): saves one synthesis term
   int no_rest;                  // FOP_NONLINEAR: omit -Phi' delta (nonlinear_advection alone)
+  int v4ld;                     // lane kernel, pair-major input: E and O of one (m, slice) in
+                                // one 256-bit load (LDG.E.256)
   const double *in[FFT_MAXF];   // E/O half spectra      [m][2][Jp][ld]
   double *out[FFT_MAXF];        // F+/F- analysis inputs [m][2][Jp][ld]
   const double *gin[2];         // grids [slice][J][I]

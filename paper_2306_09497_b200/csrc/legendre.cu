@@ -1,5 +1,6 @@
 // Grouped, parity-folded FP64 DMMA Legendre GEMMs (see legendre.cuh).
 #include "legendre.cuh"
+#include "legendre_gemv.cuh"
 
 #include <algorithm>
 
@@ -269,137 +270,31 @@ __global__ void __launch_bounds__(128) leg_anal_kernel(const __grid_constant__ L
 // keeps a few independent loads in flight per lane and reduces by shuffles.
 // Same terms, signs and edge rules as leg_synth_kernel / leg_anal_kernel.
 // ---------------------------------------------------------------------------
-constexpr int GV_L = 8;  // lanes per dot product group
-
 // one 8-lane group per (output, m, pair): lanes split the mode rows, every table
-// element is loaded once and applied to all NS slices
+// element is loaded once and applied to all NS slices (legendre_gemv.cuh).  Whole
+// warps iterate (a warp holds 4 groups), so the shuffles always see every lane.
 template <int NS>
 __global__ void __launch_bounds__(256) leg_synth_gemv(const __grid_constant__ LegArgs args) {
-  const int M = args.M, Jh = args.Jh, Jp = args.Jp, ld = args.ld;
+  const long long ng = (long long)args.nout * (args.M + 1) * args.Jh;
   const int gl = threadIdx.x & (GV_L - 1);
-  const long long ng = (long long)args.nout * (M + 1) * Jh;
-  for (long long gi = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / GV_L; gi < ng;
-       gi += (long long)gridDim.x * blockDim.x / GV_L) {
-    const int p = (int)(gi % Jh);
-    const long long q = gi / Jh;
-    const int m = (int)(q % (M + 1)), oi = (int)(q / (M + 1));
-    const LegOut &o = args.out[oi];
-    const int km = M + 1 - m, ne = (km + 1) >> 1, no = km >> 1, off = args.offsets[m];
-    double acc[2][NS][2];  // [E / O][slice][re / im]
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int j = 0; j < NS; ++j) acc[h][j][0] = acc[h][j][1] = 0.0;
-    for (int ti = 0; ti < o.nterms; ++ti) {
-      const LegTerm &T = o.t[ti];
-      const double sgm = T.sign * (T.times_im ? (double)m : 1.0);
-      for (int par = 0; par < 2; ++par) {
-        const int nr = par ? no : ne, r0 = off + (par ? ne : 0), h = par ^ T.flip;
-#pragma unroll 2
-        for (int tt = gl; tt < nr; tt += GV_L) {
-          const int r = r0 + tt;
-          const double a = __ldg(T.tab + (size_t)r * Jp + p);
-          const double sc = sgm * (T.scale ? __ldg(T.scale + r) : 1.0);
-          const double2 *src = reinterpret_cast<const double2 *>(T.src + (size_t)r * ld);
-#pragma unroll
-          for (int j = 0; j < NS; ++j) {
-            const double2 v = __ldg(src + j);
-            double x = v.x;
-            if (T.phi0 != nullptr && r == 0) x -= T.phi0[j];  // phi_prime (dynamics.py:52-56)
-            // i m X: (re, im) -> (-im, re)
-            const double bRe = T.times_im ? -v.y * sc : x * sc;
-            const double bIm = T.times_im ? x * sc : v.y * sc;
-            acc[h][j][0] = fma(a, bRe, acc[h][j][0]);
-            acc[h][j][1] = fma(a, bIm, acc[h][j][1]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int w = GV_L / 2; w > 0; w >>= 1)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int j = 0; j < NS; ++j) {
-          acc[h][j][0] += __shfl_xor_sync(0xffffffffu, acc[h][j][0], w);
-          acc[h][j][1] += __shfl_xor_sync(0xffffffffu, acc[h][j][1], w);
-        }
-    if (gl < NS) {  // lane j writes slice j
-      const double z = m ? 1.0 : 0.0;  // irfft ignores Im of the mean bin (spharm.py:257)
-      double *dE = o.dst + (size_t)m * 2 * Jp * ld, *dO = dE + (size_t)Jp * ld;
-#pragma unroll
-      for (int j = 0; j < NS; ++j)
-        if (j == gl) {
-          *reinterpret_cast<double2 *>(dE + (size_t)p * ld + 2 * j) =
-              make_double2(acc[0][j][0], z * acc[0][j][1]);
-          *reinterpret_cast<double2 *>(dO + (size_t)p * ld + 2 * j) =
-              make_double2(acc[1][j][0], z * acc[1][j][1]);
-        }
-    }
+  const long long step = (long long)gridDim.x * blockDim.x / GV_L;
+  for (long long g0 = (blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31)) / GV_L; g0 < ng;
+       g0 += step) {
+    const long long gi = g0 + (threadIdx.x & 31) / GV_L;
+    synth_gemv_group<NS, false>(args, gi, gl, gi < ng);
   }
 }
 
 // one 8-lane group per (output, mode row): lanes split the latitude pairs
 template <int NS>
 __global__ void __launch_bounds__(256) leg_anal_gemv(const __grid_constant__ LegArgs args, int K) {
-  const int M = args.M, Jh = args.Jh, Jp = args.Jp, ld = args.ld;
-  const int gl = threadIdx.x & (GV_L - 1);
   const long long ng = (long long)args.nout * K;
-  for (long long gi = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / GV_L; gi < ng;
-       gi += (long long)gridDim.x * blockDim.x / GV_L) {
-    const int k = (int)(gi % K), oi = (int)(gi / K);
-    const LegOut &o = args.out[oi];
-    // mode row k -> (m, parity): binary search of the block offsets
-    int lo = 0, hi = M;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (args.offsets[mid] <= k) lo = mid;
-      else hi = mid - 1;
-    }
-    const int m = lo, km = M + 1 - m, ne = (km + 1) >> 1;
-    const int par = (k - args.offsets[m]) >= ne;
-    double acc[NS][2];
-#pragma unroll
-    for (int j = 0; j < NS; ++j) acc[j][0] = acc[j][1] = 0.0;
-    for (int ti = 0; ti < o.nterms; ++ti) {
-      const LegTerm &T = o.t[ti];
-      const int fsel = par ^ T.flip;  // 0: F+, 1: F-
-      const double *F = T.src + ((size_t)m * 2 + (fsel ^ T.swap_pm)) * Jp * ld;
-      const double *tab = T.tab + (size_t)k * Jp;
-      double s[NS][2];
-#pragma unroll
-      for (int j = 0; j < NS; ++j) s[j][0] = s[j][1] = 0.0;
-#pragma unroll 2
-      for (int p = gl; p < Jh; p += GV_L) {
-        const double a = __ldg(tab + p) * (T.pscale ? __ldg(T.pscale + p) : 1.0);
-        const double2 *f = reinterpret_cast<const double2 *>(F + (size_t)p * ld);
-#pragma unroll
-        for (int j = 0; j < NS; ++j) {
-          const double2 v = __ldg(f + j);
-          s[j][0] = fma(a, v.x, s[j][0]);
-          s[j][1] = fma(a, v.y, s[j][1]);
-        }
-      }
-      // i m X: (re, im) -> (-m im, m re)
-      const double fc = T.sign * (T.times_im ? (double)m : 1.0);
-#pragma unroll
-      for (int j = 0; j < NS; ++j) {
-        acc[j][0] += T.times_im ? -fc * s[j][1] : fc * s[j][0];
-        acc[j][1] += T.times_im ? fc * s[j][0] : fc * s[j][1];
-      }
-    }
-#pragma unroll
-    for (int w = GV_L / 2; w > 0; w >>= 1)
-#pragma unroll
-      for (int j = 0; j < NS; ++j) {
-        acc[j][0] += __shfl_xor_sync(0xffffffffu, acc[j][0], w);
-        acc[j][1] += __shfl_xor_sync(0xffffffffu, acc[j][1], w);
-      }
-#pragma unroll
-    for (int j = 0; j < NS; ++j)
-      if (j == gl)
-        *reinterpret_cast<double2 *>(o.dst + (size_t)k * ld + 2 * j) =
-            make_double2(acc[j][0], acc[j][1]);
+  const int gl = threadIdx.x & (GV_L - 1);
+  const long long step = (long long)gridDim.x * blockDim.x / GV_L;
+  for (long long g0 = (blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31)) / GV_L; g0 < ng;
+       g0 += step) {
+    const long long gi = g0 + (threadIdx.x & 31) / GV_L;
+    anal_gemv_group<NS, false>(args, K, gi, gl, gi < ng);
   }
 }
 
