@@ -56,6 +56,9 @@ constexpr int CC_NT = 512, CC_CHUNK = 2400, CC_MPT = (CC_CHUNK + CC_NT - 1) / CC
 struct CcRanges {
   int k[CC_MAXC + 1];
 };
+// the balanced m-block split of a C-CTA cluster (spectral.cu); returns the largest
+// range (0: a range exceeds CC_CHUNK)
+int cn_cluster_ranges(int M, int C, CcRanges *rg);
 struct CcShared {
   unsigned long long red[6][CC_NT / 32];
   unsigned long long part[2][8];                // residual exchange (cluster barrier)
@@ -86,8 +89,9 @@ SWE_DEV void cc_wait(const unsigned long long *bar, unsigned parity) {
       : "memory");
 }
 
+// returns the slice's convergence (the same in every CTA of the cluster)
 template <bool CG>
-SWE_DEV void cn_cluster_body(
+SWE_DEV bool cn_cluster_body(
     int K, int B, const CcRanges &rg, int cap, const Ptr3C &x0, const Ptr3C &x1, const Ptr3C &x2,
     double s, double alpha, const double *eps, const double *phibar, const int2 *nbt,
     const double4 *cft, int rhs_given, const Ptr3 &dst, int max_iter, double tol, double dtnu,
@@ -319,6 +323,7 @@ SWE_DEV void cn_cluster_body(
     st2(dst.p[2], at(k), dtnu != 0.0 && done ? sc2(bh, d) : d);
   }
   cl.sync();  // peers may still read this CTA's maxima
+  return done;
 }
 
 

@@ -213,4 +213,6 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
 
 bool fft_lanes_ok(const FftArgs &a) { return lane_width(a, nullptr) != 0; }
 
+int fft_lanes_width(const FftArgs &a, int *rgen) { return lane_width(a, rgen); }
+
 }  // namespace swe

@@ -753,6 +753,8 @@ static int cc_ranges(int M, int C, CcRanges &rg) {
   return cap <= CC_CHUNK ? cap : 0;
 }
 
+int cn_cluster_ranges(int M, int C, CcRanges *rg) { return cc_ranges(M, C, *rg); }
+
 // cluster size for truncation M (0: the cluster path does not apply or cannot be
 // scheduled)
 int cn_cluster_size(int M, int want) {
