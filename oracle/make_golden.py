@@ -287,14 +287,17 @@ def gen_pint_blowup(name, cfg, window=32):
     k_ok = len(tr.snapshots) if blow is None else blow[0]
     snaps = np.stack([np.stack([_state_arrays(x) for x in snap]) for snap in tr.snapshots[:k_ok]])
     lv = pcfg.levels
+    # windowed states on every 16th C-point, the last one and those around slice 203
+    n = snaps.shape[1]
+    win_idx = np.array(sorted(set(range(0, n, 16)) | {n - 1} | set(range(200, 208))))
     return dict(name=name, config_json=json.dumps(cfg, sort_keys=True), window=window, sel=sel,
                 fineM=lv[0].M, coarseM=lv[1].M, dt0=lv[0].dt, T=pcfg.T, N0=pcfg.N0,
                 nlevels=pcfg.nlevels, cfactor=pcfg.cfactor, nrelax=pcfg.nrelax,
                 iters=pcfg.max_iters, nu_f=lv[0].stepper.viscosity.coeff_nu,
                 nu_c=lv[1].stepper.viscosity.coeff_nu, cycle=pcfg.cycle,
                 u0=_state_arrays(u0), phibar=u0.phibar,
-                blowup=np.array(blow if blow else (-1, -1)),
-                snap_window=snaps[..., sel], snap_maxabs=np.abs(snaps).max(axis=-1),
+                blowup=np.array(blow if blow else (-1, -1)), win_idx=win_idx,
+                snap_window=snaps[:, win_idx][..., sel], snap_maxabs=np.abs(snaps).max(axis=-1),
                 snap_full_idx=np.array([snaps.shape[1] - 1]), snap_full=snaps[:, -1:])
 
 

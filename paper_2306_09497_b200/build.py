@@ -21,7 +21,7 @@ LIB = os.path.join(HERE, "libswe_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 SOURCES = ["plan.cu", "legendre.cu", "legendre_v2.cu", "legendre_v3.cu", "fft.cu", "fft_lanes.cu", "spectral.cu",
-           "stepper.cu", "diag.cu", "settls.cu", "chain.cu"]
+           "stepper.cu", "diag.cu", "settls.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", INCLUDE]

@@ -1,6 +1,6 @@
 // Crank-Nicolson half step on one thread-block cluster per slice (device body) and
 // the per-mode helpers it shares with spectral.cu; included by spectral.cu (the
-// standalone k_cn_cluster) and chain.cu (the persistent serial-chain kernel).  CG:
+// standalone k_cn_cluster) and any kernel that fuses the half step.  CG:
 // inputs produced earlier in the same kernel are read through L2 (ld.global.cg).
 #pragma once
 #include <cooperative_groups.h>

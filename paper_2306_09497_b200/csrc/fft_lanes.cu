@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(lane_threads<LW>(), 512 / lane_threads<LW>())
   c.hem = SPLIT ? (int)(blockIdx.x & 1) : 0;
   const int grp = SPLIT ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   c.p = blockIdx.y;
+  c.pin = c.p;
   c.jn = c.p;
   c.js = a.J - 1 - c.p;
   c.eq = c.js == c.jn;

@@ -1,5 +1,5 @@
 // Device code of the "lane = row" longitude FFT (see fft_lanes.cu), shared by the
-// standalone FFT kernels and the persistent serial-chain kernel (chain.cu).  CG
+// FFT kernels (fft_lanes.cu) and any kernel that fuses the pass.  CG
 // (lane_load_eo): the E/O inputs are read through L2 (ld.global.cg), for inputs
 // produced earlier in the same kernel.
 #pragma once
@@ -186,6 +186,7 @@ SWE_DEV void lane_run_stage(double2 *X, double2 *ct, int N2, int Lp, int R, doub
 struct LCtx {
   double2 *X, *ct;
   int p, jn, js, eq, b0, nsl, S, tid, nthr;
+  int pin;  // row of the E/O input planes holding pair p (= p in fft_lanes.cu)
   int split, hem;  // split: this CTA holds only hemisphere hem's rows (row = f*S + s)
 };
 
@@ -270,9 +271,12 @@ SWE_DEV void item_ksf(int idx, int nf, int S, int &k, int &s, int &f) {
 }
 
 // E and O of one pair-major (pair, m, slice) item: one 32-byte load (sm_100 256-bit LDG)
-template <bool CG>
+template <int CG>
 SWE_DEV void ldg_eo(const double2 *p, double2 &e, double2 &o) {
-  if constexpr (CG)
+  if constexpr (CG == 2) {
+    e = p[0];
+    o = p[1];
+  } else if constexpr (CG == 1)
     asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
                  : "=d"(e.x), "=d"(e.y), "=d"(o.x), "=d"(o.y)
                  : "l"(p));
@@ -281,13 +285,15 @@ SWE_DEV void ldg_eo(const double2 *p, double2 &e, double2 &o) {
                  : "=d"(e.x), "=d"(e.y), "=d"(o.x), "=d"(o.y)
                  : "l"(p));
 }
-template <bool CG>
+// CG 0: read-only path, 1: through L2 (ld.global.cg), 2: generic (shared memory)
+template <int CG>
 SWE_DEV double2 ld_in(const double2 *p) {
-  if constexpr (CG) return __ldcg(p);
+  if constexpr (CG == 1) return __ldcg(p);
+  else if constexpr (CG == 2) return *p;
   else return __ldg(p);
 }
 
-template <int LW, bool CG = false>
+template <int LW, int CG = 0>
 SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
   const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1, S = c.S;
   const size_t eo = (size_t)a.Jp * a.ld / 2;  // E -> O offset (double2)
@@ -317,7 +323,7 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
         eoo = 1;
       } else {
         const double2 *base =
-            reinterpret_cast<const double2 *>(a.in[ok ? fs : 0] + (size_t)c.p * a.ld) + c.b0;
+            reinterpret_cast<const double2 *>(a.in[ok ? fs : 0] + (size_t)c.pin * a.ld) + c.b0;
         pk = base + (size_t)k * mstride + s;
         pk2 = base + (size_t)k2 * mstride + s;
         eoo = eo;
@@ -414,11 +420,11 @@ SWE_DEV double2 row_fm(const double2 *X, int row, int z1, int z2, double2 w) {
 // ([m][2][Jp][ld]), scaled by w01 (fields 0, 1) or w23 (2, 3); one flattened loop.
 // XN / XS hold the north / south rows (the same buffer unless split); items
 // i0, i0 + istep, ... of the (k, slice, field) range.
-template <int LW>
-SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, const double2 *XN, const double2 *XS,
-                          int nf, double w01, double w23, int i0, int istep) {
+// F+- of (field f, order k, slice s) handed to store(f, k, s, F+, F-)
+template <int LW, class Store>
+SWE_DEV void lane_extract_to(const FftArgs &a, const LCtx &c, const double2 *XN, const double2 *XS,
+                             int nf, double w01, double w23, int i0, int istep, Store store) {
   const int M = a.M, S = c.S, N2 = a.N2, per = (M + 1) * S;
-  const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
   for (int idx = i0; idx < nf * per; idx += istep) {
     int k, s, f;
     item_ksf<LW == 32>(idx, nf, S, k, s, f);
@@ -427,19 +433,29 @@ SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, const double2 *XN, co
     double2 w = __ldg(a.twh + k);
     w.y = -w.y;
     const double h = 0.5 * (f < 2 ? w01 : w23);
-    double2 *d = reinterpret_cast<double2 *>(a.out[f] + (size_t)c.p * a.ld) + c.b0 +
-                 (size_t)k * 2 * pm + s;
     const double2 fn = row_fm<LW>(XN, lrow(c, f, 0, s), z1, z2, w);
     if (c.eq) {
       const double2 v = make_double2(fn.x * h, fn.y * h);
-      d[0] = v;
-      d[pm] = v;
+      store(f, k, s, v, v);
     } else {
       const double2 fs = row_fm<LW>(XS, lrow(c, f, 1, s), z1, z2, w);
-      d[0] = make_double2((fn.x + fs.x) * h, (fn.y + fs.y) * h);
-      d[pm] = make_double2((fn.x - fs.x) * h, (fn.y - fs.y) * h);
+      store(f, k, s, make_double2((fn.x + fs.x) * h, (fn.y + fs.y) * h),
+            make_double2((fn.x - fs.x) * h, (fn.y - fs.y) * h));
     }
   }
+}
+
+template <int LW>
+SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, const double2 *XN, const double2 *XS,
+                          int nf, double w01, double w23, int i0, int istep) {
+  const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
+  lane_extract_to<LW>(a, c, XN, XS, nf, w01, w23, i0, istep,
+                      [&](int f, int k, int s, double2 fp, double2 fm) {
+                        double2 *d = reinterpret_cast<double2 *>(a.out[f] + (size_t)c.p * a.ld) +
+                                     c.b0 + (size_t)k * 2 * pm + s;
+                        d[0] = fp;
+                        d[pm] = fm;
+                      });
 }
 
 template <int LW>
@@ -456,8 +472,8 @@ __host__ __device__ constexpr int lane_slices(int op, int lw) {
 // FOP_NONLINEAR on one CTA's rows (no hemisphere split): nonlinear_advection +
 // nonlinear_rest (dynamics.py:142-160).  in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi,
 // 5 Phi (phi_prime applied here), 6 delta; out: F+- of (tphi, ke, xi u cos, xi v cos)
-template <int LW, bool GEN, bool CG>
-SWE_DEV void lane_nonlinear(const FftArgs &a, const LCtx &c) {
+template <int LW, bool GEN, int CG, class Store>
+SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   const int p = c.p, I = a.I, S = c.S;
   const double ia = a.inv_acos[p];
   lane_load_eo<LW, CG>(a, c, 7, 5);
@@ -481,7 +497,18 @@ SWE_DEV void lane_nonlinear(const FftArgs &a, const LCtx &c) {
   // only the 4 product fields x 2 hemispheres (S = 1)
   lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN>(a, c);
   const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
-  lane_extract<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr);
+  lane_extract_to<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
+}
+
+template <int LW, bool GEN, int CG>
+SWE_DEV void lane_nonlinear(const FftArgs &a, const LCtx &c) {
+  const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
+  lane_nonlinear_to<LW, GEN, CG>(a, c, [&](int f, int k, int s, double2 fp, double2 fm) {
+    double2 *d = reinterpret_cast<double2 *>(a.out[f] + (size_t)c.p * a.ld) + c.b0 +
+                 (size_t)k * 2 * pm + s;
+    d[0] = fp;
+    d[pm] = fm;
+  });
 }
 
 }  // namespace

@@ -433,8 +433,6 @@ void plan_destroy(swe_plan *pl) {
   cudaFree(pl->H);
   cudaFree(pl->offsets);
   cudaFree(pl->perm);
-  cudaFree(pl->iperm);
-  cudaFree(pl->chain_args);
   cudaFree(pl->lap_eig);
   cudaFree(pl->inv_lap);
   cudaFree(pl->eps);

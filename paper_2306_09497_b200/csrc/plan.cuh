@@ -96,7 +96,5 @@ struct swe_plan {
   std::vector<StepGraph> graphs;
   cudaStream_t cap[2] = {nullptr, nullptr};  // capture streams (step, fixed-point body)
   int iter_guess = 1;  // fixed-point iterations launched before the first host check
-  int *iperm = nullptr;             // [K] internal row -> reference packed index (chain.cu)
-  void *chain_args = nullptr;       // device ChainArgs of the persistent serial chain
   size_t table_bytes = 0;
 };

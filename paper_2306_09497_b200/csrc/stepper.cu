@@ -14,7 +14,6 @@
 #include "../../include/swe_b200.h"
 #include "plan.cuh"
 #include "spectral.cuh"
-#include "chain.cuh"
 #include "settls.cuh"
 
 namespace swe {
@@ -44,7 +43,6 @@ int g_cn_small = 1;        // one-launch CN half step for small truncations (K <
 int g_cn_fused = 1;        // speculative smem-resident fixed point (k_cn_fused) on the fine level
 int g_fft_lw32 = 0;        // nonlinear lane FFT with 32 rows (2 slices) per CTA
 int g_fft_v4 = 1;          // pair-major E/O hand-over read with 256-bit loads
-int g_chain = 0;           // serial sweeps of one slice as one persistent cluster kernel
 int g_gemv_max_b = 3;      // batches up to this size take the dot-product Legendre kernels
 int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: by batch)
 int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 when
@@ -381,9 +379,8 @@ int eval_coriolis(const Run &r, const double *xi, const double *de, double *oxi,
 }
 
 // N = N_A + N_R (dynamics.py:142-160) into k[3]; ke uses scratch spectral array `tmp`
-// the three launches of one nonlinear evaluation: synthesis of 6 fields, the FFT
-// pass with the grid products, analysis of 4 fields (eval_nonlinear, and the
-// persistent serial chain which runs the same arguments)
+// the arguments of the three launches of one nonlinear evaluation: synthesis of 6
+// fields, the FFT pass with the grid products, analysis of 4 fields
 void nonlinear_args(const Run &r, const double *const U[3], double *const k[3], double *tmp,
                     bool no_rest, bool pm, LegArgs &syn, FftArgs &f, LegArgs &an) {
   swe_plan *pl = r.pl;
@@ -1011,7 +1008,7 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
          (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16) | (g_cc_ctas << 17) | (g_gemv_max_b << 22) |
-         (g_cn_fused << 25) | (g_fft_v4 << 26) | (g_chain << 27);
+         (g_cn_fused << 25) | (g_fft_v4 << 26);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1068,96 +1065,6 @@ int step_graph(const Run &r, const swe_stepper_cfg &cfg, cudaGraphExec_t *exec) 
   g.graph = nullptr;
   g.exec = nullptr;
   pl->graphs.push_back(g);
-  return OK;
-}
-
-// The serial sweep of one slice as ONE persistent cluster kernel (chain.cu) when the
-// per-step path would run, for a slice alone, exactly the device code the kernel
-// reuses: spectral Coriolis with the reference fixed point, the 8-lane gemv Legendre
-// groups, the 16-row lane FFT with unrolled radices, the one-cluster CN half step.
-// *ran = false: not applicable, the caller takes the per-step path.  u[0] must be in
-// the workspace (b.U) already; g_int: forcing in the internal layout (nullable).
-int chain_sweep(const Run &r, const swe_stepper_cfg &cfg, double *u, const double *g_int, int n,
-                bool *ran) {
-  swe_plan *pl = r.pl;
-  *ran = false;
-  if (!g_chain || g_prof || g_fast_coriolis != 2 || !cfg.coriolis_implicit || pl->omega == 0.0 ||
-      cfg.implicit_solver != 0 || !cfg.include_nonlinear || cfg.implicit_max_iter <= 0 ||
-      r.B != 1 || r.Bsel != 1 || n < 1)
-    return OK;
-  if (!(g_leg_path == 5 || (g_leg_path == 0 && g_gemv_max_b >= 1))) return OK;
-  if (!(g_fft_path == 0 || g_fft_path == 2)) return OK;
-  FftArgs probe;
-  memset(&probe, 0, sizeof(probe));
-  fill_fft(r, probe);
-  int rgen = 0;
-  if (fft_lanes_width(probe, &rgen) != 16 || rgen != 0) return OK;
-  // the CN half step cn_half_spec takes for one slice
-  int want = g_cc_ctas ? g_cc_ctas : 16, C = 0;
-  if (g_cn_cluster)
-    for (; want >= 1 && !(C = cn_cluster_size(pl->M, want)); want /= 2) {
-    }
-  if (!(C >= 1 && (C <= want || g_cn_cluster == 2))) return OK;
-  ChainArgs ca;
-  memset(&ca, 0, sizeof(ca));
-  ca.cap = cn_cluster_ranges(pl->M, C, &ca.rg);
-  const int smem = chain_smem(pl->N2, ca.cap);
-  if (!ca.cap || !chain_ok(C, smem)) return OK;
-  const int K = pl->K;
-  if (!pl->iperm) {
-    std::vector<int> perm(K), inv(K);
-    SWE_CUDA(cudaMemcpy(perm.data(), pl->perm, sizeof(int) * K, cudaMemcpyDeviceToHost));
-    for (int k = 0; k < K; ++k) inv[perm[k]] = k;
-    SWE_CUDA(cudaMalloc(&pl->iperm, sizeof(int) * K));
-    SWE_CUDA(cudaMemcpy(pl->iperm, inv.data(), sizeof(int) * K, cudaMemcpyHostToDevice));
-  }
-  if (!pl->chain_args) SWE_CUDA(cudaMalloc(&pl->chain_args, sizeof(ChainArgs)));
-  const Bufs b = bufs(r);
-  const double *USc[3] = {b.US[0], b.US[1], b.US[2]}, *MIDc[3] = {b.MID[0], b.MID[1], b.MID[2]};
-  FftArgs f2;
-  nonlinear_args(r, USc, b.K1, b.TMP, false, false, ca.syn[0], ca.fft, ca.an[0]);
-  nonlinear_args(r, MIDc, b.K2, b.TMP, false, false, ca.syn[1], f2, ca.an[1]);
-  fill_fft(r, ca.fft);
-  ca.C = C;
-  ca.K = K;
-  ca.M = pl->M;
-  ca.n = n;
-  for (int f = 0; f < 3; ++f) {
-    ca.U[f] = b.U[f];
-    ca.US[f] = b.US[f];
-    ca.K1[f] = b.K1[f];
-    ca.K2[f] = b.K2[f];
-    ca.MID[f] = b.MID[f];
-  }
-  ca.TMP = b.TMP;
-  Work &w = pl->ws;
-  ca.lap = pl->lap_eig;
-  ca.eps = pl->eps;
-  ca.phibar = w.phibar;
-  ca.nbt = pl->cor_nb;
-  ca.cft = pl->cor_cf;
-  ca.dt = cfg.dt;
-  ca.alpha = cfg.dt / 4.0;
-  ca.dtnu = cfg.dt * cfg.visc_nu;
-  ca.halfq = cfg.visc_order / 2.0;
-  ca.tol = cfg.implicit_tol;
-  ca.max_iter = cfg.implicit_max_iter;
-  ca.iters = w.iters;
-  ca.flags = w.flags;
-  ca.counter = w.counter;
-  ca.resid = w.stats;
-  ca.fail = w.d_fail;
-  ca.g = g_int;
-  ca.u = u;
-  ca.iperm = pl->iperm;
-  // pageable source: the call returns once the struct has been staged
-  SWE_CUDA(cudaMemcpyAsync(pl->chain_args, &ca, sizeof(ca), cudaMemcpyHostToDevice, r.st));
-  SWE_CUDA(cudaMemsetAsync(w.d_fail, 0, sizeof(int), r.st));
-  SWE_CUDA(cudaMemsetAsync(w.counter, 0, sizeof(int), r.st));
-  int rc;
-  if ((rc = chain_launch(reinterpret_cast<const ChainArgs *>(pl->chain_args), C, smem, r.st)))
-    return rc;
-  *ran = true;
   return OK;
 }
 
@@ -1494,18 +1401,6 @@ int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
   SpecPtrsC sc = {{b.U[0], b.U[1], b.U[2]}};
   Ptr3 U = {{b.U[0], b.U[1], b.U[2]}};
-  {
-    // the whole chain in one persistent cluster kernel (chain.cu) where it applies
-    bool ran = false;
-    if ((rc = to_internal(u, d, 1, 3, K, pl->perm, r.st)) ||
-        (rc = chain_sweep(r, *cfg, u, g ? w.sweep_g : nullptr, n, &ran)))
-      return rc;
-    if (ran) {
-      SWE_CUDA(cudaStreamSynchronize(r.st));
-      if (!*reinterpret_cast<volatile int *>(w.h_fail)) return OK;
-      // an unconverged solve: the per-step path below reruns the sweep and raises
-    }
-  }
   cudaGraphExec_t exec = nullptr;
   if (g_graphs && !g_prof && (rc = step_graph(r, *cfg, &exec))) return rc;
   for (int pass = 0; pass < 2; ++pass) {
@@ -1636,10 +1531,6 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "cn_cluster") == 0 && value >= 0 && value <= 2) {
     g_cn_cluster = value;
-    return OK;
-  }
-  if (key && strcmp(key, "chain") == 0 && (value == 0 || value == 1)) {
-    g_chain = value;
     return OK;
   }
   if (key && strcmp(key, "fft_v4") == 0 && (value == 0 || value == 1)) {

@@ -40,15 +40,16 @@ def check_trace(g, snaps, tol=1e-10):
                 assert d < tol, (k, i, d)
         return worst
     sel, win, mx = g["sel"], g["snap_window"], g["snap_maxabs"]
-    assert snaps.shape[:2] == win.shape[:2], (snaps.shape, win.shape)
+    widx = g["win_idx"] if "win_idx" in g else np.arange(win.shape[1])
+    assert snaps.shape[:2] == mx.shape[:2], (snaps.shape, mx.shape)
     got_mx = np.abs(snaps).max(axis=-1)
     # xi = delta = 0 at the initial C-point: compare as e <= tol * scale
     assert (np.abs(got_mx - mx) <= tol * mx).all(), "maxabs"
     worst = max(worst, float((np.abs(got_mx - mx) / np.maximum(mx, 1e-300)).max()))
     for k in range(win.shape[0]):
-        for i in range(win.shape[1]):
+        for w, i in enumerate(widx):
             for f in range(3):
-                e = np.abs(snaps[k, i, f, sel] - win[k, i, f]).max()
+                e = np.abs(snaps[k, i, f, sel] - win[k, w, f]).max()
                 assert e <= tol * mx[k, i, f], ("window", k, i, f, e)
                 worst = max(worst, float(e / max(mx[k, i, f], 1e-300)))
     for j, i in enumerate(g["snap_full_idx"]):
@@ -212,3 +213,22 @@ def test_device_sweep_matches_stepwise():
         w = u.clone()
         with pytest.raises(steppers.ImplicitSolveError, match="residual"):
             bad.sweep_batch(1, w, None)
+
+
+def test_gpu_engine_cfg3_horizon_blows_up_like_reference():
+    """cfg3's level structure on its real horizon (N0 1024, dt0 60 s, 3 levels,
+    cfactor 4, nrelax 2, coarse M=51; fine level at M=64 so the reference finishes
+    here): the reference engine raises PintBlowUpError at iteration 3, slice 203
+    (golden); the GPU engine raises at the same iteration and slice, and its trace
+    before the blow-up matches the reference's."""
+    g = load_golden("pint_cfg3blow_M64.npz")
+    pint, prob, pc, u0 = _setup(g)
+    with pytest.raises(pint.PintBlowUpError) as ei:
+        pint.mgrit_run(prob, pc, u0)
+    it, sl = (int(x) for x in g["blowup"])
+    assert (ei.value.iteration, ei.value.slice_index) == (it, sl)
+    tr = ei.value.trace
+    snaps = np.stack([s.tensor.cpu().numpy() for s in tr.snapshots[:it]])
+    worst = check_trace(g, snaps)
+    print(f"[PARITY] cfg3 horizon: blow-up at iteration {it}, slice {sl} as the reference; "
+          f"trace before it worst {worst:.2e}")
