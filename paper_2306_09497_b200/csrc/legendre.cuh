@@ -9,6 +9,8 @@
 // [even n-m | odd n-m].
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace swe {
@@ -53,6 +55,9 @@ struct LegArgs {
   // zero between launches)
   unsigned long long *sched;
   const double *zeros;  // >= 1024 zero doubles (v3: source of padding rows)
+  // v3 analysis: TMA tensor maps of the P (0) and H (1) tables, [K][Jp] fp64, box
+  // 16 pairs x 32 modes, 128-byte swizzle (plan.cu)
+  CUtensorMap tmap[2];
 };
 
 // Launch helpers (legendre.cu).  items/tiles are prepared by the plan.

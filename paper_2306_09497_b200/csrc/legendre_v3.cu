@@ -48,12 +48,15 @@ struct Synth3Smem {
   unsigned long long full[S3_NS], empty[S3_NS];
   int next;  // unit handed from producer warp 0 to warp 1
 };
-struct alignas(128) Anal3Stage {
-  double A[2 * A3_BR][A3_LDA];
+// analysis table tile: 2 x 32 mode rows (E, O) x 16 latitude pairs, written by two
+// TMA tensor loads with the 128-byte swizzle: the 16-byte chunk c of row r sits at
+// chunk c ^ (r & 7) (conflict-free fragment reads without padding)
+struct alignas(1024) Anal3Stage {
+  double A[2 * A3_BR][A3_KP];
   double F[2][A3_KP][A3_LDB];
   int unit;
 };
-struct Anal3Smem {
+struct alignas(1024) Anal3Smem {
   Anal3Stage st[A3_NS];
   unsigned long long full[A3_NS], empty[A3_NS];
   int next;  // unit handed from producer thread 0 to the producer warpgroup
@@ -90,6 +93,14 @@ SWE_DEV void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
 SWE_DEV void cp_async_arrive(unsigned long long *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
+}
+// TMA tensor tile (2D) global -> shared, completion counted on `bar` in bytes
+SWE_DEV void tma2d(void *dst, const CUtensorMap *tm, int c0, int c1, unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 // TMA bulk copy global -> shared, completion counted on `bar` in bytes
 SWE_DEV void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
@@ -352,7 +363,8 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
 
 __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ LegArgs args) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Anal3Smem &sm = *reinterpret_cast<Anal3Smem *>(smem_raw);
+  // the 128-byte swizzle needs 1024-byte aligned tiles
+  Anal3Smem &sm = *reinterpret_cast<Anal3Smem *>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = args.M, Jp = args.Jp, ld = args.ld, Jh = args.Jh;
   const int ncol = (ld + V3_BN - 1) / V3_BN;
@@ -369,10 +381,10 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
 
   if (warp < V3_CW0) {
     regs_dec();
-    // the whole producer warpgroup (128 threads) streams each stage with
-    // zero-filling cp.async: table tile (2*A3_BR modes x 16 pairs) and the F+/F-
-    // rows (2 x 16 pairs x 128 columns); every thread arrives on "full" once its
-    // own copies have landed (cp.async.mbarrier.arrive.noinc)
+    // the producer warpgroup (128 threads) streams each stage: the table tile
+    // (2 x 32 modes x 16 pairs) as two TMA tensor tiles, the F+/F- rows (2 x 16 pairs
+    // x 128 columns) as 32 bulk copies; every thread arrives on "full" (thread 0
+    // after the expect_tx, the others at once: cp.async.mbarrier.arrive.noinc)
     const int ptid = tid;  // 0..127
     int it = 0;
     while (true) {
@@ -402,19 +414,19 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
         const int term = c / nch_t, q0 = (c - term * nch_t) * A3_KP;
         const LegTerm &T = o.t[term];
         Anal3Stage &S = sm.st[s];
-#pragma unroll
-        for (int piece = ptid; piece < 2 * A3_BR * 8; piece += 128) {
-          const int rr = piece >> 3, cc = (piece & 7) * 2;
-          const int par = rr / A3_BR, tt = x.tile + (rr % A3_BR);
-          const bool v = tt < (par ? no : ne);
-          const size_t row = (size_t)off + (par ? ne : 0) + tt;
-          cp_async16(&S.A[rr][cc], T.tab + (v ? row * Jp + q0 + cc : 0), v);
-        }
+        // table rows off + tile.. (E) and off + ne + tile.. (O): rows past the
+        // parity block only feed output rows that are never stored; rows past K
+        // are zero-filled by the TMA unit
         // F+/F- rows (2 x 16 pairs, up to 1 KB each) as 32 bulk copies (TMA) instead
         // of 2048 16-byte cp.async requests; pairs >= Jh come from the zero block
         const double *fb = T.src + (size_t)x.m * 2 * Jp * ld + x.c0;
         const unsigned fbytes = (unsigned)min(V3_BN, ld - x.c0) * 8u;
-        if (ptid == 0) mbar_expect_tx(&sm.full[s], 2u * A3_KP * fbytes);
+        if (ptid == 0) {
+          mbar_expect_tx(&sm.full[s], 2u * A3_KP * fbytes + (unsigned)sizeof(S.A));
+          const CUtensorMap *tm = &args.tmap[T.flip];
+          tma2d(&S.A[0][0], tm, q0, off + x.tile, &sm.full[s]);
+          tma2d(&S.A[A3_BR][0], tm, q0, off + ne + x.tile, &sm.full[s]);
+        }
         if (ptid < 2 * A3_KP) {
           const int hs = ptid / A3_KP, pr = ptid % A3_KP, p = q0 + pr;
           bulk_g2s(&S.F[hs][pr][0],
@@ -433,6 +445,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
 
   regs_inc();
   const int cw = warp - V3_CW0, g = lane >> 2, t = lane & 3;
+  const int gr = ((g & 3) << 1) | (g >> 2);  // tile row of fragment row g
   const int wpar = cw & 1, wrq = (cw >> 1) & 1, wch = cw >> 2;
   int it = 0;
   while (true) {
@@ -465,12 +478,17 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
 #pragma unroll
         for (int kk = 0; kk < A3_KP / 4; ++kk)
           ps[kk] = T.pscale ? __ldg(T.pscale + q0 + kk * 4 + t) : 1.0;
-        const double *Ab = &S.A[wpar * A3_BR + wrq * A3_RW + g][t];
+        // fragment row g reads tile row wpar*32 + wrq*16 + i*8 + gr, gr = the even rows
+        // for lanes 0-15 and the odd ones for 16-31 (a half-warp's 64-bit loads then
+        // hit 8 distinct 16-byte chunks); k index kk*4 + t sits in chunk
+        // (2 kk + t/2) ^ gr, element t & 1
+        const double *Ab = &S.A[wpar * A3_BR + wrq * A3_RW + gr][t & 1];
         const double *Bb = &S.F[fsel][t][wch * 64 + (g ^ tim)];
         double a[2][A3_FR], b[2][8];
         auto frag = [&](int kk, int q) {
+          const int cs = ((2 * kk + (t >> 1)) ^ gr) << 1;
 #pragma unroll
-          for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 8 * A3_LDA + kk * 4] * (asc * ps[kk]);
+          for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 8 * A3_KP + cs] * (asc * ps[kk]);
 #pragma unroll
           for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * A3_LDB + j * 8], bmask);
         };
@@ -494,7 +512,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     const int off = args.offsets[x.m];
 #pragma unroll
     for (int i = 0; i < A3_FR; ++i) {
-      const int tt = x.tile + wrq * A3_RW + i * 8 + g;
+      const int tt = x.tile + wrq * A3_RW + i * 8 + gr;
       if (tt >= nt) continue;
       const size_t k = (size_t)off + (wpar ? ne : 0) + tt;
 #pragma unroll
@@ -533,7 +551,7 @@ int leg_synth_v3_launch(const LegArgs &a, cudaStream_t st) {
 
 int leg_anal_v3_launch(const LegArgs &a, cudaStream_t st) {
   static bool attr = false;
-  const int smem = (int)sizeof(Anal3Smem);
+  const int smem = (int)sizeof(Anal3Smem) + 1024;  // + alignment slack (1024-byte tiles)
   if (!attr) {
     SWE_CUDA(cudaFuncSetAttribute(leg_anal_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;

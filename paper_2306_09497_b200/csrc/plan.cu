@@ -7,6 +7,8 @@
 #include <algorithm>
 
 #include "plan.cuh"
+
+#include <cudaTypedefs.h>
 #include "spectral.cuh"
 
 namespace swe {
@@ -279,6 +281,37 @@ int plan_create(int M, double a, double omega, double gravity, int device, swe_p
     SWE_LAUNCH_CHECK();
     SWE_CUDA(cudaDeviceSynchronize());
     SWE_CUDA(cudaFree(dmu));
+  }
+
+  // TMA tensor maps of the tables for the analysis GEMM: [K rows][Jp] fp64, box of
+  // 16 latitude pairs (128 bytes) x 32 mode rows, 128-byte swizzle (the consumers
+  // read the tile with the matching XOR); rows past K are zero-filled
+  {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void *fn = nullptr;
+      SWE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !fn) {
+        set_error("cuTensorMapEncodeTiled not available");
+        return E_CUDA;
+      }
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)Jp, (cuuint64_t)K};
+    const cuuint64_t strides[1] = {(cuuint64_t)Jp * sizeof(double)};
+    const cuuint32_t box[2] = {16, 32}, estr[2] = {1, 1};
+    double *tabs[2] = {pl->P, pl->H};
+    for (int t = 0; t < 2; ++t) {
+      const CUresult cr = encode(&pl->tmap[t], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, tabs[t], dims,
+                                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
+        return E_CUDA;
+      }
+    }
   }
 
   // FFT: roots of unity in long double, rounded once

@@ -97,4 +97,5 @@ struct swe_plan {
   cudaStream_t cap[2] = {nullptr, nullptr};  // capture streams (step, fixed-point body)
   int iter_guess = 1;  // fixed-point iterations launched before the first host check
   size_t table_bytes = 0;
+  CUtensorMap tmap[2];  // TMA descriptors of P and H (legendre_v3.cu analysis tiles)
 };

@@ -115,6 +115,8 @@ LegArgs leg_args(const Run &r) {
   a.offsets = r.pl->offsets;
   a.sched = r.pl->ws.sched;
   a.zeros = r.pl->zeros;
+  a.tmap[0] = r.pl->tmap[0];
+  a.tmap[1] = r.pl->tmap[1];
   return a;
 }
 
