@@ -6,6 +6,16 @@
 
 #define SWE_DEV __device__ __forceinline__
 
+// a / b, correctly rounded, from r = RN(1 / b) (Markstein: q0 = RN(a r), the
+// remainder e = a - b q0 exact by FMA, RN(q0 + e r) = RN(a / b) for normal
+// operands); 3 DFMA instead of the division sequence when b repeats.  e == 0: q0 is
+// exact (keeps the sign of a zero quotient)
+SWE_DEV double ddiv_r(double a, double b, double r) {
+  const double q0 = a * r;
+  const double e = fma(-q0, b, a);
+  return e == 0.0 ? q0 : fma(e, r, q0);
+}
+
 namespace swe {
 
 // ---- error plumbing (host) -------------------------------------------------

@@ -1164,6 +1164,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
   const double pb = act ? phibar[b] : 0.0, apb = alpha * pb, aap = alpha * alpha * pb;
   int lo[CF_EPT], hi[CF_EPT];
   double2 pv[CF_EPT], q0[CF_EPT];
+  double rden[CF_EPT];  // 1 / (1 + a^2 Pb eps) of each element: divisions as ddiv_r
   // ---- prologue (as k_cn_start): X staged in the B copies.  The xi/delta inputs go
   // global -> shared by cp.async (no registers, all loads of a thread in flight):
   // a single input straight into XB/DB; with the Heun terms x0 -> XA/DA, x1 ->
@@ -1254,8 +1255,9 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
         st2(R.p[2], i, r2);
       }
       const double apb_ = alpha * pb, denom = 1.0 + alpha * alpha * pb * e_;
-      const double2 nph =
-          make_double2((r0.x - apb_ * r2.x) / denom, (r0.y - apb_ * r2.y) / denom);
+      rden[j] = 1.0 / denom;
+      const double2 nph = make_double2(ddiv_r(r0.x - apb_ * r2.x, denom, rden[j]),
+                                       ddiv_r(r0.y - apb_ * r2.y, denom, rden[j]));
       const double ae = alpha * e_;
       pv[j] = nph;
       XA[e] = r1;
@@ -1297,7 +1299,8 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
         }
         const double2 rx = add2(r1, sc2(alpha, lx)), rd = add2(r2, sc2(alpha, lc));
         const double denom = 1.0 + aap * e_;
-        const double2 ph = make_double2((rp.x - apb * rd.x) / denom, (rp.y - apb * rd.y) / denom);
+        const double2 ph = make_double2(ddiv_r(rp.x - apb * rd.x, denom, rden[j]),
+                                        ddiv_r(rp.y - apb * rd.y, denom, rden[j]));
         const double ae = alpha * e_;
         const double2 de = make_double2(rd.x + ae * ph.x, rd.y + ae * ph.y);
         mx[0] = max(mx[0], sqmag_bits(ph.x, ph.y));
