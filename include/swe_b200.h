@@ -176,7 +176,7 @@ int swe_profile(int enable);
  * half step when its cluster of CTAs per slice is no larger than the batch asks
  * for (one CTA per slice from 32 slices, up to 16 for one slice; K up to ~38k
  * modes), 2 at any cluster size, 0 never; "cn_cluster_ctas" forces the CTAs per
- * slice (0 = by batch size).  "fft_lw32" 1: 32-row nonlinear lane FFT (default 0).
+ * slice (0 = by batch size). 
  * "cn_fused": 1 (default) speculative shared-memory fixed point for M <= 262 (the
  * guessed iteration count runs in one pass per m-block pair; slices converging
  * earlier are recomputed, later ones continue in the tiled loop), 0 off.  Results

@@ -45,7 +45,6 @@ struct FftArgs {
   const double *phisub;         // [slice] phibar*sqrt2*P_00, subtracted from field 5 (FOP_NONLINEAR)
   int in_pm;                    // FOP_NONLINEAR, lane kernel: inputs in the pair-major layout
                                 // [Jh][ld/2][M+1][E,O] (LegOut::layout 1)
-  int lw32;                     // FOP_NONLINEAR, lane kernel: 32 rows = 2 slices per CTA
   int dlam;                     // FOP_NONLINEAR: field 2 (d_lambda Phi) is i m times field 5's
                                 // half spectrum (in[2] unused): saves one synthesis term
   int no_rest;                  // FOP_NONLINEAR: omit -Phi' delta (nonlinear_advection alone)

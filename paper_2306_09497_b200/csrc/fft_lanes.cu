@@ -205,9 +205,6 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
     return E_SHAPE;
   }
   const int smem = (int)(((size_t)a.N2 * lw + g) * sizeof(double2));
-  if (a.lw32 && op == FOP_NONLINEAR && !g && lw == 16 &&
-      (size_t)a.N2 * 32 * sizeof(double2) <= 227 * 1024)
-    return launch_lanes<FOP_NONLINEAR, 32, false>(a, a.N2 * 32 * (int)sizeof(double2), st);
   if (g) return lw == 16 ? launch_width<16, true>(op, a, smem, st) : launch_width<8, true>(op, a, smem, st);
   return lw == 16 ? launch_width<16, false>(op, a, smem, st) : launch_width<8, false>(op, a, smem, st);
 }

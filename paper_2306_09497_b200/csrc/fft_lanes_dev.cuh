@@ -307,7 +307,7 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
       int k, s, f;
-      item_ksf<LW == 32>(idx, nf, S, k, s, f);
+      item_ksf<false>(idx, nf, S, k, s, f);
       const bool ok = idx < total && s < c.nsl;
       const int k2 = k == 0 ? N2 : N2 - k;
       const double2 z = make_double2(0.0, 0.0);
@@ -347,7 +347,7 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
     for (int u = 0; u < U; ++u) {
       const int idx = i0 + u * c.nthr;
       int k, s, f;
-      item_ksf<LW == 32>(idx, nf, S, k, s, f);
+      item_ksf<false>(idx, nf, S, k, s, f);
       if (idx >= total || s >= c.nsl) continue;
       if (f == subf && k == 0) e[u].x -= a.phisub[c.b0 + s];
       const int k2 = N2 - k;
@@ -427,7 +427,7 @@ SWE_DEV void lane_extract_to(const FftArgs &a, const LCtx &c, const double2 *XN,
   const int M = a.M, S = c.S, N2 = a.N2, per = (M + 1) * S;
   for (int idx = i0; idx < nf * per; idx += istep) {
     int k, s, f;
-    item_ksf<LW == 32>(idx, nf, S, k, s, f);
+    item_ksf<false>(idx, nf, S, k, s, f);
     if (s >= c.nsl) continue;
     const int z1 = __ldg(a.pos_z + k), z2 = __ldg(a.pos_z + (k == 0 ? 0 : N2 - k));
     double2 w = __ldg(a.twh + k);
@@ -459,14 +459,12 @@ SWE_DEV void lane_extract(const FftArgs &a, const LCtx &c, const double2 *XN, co
 }
 
 template <int LW>
-constexpr int lane_threads() { return LW == 16 ? 256 : 512; }  // 8 and 32 rows: one CTA per SM
+constexpr int lane_threads() { return LW == 16 ? 256 : 512; }  // 8 rows: one CTA per SM
 
 // slices per CTA (rows = fields x 2 hemispheres x slices; the LW = 8 nonlinear pass
 // holds one hemisphere of one slice per CTA)
 __host__ __device__ constexpr int lane_slices(int op, int lw) {
-  return lw == 16   ? fft_lane_slices(op)
-         : lw == 32 ? 2 * fft_lane_slices(op)
-                    : (op == FOP_NONLINEAR ? 1 : fft_lane_slices(op) / 2);
+  return lw == 16 ? fft_lane_slices(op) : (op == FOP_NONLINEAR ? 1 : fft_lane_slices(op) / 2);
 }
 
 // FOP_NONLINEAR on one CTA's rows (no hemisphere split): nonlinear_advection +

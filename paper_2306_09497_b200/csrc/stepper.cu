@@ -41,7 +41,6 @@ int g_graphs = 1;          // swe_imex_step replays one captured CUDA graph per 
 int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
 int g_cn_fused = 1;        // speculative smem-resident fixed point (k_cn_fused) on the fine level
-int g_fft_lw32 = 0;        // nonlinear lane FFT with 32 rows (2 slices) per CTA
 int g_fft_v4 = 1;          // pair-major E/O hand-over read with 256-bit loads
 int g_gemv_max_b = 3;      // batches up to this size take the dot-product Legendre kernels
 int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: by batch)
@@ -411,7 +410,6 @@ void nonlinear_args(const Run &r, const double *const U[3], double *const k[3], 
     f.no_rest = no_rest ? 1 : 0;
     f.in_pm = pm;
     f.v4ld = pm && g_fft_v4;
-    f.lw32 = g_fft_lw32;
   }
   {
     LegArgs &a = an;
@@ -1009,7 +1007,7 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
-         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_fft_lw32 << 16) | (g_cc_ctas << 17) | (g_gemv_max_b << 22) |
+         (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_cc_ctas << 17) | (g_gemv_max_b << 22) |
          (g_cn_fused << 25) | (g_fft_v4 << 26);
 }
 
@@ -1525,10 +1523,6 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "cn_cluster_ctas") == 0 && value >= 0 && value <= 16) {
     g_cc_ctas = value;
-    return OK;
-  }
-  if (key && strcmp(key, "fft_lw32") == 0 && (value == 0 || value == 1)) {
-    g_fft_lw32 = value;
     return OK;
   }
   if (key && strcmp(key, "cn_cluster") == 0 && value >= 0 && value <= 2) {

@@ -605,32 +605,6 @@ def test_direct_implicit_solve_settls(mods):
         assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max(), f
 
 
-@pytest.mark.parametrize("M,B", [(256, 3), (256, 64), (51, 7)])
-def test_nonlinear_lw32_matches_lw16(mods, M, B):
-    """The 32-row (two slices per CTA) nonlinear lane FFT gives bitwise the 16-row
-    kernel's tendencies (odd batches leave a half-empty CTA)."""
-    spharm, dynamics, _, scenarios = mods
-    import torch
-    from paper_2306_09497_b200 import _lib
-    grid = spharm.get_grid(M)
-    s = scenarios.gaussian_bumps(grid, batch=B)
-    rng = np.random.default_rng(B)
-    taper = torch.from_numpy((grid.n_of + 1.0) ** -2).cuda()
-    noise = torch.from_numpy(rng.standard_normal((B, grid.n_modes))).cuda() * taper
-    noise[:, : M + 1] = noise[:, : M + 1].real
-    s.data[:, 1] += 1e-5 * noise
-    s.data[:, 2] += 1e-6 * noise
-    out = {}
-    for lw in (0, 1):
-        _lib.set_option("fft_lw32", lw)
-        try:
-            out[lw] = [t.cpu().numpy() for t in dynamics.nonlinear(s)]
-        finally:
-            _lib.set_option("fft_lw32", 0)
-    for f in range(3):
-        assert np.array_equal(out[0][f], out[1][f]), f
-
-
 @pytest.mark.parametrize("B", [65, 130])
 def test_odd_and_wide_batches_match_single_slice(mods, B):
     """M=256 batches past the 64/128-column GEMM tiles and the 32-slice CN tiles
