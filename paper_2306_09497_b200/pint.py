@@ -231,6 +231,40 @@ class Comm:
         return int(t[0])
 
 
+class LevelWindow:
+    """Rows [base, base + n) of a level array of `total` rows, addressed with the
+    global row indices the engine uses (ints, slices, index tensors); row 0 (the
+    initial condition) is kept separately when it lies outside the window.  A
+    rank holding a contiguous block of slices keeps O(N0 / ranks) level-0 states
+    instead of all N0 + 1."""
+
+    def __init__(self, data: torch.Tensor, base: int, total: int, row0: torch.Tensor):
+        self.data, self.base, self.total, self.row0 = data, base, total, row0
+
+    @property
+    def shape(self):
+        return (self.total,) + tuple(self.data.shape[1:])
+
+    @property
+    def device(self):
+        return self.data.device
+
+    def _loc(self, i):
+        if isinstance(i, slice):
+            start = 0 if i.start is None else i.start
+            stop = self.total if i.stop is None else i.stop
+            return slice(start - self.base, stop - self.base, i.step)
+        return i - self.base
+
+    def __getitem__(self, i):
+        if self.base > 0 and isinstance(i, slice) and i.start in (0, None) and i.stop == 1:
+            return self.row0
+        return self.data[self._loc(i)]
+
+    def __setitem__(self, i, v):
+        self.data[self._loc(i)] = v
+
+
 class MgritEngine:
     """FAS-MGRIT / Parareal over a batched problem (pint.py:197-400 semantics).
 
@@ -456,12 +490,24 @@ class MgritEngine:
         _, mx0 = self.problem.stats_batch(0, u0)
         limit = 1e10 * max(float(mx0[0]), 1e-300)
         self._check_finite(trace, 0, guess, limit)
-        u = self.problem.zeros(0, n0 + 1)
-        u[0:1] = u0
-        idx = torch.arange(1, n1 + 1, device=u.device)
-        u[m * idx] = guess[1:]
+        if self.G == 1:
+            u = self.problem.zeros(0, n0 + 1)
+            u[0:1] = u0
+            idx = torch.arange(1, n1 + 1, device=u.device)
+        else:
+            # this rank's slices lo..hi and the C-point before them (the halo)
+            lo, hi = self._own(0, n1)
+            base = m * (lo - 1)
+            u = LevelWindow(self.problem.zeros(0, m * (hi - lo + 1) + 1), base, n0 + 1,
+                            u0.clone())
+            if base == 0:
+                u[0:1] = u0
+            else:
+                u[base:base + 1] = guess[lo - 1:lo]
+            idx = torch.arange(lo, hi + 1, device=u.device)
+        u[m * idx] = guess[idx]
         for s in range(1, m):
-            u[m * (idx - 1) + s] = guess[:-1]
+            u[m * (idx - 1) + s] = guess[idx - 1]
         for k in range(1, cfg.max_iters + 1):
             f0 = self.fine_steps
             if clock is not None:

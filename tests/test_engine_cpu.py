@@ -235,3 +235,20 @@ def test_stepper_config_implicit_solver():
     assert steppers.StepperConfig(implicit_solver="direct").to_c().implicit_solver == 1
     with pytest.raises(ValueError):
         steppers.StepperConfig(implicit_solver="lu")
+
+
+def test_level_window_matches_full_array():
+    """pint.LevelWindow (a rank's rows of the level-0 array, O(N0 / ranks)) reads and
+    writes like the full array for every index form the engine uses."""
+    import torch
+    full = torch.arange(41, dtype=torch.float64).reshape(41, 1) * 1.5
+    base, n = 16, 13   # rows 16..28: slices 9..14 of cfactor 2 plus their halo C-point
+    w = pint.LevelWindow(full[base:base + n].clone(), base, 41, full[0:1].clone())
+    assert w.shape == (41, 1)
+    assert torch.equal(w[0:1], full[0:1]) and torch.equal(w[20], full[20])
+    idx = torch.arange(base, base + n - 1, 2)
+    assert torch.equal(w[idx], full[idx]) and torch.equal(w[idx + 1], full[idx + 1])
+    assert torch.equal(w[base:base + n:2], full[base:base + n:2])
+    w[idx + 1] = -w[idx]
+    full[idx + 1] = -full[idx]
+    assert torch.equal(w.data, full[base:base + n])
