@@ -728,8 +728,8 @@ def run_ours(args):
 
 def launch_ranks(args):
     """--gpus N > 1 outside torchrun: relaunch this script with one rank per GPU
-    (torch.distributed.run, 127.0.0.1 rendezvous); NCCL_DEBUG=INFO (init lines)
-    shows the communicator's rank count in the log."""
+    (torch.distributed.run, 127.0.0.1 rendezvous); NCCL_DEBUG=INFO (init lines,
+    on stderr) shows the communicator's rank count in the log."""
     import socket
     sock = socket.socket()
     sock.bind(("127.0.0.1", 0))
@@ -738,6 +738,8 @@ def launch_ranks(args):
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    # NCCL's lines on stderr, so rank 0's JSON line stays alone on stdout
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
            f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]

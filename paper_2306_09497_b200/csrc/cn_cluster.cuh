@@ -141,6 +141,7 @@ SWE_DEV bool cn_cluster_body(
   __syncthreads();
   // ---- rhs R and the first Helmholtz iterate (version 1)
   double2 vx[CC_MPT], vd[CC_MPT];
+  double rden[CC_MPT];
 #pragma unroll
   for (int j = 0; j < CC_MPT; ++j) {
     const int kk = tid + j * CC_NT, k = k0 + kk;
@@ -165,7 +166,9 @@ SWE_DEV bool cn_cluster_body(
     R1[kk] = r1;
     R2[kk] = r2;
     const double denom = 1.0 + aap * e;
-    const double2 nph = make_double2((r0.x - apb * r2.x) / denom, (r0.y - apb * r2.y) / denom);
+    rden[j] = 1.0 / denom;  // the iterations divide by the reciprocal (ddiv_r, exact)
+    const double2 nph = make_double2(ddiv_r(r0.x - apb * r2.x, denom, rden[j]),
+                                     ddiv_r(r0.y - apb * r2.y, denom, rden[j]));
     const double ae = alpha * e;
     P[kk] = nph;
     vx[j] = r1;
@@ -196,7 +199,8 @@ SWE_DEV bool cn_cluster_body(
       lcop(k, ver, x, d, lx, lc);
       const double2 rx = add2(r1, sc2(alpha, lx)), rd = add2(r2, sc2(alpha, lc));
       const double denom = 1.0 + aap * e;
-      const double2 ph = make_double2((rp.x - apb * rd.x) / denom, (rp.y - apb * rd.y) / denom);
+      const double2 ph = make_double2(ddiv_r(rp.x - apb * rd.x, denom, rden[j]),
+                                      ddiv_r(rp.y - apb * rd.y, denom, rden[j]));
       const double ae = alpha * e;
       const double2 de = make_double2(rd.x + ae * ph.x, rd.y + ae * ph.y);
       const double2 o0 = P[kk];
