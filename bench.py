@@ -666,6 +666,12 @@ def run_ours(args):
                                  "14 terms per nonlinear evaluation, 2 evaluations per step",
                 "time_share": leg_ms / max(prof_ms, 1e-9)}
     ach_f = fft_bytes / (fft_ms * 1e-3) / 1e9
+    # SURVEY.md §8(d)'s executed-work figure: the 12 longitude transforms one
+    # reference nonlinear evaluation runs (9 for nonlinear_advection, 3 for
+    # nonlinear_rest) at J*I*8 + J*(M+1)*16 bytes each, per slice and launch
+    g = grid
+    b8d = 12.0 * (g.nlat * g.nlon * 8 + g.nlat * (M + 1) * 16) * B * prof["fft_grid"][2]
+    ach_8d = b8d / (fft_ms * 1e-3) / 1e9
     roof_fft = {"kernel": "fft_lanes_kernel<5,16,0> (inverse FFT, grid products, forward FFT)",
                 "bound": "hbm", "achieved": ach_f, "peak": hbm, "unit": "GB/s",
                 "frac": ach_f / hbm, "traffic": traffic.get("fft"),
@@ -675,6 +681,10 @@ def run_ours(args):
                                  "fields read, 4 F+/F- fields written",
                 "binding_unit": "shared-memory / L1 data pipe (ncu "
                                 "l1tex__data_pipe_lsu_wavefronts), not HBM",
+                "achieved_survey_8d": ach_8d, "frac_survey_8d": ach_8d / hbm,
+                "survey_8d_work": "12 transforms x (J*I*8 + J*(M+1)*16) B per slice per launch "
+                                  "(the reference's rfft/irfft count of one nonlinear "
+                                  "evaluation; executed-work bytes, SURVEY.md 8d)",
                 "time_share": fft_ms / max(prof_ms, 1e-9)}
     # the dominant single kernel is the FFT pass; the Legendre GEMM pair is the
     # dominant kernel family and is reported alongside

@@ -48,6 +48,8 @@ struct FftArgs {
   int dlam;                     // FOP_NONLINEAR: field 2 (d_lambda Phi) is i m times field 5's
                                 // half spectrum (in[2] unused): saves one synthesis term
   int no_rest;                  // FOP_NONLINEAR: omit -Phi' delta (nonlinear_advection alone)
+  int out_il;                   // FOP_NONLINEAR, lane kernel: F+ and F- of one (m, pair, slice)
+                                // adjacent ([m][Jp][slice][F+, F-] complex), one 32-byte store
   int v4ld;                     // lane kernel, pair-major input: E and O of one (m, slice) in
                                 // one 256-bit load (LDG.E.256)
   const double *in[FFT_MAXF];   // E/O half spectra      [m][2][Jp][ld]

@@ -500,6 +500,17 @@ SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
 
 template <int LW, bool GEN, int CG>
 SWE_DEV void lane_nonlinear(const FftArgs &a, const LCtx &c) {
+  if (a.out_il) {
+    // [m][Jp][slice][F+, F-]: one 32-byte store per (field, order, slice)
+    const size_t nsl = a.ld >> 1;
+    lane_nonlinear_to<LW, GEN, CG>(a, c, [&](int f, int k, int s, double2 fp, double2 fm) {
+      double *d = a.out[f] + (((size_t)k * a.Jp + c.p) * nsl + c.b0 + s) * 4;
+      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(d), "d"(fp.x), "d"(fp.y),
+                   "d"(fm.x), "d"(fm.y)
+                   : "memory");
+    });
+    return;
+  }
   const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
   lane_nonlinear_to<LW, GEN, CG>(a, c, [&](int f, int k, int s, double2 fp, double2 fm) {
     double2 *d = reinterpret_cast<double2 *>(a.out[f] + (size_t)c.p * a.ld) + c.b0 +

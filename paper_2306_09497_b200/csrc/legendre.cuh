@@ -30,6 +30,8 @@ struct LegTerm {
   int times_im;
   int flip;     // 0: P-like parity, 1: H-like (odd in mu for even n-m)
   int swap_pm;  // analysis only: read plane 1 as F+ and plane 0 as F- (E/O input)
+  int f_il;     // analysis (v3) only: F+- interleaved per slice, [m][Jp][slice][F+, F-]
+                // complex (the lane FFT's 32-byte stores), instead of planes [m][2][Jp][ld]
 };
 
 struct LegOut {

@@ -34,6 +34,9 @@ constexpr int S3_KT = 16, S3_NS = 4, S3_LDA = 72 + 4, S3_LDB = V3_BN + 4;
 // of costing a whole extra work unit (plan.cu synth_items_v3)
 constexpr int S3_TW = 64, S3_XTRA = 8;
 constexpr int A3_KP = 16, A3_NS = 4, A3_LDA = A3_KP + 4, A3_LDB = V3_BN + 4;
+// interleaved F+- rows ([slice][F+, F-] complex, LegTerm::f_il): 2 x 128 doubles per
+// pair row, padded to 258 (= 2 mod 16 eight-byte banks: conflict-free B fragments)
+constexpr int A3_LDBI = 2 * V3_BN + 2;
 constexpr int A3_BR = V3_ABR;  // analysis modes per parity per unit
 constexpr int A3_RW = A3_BR / 2, A3_FR = A3_RW / 8;  // rows / 8-row fragments per consumer warp
 
@@ -427,7 +430,15 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
           tma2d(&S.A[0][0], tm, q0, off + x.tile, &sm.full[s]);
           tma2d(&S.A[A3_BR][0], tm, q0, off + ne + x.tile, &sm.full[s]);
         }
-        if (ptid < 2 * A3_KP) {
+        if (T.f_il) {
+          // one row of 2 x fbytes (F+ and F- of every slice) per pair
+          if (ptid < A3_KP) {
+            const int p = q0 + ptid;
+            double *Fi = &S.F[0][0][0] + (size_t)ptid * A3_LDBI;
+            bulk_g2s(Fi, p < Jh ? T.src + ((size_t)x.m * Jp + p) * 2 * ld + 2 * x.c0 : args.zeros,
+                     2 * fbytes, &sm.full[s]);
+          }
+        } else if (ptid < 2 * A3_KP) {
           const int hs = ptid / A3_KP, pr = ptid % A3_KP, p = q0 + pr;
           bulk_g2s(&S.F[hs][pr][0],
                    p < Jh ? fb + ((size_t)(hs ^ T.swap_pm) * Jp + p) * ld : args.zeros, fbytes,
@@ -462,6 +473,9 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     for (int i = 0; i < A3_FR; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // the unit's F layout as a compile-time switch (interleaved rows or planes)
+    auto mainloop = [&](auto ilc) {
+    constexpr bool IL = decltype(ilc)::value;
     for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
       const int s = it % A3_NS;
       if (c > 0) mbar_wait(&sm.full[s], (it / A3_NS) & 1);
@@ -483,14 +497,23 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
         // hit 8 distinct 16-byte chunks); k index kk*4 + t sits in chunk
         // (2 kk + t/2) ^ gr, element t & 1
         const double *Ab = &S.A[wpar * A3_BR + wrq * A3_RW + gr][t & 1];
-        const double *Bb = &S.F[fsel][t][wch * 64 + (g ^ tim)];
+        // B column n = wch*64 + j*8 + g' (g' = g ^ tim: re/im swap for i m X).  Planes:
+        // slice n/2 of plane fsel.  Interleaved rows: DMMA j's 8 columns are slices
+        // wch*32 + (j/2)*8 + (j&1) + 2 (g'/2), so a half-warp's 64-bit loads fall on 16
+        // distinct banks (row stride 258 = 2 mod 16); the epilogue stores the same map
+        const int gp = g ^ tim;
+        const double *Bb =
+            IL ? &S.F[0][0][0] + t * A3_LDBI + (wch * 32 + 2 * (gp >> 1)) * 4 + fsel * 2 + (gp & 1)
+               : &S.F[fsel][t][wch * 64 + gp];
+        constexpr int kst = IL ? 4 * A3_LDBI : 4 * A3_LDB;
         double a[2][A3_FR], b[2][8];
         auto frag = [&](int kk, int q) {
           const int cs = ((2 * kk + (t >> 1)) ^ gr) << 1;
 #pragma unroll
           for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 8 * A3_KP + cs] * (asc * ps[kk]);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * A3_LDB + j * 8], bmask);
+          for (int j = 0; j < 8; ++j)
+            b[q][j] = flip_sign(Bb[kk * kst + (IL ? (j >> 1) * 32 + (j & 1) * 4 : j * 8)], bmask);
         };
         frag(0, 0);
 #pragma unroll
@@ -508,6 +531,10 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
+    };
+    const int il = o.t[0].f_il;
+    if (il) mainloop(std::true_type{});
+    else mainloop(std::false_type{});
     const int nt = wpar ? no : ne;
     const int off = args.offsets[x.m];
 #pragma unroll
@@ -517,7 +544,8 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
       const size_t k = (size_t)off + (wpar ? ne : 0) + tt;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
+        const int col = il ? x.c0 + 2 * (wch * 32 + (j >> 1) * 8 + (j & 1) + 2 * t)
+                           : x.c0 + wch * 64 + j * 8 + 2 * t;
         if (col < ld)
           *reinterpret_cast<double2 *>(o.dst + k * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
       }

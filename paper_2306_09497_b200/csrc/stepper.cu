@@ -42,6 +42,7 @@ int g_helm_tiled = 1;      // smem-tiled fixed-point kernel for batches >= 32
 int g_cn_small = 1;        // one-launch CN half step for small truncations (K <= 2800)
 int g_cn_fused = 1;        // speculative smem-resident fixed point (k_cn_fused) on the fine level
 int g_fft_v4 = 1;          // pair-major E/O hand-over read with 256-bit loads
+int g_f_il = 1;            // F+- hand-over interleaved per slice (32-byte FFT stores)
 int g_gemv_max_b = 3;      // batches up to this size take the dot-product Legendre kernels
 int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: by batch)
 int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 when
@@ -285,7 +286,7 @@ int fft(const Run &r, int op, FftArgs &a) {
   // F+- rows of pairs Jh..Jp-1 are read by the analysis GEMM (TMA rows are not
   // zero-filled) but never written by the FFT: keep them zero for this layout
   static const int nfout[6] = {0, 0, 1, 2, 2, 4};
-  for (int o = 0; o < nfout[op]; ++o)
+  for (int o = 0; o < (a.out_il ? 0 : nfout[op]); ++o)
     if (pl->Jp > pl->Jh)
       SWE_CUDA(cudaMemset2DAsync(a.out[o] + (size_t)pl->Jh * r.ld, (size_t)pl->Jp * r.ld * 8, 0,
                                  (size_t)(pl->Jp - pl->Jh) * r.ld * 8, (size_t)(pl->M + 1) * 2,
@@ -386,6 +387,15 @@ void nonlinear_args(const Run &r, const double *const U[3], double *const k[3], 
                     bool no_rest, bool pm, LegArgs &syn, FftArgs &f, LegArgs &an) {
   swe_plan *pl = r.pl;
   const double *P = pl->P, *H = pl->H, *il = pl->inv_lap;
+  // interleaved F+- hand-over: the 16-row (unsplit) lane FFT writes it
+  bool fil = pm && g_f_il;
+  if (fil) {
+    FftArgs probe;
+    memset(&probe, 0, sizeof(probe));
+    fill_fft(r, probe);
+    int rgen = 0;
+    fil = fft_lanes_width(probe, &rgen) == 16;
+  }
   {
     LegArgs &a = syn;
     a = leg_args(r);
@@ -410,6 +420,7 @@ void nonlinear_args(const Run &r, const double *const U[3], double *const k[3], 
     f.no_rest = no_rest ? 1 : 0;
     f.in_pm = pm;
     f.v4ld = pm && g_fft_v4;
+    f.out_il = fil;
   }
   {
     LegArgs &a = an;
@@ -420,6 +431,10 @@ void nonlinear_args(const Run &r, const double *const U[3], double *const k[3], 
     set_out(a, 1, tmp, term(P, r.fsp(1)), nullptr, H);           // ke
     set_out(a, 2, k[1], term(P, r.fsp(2), -1.0, 1), &hx, H);     // -div(xi V)
     set_out(a, 3, k[2], term(P, r.fsp(3), 1.0, 1), &hd, H);      // curl(xi V)
+    // the lane FFT's interleaved F+- hand-over (FftArgs::out_il)
+    if (fil)
+      for (int i = 0; i < a.nout; ++i)
+        for (int t = 0; t < a.out[i].nterms; ++t) a.out[i].t[t].f_il = 1;
   }
 }
 
@@ -1008,7 +1023,7 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
          (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_cc_ctas << 17) | (g_gemv_max_b << 22) |
-         (g_cn_fused << 25) | (g_fft_v4 << 26);
+         (g_cn_fused << 25) | (g_fft_v4 << 26) | (g_f_il << 27);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1527,6 +1542,10 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "cn_cluster") == 0 && value >= 0 && value <= 2) {
     g_cn_cluster = value;
+    return OK;
+  }
+  if (key && strcmp(key, "f_il") == 0 && (value == 0 || value == 1)) {
+    g_f_il = value;
     return OK;
   }
   if (key && strcmp(key, "fft_v4") == 0 && (value == 0 || value == 1)) {
