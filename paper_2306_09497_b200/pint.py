@@ -448,6 +448,11 @@ class MgritEngine:
         v = pr.zeros(1, n1 + 1)
         v[0:1] = pr.restrict_batch(0, u0)
         track = self._tracks(1) and self.L == 2
+        sweep = getattr(pr, "sweep_batch", None)
+        if not track and sweep is not None and sweep(1, v, None):
+            # the whole serial run on the device (swe_imex_sweep: one step graph per
+            # point, one host check), bitwise the per-step loop below
+            return pr.prolong_batch(1, v)
         modes = settls_boundary_policy(self.L, 1, n1, self.m, self.cfg.chunk_size)
         for j in range(1, n1 + 1):
             hist = v[j - 2:j - 1] if track and j >= 2 and modes[j - 1] == TWO_STEP else None
