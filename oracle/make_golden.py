@@ -301,6 +301,40 @@ def gen_pint_blowup(name, cfg, window=32):
                 snap_full_idx=np.array([snaps.shape[1] - 1]), snap_full=snaps[:, -1:])
 
 
+# BASELINE cfg2 at its real parameters (M=256/51, dt 60/120 s, nu 1e5, cfactor 2,
+# nrelax 1, N0 128), first 2 iterations (the reference needs ~15 min per iteration)
+CFG2 = {
+    "scenario": "gaussian_bumps", "T": 128 * 60.0,
+    "fine": {"M": 256, "dt": 60.0, "scheme": "imex", "viscosity": {"order": 2, "coeff": 1.0e5}},
+    "pint": {"nlevels": 2, "cfactor": 2, "nrelax": 1, "max_iters": 2, "chunk_size": 0,
+             "coarse": {"M": 51, "scheme": "imex", "viscosity": {"order": 2, "coeff": 1.0e5}}},
+    "diagnostics": {"rnorms": [8, 32], "spectrum_iterations": [0, 2], "l2": False},
+}
+
+
+def gen_pint_big(name, cfg, window=24):
+    """Reference mgrit_run (no serial fine run) stored compactly: every C-point of
+    every iteration on n <= window, max|.| per field, the full last C-point."""
+    from pintswe import pint, runner
+    pcfg = runner.build_pint_config(cfg)
+    geometry = runner.build_geometry(cfg)
+    prob = pint.SweProblem(pcfg, geometry)
+    u0 = runner.initial_state(cfg, pcfg.levels[0].M, geometry)
+    tr = pint.mgrit_run(prob, pcfg, u0)
+    g0 = prob.grids[0]
+    sel = np.flatnonzero(g0.n_of <= window)
+    snaps = np.stack([np.stack([_state_arrays(x) for x in snap]) for snap in tr.snapshots])
+    lv = pcfg.levels
+    return dict(name=name, config_json=json.dumps(cfg, sort_keys=True), window=window, sel=sel,
+                fineM=lv[0].M, coarseM=lv[1].M, dt0=lv[0].dt, T=pcfg.T, N0=pcfg.N0,
+                nlevels=pcfg.nlevels, cfactor=pcfg.cfactor, nrelax=pcfg.nrelax,
+                iters=pcfg.max_iters, nu_f=lv[0].stepper.viscosity.coeff_nu,
+                nu_c=lv[1].stepper.viscosity.coeff_nu, cycle=pcfg.cycle,
+                u0=_state_arrays(u0), phibar=u0.phibar,
+                snap_window=snaps[..., sel], snap_maxabs=np.abs(snaps).max(axis=-1),
+                snap_full_idx=np.array([snaps.shape[1] - 1]), snap_full=snaps[:, -1:])
+
+
 def gen_m1024_step(window=64):
     """cfg5's step (M=1024, dt=2 s, nu=0, gaussian_bumps, steppers.py:155-168) on
     the modes n <= window, with per-field max|.| of the whole output."""
@@ -341,6 +375,7 @@ def main_r2(which):
         "ac10agg": ("pint_ac10agg_M64.npz", lambda: gen_pint_run("ac10agg", AC10_AGGRESSIVE)),
         "cfg3s": ("pint_cfg3s_M64.npz", lambda: gen_pint_run("cfg3s", CFG3_STRUCT)),
         "m1024": ("step_window_M1024.npz", gen_m1024_step),
+        "cfg2": ("pint_cfg2_M256.npz", lambda: gen_pint_big("cfg2", CFG2)),
         "cfg3blow": ("pint_cfg3blow_M64.npz", lambda: gen_pint_blowup("cfg3blow", CFG3_BLOWUP)),
         "m1024sht": ("sht_M1024.npz", gen_m1024_sht),
     }
