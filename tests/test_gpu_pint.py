@@ -232,3 +232,58 @@ def test_gpu_engine_cfg3_horizon_blows_up_like_reference():
     worst = check_trace(g, snaps)
     print(f"[PARITY] cfg3 horizon: blow-up at iteration {it}, slice {sl} as the reference; "
           f"trace before it worst {worst:.2e}")
+
+
+def _swe_cfg(pint, steppers, dynamics, n0, dt0, max_iters, M=16):
+    """swe_pint_config of the reference tests (tests/test_pint.py:28-37)."""
+    lv = [pint.LevelSpec(0, M, steppers.StepperConfig(dt=dt0)),
+          pint.LevelSpec(1, M, steppers.StepperConfig(dt=2 * dt0,
+                                                       viscosity=dynamics.ViscositySpec(2, 0.0)))]
+    return pint.PintConfig(levels=tuple(lv), T=n0 * dt0, N0=n0, cfactor=2, nrelax=0,
+                           max_iters=max_iters)
+
+
+def test_gpu_parareal_exact_finite_convergence():
+    """Parareal reproduces the serial fine solution after N0 / cfactor iterations
+    (test_pint.py:282-288, SPEC exact convergence), on the GPU engine."""
+    from paper_2306_09497_b200 import dynamics, pint, scenarios, steppers
+    pc = _swe_cfg(pint, steppers, dynamics, 16, 450.0, 8)
+    prob = pint.SweProblem(pc)
+    u0 = scenarios.gaussian_bumps(prob.grids[0])
+    fine = pint.fine_serial_cpoints(prob, pc, u0)
+    tr = pint.parareal_run(prob, pc, u0)
+    got, want = tr.snapshots[8].tensor[-1].cpu().numpy(), fine.tensor[-1].cpu().numpy()
+    assert rel_diff(got, want) < 1e-10
+
+
+def test_gpu_parareal_matches_textbook_predictor_corrector():
+    """The engine's Parareal iterates equal the textbook two-level update
+    U[k][i] = G(U[k][i-1]) + F(U[k-1][i-1]) - G(U[k-1][i-1]) computed directly from
+    single GPU steps (test_pint.py:291-319), to 1e-12."""
+    from paper_2306_09497_b200 import dynamics, pint, scenarios, steppers
+    pc = _swe_cfg(pint, steppers, dynamics, 8, 600.0, 3)
+    prob = pint.SweProblem(pc)
+    u0 = scenarios.gaussian_bumps(prob.grids[0])
+    tr = pint.parareal_run(prob, pc, u0)
+
+    def coarse(v):
+        return prob.step(1, v)
+
+    def fine(v):
+        for _ in range(pc.cfactor):
+            v = prob.step(0, v)
+        return v
+
+    nsl = 4
+    u = [[None] * (nsl + 1) for _ in range(4)]
+    u[0][0] = u0
+    for i in range(1, nsl + 1):
+        u[0][i] = coarse(u[0][i - 1])
+    for k in range(1, 4):
+        u[k][0] = u0
+        for i in range(1, nsl + 1):
+            u[k][i] = coarse(u[k][i - 1]) + fine(u[k - 1][i - 1]) - coarse(u[k - 1][i - 1])
+    for k in range(4):
+        for i in range(nsl + 1):
+            got = tr.snapshots[k].tensor[i].cpu().numpy()
+            assert rel_diff(got, u[k][i].data[0].cpu().numpy()) < 1e-12, (k, i)
