@@ -1721,6 +1721,32 @@ int axpy3(size_t n, Ptr3C a, Ptr3C x1, Ptr3C x2, double s, Ptr3 y, cudaStream_t 
   return OK;
 }
 
+// k_tend_finish of K1 fused with the Heun midpoint MID = U* + s K1 (k_axpy3): the
+// same two expressions, one pass
+__global__ void k_finish_axpy(int K, int B, double *kd, const double *ke, const double *lap,
+                              Ptr3C us, Ptr3C k1, double s, Ptr3 mid) {
+  FOR_KB(K, B) {
+    const int k = (int)(_i / B);
+    const double2 ke2 = ld2(ke, _i);
+    const double l = lap[k];
+    double2 d = ld2(kd, _i);
+    d = make_double2(d.x - ke2.x * l, d.y - ke2.y * l);
+    st2(kd, _i, d);
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const double2 t = f == 2 ? d : ld2(k1.p[f], _i);
+      st2(mid.p[f], _i, add2(ld2(us.p[f], _i), sc2(s, t)));
+    }
+  }
+}
+
+int finish_axpy(int K, int B, double *kd, const double *ke, const double *lap, Ptr3C us, Ptr3C k1,
+                double s, Ptr3 mid, cudaStream_t st) {
+  k_finish_axpy<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, kd, ke, lap, us, k1, s, mid);
+  SWE_LAUNCH_CHECK();
+  return OK;
+}
+
 int tend_finish(int K, int B, double *kd, const double *ke, const double *lap, double *kx,
                 const double *lcx, const double *lcd, cudaStream_t st) {
   k_tend_finish<<<nblocks((size_t)K * B), 256, 0, st>>>(K, B, kd, ke, lap, kx, lcx, lcd);

@@ -105,6 +105,9 @@ int decide(int B, double *stats, int *active, int *iters, int *counter, double t
            cudaStream_t st);
 int fill_int(int *p, int n, int v, cudaStream_t st);
 int axpy3(size_t n, Ptr3C a, Ptr3C x1, Ptr3C x2, double s, Ptr3 y, cudaStream_t st);
+// kd -= lap ke (k_tend_finish), then mid = us + s (k1 with kd as its third field)
+int finish_axpy(int K, int B, double *kd, const double *ke, const double *lap, Ptr3C us, Ptr3C k1,
+                double s, Ptr3 mid, cudaStream_t st);
 int tend_finish(int K, int B, double *kd, const double *ke, const double *lap, double *kx,
                 const double *lcx, const double *lcd, cudaStream_t st);
 int visc(int K, int B, Ptr3 u, const double *nn1a2, double dtnu, double halfq, cudaStream_t st);

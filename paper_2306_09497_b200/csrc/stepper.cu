@@ -450,13 +450,16 @@ int eval_nonlinear(const Run &r, const double *const U[3], double *const k[3], d
 }
 
 // explicit tendency (steppers.py:127-140)
+// defer: with implicit Coriolis the caller applies k[2] -= lap tmp itself (finish_axpy)
 int explicit_tendency(const Run &r, const swe_stepper_cfg &cfg, const double *const U[3],
-                      double *const k[3], double *tmp, double *lcx, double *lcd) {
+                      double *const k[3], double *tmp, double *lcx, double *lcd,
+                      bool defer = false) {
   int rc;
   const size_t n = (size_t)r.pl->K * r.B;
   const bool expl = !cfg.coriolis_implicit;
   if (cfg.include_nonlinear) {
     if ((rc = eval_nonlinear(r, U, k, tmp))) return rc;
+    if (defer && !expl) return OK;
     if (expl && (rc = eval_coriolis(r, U[1], U[2], lcx, lcd))) return rc;
     return tend_finish(r.pl->K, r.B, k[2], tmp, r.pl->lap_eig, k[1], expl ? lcx : nullptr,
                        expl ? lcd : nullptr, r.st);
@@ -871,11 +874,17 @@ int imex_internal(const Run &r, const swe_stepper_cfg &cfg, int *iters_host, dou
   }
   // Heun on the explicit part (steppers.py:162-166)
   const double *USc[3] = {b.US[0], b.US[1], b.US[2]};
-  if ((rc = explicit_tendency(r, cfg, USc, b.K1, b.TMP, b.LC[0], b.LC[1]))) return rc;
+  const bool fuse = cfg.include_nonlinear && cfg.coriolis_implicit;
+  if ((rc = explicit_tendency(r, cfg, USc, b.K1, b.TMP, b.LC[0], b.LC[1], fuse))) return rc;
   Ptr3C us = {{b.US[0], b.US[1], b.US[2]}}, k1 = {{b.K1[0], b.K1[1], b.K1[2]}};
   Ptr3C k2 = {{b.K2[0], b.K2[1], b.K2[2]}}, none = {{nullptr, nullptr, nullptr}};
   Ptr3 mid = {{b.MID[0], b.MID[1], b.MID[2]}};
-  if ((rc = axpy3(n, us, k1, none, dt, mid, r.st))) return rc;
+  if (fuse) {
+    if ((rc = finish_axpy(pl->K, r.B, b.K1[2], b.TMP, pl->lap_eig, us, k1, dt, mid, r.st)))
+      return rc;
+  } else if ((rc = axpy3(n, us, k1, none, dt, mid, r.st))) {
+    return rc;
+  }
   const double *MIDc[3] = {b.MID[0], b.MID[1], b.MID[2]};
   if ((rc = explicit_tendency(r, cfg, MIDc, b.K2, b.TMP, b.LC[0], b.LC[1]))) return rc;
   if (spec) {

@@ -287,3 +287,18 @@ def test_gpu_parareal_matches_textbook_predictor_corrector():
         for i in range(nsl + 1):
             got = tr.snapshots[k].tensor[i].cpu().numpy()
             assert rel_diff(got, u[k][i].data[0].cpu().numpy()) < 1e-12, (k, i)
+
+
+def test_gpu_engine_cfg2_real_parameters_match_reference():
+    """BASELINE cfg2 at its real parameters (M=256/51, dt 60/120 s, nu 1e5, cfactor 2,
+    nrelax 1, 64 C-slices): the first two MGRIT iterations against the reference
+    engine's own trace (oracle/make_golden.py cfg2, ~25 min of reference run time):
+    every C-point of every iteration on n <= 24, max|.| per field, and the full last
+    C-point incl. Phi', 1e-10."""
+    g = load_golden("pint_cfg2_M256.npz")
+    pint, prob, pc, u0 = _setup(g)
+    tr = pint.mgrit_run(prob, pc, u0)
+    snaps = np.stack([s.tensor.cpu().numpy() for s in tr.snapshots])
+    worst = check_trace(g, snaps)
+    print(f"[PARITY] cfg2 (M=256/51, 64 C-slices), {tr.iterations} iterations vs reference: "
+          f"worst {worst:.2e}")
