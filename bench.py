@@ -353,8 +353,9 @@ def pint_leg(torch, name, comm=None, iters=None):
             "ms_per_iteration": 1e3 * med, "ms_per_iteration_mean": 1e3 * float(its.mean()),
             "value_from_mean": per_it / float(its.mean()),
             "timing": "CUDA events around each MGRIT cycle, max over ranks, median iteration",
-            "collectives": ("NCCL halo send/recv + all-gather of the coarse forcing + "
-                            "all-reduced blow-up check per iteration") if G > 1 else "none"}
+            "collectives": (f"{comm.dist.get_backend().upper()} halo send/recv + all-gather "
+                            "of the coarse forcing + all-reduced blow-up check per iteration")
+            if G > 1 else "none"}
 
 
 def coriolis_legs(torch, steppers, cfg, state, steps, flush):

@@ -312,7 +312,18 @@ CFG2 = {
 }
 
 
-def gen_pint_big(name, cfg, window=24):
+# BASELINE cfg3 at its real parameters (M=256/51/51, dt 60/240/960 s, nu 1e5, cfactor 4,
+# nrelax 2, F_then_V, N0 1024): the first iteration only (~4 h of reference time)
+CFG3 = {
+    "scenario": "gaussian_bumps", "T": 1024 * 60.0,
+    "fine": {"M": 256, "dt": 60.0, "scheme": "imex", "viscosity": {"order": 2, "coeff": 1.0e5}},
+    "pint": {"nlevels": 3, "cfactor": 4, "nrelax": 2, "max_iters": 1, "chunk_size": 0,
+             "coarse": {"M": 51, "scheme": "imex", "viscosity": {"order": 2, "coeff": 1.0e5}}},
+    "diagnostics": {"rnorms": [8, 32], "spectrum_iterations": [0, 1], "l2": False},
+}
+
+
+def gen_pint_big(name, cfg, window=24, workers=1):
     """Reference mgrit_run (no serial fine run) stored compactly: every C-point of
     every iteration on n <= window, max|.| per field, the full last C-point."""
     from pintswe import pint, runner
@@ -320,10 +331,14 @@ def gen_pint_big(name, cfg, window=24):
     geometry = runner.build_geometry(cfg)
     prob = pint.SweProblem(pcfg, geometry)
     u0 = runner.initial_state(cfg, pcfg.levels[0].M, geometry)
-    tr = pint.mgrit_run(prob, pcfg, u0)
+    tr = pint.mgrit_run(prob, pcfg, u0, workers=workers)
     g0 = prob.grids[0]
     sel = np.flatnonzero(g0.n_of <= window)
     snaps = np.stack([np.stack([_state_arrays(x) for x in snap]) for snap in tr.snapshots])
+    if snaps.shape[1] > 65:   # long horizons: every 8th C-point and the last few
+        keep = np.array(sorted(set(range(0, snaps.shape[1], 8)) | {snaps.shape[1] - 1}))
+    else:
+        keep = np.arange(snaps.shape[1])
     lv = pcfg.levels
     return dict(name=name, config_json=json.dumps(cfg, sort_keys=True), window=window, sel=sel,
                 fineM=lv[0].M, coarseM=lv[1].M, dt0=lv[0].dt, T=pcfg.T, N0=pcfg.N0,
@@ -331,7 +346,8 @@ def gen_pint_big(name, cfg, window=24):
                 iters=pcfg.max_iters, nu_f=lv[0].stepper.viscosity.coeff_nu,
                 nu_c=lv[1].stepper.viscosity.coeff_nu, cycle=pcfg.cycle,
                 u0=_state_arrays(u0), phibar=u0.phibar,
-                snap_window=snaps[..., sel], snap_maxabs=np.abs(snaps).max(axis=-1),
+                win_idx=keep, snap_window=snaps[:, keep][..., sel],
+                snap_maxabs=np.abs(snaps).max(axis=-1),
                 snap_full_idx=np.array([snaps.shape[1] - 1]), snap_full=snaps[:, -1:])
 
 
@@ -376,6 +392,7 @@ def main_r2(which):
         "cfg3s": ("pint_cfg3s_M64.npz", lambda: gen_pint_run("cfg3s", CFG3_STRUCT)),
         "m1024": ("step_window_M1024.npz", gen_m1024_step),
         "cfg2": ("pint_cfg2_M256.npz", lambda: gen_pint_big("cfg2", CFG2)),
+        "cfg3": ("pint_cfg3_M256.npz", lambda: gen_pint_big("cfg3", CFG3, workers=6)),
         "cfg3blow": ("pint_cfg3blow_M64.npz", lambda: gen_pint_blowup("cfg3blow", CFG3_BLOWUP)),
         "m1024sht": ("sht_M1024.npz", gen_m1024_sht),
     }
