@@ -250,6 +250,11 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     // four warps of this parity by 32-column quarter so the unit stays balanced
     const int xq = wph * 2 + wch;  // this warp's column quarter of the remainder
     const bool xtra = wide && x.tile + S3_TW < Jh;
+    // column fragments holding real columns (small batches: a column's sums do not
+    // depend on the others, so skipping empty fragments changes no result)
+    const int bcols = min(V3_BN, ld - x.c0);
+    const bool wcols = bcols > wch * 64;  // this warp's 64 columns hold real ones
+    const bool xcols = bcols > xq * 32;
     double acc[4][8][2], acx[4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -264,7 +269,9 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
       for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
         const int s = it % S3_NS;
         if (c > 0) mbar_wait(&sm.full[s], (it / S3_NS) & 1);
-        if (nfr > 0 || XT) {
+        // small batches: warps whose columns are all padding skip the stage (a
+        // column's sums do not depend on the others: no result changes)
+        if ((nfr > 0 || XT) && (wcols || (XT && xcols))) {
           const Synth3Stage &S = sm.st[s];
           const LegTerm &T = o.t[c / nch_t];
           const int rpar = wpar ^ T.flip;
@@ -473,13 +480,16 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     for (int i = 0; i < A3_FR; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // small batches: a warp whose 64 columns (planes: wch*64..; interleaved rows:
+    // slices wch*32..) are all padding skips the stages (see leg_synth_v3)
+    const bool wcols = min(V3_BN, ld - x.c0) > wch * 64;
     // the unit's F layout as a compile-time switch (interleaved rows or planes)
     auto mainloop = [&](auto ilc) {
     constexpr bool IL = decltype(ilc)::value;
     for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
       const int s = it % A3_NS;
       if (c > 0) mbar_wait(&sm.full[s], (it / A3_NS) & 1);
-      if (nfr > 0) {
+      if (nfr > 0 && wcols) {
         const Anal3Stage &S = sm.st[s];
         const LegTerm &T = o.t[c / nch_t];
         const int tim = T.times_im;
