@@ -264,8 +264,9 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     for (int j = 0; j < 4; ++j) acx[j][0] = acx[j][1] = 0.0;
     // the remainder path is a separate instantiation, so ordinary units keep the
     // lean register allocation of the plain 4 x 8 fragment loop
-    auto mainloop = [&](auto xt_tag) {
+    auto mainloop = [&](auto xt_tag, auto nj_tag) {
       constexpr bool XT = decltype(xt_tag)::value;
+      constexpr int NJ = decltype(nj_tag)::value;  // column fragments computed (8, 4, 2)
       for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
         const int s = it % S3_NS;
         if (c > 0) mbar_wait(&sm.full[s], (it / S3_NS) & 1);
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
 #pragma unroll
             for (int i = 0; i < 4; ++i) a[q][i] = Ab[kk * 4 * S3_LDA + i * 8] * sc;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) b[q][j] = flip_sign(Bb[kk * 4 * S3_LDB + j * 8], bmask);
+            for (int j = 0; j < NJ; ++j) b[q][j] = flip_sign(Bb[kk * 4 * S3_LDB + j * 8], bmask);
           };
           frag(0, 0);
 #pragma unroll
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
             for (int i = 0; i < 4; ++i)
               if (i < nfr) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+                for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
               }
             if constexpr (XT) {
               const double *Ax = &S.A[rpar * S3_KT + t][S3_TW + g];
@@ -313,8 +314,15 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
         if (lane == 0) mbar_arrive(&sm.empty[s]);
       }
     };
-    if (xtra) mainloop(std::true_type{});
-    else mainloop(std::false_type{});
+    // narrow batches (<= 16 / 32 real columns in the tile) compute only the fragments
+    // that hold them: a column's sums never depend on the others
+    using N8 = std::integral_constant<int, 8>;
+    using N4 = std::integral_constant<int, 4>;
+    using N2 = std::integral_constant<int, 2>;
+    if (xtra) mainloop(std::true_type{}, N8{});
+    else if (bcols <= 16) mainloop(std::false_type{}, N2{});
+    else if (bcols <= 32) mainloop(std::false_type{}, N4{});
+    else mainloop(std::false_type{}, N8{});
     if (o.layout == 0) {
       // E or O plane of [m][2][Jp][ld]
       double *dst = o.dst + ((size_t)x.m * 2 + wpar) * Jp * ld;
@@ -484,8 +492,9 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     // slices wch*32..) are all padding skips the stages (see leg_synth_v3)
     const bool wcols = min(V3_BN, ld - x.c0) > wch * 64;
     // the unit's F layout as a compile-time switch (interleaved rows or planes)
-    auto mainloop = [&](auto ilc) {
+    auto mainloop = [&](auto ilc, auto nj_tag) {
     constexpr bool IL = decltype(ilc)::value;
+    constexpr int NJ = decltype(nj_tag)::value;  // column fragments computed (8, 4, 2)
     for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
       const int s = it % A3_NS;
       if (c > 0) mbar_wait(&sm.full[s], (it / A3_NS) & 1);
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
 #pragma unroll
           for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 8 * A3_KP + cs] * (asc * ps[kk]);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < NJ; ++j)
             b[q][j] = flip_sign(Bb[kk * kst + (IL ? (j >> 1) * 32 + (j & 1) * 4 : j * 8)], bmask);
         };
         frag(0, 0);
@@ -534,7 +543,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
           for (int i = 0; i < A3_FR; ++i)
             if (i < nfr) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+              for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
             }
         }
       }
@@ -543,8 +552,21 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     }
     };
     const int il = o.t[0].f_il;
-    if (il) mainloop(std::true_type{});
-    else mainloop(std::false_type{});
+    // narrow batches: only the fragments holding real columns (planes: columns
+    // j*8..; interleaved rows: j = 0, 1 hold slices 0..7, j < 4 slices 0..15)
+    using N8 = std::integral_constant<int, 8>;
+    using N4 = std::integral_constant<int, 4>;
+    using N2 = std::integral_constant<int, 2>;
+    const int bc = min(V3_BN, ld - x.c0);
+    if (il) {
+      if (bc <= 16) mainloop(std::true_type{}, N2{});
+      else if (bc <= 32) mainloop(std::true_type{}, N4{});
+      else mainloop(std::true_type{}, N8{});
+    } else {
+      if (bc <= 16) mainloop(std::false_type{}, N2{});
+      else if (bc <= 32) mainloop(std::false_type{}, N4{});
+      else mainloop(std::false_type{}, N8{});
+    }
     const int nt = wpar ? no : ne;
     const int off = args.offsets[x.m];
 #pragma unroll
