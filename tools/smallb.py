@@ -21,3 +21,14 @@ for B in (64, 32, 16, 8):
     e1.synchronize()
     out.append(f"B={B}: {e0.elapsed_time(e1) / 10:.3f} ms")
 print("per-rank fine step, select_batch 64: " + ", ".join(out))
+
+# per-class device time at 8 slices (the per-rank batch at 8 GPUs)
+s = bench.make_states(g, 8, 0)
+steppers.imex_steps_inplace(s, cfg, 1, select_batch=64)
+_lib.profile(True)
+for _ in range(5):
+    steppers.imex_steps_inplace(s, cfg, 1, select_batch=64)
+torch.cuda.synchronize()
+_lib.profile(False)
+p = _lib.profile_read()
+print("B=8 classes (ms/step): " + ", ".join(f"{k} {v[0] / 5:.3f} ({v[2] // 5} launches)" for k, v in p.items()))
