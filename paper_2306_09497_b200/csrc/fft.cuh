@@ -44,7 +44,7 @@ struct FftArgs {
   int Jh, Jp;                   // latitude pairs (incl. equator), padded pair count
   const double *phisub;         // [slice] phibar*sqrt2*P_00, subtracted from field 5 (FOP_NONLINEAR)
   int in_pm;                    // FOP_NONLINEAR, lane kernel: inputs in the pair-major layout
-                                // [Jh][ld/2][M+1][E,O] (LegOut::layout 1)
+                                // [Jh][M+1][ld/2][E,O] (LegOut::layout 1)
   int dlam;                     // FOP_NONLINEAR: field 2 (d_lambda Phi) is i m times field 5's
                                 // half spectrum (in[2] unused): saves one synthesis term
   int no_rest;                  // FOP_NONLINEAR: omit -Phi' delta (nonlinear_advection alone)
@@ -52,6 +52,9 @@ struct FftArgs {
                                 // adjacent ([m][Jp][slice][F+, F-] complex), one 32-byte store
   int v4ld;                     // lane kernel, pair-major input: E and O of one (m, slice) in
                                 // one 256-bit load (LDG.E.256)
+  int pf_pairs;                 // FOP_NONLINEAR, lane kernel, pair-major input: each CTA
+                                // prefetches into L2 its share of the E/O block of the pair
+                                // this many pairs ahead (0: off)
   const double *in[FFT_MAXF];   // E/O half spectra      [m][2][Jp][ld]
   double *out[FFT_MAXF];        // F+/F- analysis inputs [m][2][Jp][ld]
   const double *gin[2];         // grids [slice][J][I]

@@ -314,7 +314,7 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
       const int fs = (f == 2 && a.dlam) ? 5 : f;
       const double2 *pk, *pk2;
       size_t eoo;
-      if (a.in_pm) {  // [Jh][ld/2][M+1][E,O]: this (pair, slice) is one contiguous block
+      if (a.in_pm) {  // [Jh][M+1][ld/2][E,O]: one (pair, m, slice) is one 32-byte E/O item
         const int nsl = a.ld >> 1;
         const double2 *blk = reinterpret_cast<const double2 *>(a.in[ok ? fs : 0]) +
                              ((size_t)c.p * (M + 1) * nsl + c.b0 + s) * 2;
@@ -470,10 +470,29 @@ __host__ __device__ constexpr int lane_slices(int op, int lw) {
 // FOP_NONLINEAR on one CTA's rows (no hemisphere split): nonlinear_advection +
 // nonlinear_rest (dynamics.py:142-160).  in: 0 u, 1 v, 2 d_lambda Phi, 3 H.Phi, 4 xi,
 // 5 Phi (phi_prime applied here), 6 delta; out: F+- of (tphi, ke, xi u cos, xi v cos)
+// L2 prefetch of this CTA's 1/gridDim.x share of the pair-major E/O blocks
+// ([Jh][M+1][ld/2][E,O], one contiguous block per pair and field) of the pair
+// a.pf_pairs ahead: CTAs run in (slice, pair) order, so that pair's CTAs start about
+// one wave later and find their scattered 32-byte E/O reads in L2 instead of HBM
+SWE_DEV void lane_prefetch_eo(const FftArgs &a, const LCtx &c, int nf) {
+  const int pp = c.p + a.pf_pairs;
+  if (!a.pf_pairs || !a.in_pm || pp >= a.Jh || c.tid >= nf) return;
+  const int fs = (c.tid == 2 && a.dlam) ? 5 : c.tid;
+  if (c.tid == 2 && a.dlam) return;  // field 2 is formed from field 5
+  const size_t blk = (size_t)(a.M + 1) * (a.ld >> 1) * 32;  // bytes per pair and field
+  const size_t chunk = ((blk + gridDim.x - 1) / gridDim.x + 15) & ~(size_t)15;
+  const size_t off = (size_t)blockIdx.x * chunk;
+  if (off >= blk) return;
+  const unsigned bytes = (unsigned)min(chunk, blk - off);
+  const char *src = reinterpret_cast<const char *>(a.in[fs]) + (size_t)pp * blk + off;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 template <int LW, bool GEN, int CG, class Store>
 SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   const int p = c.p, I = a.I, S = c.S;
   const double ia = a.inv_acos[p];
+  lane_prefetch_eo(a, c, 7);
   lane_load_eo<LW, CG>(a, c, 7, 5);
   __syncthreads();
   lane_ifft<LW, GEN>(a, c);

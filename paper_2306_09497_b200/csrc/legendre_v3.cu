@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
         }
       }
     } else {
-      // pair-major [Jh][ld/2][M+1][E,O]: E and O of one (pair, slice, m) share a
+      // pair-major [Jh][M+1][ld/2][E,O]: E and O of one (pair, slice, m) share a
       // 32-byte sector, written by the two parity warps of this unit
       double2 *dst = reinterpret_cast<double2 *>(o.dst);
       const int nsl = ld >> 1;

@@ -43,6 +43,7 @@ int g_cn_small = 1;        // one-launch CN half step for small truncations (K <
 int g_cn_fused = 1;        // speculative smem-resident fixed point (k_cn_fused) on the fine level
 int g_fft_v4 = 1;          // pair-major E/O hand-over read with 256-bit loads
 int g_f_il = 1;            // F+- hand-over interleaved per slice (32-byte FFT stores)
+int g_fft_pf = 2;          // nonlinear lane FFT: L2 prefetch of the E/O block this many pairs ahead
 int g_gemv_max_b = 3;      // batches up to this size take the dot-product Legendre kernels
 int g_cc_ctas = 0;         // CTAs per slice for the shared-memory half step (0: by batch)
 int g_cn_cluster = 1;      // one-launch CN half step with the rhs in shared memory: 1 when
@@ -420,6 +421,7 @@ void nonlinear_args(const Run &r, const double *const U[3], double *const k[3], 
     f.no_rest = no_rest ? 1 : 0;
     f.in_pm = pm;
     f.v4ld = pm && g_fft_v4;
+    f.pf_pairs = pm ? g_fft_pf : 0;
     f.out_il = fil;
   }
   {
@@ -1032,7 +1034,7 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
 int options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
          (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_cc_ctas << 17) | (g_gemv_max_b << 22) |
-         (g_cn_fused << 25) | (g_fft_v4 << 26) | (g_f_il << 27);
+         (g_cn_fused << 25) | (g_fft_v4 << 26) | (g_f_il << 27) | (g_fft_pf << 28);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1558,6 +1560,10 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "f_il") == 0 && (value == 0 || value == 1)) {
     g_f_il = value;
+    return OK;
+  }
+  if (key && strcmp(key, "fft_pf") == 0 && value >= 0 && value <= 7) {
+    g_fft_pf = value;
     return OK;
   }
   if (key && strcmp(key, "fft_v4") == 0 && (value == 0 || value == 1)) {
