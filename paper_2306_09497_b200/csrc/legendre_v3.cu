@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     if (u < 0) break;
     const Unit x = decode(args, u, ncol, 64);
     const LegOut &o = args.out[x.out];
-    const int km = M + 1 - x.m, ne = (km + 1) >> 1;
+    const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
     const int nch_t = (ne + S3_KT - 1) / S3_KT;
     const int pw0 = x.tile + wph * 32;
     const bool wide = x.tile + S3_TW + S3_XTRA >= Jh;  // carries the remainder pairs
@@ -289,26 +289,36 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
 #pragma unroll
             for (int j = 0; j < NJ; ++j) b[q][j] = flip_sign(Bb[kk * 4 * S3_LDB + j * 8], bmask);
           };
-          frag(0, 0);
+          // NKK k-steps of 4 modes: the last chunk of an order runs only those holding
+          // modes of this warp's parity (the rest are zero rows: no sum changes)
+          auto steps = [&](auto nkk_tag) {
+            constexpr int NKK = decltype(nkk_tag)::value;
+            frag(0, 0);
 #pragma unroll
-          for (int kk = 0; kk < S3_KT / 4; ++kk) {
-            const int q = kk & 1;
-            if (kk + 1 < S3_KT / 4) frag(kk + 1, q ^ 1);
+            for (int kk = 0; kk < NKK; ++kk) {
+              const int q = kk & 1;
+              if (kk + 1 < NKK) frag(kk + 1, q ^ 1);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (i < nfr) {
+              for (int i = 0; i < 4; ++i)
+                if (i < nfr) {
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+                  for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+                }
+              if constexpr (XT) {
+                const double *Ax = &S.A[rpar * S3_KT + t][S3_TW + g];
+                const double *Bx = &S.B[rpar * S3_KT + t][xq * 32 + (g ^ tim)];
+                const double ax = Ax[kk * 4 * S3_LDA] * Sb[kk * 4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  dmma(acx[j][0], acx[j][1], ax, flip_sign(Bx[kk * 4 * S3_LDB + j * 8], bmask));
               }
-            if constexpr (XT) {
-              const double *Ax = &S.A[rpar * S3_KT + t][S3_TW + g];
-              const double *Bx = &S.B[rpar * S3_KT + t][xq * 32 + (g ^ tim)];
-              const double ax = Ax[kk * 4 * S3_LDA] * Sb[kk * 4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                dmma(acx[j][0], acx[j][1], ax, flip_sign(Bx[kk * 4 * S3_LDB + j * 8], bmask));
             }
-          }
+          };
+          const int rem = (rpar ? no : ne) - (c % nch_t) * S3_KT;
+          if (rem >= S3_KT - 3) steps(std::integral_constant<int, 4>{});
+          else if (rem > 8) steps(std::integral_constant<int, 3>{});
+          else if (rem > 4) steps(std::integral_constant<int, 2>{});
+          else if (rem > 0) steps(std::integral_constant<int, 1>{});
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
