@@ -544,18 +544,28 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
           for (int j = 0; j < NJ; ++j)
             b[q][j] = flip_sign(Bb[kk * kst + (IL ? (j >> 1) * 32 + (j & 1) * 4 : j * 8)], bmask);
         };
-        frag(0, 0);
+        // NKK k-steps of 4 pairs: the last chunk runs only those holding pairs < Jh
+        // (pairs past Jh are zero rows: no sum changes)
+        auto steps = [&](auto nkk_tag) {
+          constexpr int NKK = decltype(nkk_tag)::value;
+          frag(0, 0);
 #pragma unroll
-        for (int kk = 0; kk < A3_KP / 4; ++kk) {
-          const int q = kk & 1;
-          if (kk + 1 < A3_KP / 4) frag(kk + 1, q ^ 1);
+          for (int kk = 0; kk < NKK; ++kk) {
+            const int q = kk & 1;
+            if (kk + 1 < NKK) frag(kk + 1, q ^ 1);
 #pragma unroll
-          for (int i = 0; i < A3_FR; ++i)
-            if (i < nfr) {
+            for (int i = 0; i < A3_FR; ++i)
+              if (i < nfr) {
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
-            }
-        }
+                for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
+              }
+          }
+        };
+        const int rem = Jh - q0;
+        if (rem >= A3_KP - 3) steps(std::integral_constant<int, 4>{});
+        else if (rem > 8) steps(std::integral_constant<int, 3>{});
+        else if (rem > 4) steps(std::integral_constant<int, 2>{});
+        else if (rem > 0) steps(std::integral_constant<int, 1>{});
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
