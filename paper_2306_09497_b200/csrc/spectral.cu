@@ -1332,14 +1332,18 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
       }
       asm volatile("" ::: "memory");  // one element's loads in flight at a time (registers)
     }
-    // per-slice maxima: lanes of one slice differ in bits 2..4
+    // per-slice maxima: lanes of one slice differ in bits 2..4 (shuffle reduction),
+    // then lane sl + 4 q adds maximum q of slice sl: one shared atomic per warp
     if (fst && it <= CF_KS) {
 #pragma unroll
-      for (int q = 0; q < 6; ++q) {
+      for (int q = 0; q < 6; ++q)
 #pragma unroll
         for (int o = CF_S; o < 32; o <<= 1) mx[q] = max(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], o));
-        if (lane < CF_S && mx[q]) atomicMax(&sst[it - 1][lane][q], mx[q]);
-      }
+      const int q = lane >> 2;
+      unsigned long long v = mx[0];
+#pragma unroll
+      for (int qq = 1; qq < 6; ++qq) v = q == qq ? mx[qq] : v;
+      if (q < 6 && v) atomicMax(&sst[it - 1][lane & 3][q], v);
     }
     __syncthreads();
   }
