@@ -449,6 +449,7 @@ void work_free(Work &w) {
   cudaFree(w.grids);
   cudaFree(w.sweep_g);
   cudaFreeHost(w.h_fail);
+  cudaFree(w.d_fail);
   cudaFree(w.phi0);
   cudaFree(w.phibar);
   w = Work();
@@ -520,8 +521,8 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaHostAlloc(&w.h_bad, sizeof(int), cudaHostAllocMapped));
   SWE_CUDA(cudaHostGetDevicePointer(&w.d_bad, w.h_bad, 0));
   SWE_CUDA(cudaMemset(w.hdone, 0, sizeof(unsigned)));
-  SWE_CUDA(cudaHostAlloc(&w.h_fail, sizeof(int), cudaHostAllocMapped));
-  SWE_CUDA(cudaHostGetDevicePointer(&w.d_fail, w.h_fail, 0));
+  SWE_CUDA(cudaMallocHost(&w.h_fail, sizeof(int)));
+  SWE_CUDA(cudaMalloc(&w.d_fail, sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.sched, 2 * sizeof(unsigned long long)));
   SWE_CUDA(cudaMemset(w.sched, 0, 2 * sizeof(unsigned long long)));
   SWE_CUDA(cudaMalloc(&w.phi0, (size_t)B * sizeof(double)));

@@ -41,7 +41,7 @@ struct Work {
   double *sweep_g = nullptr;            // serial-sweep forcing, internal layout 3 x [K][2 scap]
   int scap = 0;
   int gcap = 0;
-  int *h_fail = nullptr, *d_fail = nullptr;  // graph mode: unconverged-solve flag (mapped)
+  int *h_fail = nullptr, *d_fail = nullptr;  // graph mode: unconverged-solve flag (device) and its host copy
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
 };

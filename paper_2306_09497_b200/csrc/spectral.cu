@@ -34,7 +34,8 @@ __global__ void k_to_internal(const double2 *__restrict__ src, SpecPtrs dst, int
 }
 
 __global__ void k_to_boundary(SpecPtrsC src, double2 *__restrict__ dst, int B, int F, int K,
-                              const int *__restrict__ perm) {
+                              const int *__restrict__ perm, const int *__restrict__ skip) {
+  if (skip && *skip) return;
   __shared__ double2 tile[32][33];
   const int f = blockIdx.z, k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
   const double2 *s = reinterpret_cast<const double2 *>(src.p[f]);
@@ -58,9 +59,9 @@ int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, con
 }
 
 int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, const int *perm,
-                cudaStream_t st) {
+                cudaStream_t st, const int *skip) {
   dim3 grid((K + 31) / 32, (B + 31) / 32, F), blk(32, 8);
-  k_to_boundary<<<grid, blk, 0, st>>>(src, reinterpret_cast<double2 *>(dst), B, F, K, perm);
+  k_to_boundary<<<grid, blk, 0, st>>>(src, reinterpret_cast<double2 *>(dst), B, F, K, perm, skip);
   SWE_LAUNCH_CHECK();
   return OK;
 }

@@ -22,8 +22,10 @@ struct Ptr3C {
 
 int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, const int *perm,
                 cudaStream_t st);
+// skip (nullable, device): the copy is skipped when *skip != 0 (an unconverged graph
+// step leaves the caller's input in place for the host-driven rerun)
 int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, const int *perm,
-                cudaStream_t st);
+                cudaStream_t st, const int *skip = nullptr);
 int lin_rhs(int K, int B, const double *const U[3], const double *lcx, const double *lcd,
             double alpha, const double *eps, const double *phibar, double *const R[3],
             cudaStream_t st);

@@ -1372,21 +1372,19 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
     return rc;
   if (exec) {
     // one graph launch per step, one host check per call; an unconverged solve
-    // (flagged on device) reruns the call on the host-driven path from the saved
+    // (flagged on device) reruns the call on the host-driven path from the caller's
     // input so the error and residual are reported exactly as steppers.py does
-    const size_t bytes = (size_t)pl->K * r.ld * sizeof(double);
-    for (int f = 0; f < 3; ++f)
-      SWE_CUDA(cudaMemcpyAsync(r.spec(21 + f), b.U[f], bytes, cudaMemcpyDeviceToDevice, r.st));
     SWE_CUDA(cudaMemsetAsync(pl->ws.d_fail, 0, sizeof(int), r.st));
     for (int s = 0; s < nsteps; ++s) SWE_CUDA(cudaGraphLaunch(exec, r.st));
     // the result goes out before the host check (no idle gap between the graph and
-    // the layout kernel); an unconverged call is redone below and overwrites it
+    // the layout kernel) unless the device flag is up: then `state` still holds the
+    // input (no backup copy needed) and the call is redone below
     SpecPtrsC so = {{b.U[0], b.U[1], b.U[2]}};
-    if ((rc = to_boundary(so, state, batch, 3, pl->K, pl->perm, r.st))) return rc;
+    if ((rc = to_boundary(so, state, batch, 3, pl->K, pl->perm, r.st, pl->ws.d_fail))) return rc;
+    SWE_CUDA(cudaMemcpyAsync(pl->ws.h_fail, pl->ws.d_fail, sizeof(int), cudaMemcpyDeviceToHost, r.st));
     SWE_CUDA(cudaStreamSynchronize(r.st));
-    if (!*reinterpret_cast<volatile int *>(pl->ws.h_fail)) return OK;
-    for (int f = 0; f < 3; ++f)
-      SWE_CUDA(cudaMemcpyAsync(b.U[f], r.spec(21 + f), bytes, cudaMemcpyDeviceToDevice, r.st));
+    if (!*pl->ws.h_fail) return OK;
+    if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st))) return rc;
     exec = nullptr;
   }
   if (!exec)
@@ -1446,8 +1444,9 @@ int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double
       if ((rc = to_boundary(sc, u + (size_t)j * stride, 1, 3, K, pl->perm, r.st))) return rc;
     }
     if (!graph) return OK;
+    SWE_CUDA(cudaMemcpyAsync(w.h_fail, w.d_fail, sizeof(int), cudaMemcpyDeviceToHost, r.st));
     SWE_CUDA(cudaStreamSynchronize(r.st));
-    if (!*reinterpret_cast<volatile int *>(w.h_fail)) return OK;
+    if (!*w.h_fail) return OK;
     // an unconverged solve inside the graph: redo the sweep on the host-driven path,
     // which raises at the failing step with the residual like steppers.py
   }
