@@ -73,6 +73,7 @@ __host__ __device__ constexpr int fft_lane_slices(int op) {
   return op == FOP_NONLINEAR ? 1 : ((op == FOP_SYNTH_GRID || op == FOP_ANALYSIS) ? 8 : 4);
 }
 int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st);
+extern int g_fft_rm;  // 1: radix-specialised nonlinear lane kernels for the hot lengths
 // rows per CTA of the lane kernel for this length (0: does not apply); *rgen: the
 // largest radix that runs as a generic stage (0: all unrolled)
 int fft_lanes_width(const FftArgs &a, int *rgen);

@@ -26,10 +26,9 @@ namespace swe {
 
 using namespace fftcore;
 
-namespace {
-}  // namespace
+int g_fft_rm = 1;  // radix-specialised nonlinear lane kernels (option "fft_rm")
 
-template <int OP, int LW, bool GEN>
+template <int OP, int LW, bool GEN, int RM = 0>
 __global__ void __launch_bounds__(lane_threads<LW>(), 512 / lane_threads<LW>())
     fft_lanes_kernel(const __grid_constant__ FftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -95,7 +94,7 @@ __global__ void __launch_bounds__(lane_threads<LW>(), 512 / lane_threads<LW>())
     const double w = a.wsin2[p] * a.inv_I * a.inv_a;
     lane_extract<LW>(a, c, c.X, c.X, 2, w, w, c.tid, c.nthr);
   } else if constexpr (OP == FOP_NONLINEAR && !SPLIT) {
-    lane_nonlinear<LW, GEN, false>(a, c);
+    lane_nonlinear<LW, GEN, false, RM>(a, c);
   } else if constexpr (OP == FOP_NONLINEAR) {
     // nonlinear_advection + nonlinear_rest (dynamics.py:142-160), hemispheres split
     // over a two-CTA cluster
@@ -152,11 +151,11 @@ int lane_width(const FftArgs &a, int *rgen) {
   return 0;
 }
 
-template <int OP, int LW, bool GEN>
+template <int OP, int LW, bool GEN, int RM = 0>
 int launch_lanes(const FftArgs &a, int smem, cudaStream_t st) {
   static int attr = 0;
   if (smem > attr) {
-    SWE_CUDA(cudaFuncSetAttribute(fft_lanes_kernel<OP, LW, GEN>,
+    SWE_CUDA(cudaFuncSetAttribute(fft_lanes_kernel<OP, LW, GEN, RM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = smem;
   }
@@ -176,7 +175,7 @@ int launch_lanes(const FftArgs &a, int smem, cudaStream_t st) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
   }
-  SWE_CUDA(cudaLaunchKernelEx(&cfg, fft_lanes_kernel<OP, LW, GEN>, a));
+  SWE_CUDA(cudaLaunchKernelEx(&cfg, fft_lanes_kernel<OP, LW, GEN, RM>, a));
   SWE_LAUNCH_CHECK();
   return OK;
 }
@@ -205,6 +204,16 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
     return E_SHAPE;
   }
   const int smem = (int)(((size_t)a.N2 * lw + g) * sizeof(double2));
+  // the nonlinear pass of the hot factorisations: kernels holding only their stages
+  if (op == FOP_NONLINEAR && lw == 16 && !g && g_fft_rm) {
+    int m = 0;
+    for (int s = 0; s < a.nst; ++s) m |= r_bit(a.radix[s]);
+    m |= a.pfa ? RM_PFA : RM_CT;
+    constexpr int R5711 = 8 | 16 | 32 | RM_PFA, R711 = 16 | 32 | RM_PFA, R7 = 16 | RM_CT;
+    if (m == R5711) return launch_lanes<FOP_NONLINEAR, 16, false, R5711>(a, smem, st);
+    if (m == R711) return launch_lanes<FOP_NONLINEAR, 16, false, R711>(a, smem, st);
+    if (m == R7) return launch_lanes<FOP_NONLINEAR, 16, false, R7>(a, smem, st);
+  }
   if (g) return lw == 16 ? launch_width<16, true>(op, a, smem, st) : launch_width<8, true>(op, a, smem, st);
   return lw == 16 ? launch_width<16, false>(op, a, smem, st) : launch_width<8, false>(op, a, smem, st);
 }

@@ -149,28 +149,39 @@ SWE_DEV void lane_stage_gen(double2 *X, double2 *ct, int N2, int Lp, int R, doub
   }
 }
 
+// Radix set of a kernel instantiation (RM): bit r_bit(R) for each unrolled radix it
+// contains, RM_PFA / RM_CT when the transform kind is known; RM = 0: every radix,
+// kind chosen at run time.  A launch of few CTAs (a single-slice coarse step) runs
+// each stage body once, so it pays the instruction fetch of all code it contains:
+// the factorisations of the hot levels get kernels holding only their stages.
+constexpr int r_bit(int R) {
+  return R == 2 ? 1 : R == 3 ? 2 : R == 4 ? 4 : R == 5 ? 8 : R == 7 ? 16 : R == 11 ? 32 : R == 13 ? 64 : 0;
+}
+constexpr int RM_PFA = 128, RM_CT = 256;
+constexpr bool rm_ok(int RM, int R) { return RM == 0 || (RM & r_bit(R)) != 0; }
+
 // one stage over rows 0..RW-1, ends with a CTA barrier.  GEN: the length has a
 // non-unrolled radix (kernels without it keep the small-radix register budget)
-template <int MODE, int RW, int LW, bool GEN>
+template <int MODE, int RW, int LW, bool GEN, int RM = 0>
 SWE_DEV void lane_run_stage(double2 *X, double2 *ct, int N2, int Lp, int R, double dir,
                             const double2 *tw, int tid, int nthr) {
   const int warp = tid >> 5, nw = nthr >> 5, lane = tid & 31;
   switch (R) {
-    case 2: lane_stage<2, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 3: lane_stage<3, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 4: lane_stage<4, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 5: lane_stage<5, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
-    case 7: lane_stage<7, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 2: if constexpr (rm_ok(RM, 2)) lane_stage<2, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 3: if constexpr (rm_ok(RM, 3)) lane_stage<3, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 4: if constexpr (rm_ok(RM, 4)) lane_stage<4, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 5: if constexpr (rm_ok(RM, 5)) lane_stage<5, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
+    case 7: if constexpr (rm_ok(RM, 7)) lane_stage<7, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane); break;
     // (with a generic radix in the length, 11 and 13 go generic too: their unrolled
     // register footprint next to the generic stage would spill)
     case 11:
       if constexpr (!GEN) {
-        lane_stage<11, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane);
+        if constexpr (rm_ok(RM, 11)) lane_stage<11, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane);
         break;
       }
     case 13:
       if constexpr (!GEN) {
-        lane_stage<13, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane);
+        if constexpr (rm_ok(RM, 13)) lane_stage<13, MODE, RW, LW>(X, N2, Lp, dir, tw, warp, nw, lane);
         break;
       }
     default:
@@ -194,34 +205,47 @@ SWE_DEV int lrow(const LCtx &c, int f, int h, int s) {
   return c.split ? f * c.S + s : (f * 2 + h) * c.S + s;
 }
 
-template <int LW, bool GEN>
+// prime-factor (no twiddles) or Cooley-Tukey: fixed by RM or read from a.pfa
+template <int RM>
+SWE_DEV bool rm_pfa(const FftArgs &a) {
+  return (RM & RM_PFA) ? true : (RM & RM_CT) ? false : a.pfa != 0;
+}
+
+template <int LW, bool GEN, int RM = 0>
 SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
   int Lp = 1;
   for (int s = 0; s < a.nst; ++s) {
-    if (a.pfa)
-      lane_run_stage<2, LW, LW, GEN>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
-    else
-      lane_run_stage<0, LW, LW, GEN>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
+    if (rm_pfa<RM>(a)) {
+      if constexpr (!(RM & RM_CT))
+        lane_run_stage<2, LW, LW, GEN, RM>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
+    } else {
+      if constexpr (!(RM & RM_PFA))
+        lane_run_stage<0, LW, LW, GEN, RM>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
+    }
     Lp *= a.radix[s];
   }
 }
 
 // forward transform of rows 0..RW-1
-template <int RW, int LW, bool GEN>
+template <int RW, int LW, bool GEN, int RM = 0>
 SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
-  if (a.pfa) {
-    int Lp = 1;
-    for (int s = 0; s < a.nst; ++s) {
-      lane_run_stage<2, RW, LW, GEN>(c.X, c.ct, a.N2, Lp, a.radix[s], -1.0, a.tw, c.tid, c.nthr);
-      Lp *= a.radix[s];
+  if (rm_pfa<RM>(a)) {
+    if constexpr (!(RM & RM_CT)) {
+      int Lp = 1;
+      for (int s = 0; s < a.nst; ++s) {
+        lane_run_stage<2, RW, LW, GEN, RM>(c.X, c.ct, a.N2, Lp, a.radix[s], -1.0, a.tw, c.tid, c.nthr);
+        Lp *= a.radix[s];
+      }
     }
     return;
   }
-  int L = a.N2;
-  for (int s = a.nst - 1; s >= 0; --s) {
-    const int R = a.radix[s];
-    lane_run_stage<1, RW, LW, GEN>(c.X, c.ct, a.N2, L / R, R, -1.0, a.tw, c.tid, c.nthr);
-    L /= R;
+  if constexpr (!(RM & RM_PFA)) {
+    int L = a.N2;
+    for (int s = a.nst - 1; s >= 0; --s) {
+      const int R = a.radix[s];
+      lane_run_stage<1, RW, LW, GEN, RM>(c.X, c.ct, a.N2, L / R, R, -1.0, a.tw, c.tid, c.nthr);
+      L /= R;
+    }
   }
 }
 
@@ -488,14 +512,14 @@ SWE_DEV void lane_prefetch_eo(const FftArgs &a, const LCtx &c, int nf) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
-template <int LW, bool GEN, int CG, class Store>
+template <int LW, bool GEN, int CG, int RM, class Store>
 SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   const int p = c.p, I = a.I, S = c.S;
   const double ia = a.inv_acos[p];
   lane_prefetch_eo(a, c, 7);
   lane_load_eo<LW, CG>(a, c, 7, 5);
   __syncthreads();
-  lane_ifft<LW, GEN>(a, c);
+  lane_ifft<LW, GEN, RM>(a, c);
   const double cs = a.coslat[p];
   constexpr int NH = 2;  // hemispheres held by this CTA
   // lanes: (slot, hemisphere, x/y) fastest, so a half-warp reads one bank each
@@ -512,17 +536,17 @@ SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   }
   __syncthreads();
   // only the 4 product fields x 2 hemispheres (S = 1)
-  lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN>(a, c);
+  lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN, RM>(a, c);
   const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
   lane_extract_to<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
 }
 
-template <int LW, bool GEN, int CG>
+template <int LW, bool GEN, int CG, int RM = 0>
 SWE_DEV void lane_nonlinear(const FftArgs &a, const LCtx &c) {
   if (a.out_il) {
     // [m][Jp][slice][F+, F-]: one 32-byte store per (field, order, slice)
     const size_t nsl = a.ld >> 1;
-    lane_nonlinear_to<LW, GEN, CG>(a, c, [&](int f, int k, int s, double2 fp, double2 fm) {
+    lane_nonlinear_to<LW, GEN, CG, RM>(a, c, [&](int f, int k, int s, double2 fp, double2 fm) {
       double *d = a.out[f] + (((size_t)k * a.Jp + c.p) * nsl + c.b0 + s) * 4;
       asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(d), "d"(fp.x), "d"(fp.y),
                    "d"(fm.x), "d"(fm.y)
@@ -531,7 +555,7 @@ SWE_DEV void lane_nonlinear(const FftArgs &a, const LCtx &c) {
     return;
   }
   const size_t pm = (size_t)a.Jp * a.ld / 2;  // F+ -> F- offset (double2)
-  lane_nonlinear_to<LW, GEN, CG>(a, c, [&](int f, int k, int s, double2 fp, double2 fm) {
+  lane_nonlinear_to<LW, GEN, CG, RM>(a, c, [&](int f, int k, int s, double2 fp, double2 fm) {
     double2 *d = reinterpret_cast<double2 *>(a.out[f] + (size_t)c.p * a.ld) + c.b0 +
                  (size_t)k * 2 * pm + s;
     d[0] = fp;

@@ -89,7 +89,8 @@ struct swe_plan {
   struct StepGraph {
     int B, Bsel;
     double dt, nu, tol;
-    int order, cor_impl, nonlin, max_iter, opts, solver;
+    int order, cor_impl, nonlin, max_iter, solver;
+    long long opts;
     cudaGraph_t graph;
     cudaGraphExec_t exec;
   };

@@ -1031,10 +1031,10 @@ int settls_internal(const Run &r, const swe_stepper_cfg &cfg, double *resid_host
                       nullptr, resid_host, true);
 }
 
-int options_key() {
+long long options_key() {
   return g_fft_path | (g_leg_path << 4) | (g_fast_coriolis << 8) | (g_cn_small << 12) |
          (g_helm_tiled << 13) | (g_cn_cluster << 14) | (g_cc_ctas << 17) | (g_gemv_max_b << 22) |
-         (g_cn_fused << 25) | (g_fft_v4 << 26) | (g_f_il << 27) | (g_fft_pf << 28);
+         (g_cn_fused << 25) | (g_fft_v4 << 26) | (g_f_il << 27) | ((long long)g_fft_pf << 28) | ((long long)g_fft_rm << 32);
 }
 
 // CUDA graph of one IMEX step on the workspace (U -> U), captured on the plan's
@@ -1045,7 +1045,7 @@ int step_graph(const Run &r, const swe_stepper_cfg &cfg, cudaGraphExec_t *exec) 
   swe_plan *pl = r.pl;
   *exec = nullptr;
   if (g_fast_coriolis != 2 && cfg.coriolis_implicit) return OK;
-  const int opts = options_key();
+  const long long opts = options_key();
   for (auto &g : pl->graphs)
     if (g.B == r.B && g.Bsel == r.Bsel && g.dt == cfg.dt && g.nu == cfg.visc_nu && g.tol == cfg.implicit_tol &&
         g.order == cfg.visc_order && g.cor_impl == cfg.coriolis_implicit &&
@@ -1559,6 +1559,10 @@ int swe_set_option(const char *key, int value) {
   }
   if (key && strcmp(key, "f_il") == 0 && (value == 0 || value == 1)) {
     g_f_il = value;
+    return OK;
+  }
+  if (key && strcmp(key, "fft_rm") == 0 && (value == 0 || value == 1)) {
+    g_fft_rm = value;
     return OK;
   }
   if (key && strcmp(key, "fft_pf") == 0 && value >= 0 && value <= 7) {
