@@ -2,8 +2,11 @@
 64 slices) under library options given as k=v[,k=v] specs."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2306_09497_b200 import _lib
+if len(sys.argv) > 1 and sys.argv[1].endswith(".so"):  # optional library build to time
+    _lib.load.__defaults__ = (os.path.abspath(sys.argv.pop(1)),)
 import torch
-from paper_2306_09497_b200 import _lib, dynamics, spharm
+from paper_2306_09497_b200 import dynamics, spharm
 import bench
 
 g = spharm.get_grid(256)
