@@ -200,10 +200,11 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
       const bool wide = x.tile + S3_TW + S3_XTRA >= Jh;
       const unsigned abytes = (unsigned)min(wide ? S3_TW + S3_XTRA : S3_TW, Jp - x.tile) * 8u;
       const int bcols = min(V3_BN, ld - x.c0);
-      for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+      // stage c = (term, chunk cc), chunk fastest (counters instead of divisions)
+      for (int c = 0, term = 0, cc = 0; c < nch_t * o.nterms; ++c, ++it, cc = cc + 1 == nch_t ? 0 : cc + 1, term += cc == 0) {
         const int s = it % S3_NS;
         mbar_wait(&sm.empty[s], ((it / S3_NS) & 1) ^ 1);
-        const int term = c / nch_t, tt = (c - term * nch_t) * S3_KT + (r & 15);
+        const int tt = cc * S3_KT + (r & 15);
         const LegTerm &T = o.t[term];
         Synth3Stage &S = sm.st[s];
         const bool v = tt < (par ? no : ne);
@@ -267,14 +268,14 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     auto mainloop = [&](auto xt_tag, auto nj_tag) {
       constexpr bool XT = decltype(xt_tag)::value;
       constexpr int NJ = decltype(nj_tag)::value;  // column fragments computed (8, 4, 2)
-      for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+      for (int c = 0, term = 0, cc = 0; c < nch_t * o.nterms; ++c, ++it, cc = cc + 1 == nch_t ? 0 : cc + 1, term += cc == 0) {
         const int s = it % S3_NS;
         if (c > 0) mbar_wait(&sm.full[s], (it / S3_NS) & 1);
         // small batches: warps whose columns are all padding skip the stage (a
         // column's sums do not depend on the others: no result changes)
         if ((nfr > 0 || XT) && (wcols || (XT && xcols))) {
           const Synth3Stage &S = sm.st[s];
-          const LegTerm &T = o.t[c / nch_t];
+          const LegTerm &T = o.t[term];
           const int rpar = wpar ^ T.flip;
           const int tim = T.times_im;
           const unsigned long long bmask = (tim && !(g & 1)) ? 0x8000000000000000ULL : 0ULL;
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
               }
             }
           };
-          const int rem = (rpar ? no : ne) - (c % nch_t) * S3_KT;
+          const int rem = (rpar ? no : ne) - cc * S3_KT;
           if (rem >= S3_KT - 3) steps(std::integral_constant<int, 4>{});
           else if (rem > 8) steps(std::integral_constant<int, 3>{});
           else if (rem > 4) steps(std::integral_constant<int, 2>{});
@@ -436,10 +437,10 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
       const LegOut &o = args.out[x.out];
       const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
       const int off = args.offsets[x.m];
-      for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+      for (int c = 0, term = 0, cc = 0; c < nch_t * o.nterms; ++c, ++it, cc = cc + 1 == nch_t ? 0 : cc + 1, term += cc == 0) {
         const int s = it % A3_NS;
         mbar_wait(&sm.empty[s], ((it / A3_NS) & 1) ^ 1);
-        const int term = c / nch_t, q0 = (c - term * nch_t) * A3_KP;
+        const int q0 = cc * A3_KP;
         const LegTerm &T = o.t[term];
         Anal3Stage &S = sm.st[s];
         // table rows off + tile.. (E) and off + ne + tile.. (O): rows past the
@@ -505,19 +506,19 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     auto mainloop = [&](auto ilc, auto nj_tag) {
     constexpr bool IL = decltype(ilc)::value;
     constexpr int NJ = decltype(nj_tag)::value;  // column fragments computed (8, 4, 2)
-    for (int c = 0; c < nch_t * o.nterms; ++c, ++it) {
+    for (int c = 0, term = 0, cc = 0; c < nch_t * o.nterms; ++c, ++it, cc = cc + 1 == nch_t ? 0 : cc + 1, term += cc == 0) {
       const int s = it % A3_NS;
       if (c > 0) mbar_wait(&sm.full[s], (it / A3_NS) & 1);
       if (nfr > 0 && wcols) {
         const Anal3Stage &S = sm.st[s];
-        const LegTerm &T = o.t[c / nch_t];
+        const LegTerm &T = o.t[term];
         const int tim = T.times_im;
         const int fsel = wpar ^ T.flip;
         const unsigned long long bmask = (tim && !(g & 1)) ? 0x8000000000000000ULL : 0ULL;
         const double asc = T.sign * (tim ? (double)x.m : 1.0);
         // per-pair scale of this lane's k row for each k-step (read-only, L1-cached)
         double ps[A3_KP / 4];
-        const int q0 = (c % nch_t) * A3_KP;
+        const int q0 = cc * A3_KP;
 #pragma unroll
         for (int kk = 0; kk < A3_KP / 4; ++kk)
           ps[kk] = T.pscale ? __ldg(T.pscale + q0 + kk * 4 + t) : 1.0;
