@@ -339,6 +339,47 @@ def test_step_graph_nonconvergence_raises(mods):
             steppers.imex_step(s, cfg)
 
 
+def test_step_graph_nonconvergence_keeps_input(mods):
+    """In place: a replayed step graph whose fixed point does not converge leaves the
+    caller's state untouched (the layout kernel is skipped on the device flag) so the
+    host-driven rerun starts from the true input and raises like the reference."""
+    _, dynamics, steppers, _ = mods
+    import torch
+    g = load_golden("step_M16.npz")
+    cfg = steppers.StepperConfig(dt=600.0, implicit_max_iter=1)
+    for call in range(3):  # eager, capture, replay
+        s = _state(mods, 16, g["bumps_dt600_nu1e5_in"], g["phibar"])
+        before = s.data.clone()
+        with pytest.raises(steppers.ImplicitSolveError, match="residual"):
+            steppers.imex_steps_inplace(s, cfg, 1)
+        torch.cuda.synchronize()
+        assert torch.equal(s.data, before), f"call {call}: input modified by a failed step"
+
+
+@pytest.mark.parametrize("M", [32, 51, 256])
+def test_fft_kernel_variants_bitwise(mods, M):
+    """The radix-specialised nonlinear lane kernels (49 = 7x7, 77 = 7x11, 385 = 5x7x11)
+    and the L2 prefetch of the E/O blocks give bitwise the generic kernel's step."""
+    spharm, dynamics, steppers, scenarios = mods
+    import torch
+    from paper_2306_09497_b200 import _lib
+    grid = spharm.get_grid(M)
+    cfg = steppers.StepperConfig(dt=120.0, viscosity=dynamics.ViscositySpec(2, 1e5))
+    outs = {}
+    try:
+        for rm, pf in ((0, 0), (1, 0), (1, 2)):
+            _lib.set_option("fft_rm", rm)
+            _lib.set_option("fft_pf", pf)
+            s = scenarios.gaussian_bumps(grid, batch=4)
+            steppers.imex_steps_inplace(s, cfg, 2)
+            outs[(rm, pf)] = s.data.cpu()
+    finally:
+        _lib.set_option("fft_rm", 1)
+        _lib.set_option("fft_pf", 2)
+    assert torch.equal(outs[(0, 0)], outs[(1, 0)])
+    assert torch.equal(outs[(0, 0)], outs[(1, 2)])
+
+
 def test_tiled_fixed_point_matches_untiled(mods):
     """The shared-memory-tiled fixed-point kernel (batches >= 32) matches the
     gather kernel: same iteration counts, states to roundoff."""
