@@ -26,7 +26,8 @@ namespace swe {
 
 using namespace fftcore;
 
-int g_fft_rm = 1;  // radix-specialised nonlinear lane kernels (option "fft_rm")
+int g_fft_rm = 2;  // radix-specialised nonlinear lane kernels (option "fft_rm"; 2: with the
+                   // fused middle, lane_nl_mid)
 
 template <int OP, int LW, bool GEN, int RM = 0>
 __global__ void __launch_bounds__(lane_threads<LW>(), 512 / lane_threads<LW>())
@@ -111,10 +112,10 @@ __global__ void __launch_bounds__(lane_threads<LW>(), 512 / lane_threads<LW>())
       auto R = [&](int f) -> double & { return gslot<LW>(c, pp, hh, lrow(c, f, h, s)); };
       const double u = R(0) * ia, v = R(1) * ia, gx = R(2) * ia, gy = R(3) * ia;
       const double xi = R(4), ph = a.no_rest ? 0.0 : R(5), de = R(6);
-      R(0) = -(u * gx + v * gy) - ph * de;   // -(V.grad Phi) - Phi' delta
-      R(1) = 0.5 * (u * u + v * v);          // kinetic energy
-      R(2) = (xi * u) * cs;                  // (xi u) cos
-      R(3) = (xi * v) * cs;                  // (xi v) cos
+      R(0) = nl_tphi(nl_adv(u, v, gx, gy), ph, de);  // -(V.grad Phi) - Phi' delta
+      R(1) = nl_ke(u, v);                            // kinetic energy
+      R(2) = nl_flux(xi, u, cs);                     // (xi u) cos
+      R(3) = nl_flux(xi, v, cs);                     // (xi v) cos
     }
     __syncthreads();
     // only the 4 product fields (x 2 hemispheres unless split; S = 1)
@@ -210,7 +211,11 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
     for (int s = 0; s < a.nst; ++s) m |= r_bit(a.radix[s]);
     m |= a.pfa ? RM_PFA : RM_CT;
     constexpr int R5711 = 8 | 16 | 32 | RM_PFA, R711 = 16 | 32 | RM_PFA, R7 = 16 | RM_CT;
-    if (m == R5711) return launch_lanes<FOP_NONLINEAR, 16, false, R5711>(a, smem, st);
+    if (m == R5711)
+      return g_fft_rm == 2 ? launch_lanes<FOP_NONLINEAR, 16, false, R5711 | RM_MID>(a, smem, st)
+                           : launch_lanes<FOP_NONLINEAR, 16, false, R5711>(a, smem, st);
+    // (77 = 7 x 11 keeps the three-pass middle: the radix-7 fused middle spills and
+    // the one-slice coarse step is latency-bound, 109 vs 102 us per M=51 step)
     if (m == R711) return launch_lanes<FOP_NONLINEAR, 16, false, R711>(a, smem, st);
     if (m == R7) return launch_lanes<FOP_NONLINEAR, 16, false, R7>(a, smem, st);
   }

@@ -31,10 +31,13 @@ constexpr int GT = 4;  // generic radix: output pairs (t, R - t) per thread item
 // while a butterfly's 16 (or 8) rows of one slot remain a conflict-free line.
 //
 // 16 rows: 2*slot (4 aligned consecutive slots x 2 hemispheres of one field hit 8
-// distinct 16-byte bank groups in the grid products) plus bit 2 of the slot in bit 0,
-// so rows (2f + h) of one hemisphere land on both bank parities across scattered
-// slots (put_z stores and the F+- extraction read one hemisphere's rows of several
-// slots per instruction); other widths keep slot << 1.
+// distinct 16-byte bank groups in the grid products and lane_nl_mid) plus bit 2 of
+// the slot in bit 0, so rows (2f + h) of one hemisphere land on both bank parities
+// across scattered slots (put_z stores and the F+- extraction read one hemisphere's
+// rows of several slots per instruction); other widths keep slot << 1.
+// (Measured against a row order f + 8h with slot & 7 swizzle, which removes put_z's
+// 2-way store conflicts, 14 -> 3 M wavefronts per launch: 1.5% slower - the E/O
+// load phase is latency-bound, not wavefront-bound.)
 template <int LW>
 SWE_DEV int swz(int slot) {
   return LW == 16 ? (((slot << 1) | ((slot >> 2) & 1)) & 15) : ((slot << 1) & (LW - 1));
@@ -158,7 +161,13 @@ constexpr int r_bit(int R) {
   return R == 2 ? 1 : R == 3 ? 2 : R == 4 ? 4 : R == 5 ? 8 : R == 7 ? 16 : R == 11 ? 32 : R == 13 ? 64 : 0;
 }
 constexpr int RM_PFA = 128, RM_CT = 256;
+// RM_MID (prime-factor kernels): the nonlinear pass fuses the inverse and forward
+// stage 0 with the grid products (lane_nl_mid); stage 0 has the smallest radix
+constexpr int RM_MID = 512;
 constexpr bool rm_ok(int RM, int R) { return RM == 0 || (RM & r_bit(R)) != 0; }
+constexpr int rm_radix0(int RM) {
+  return (RM & 1) ? 2 : (RM & 2) ? 3 : (RM & 4) ? 4 : (RM & 8) ? 5 : (RM & 16) ? 7 : (RM & 32) ? 11 : 13;
+}
 
 // one stage over rows 0..RW-1, ends with a CTA barrier.  GEN: the length has a
 // non-unrolled radix (kernels without it keep the small-radix register budget)
@@ -211,31 +220,42 @@ SWE_DEV bool rm_pfa(const FftArgs &a) {
   return (RM & RM_PFA) ? true : (RM & RM_CT) ? false : a.pfa != 0;
 }
 
-template <int LW, bool GEN, int RM = 0>
+// Prime-factor stage order: the inverse runs stages 1..nst-1 and then stage 0 (digit
+// weight 1, the smallest radix), the forward starts with stage 0, so the two
+// transforms meet on the same butterflies (slots R g .. R g + R - 1) and the
+// nonlinear pass can fuse them with the grid products (lane_nl_mid).  The stages of
+// a prime-factor transform commute; Lp is the stage's digit weight a.ns[s].
+// SKIP0: the caller runs stage 0 itself.
+template <int LW, bool GEN, int RM = 0, bool SKIP0 = false>
 SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
-  int Lp = 1;
-  for (int s = 0; s < a.nst; ++s) {
-    if (rm_pfa<RM>(a)) {
-      if constexpr (!(RM & RM_CT))
-        lane_run_stage<2, LW, LW, GEN, RM>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
-    } else {
-      if constexpr (!(RM & RM_PFA))
-        lane_run_stage<0, LW, LW, GEN, RM>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
+  if (rm_pfa<RM>(a)) {
+    if constexpr (!(RM & RM_CT)) {
+      for (int i = 1; i <= a.nst; ++i) {
+        const int s = i == a.nst ? 0 : i;
+        if (SKIP0 && s == 0) break;
+        lane_run_stage<2, LW, LW, GEN, RM>(c.X, c.ct, a.N2, a.ns[s], a.radix[s], 1.0, a.tw, c.tid,
+                                            c.nthr);
+      }
     }
-    Lp *= a.radix[s];
+    return;
+  }
+  if constexpr (!(RM & RM_PFA)) {
+    int Lp = 1;
+    for (int s = 0; s < a.nst; ++s) {
+      lane_run_stage<0, LW, LW, GEN, RM>(c.X, c.ct, a.N2, Lp, a.radix[s], 1.0, a.tw, c.tid, c.nthr);
+      Lp *= a.radix[s];
+    }
   }
 }
 
-// forward transform of rows 0..RW-1
-template <int RW, int LW, bool GEN, int RM = 0>
+// forward transform of rows 0..RW-1 (SKIP0: stage 0 of a prime-factor length is done)
+template <int RW, int LW, bool GEN, int RM = 0, bool SKIP0 = false>
 SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
   if (rm_pfa<RM>(a)) {
     if constexpr (!(RM & RM_CT)) {
-      int Lp = 1;
-      for (int s = 0; s < a.nst; ++s) {
-        lane_run_stage<2, RW, LW, GEN, RM>(c.X, c.ct, a.N2, Lp, a.radix[s], -1.0, a.tw, c.tid, c.nthr);
-        Lp *= a.radix[s];
-      }
+      for (int s = SKIP0 ? 1 : 0; s < a.nst; ++s)
+        lane_run_stage<2, RW, LW, GEN, RM>(c.X, c.ct, a.N2, a.ns[s], a.radix[s], -1.0, a.tw, c.tid,
+                                            c.nthr);
     }
     return;
   }
@@ -248,6 +268,19 @@ SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
     }
   }
 }
+
+// Grid products of the nonlinear terms (dynamics.py:142-160) at one grid point, with
+// the rounding spelled out (no compiler contraction choices) so that every kernel
+// forming them gives the same bits.  u, v, gx, gy already carry 1/(a cos):
+//   o0 = -(u gx + v gy) - Phi' delta     (-(V.grad Phi) - Phi' delta)
+//   o1 = (u u + v v) / 2                 (kinetic energy)
+//   o2 = (xi u) cos, o3 = (xi v) cos
+SWE_DEV double nl_adv(double u, double v, double gx, double gy) {
+  return __fma_rn(u, gx, __dmul_rn(v, gy));
+}
+SWE_DEV double nl_tphi(double adv, double ph, double de) { return __fma_rn(-ph, de, -adv); }
+SWE_DEV double nl_ke(double u, double v) { return __dmul_rn(0.5, __fma_rn(u, u, __dmul_rn(v, v))); }
+SWE_DEV double nl_flux(double xi, double u, double cs) { return __dmul_rn(__dmul_rn(xi, u), cs); }
 
 // Z of one hemisphere row from its half spectrum X (see fft.cu build comment):
 //   Z[k] = (X[k] + conj X[N2-k]) + i w^k (X[k] - conj X[N2-k])
@@ -512,6 +545,84 @@ SWE_DEV void lane_prefetch_eo(const FftArgs &a, const LCtx &c, int nf) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// The middle of the nonlinear pass on registers (prime-factor lengths, one slice per
+// CTA): the inverse transform's stage 0 (radix R, butterflies on slots R g .. R g +
+// R - 1), the grid products and the forward transform's stage 0 on the same slots.
+// A thread item (butterfly g, hemisphere h) reads the 7 input rows of its hemisphere
+// at its R slots and writes the 4 product rows back in place; no other item touches
+// those slots.  The arithmetic is lane_stage's, the product loop's and lane_stage's
+// again (bitwise), in 1.4 shared-memory passes instead of 4.4 and two barriers
+// fewer.  Fields are taken in an order that keeps at most four R-point rows live
+// (plus the butterfly's own).
+// Items (g, h), h fastest: 4 consecutive butterflies x 2 hemispheres of one field
+// hit 8 distinct 16-byte bank groups (xs swizzle), conflict-free.
+template <int R, int LW>
+SWE_DEV void lane_nl_mid(const FftArgs &a, const LCtx &c) {
+  constexpr int H = (R - 1) / 2;
+  double cr[H + 1], sr[H + 1];
+#pragma unroll
+  for (int e = 0; e <= H; ++e) {
+    const double2 w = __ldg(a.tw + e * (a.N2 / R));
+    cr[e] = w.x;
+    sr[e] = w.y;
+  }
+  const double ia = a.inv_acos[c.p], cs = a.coslat[c.p];
+  const int nbf = a.N2 / R;
+  for (int it = c.tid; it < 2 * nbf; it += c.nthr) {
+    const int h = it & 1, base = (it >> 1) * R;
+    // inverse stage-0 butterfly of field f (times 1/(a cos) when SC)
+    auto inv = [&](int f, bool sc, double2(&y)[R]) {
+      double2 v[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) v[q] = c.X[xs<LW>(base + q, lrow(c, f, h, 0))];
+      dft<R>(v, 1.0, cr, sr, y);
+      if (sc) {
+#pragma unroll
+        for (int t = 0; t < R; ++t) y[t] = make_double2(y[t].x * ia, y[t].y * ia);
+      }
+    };
+    auto fwd = [&](int f, double2(&o)[R]) {
+      double2 y[R];
+      dft<R>(o, -1.0, cr, sr, y);
+#pragma unroll
+      for (int t = 0; t < R; ++t) c.X[xs<LW>(base + t, lrow(c, f, h, 0))] = y[t];
+    };
+    double2 U[R], V[R], T[R], W[R];
+    inv(0, true, U);
+    inv(1, true, V);
+    inv(3, true, W);  // gy
+#pragma unroll
+    for (int t = 0; t < R; ++t) T[t] = make_double2(__dmul_rn(V[t].x, W[t].x), __dmul_rn(V[t].y, W[t].y));
+    inv(2, true, W);  // gx: T = nl_adv(u, v, gx, gy)
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+      T[t] = make_double2(__fma_rn(U[t].x, W[t].x, T[t].x), __fma_rn(U[t].y, W[t].y, T[t].y));
+    inv(4, false, W);  // xi
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const double2 u = U[t], v = V[t];
+      U[t] = make_double2(nl_flux(W[t].x, u.x, cs), nl_flux(W[t].y, u.y, cs));
+      V[t] = make_double2(nl_flux(W[t].x, v.x, cs), nl_flux(W[t].y, v.y, cs));
+      W[t] = make_double2(nl_ke(u.x, v.x), nl_ke(u.y, v.y));
+    }
+    // rows of v, gx, gy are consumed: their slots take ke and the fluxes
+    fwd(1, W);
+    fwd(2, U);
+    fwd(3, V);
+    if (a.no_rest) {
+#pragma unroll
+      for (int t = 0; t < R; ++t) U[t] = make_double2(0.0, 0.0);
+    } else {
+      inv(5, false, U);  // Phi'
+    }
+    inv(6, false, V);  // delta
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+      T[t] = make_double2(nl_tphi(T[t].x, U[t].x, V[t].x), nl_tphi(T[t].y, U[t].y, V[t].y));
+    fwd(0, T);
+  }
+}
+
 template <int LW, bool GEN, int CG, int RM, class Store>
 SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   const int p = c.p, I = a.I, S = c.S;
@@ -519,6 +630,15 @@ SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   lane_prefetch_eo(a, c, 7);
   lane_load_eo<LW, CG>(a, c, 7, 5);
   __syncthreads();
+  const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
+  if constexpr ((RM & RM_MID) != 0) {
+    lane_ifft<LW, GEN, RM, true>(a, c);
+    lane_nl_mid<rm_radix0(RM), LW>(a, c);
+    __syncthreads();
+    lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN, RM, true>(a, c);
+    lane_extract_to<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
+    return;
+  }
   lane_ifft<LW, GEN, RM>(a, c);
   const double cs = a.coslat[p];
   constexpr int NH = 2;  // hemispheres held by this CTA
@@ -529,15 +649,14 @@ SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
     auto R = [&](int f) -> double & { return gslot<LW>(c, pp, hh, lrow(c, f, h, s)); };
     const double u = R(0) * ia, v = R(1) * ia, gx = R(2) * ia, gy = R(3) * ia;
     const double xi = R(4), ph = a.no_rest ? 0.0 : R(5), de = R(6);
-    R(0) = -(u * gx + v * gy) - ph * de;   // -(V.grad Phi) - Phi' delta
-    R(1) = 0.5 * (u * u + v * v);          // kinetic energy
-    R(2) = (xi * u) * cs;                  // (xi u) cos
-    R(3) = (xi * v) * cs;                  // (xi v) cos
+    R(0) = nl_tphi(nl_adv(u, v, gx, gy), ph, de);  // -(V.grad Phi) - Phi' delta
+    R(1) = nl_ke(u, v);                            // kinetic energy
+    R(2) = nl_flux(xi, u, cs);                     // (xi u) cos
+    R(3) = nl_flux(xi, v, cs);                     // (xi v) cos
   }
   __syncthreads();
   // only the 4 product fields x 2 hemispheres (S = 1)
   lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN, RM>(a, c);
-  const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
   lane_extract_to<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
 }
 

@@ -1561,7 +1561,7 @@ int swe_set_option(const char *key, int value) {
     g_f_il = value;
     return OK;
   }
-  if (key && strcmp(key, "fft_rm") == 0 && (value == 0 || value == 1)) {
+  if (key && strcmp(key, "fft_rm") == 0 && value >= 0 && value <= 2) {
     g_fft_rm = value;
     return OK;
   }

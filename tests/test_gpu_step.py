@@ -296,7 +296,10 @@ def test_nonlinear_m1024_lanes_match_rows(mods):
     for f in range(3):
         a, b = got[1][f], got[2][f]
         assert np.isfinite(b).all()
-        assert np.abs(b - a).max() <= 1e-11 * np.abs(a).max(), f  # as vs the oracle
+        # north_star's 1e-10 relative L-inf: the two kernels run the prime-factor
+        # stages in different orders (the lane kernel ends its inverse on stage 0 for
+        # the fused middle), and the delta tendency is a small difference of flux terms
+        assert np.abs(b - a).max() <= 1e-10 * np.abs(a).max(), f
 
 
 @pytest.mark.parametrize("M,B", [(32, 3), (51, 40)])
@@ -358,8 +361,10 @@ def test_step_graph_nonconvergence_keeps_input(mods):
 
 @pytest.mark.parametrize("M", [32, 51, 256])
 def test_fft_kernel_variants_bitwise(mods, M):
-    """The radix-specialised nonlinear lane kernels (49 = 7x7, 77 = 7x11, 385 = 5x7x11)
-    and the L2 prefetch of the E/O blocks give bitwise the generic kernel's step."""
+    """The radix-specialised nonlinear lane kernels (49 = 7x7, 77 = 7x11, 385 = 5x7x11),
+    their fused middle (inverse and forward stage 0 with the grid products on
+    registers, fft_rm=2) and the L2 prefetch of the E/O blocks give bitwise the
+    generic kernel's step."""
     spharm, dynamics, steppers, scenarios = mods
     import torch
     from paper_2306_09497_b200 import _lib
@@ -367,17 +372,17 @@ def test_fft_kernel_variants_bitwise(mods, M):
     cfg = steppers.StepperConfig(dt=120.0, viscosity=dynamics.ViscositySpec(2, 1e5))
     outs = {}
     try:
-        for rm, pf in ((0, 0), (1, 0), (1, 2)):
+        for rm, pf in ((0, 0), (1, 0), (1, 2), (2, 0), (2, 2)):
             _lib.set_option("fft_rm", rm)
             _lib.set_option("fft_pf", pf)
             s = scenarios.gaussian_bumps(grid, batch=4)
             steppers.imex_steps_inplace(s, cfg, 2)
             outs[(rm, pf)] = s.data.cpu()
     finally:
-        _lib.set_option("fft_rm", 1)
+        _lib.set_option("fft_rm", 2)
         _lib.set_option("fft_pf", 2)
-    assert torch.equal(outs[(0, 0)], outs[(1, 0)])
-    assert torch.equal(outs[(0, 0)], outs[(1, 2)])
+    for key in ((1, 0), (1, 2), (2, 0), (2, 2)):
+        assert torch.equal(outs[(0, 0)], outs[key]), key
 
 
 def test_tiled_fixed_point_matches_untiled(mods):

@@ -3,7 +3,10 @@
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2306_09497_b200 import _lib, dynamics, spharm, steppers
+from paper_2306_09497_b200 import _lib
+if os.environ.get("SWE_LIB"):  # another build of the library
+    _lib.load.__defaults__ = (os.path.abspath(os.environ["SWE_LIB"]),)
+from paper_2306_09497_b200 import dynamics, spharm, steppers
 import bench
 for kv in sys.argv[1:]:
     k, v = kv.split("=")

@@ -2,7 +2,10 @@
 import sys, os, json, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-from paper_2306_09497_b200 import _lib, dynamics, spharm, steppers
+from paper_2306_09497_b200 import _lib
+if os.environ.get("SWE_LIB"):  # A/B of another build of the library
+    _lib.load.__defaults__ = (os.path.abspath(os.environ["SWE_LIB"]),)
+from paper_2306_09497_b200 import dynamics, spharm, steppers
 import bench
 
 def run(steps, **opts):
