@@ -223,6 +223,17 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
   return lw == 16 ? launch_width<16, false>(op, a, smem, st) : launch_width<8, false>(op, a, smem, st);
 }
 
+#ifdef SWE_FFT_PHASES
+extern "C" int swe_debug_fft_phases(unsigned long long *out, int reset) {
+  if (out) SWE_CUDA(cudaMemcpyFromSymbol(out, g_fft_phase, sizeof(g_fft_phase)));
+  if (reset) {
+    static const unsigned long long z[16] = {};
+    SWE_CUDA(cudaMemcpyToSymbol(g_fft_phase, z, sizeof(z)));
+  }
+  return OK;
+}
+#endif
+
 bool fft_lanes_ok(const FftArgs &a) { return lane_width(a, nullptr) != 0; }
 
 int fft_lanes_width(const FftArgs &a, int *rgen) { return lane_width(a, rgen); }

@@ -16,6 +16,35 @@ namespace swe {
 
 using namespace fftcore;
 
+#ifdef SWE_FFT_PHASES
+// debug builds (tools/fft_phases.py): per-phase clock cycles of thread 0 of every
+// CTA of the nonlinear lane pass, summed over CTAs
+__device__ unsigned long long g_fft_phase[16];
+struct PhaseClock {
+  long long t = 0;
+  __device__ PhaseClock() {
+#ifdef __CUDA_ARCH__
+    t = clock64();
+#endif
+  }
+  __device__ void mark(int id) {
+#ifdef __CUDA_ARCH__
+    if (threadIdx.x == 0) {
+      const long long n = clock64();
+      atomicAdd(&g_fft_phase[id], (unsigned long long)(n - t));
+      t = n;
+    }
+#endif
+  }
+};
+#define SWE_PHASE(pc, id) pc.mark(id)
+#else
+struct PhaseClock {
+  __device__ void mark(int) {}
+};
+#define SWE_PHASE(pc, id)
+#endif
+
 namespace {
 
 // LW rows per CTA.  16: a half-warp covers them, each warp runs two butterflies per
@@ -227,7 +256,7 @@ SWE_DEV bool rm_pfa(const FftArgs &a) {
 // a prime-factor transform commute; Lp is the stage's digit weight a.ns[s].
 // SKIP0: the caller runs stage 0 itself.
 template <int LW, bool GEN, int RM = 0, bool SKIP0 = false>
-SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
+SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c, PhaseClock *pc = nullptr) {
   if (rm_pfa<RM>(a)) {
     if constexpr (!(RM & RM_CT)) {
       for (int i = 1; i <= a.nst; ++i) {
@@ -235,6 +264,7 @@ SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
         if (SKIP0 && s == 0) break;
         lane_run_stage<2, LW, LW, GEN, RM>(c.X, c.ct, a.N2, a.ns[s], a.radix[s], 1.0, a.tw, c.tid,
                                             c.nthr);
+        if (pc) SWE_PHASE((*pc), 1 + s);
       }
     }
     return;
@@ -250,12 +280,14 @@ SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c) {
 
 // forward transform of rows 0..RW-1 (SKIP0: stage 0 of a prime-factor length is done)
 template <int RW, int LW, bool GEN, int RM = 0, bool SKIP0 = false>
-SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c) {
+SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c, PhaseClock *pc = nullptr) {
   if (rm_pfa<RM>(a)) {
     if constexpr (!(RM & RM_CT)) {
-      for (int s = SKIP0 ? 1 : 0; s < a.nst; ++s)
+      for (int s = SKIP0 ? 1 : 0; s < a.nst; ++s) {
         lane_run_stage<2, RW, LW, GEN, RM>(c.X, c.ct, a.N2, a.ns[s], a.radix[s], -1.0, a.tw, c.tid,
                                             c.nthr);
+        if (pc) SWE_PHASE((*pc), 9 + s);
+      }
     }
     return;
   }
@@ -356,7 +388,7 @@ SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
   const size_t eo = (size_t)a.Jp * a.ld / 2;  // E -> O offset (double2)
   const size_t mstride = 2 * eo;
   const int per = npair * S, total = nf * per;
-  constexpr int U = 2;
+  constexpr int U = 2;  // (3 and 4 measured slower)
   for (int i0 = c.tid; i0 < total; i0 += U * c.nthr) {
     double2 e[U], o[U], e2[U], o2[U], w1[U], w2[U];
     int z1[U], z2[U];
@@ -627,16 +659,23 @@ template <int LW, bool GEN, int CG, int RM, class Store>
 SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   const int p = c.p, I = a.I, S = c.S;
   const double ia = a.inv_acos[p];
+  PhaseClock pc;
   lane_prefetch_eo(a, c, 7);
   lane_load_eo<LW, CG>(a, c, 7, 5);
   __syncthreads();
+  SWE_PHASE(pc, 0);
   const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
   if constexpr ((RM & RM_MID) != 0) {
-    lane_ifft<LW, GEN, RM, true>(a, c);
+    lane_ifft<LW, GEN, RM, true>(a, c, &pc);
     lane_nl_mid<rm_radix0(RM), LW>(a, c);
     __syncthreads();
-    lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN, RM, true>(a, c);
+    SWE_PHASE(pc, 8);
+    lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN, RM, true>(a, c, &pc);
     lane_extract_to<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
+#ifdef SWE_FFT_PHASES
+    __syncthreads();
+    SWE_PHASE(pc, 15);
+#endif
     return;
   }
   lane_ifft<LW, GEN, RM>(a, c);
