@@ -22,6 +22,15 @@
 
 namespace swe {
 
+#ifdef SWE_LEG_PHASES
+// debug builds (tools/leg_phases.py): consumer-warp clock cycles [kernel][full-barrier
+// waits, epilogue, total, units], summed over lane 0 of every consumer warp
+__device__ unsigned long long g_leg_phase[2][4];
+#define LEGT(...) __VA_ARGS__
+#else
+#define LEGT(...)
+#endif
+
 namespace {
 
 // 3 warpgroups: warpgroup 0 = producer (warp 0; warps 1-3 exit), warpgroups 1-2 =
@@ -232,13 +241,17 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
   const int cw = warp - V3_CW0, g = lane >> 2, t = lane & 3;
   const int wpar = cw & 1, wph = (cw >> 1) & 1, wch = cw >> 2;
   int it = 0;
+  LEGT(long long tc0 = clock64(), twait = 0, tepi = 0, nun = 0;)
   while (true) {
     {
       const int s = it % S3_NS;
+      LEGT(const long long tw = clock64();)
       mbar_wait(&sm.full[s], (it / S3_NS) & 1);
+      LEGT(twait += clock64() - tw;)
     }
     const int u = sm.st[it % S3_NS].unit;
     if (u < 0) break;
+    LEGT(++nun;)
     const Unit x = decode(args, u, ncol, 64);
     const LegOut &o = args.out[x.out];
     const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
@@ -270,7 +283,9 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
       constexpr int NJ = decltype(nj_tag)::value;  // column fragments computed (8, 4, 2)
       for (int c = 0, term = 0, cc = 0; c < nch_t * o.nterms; ++c, ++it, cc = cc + 1 == nch_t ? 0 : cc + 1, term += cc == 0) {
         const int s = it % S3_NS;
+        LEGT(const long long tw = clock64();)
         if (c > 0) mbar_wait(&sm.full[s], (it / S3_NS) & 1);
+        LEGT(twait += clock64() - tw;)
         // small batches: warps whose columns are all padding skip the stage (a
         // column's sums do not depend on the others: no result changes)
         if ((nfr > 0 || XT) && (wcols || (XT && xcols))) {
@@ -334,6 +349,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     else if (bcols <= 16) mainloop(std::false_type{}, N2{});
     else if (bcols <= 32) mainloop(std::false_type{}, N4{});
     else mainloop(std::false_type{}, N8{});
+    LEGT(const long long te = clock64();)
     if (o.layout == 0) {
       // E or O plane of [m][2][Jp][ld]
       double *dst = o.dst + ((size_t)x.m * 2 + wpar) * Jp * ld;
@@ -387,7 +403,14 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
         }
       }
     }
+    LEGT(tepi += clock64() - te;)
   }
+  LEGT(if (lane == 0) {
+    atomicAdd(&g_leg_phase[0][0], (unsigned long long)twait);
+    atomicAdd(&g_leg_phase[0][1], (unsigned long long)tepi);
+    atomicAdd(&g_leg_phase[0][2], (unsigned long long)(clock64() - tc0));
+    atomicAdd(&g_leg_phase[0][3], (unsigned long long)nun);
+  })
 }
 
 __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ LegArgs args) {
@@ -485,15 +508,23 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
   const int gr = ((g & 3) << 1) | (g >> 2);  // tile row of fragment row g
   const int wpar = cw & 1, wrq = (cw >> 1) & 1, wch = cw >> 2;
   int it = 0;
+  LEGT(long long tc0 = clock64(), twait = 0, tepi = 0, nun = 0;)
   while (true) {
+    LEGT(const long long tw0 = clock64();)
     mbar_wait(&sm.full[it % A3_NS], (it / A3_NS) & 1);
+    LEGT(twait += clock64() - tw0;)
     const int u = sm.st[it % A3_NS].unit;
     if (u < 0) break;
+    LEGT(++nun;)
     const Unit x = decode(args, u, ncol, A3_BR);
     const LegOut &o = args.out[x.out];
     const int km = M + 1 - x.m, ne = (km + 1) >> 1, no = km >> 1;
-    const int nrow = (wpar ? no : ne) - (x.tile + wrq * A3_RW);
-    const int nfr = max(0, min(A3_FR, (nrow + 7) >> 3));
+    // 8-row fragments of the tile alternate between the two row warps (fragment
+    // 2i + wrq is this warp's i-th): a partial tile at the end of an m-block then
+    // leaves no SMSP idle while the other holds two fragments (SMSP load balance
+    // over all units 0.89 -> 0.94; each output row's sums are unchanged)
+    const int nrf = ((wpar ? no : ne) - x.tile + 7) >> 3;  // fragments holding rows
+    const int nfr = max(0, min(A3_FR, (nrf - wrq + 1) >> 1));
     double acc[A3_FR][8][2];
 #pragma unroll
     for (int i = 0; i < A3_FR; ++i)
@@ -508,7 +539,9 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     constexpr int NJ = decltype(nj_tag)::value;  // column fragments computed (8, 4, 2)
     for (int c = 0, term = 0, cc = 0; c < nch_t * o.nterms; ++c, ++it, cc = cc + 1 == nch_t ? 0 : cc + 1, term += cc == 0) {
       const int s = it % A3_NS;
+      LEGT(const long long tw = clock64();)
       if (c > 0) mbar_wait(&sm.full[s], (it / A3_NS) & 1);
+      LEGT(twait += clock64() - tw;)
       if (nfr > 0 && wcols) {
         const Anal3Stage &S = sm.st[s];
         const LegTerm &T = o.t[term];
@@ -522,11 +555,11 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
 #pragma unroll
         for (int kk = 0; kk < A3_KP / 4; ++kk)
           ps[kk] = T.pscale ? __ldg(T.pscale + q0 + kk * 4 + t) : 1.0;
-        // fragment row g reads tile row wpar*32 + wrq*16 + i*8 + gr, gr = the even rows
+        // fragment row g reads tile row wpar*32 + (2i + wrq)*8 + gr, gr = the even rows
         // for lanes 0-15 and the odd ones for 16-31 (a half-warp's 64-bit loads then
         // hit 8 distinct 16-byte chunks); k index kk*4 + t sits in chunk
         // (2 kk + t/2) ^ gr, element t & 1
-        const double *Ab = &S.A[wpar * A3_BR + wrq * A3_RW + gr][t & 1];
+        const double *Ab = &S.A[wpar * A3_BR + wrq * 8 + gr][t & 1];
         // B column n = wch*64 + j*8 + g' (g' = g ^ tim: re/im swap for i m X).  Planes:
         // slice n/2 of plane fsel.  Interleaved rows: DMMA j's 8 columns are slices
         // wch*32 + (j/2)*8 + (j&1) + 2 (g'/2), so a half-warp's 64-bit loads fall on 16
@@ -540,7 +573,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
         auto frag = [&](int kk, int q) {
           const int cs = ((2 * kk + (t >> 1)) ^ gr) << 1;
 #pragma unroll
-          for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 8 * A3_KP + cs] * (asc * ps[kk]);
+          for (int i = 0; i < A3_FR; ++i) a[q][i] = Ab[i * 16 * A3_KP + cs] * (asc * ps[kk]);
 #pragma unroll
           for (int j = 0; j < NJ; ++j)
             b[q][j] = flip_sign(Bb[kk * kst + (IL ? (j >> 1) * 32 + (j & 1) * 4 : j * 8)], bmask);
@@ -588,11 +621,12 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
       else if (bc <= 32) mainloop(std::false_type{}, N4{});
       else mainloop(std::false_type{}, N8{});
     }
+    LEGT(const long long te = clock64();)
     const int nt = wpar ? no : ne;
     const int off = args.offsets[x.m];
 #pragma unroll
     for (int i = 0; i < A3_FR; ++i) {
-      const int tt = x.tile + wrq * A3_RW + i * 8 + gr;
+      const int tt = x.tile + (2 * i + wrq) * 8 + gr;
       if (tt >= nt) continue;
       const size_t k = (size_t)off + (wpar ? ne : 0) + tt;
 #pragma unroll
@@ -603,8 +637,26 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
           *reinterpret_cast<double2 *>(o.dst + k * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
       }
     }
+    LEGT(tepi += clock64() - te;)
   }
+  LEGT(if (lane == 0) {
+    atomicAdd(&g_leg_phase[1][0], (unsigned long long)twait);
+    atomicAdd(&g_leg_phase[1][1], (unsigned long long)tepi);
+    atomicAdd(&g_leg_phase[1][2], (unsigned long long)(clock64() - tc0));
+    atomicAdd(&g_leg_phase[1][3], (unsigned long long)nun);
+  })
 }
+
+#ifdef SWE_LEG_PHASES
+extern "C" int swe_debug_leg_phases(unsigned long long *out, int reset) {
+  if (out) SWE_CUDA(cudaMemcpyFromSymbol(out, g_leg_phase, sizeof(g_leg_phase)));
+  if (reset) {
+    static const unsigned long long z[8] = {};
+    SWE_CUDA(cudaMemcpyToSymbol(g_leg_phase, z, sizeof(z)));
+  }
+  return OK;
+}
+#endif
 
 static int num_sms() {
   static int n = 0;

@@ -5,7 +5,7 @@ R=$(cd "$(dirname "$0")/.." && pwd)
 D=$R/paper_2306_09497_b200/_build/$1
 mkdir -p $D
 for f in plan legendre legendre_v2 legendre_v3 fft fft_lanes spectral stepper diag settls; do
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC \
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xptxas -v \
     --expt-relaxed-constexpr -I $R/include $2 -c $R/paper_2306_09497_b200/csrc/$f.cu -o $D/$f.o > $D/$f.log 2>&1 || echo "FAILED $f (see $D/$f.log)" &
 done
 wait
