@@ -8,6 +8,10 @@
 namespace swe {
 
 constexpr int GV_L = 8;  // lanes per dot product group
+// dot-product loop unroll: all of a lane's table / input loads of a term in flight
+// (the heaviest groups, m = 0 of a single-slice M = 51 step, run 4 rows per lane and
+// parity; 8 vs 2: 101 -> 99 us per coarse step, the accumulation order unchanged)
+constexpr int GV_UNROLL = 8;
 
 // LDM 0: read-only path (__ldg), 1: through L2 (ld.global.cg, for inputs written
 // earlier in the same kernel), 2: generic load (shared-memory copies)
@@ -36,7 +40,7 @@ SWE_DEV void synth_group_core(const LegOut &o, int M, int m, int gl, const int *
     const double sgm = T.sign * (T.times_im ? (double)m : 1.0);
     for (int par = 0; par < 2; ++par) {
       const int nr = par ? no : ne, r0 = off + (par ? ne : 0), h = par ^ T.flip;
-#pragma unroll 2
+#pragma unroll GV_UNROLL
       for (int tt = gl; tt < nr; tt += GV_L) {
         const int r = r0 + tt;
         const double a = tab(ti, r);
@@ -125,7 +129,7 @@ SWE_DEV void anal_group_core(const LegOut &o, int m, int par, int Jh, int gl, Ta
     double s[NS][2];
 #pragma unroll
     for (int j = 0; j < NS; ++j) s[j][0] = s[j][1] = 0.0;
-#pragma unroll 2
+#pragma unroll GV_UNROLL
     for (int p = gl; p < Jh; p += GV_L) {
       const double a = tab(ti, p) * (T.pscale ? __ldg(T.pscale + p) : 1.0);
 #pragma unroll

@@ -4,7 +4,10 @@ launch list."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-from paper_2306_09497_b200 import _lib, dynamics, spharm, steppers, scenarios
+from paper_2306_09497_b200 import _lib
+if os.environ.get("SWE_LIB"):  # another build of the library
+    _lib.load.__defaults__ = (os.path.abspath(os.environ["SWE_LIB"]),)
+from paper_2306_09497_b200 import dynamics, spharm, steppers, scenarios
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 51
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 for kv in (sys.argv[3].split(",") if len(sys.argv) > 3 else []):
@@ -19,8 +22,11 @@ from paper_2306_09497_b200.spharm import _ptr, _stream
 c = cfg.to_c()
 pb = s.phibar_t[:1].contiguous()
 resid = np.zeros(1)
+# forcing (as the MGRIT coarsest sweep passes, pint.py:306-320) with FORCING=1
+gf = torch.zeros_like(u) if os.environ.get("FORCING") else None
 def sweep():
-    _lib.check(g._lib.swe_imex_sweep(g.plan, _ptr(u), None, n, _ptr(pb), ctypes.byref(c),
+    _lib.check(g._lib.swe_imex_sweep(g.plan, _ptr(u), _ptr(gf) if gf is not None else None, n,
+                                     _ptr(pb), ctypes.byref(c),
                                      resid.ctypes.data_as(ctypes.c_void_p), _stream()), "sweep")
 for _ in range(2):
     sweep()
