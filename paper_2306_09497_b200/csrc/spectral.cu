@@ -1681,17 +1681,29 @@ int loop_cond(cudaGraphConditionalHandle h, const int *counter, int *loop, int m
 
 // y[k] += g[k][col] for one batch-1 spectral field set (3 fields, [K][2]) from a
 // batch-n set ([K][2n]) (serial coarse sweep forcing)
-__global__ void k_add_col(int K, int n, int col, Ptr3 y, Ptr3C g) {
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x)
+// one point of the serial sweep (B = 1): y += g[:, col] (when g is given, as
+// add_col) and the result stored to dst in the boundary layout (as to_boundary):
+// one launch per point instead of two
+__global__ void k_sweep_point(int K, int n, int col, Ptr3 y, Ptr3C g, double2 *__restrict__ dst,
+                              const int *__restrict__ perm) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+    const int r = perm[k];
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
-      const double2 a = ld2(y.p[f], k), b = ld2(g.p[f], (size_t)k * n + col);
-      st2(y.p[f], k, add2(a, b));
+      double2 a = ld2(y.p[f], r);
+      if (g.p[0]) {
+        a = add2(a, ld2(g.p[f], (size_t)r * n + col));
+        st2(y.p[f], r, a);
+      }
+      dst[(size_t)f * K + k] = a;
     }
+  }
 }
 
-int add_col(int K, int n, int col, Ptr3 y, Ptr3C g, cudaStream_t st) {
-  k_add_col<<<(K + 255) / 256, 256, 0, st>>>(K, n, col, y, g);
+int sweep_point(int K, int n, int col, Ptr3 y, Ptr3C g, double *dst, const int *perm,
+                cudaStream_t st) {
+  k_sweep_point<<<(K + 255) / 256, 256, 0, st>>>(K, n, col, y, g, reinterpret_cast<double2 *>(dst),
+                                                 perm);
   SWE_LAUNCH_CHECK();
   return OK;
 }

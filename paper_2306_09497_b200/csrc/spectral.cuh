@@ -92,7 +92,9 @@ int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *
 int cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters, int *target2,
               int *counter, int *loop, double tol, const cudaGraphConditionalHandle *h,
               int max_iter, cudaStream_t st);
-int add_col(int K, int n, int col, Ptr3 y, Ptr3C g, cudaStream_t st);
+// serial-sweep point (B = 1): y += g[:, col] if g.p[0], then y -> dst (boundary layout)
+int sweep_point(int K, int n, int col, Ptr3 y, Ptr3C g, double *dst, const int *perm,
+                cudaStream_t st);
 int cn_start(int K, int B, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              const double *eps, const double *phibar, const CorOp &c, Ptr3 R, Ptr3 dst,
              cudaStream_t st);

@@ -1426,7 +1426,6 @@ int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double
   }
   const size_t stride = (size_t)3 * K * 2;  // doubles per state
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
-  SpecPtrsC sc = {{b.U[0], b.U[1], b.U[2]}};
   Ptr3 U = {{b.U[0], b.U[1], b.U[2]}};
   cudaGraphExec_t exec = nullptr;
   if (g_graphs && !g_prof && (rc = step_graph(r, *cfg, &exec))) return rc;
@@ -1440,8 +1439,7 @@ int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double
       } else if ((rc = imex_internal(r, *cfg, nullptr, resid_out))) {
         return rc;
       }
-      if (g && (rc = add_col(K, n, j - 1, U, G, r.st))) return rc;
-      if ((rc = to_boundary(sc, u + (size_t)j * stride, 1, 3, K, pl->perm, r.st))) return rc;
+      if ((rc = sweep_point(K, n, j - 1, U, G, u + (size_t)j * stride, pl->perm, r.st))) return rc;
     }
     if (!graph) return OK;
     SWE_CUDA(cudaMemcpyAsync(w.h_fail, w.d_fail, sizeof(int), cudaMemcpyDeviceToHost, r.st));
