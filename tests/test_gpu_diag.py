@@ -53,8 +53,11 @@ def test_diagnostics_match_oracle():
 
 def test_run_pint_outputs_match_frozen_fixtures(tmp_path):
     """The fixture run (gaussian_bumps, M=16, dt=600, Parareal, 4 iterations) on the
-    GPU path reproduces errors.csv / spectrum.csv: the spectrum to 1e-10 relative,
-    the errors (differences of nearly equal iterates, ~1e-7 and below) to 1e-6."""
+    GPU path reproduces errors.csv / spectrum.csv: the spectrum to 1e-10 relative;
+    the errors are relative L2 norms of differences of nearly equal iterates
+    (~1e-7 and below), so the iterates' own agreement (~1e-13 relative) bounds them
+    in absolute terms: 1e-14 absolute, measured 1.4e-17 (a relative bound on the error value itself
+    would only measure the cancellation)."""
     from paper_2306_09497_b200 import runner
     man = json.load(open(os.path.join(GOLDEN, "fixtures", "manifest.json")))
     code = runner.cmd_run_pint(man["config"], str(tmp_path))
@@ -62,10 +65,12 @@ def test_run_pint_outputs_match_frozen_fixtures(tmp_path):
     hdr, rows = _read(tmp_path / "errors.csv")
     rhdr, ref = _read(os.path.join(GOLDEN, "fixtures", "errors.csv"))
     assert hdr == rhdr and len(rows) == len(ref)
+    dev = 0.0
     for got, want in zip(rows, ref):
         assert got[:3] == want[:3]
-        w = float(want[3])
-        assert abs(float(got[3]) - w) <= max(1e-6 * w, 1e-12), (got, want)
+        dev = max(dev, abs(float(got[3]) - float(want[3])))
+    print(f"[DIAG] errors.csv max abs deviation {dev:.3e}")
+    assert dev <= 1e-14, dev
     hdr, rows = _read(tmp_path / "spectrum.csv")
     rhdr, ref = _read(os.path.join(GOLDEN, "fixtures", "spectrum.csv"))
     assert hdr == rhdr and len(rows) == len(ref)
