@@ -523,6 +523,7 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaMemset(w.hdone, 0, sizeof(unsigned)));
   SWE_CUDA(cudaMallocHost(&w.h_fail, sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.d_fail, sizeof(int)));
+  SWE_CUDA(cudaMemset(w.d_fail, 0, sizeof(int)));  // swe_imex_step_async accumulates into it
   SWE_CUDA(cudaMalloc(&w.sched, 2 * sizeof(unsigned long long)));
   SWE_CUDA(cudaMemset(w.sched, 0, 2 * sizeof(unsigned long long)));
   SWE_CUDA(cudaMalloc(&w.phi0, (size_t)B * sizeof(double)));

@@ -1397,6 +1397,44 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
   return to_boundary(s, state, batch, 3, pl->K, pl->perm, r.st);
 }
 
+int swe_imex_step_async(swe_plan *pl, double *state, const double *phibar, int batch,
+                        const swe_stepper_cfg *cfg, int nsteps, void *stream) {
+  int rc;
+  if ((rc = check_cfg(cfg))) return rc;
+  if (!phibar) {
+    set_error("phibar is NULL");
+    return E_SHAPE;
+  }
+  if ((rc = prepare(pl, batch, phibar, (cudaStream_t)stream))) return rc;
+  Run r = make_run(pl, batch, stream);
+  r.Bsel = cfg->select_batch > 0 ? cfg->select_batch : r.B;
+  cudaGraphExec_t exec = nullptr;
+  if (g_graphs && !g_prof && nsteps > 0 && (rc = step_graph(r, *cfg, &exec))) return rc;
+  if (!exec)  // no step graph for this configuration: the synchronous call
+    return swe_imex_step(pl, state, phibar, batch, cfg, nsteps, nullptr, nullptr, stream);
+  const Bufs b = bufs(r);
+  SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
+  if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st))) return rc;
+  for (int s = 0; s < nsteps; ++s) SWE_CUDA(cudaGraphLaunch(exec, r.st));
+  // the flag stays up once any queued step failed (no per-call reset): this and every
+  // later queued call leave their state untouched until swe_plan_status resets it
+  SpecPtrsC so = {{b.U[0], b.U[1], b.U[2]}};
+  return to_boundary(so, state, batch, 3, pl->K, pl->perm, r.st, pl->ws.d_fail);
+}
+
+int swe_plan_status(swe_plan *pl, int *failed, int reset, void *stream) {
+  if (!pl || !failed) {
+    set_error("swe_plan_status: null argument");
+    return E_SHAPE;
+  }
+  const cudaStream_t st = (cudaStream_t)stream;
+  SWE_CUDA(cudaMemcpyAsync(pl->ws.h_fail, pl->ws.d_fail, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SWE_CUDA(cudaStreamSynchronize(st));
+  *failed = *pl->ws.h_fail;
+  if (reset) SWE_CUDA(cudaMemsetAsync(pl->ws.d_fail, 0, sizeof(int), st));
+  return OK;
+}
+
 int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double *phibar,
                    const swe_stepper_cfg *cfg, double *resid_out, void *stream) {
   int rc;

@@ -112,6 +112,38 @@ def imex_steps_inplace(state: PrognosticState, cfg: StepperConfig, nsteps: int =
     return state
 
 
+def imex_steps_async(state: PrognosticState, cfg: StepperConfig, nsteps: int = 1,
+                     select_batch: int = 0) -> PrognosticState:
+    """imex_steps_inplace without the per-call host check (swe_imex_step_async): the
+    steps are queued on the current stream and the call returns at once.  An
+    unconverged Coriolis solve is reported by `check_async_steps` (and leaves this
+    and every later queued state untouched until then)."""
+    if cfg.scheme != IMEX:
+        raise ValueError("imex_steps_async needs scheme='imex'")
+    grid = state.grid
+    c = cfg.to_c(select_batch)
+    rc = grid._lib.swe_imex_step_async(grid.plan, _ptr(state.data), _ptr(state.phibar_t),
+                                       state.batch, ctypes.byref(c), int(nsteps), _stream())
+    try:
+        _lib.check(rc, "swe_imex_step_async")  # (configurations run synchronously)
+    except _lib.NoConvergence as exc:
+        raise ImplicitSolveError(str(exc)) from None
+    return state
+
+
+def check_async_steps(grid: SphereGrid, reset: bool = True):
+    """Wait for the queued imex_steps_async calls of `grid`'s plan and raise
+    ImplicitSolveError if any of them hit an unconverged solve (steppers.py:113-118)."""
+    failed = ctypes.c_int(0)
+    _lib.check(grid._lib.swe_plan_status(grid.plan, ctypes.byref(failed), int(reset), _stream()),
+               "swe_plan_status")
+    if failed.value:
+        raise ImplicitSolveError(
+            "Coriolis iteration did not converge in a queued step; the states of that and "
+            "every later queued call were left unchanged (rerun them with imex_steps_inplace "
+            "for the residual)")
+
+
 def imex_step(state: PrognosticState, cfg: StepperConfig) -> PrognosticState:
     """Implicit half step, explicit Heun step on N, implicit half step, viscosity
     (steppers.py:155-168).  Returns a new state; the input is untouched."""
@@ -186,8 +218,10 @@ class HostPipeline:
     back, H2D(i) and D2H(i-2) run while batch i-1 steps (PCIe is full duplex),
     and a stream of host batches runs at the device step rate once the copies fit
     under it.  `depth` device buffers rotate; host buffers must be pinned for the
-    copies to be asynchronous.  flush() launches the last deferred batch and
-    waits for every copy back.
+    copies to be asynchronous.  The steps are queued with imex_steps_async (no
+    host round trip per batch, so the device never idles between batches); flush()
+    launches the last deferred batch, waits for every copy back and raises
+    ImplicitSolveError if any queued step did not converge.
     """
 
     def __init__(self, grid: SphereGrid, cfg: StepperConfig, batch: int, nsteps: int = 1,
@@ -213,7 +247,8 @@ class HostPipeline:
         d, pb = self.slots[j], self.pbs[j]
         self.compute.wait_event(ready)
         with torch.cuda.stream(self.compute):
-            imex_steps_inplace(PrognosticState(self.grid, d, pb), self.cfg, self.nsteps)
+            # queued without a host round trip per batch; flush() checks convergence
+            imex_steps_async(PrognosticState(self.grid, d, pb), self.cfg, self.nsteps)
             done = torch.cuda.Event()
             done.record(self.compute)
         self.d2h.wait_event(done)
@@ -251,4 +286,6 @@ class HostPipeline:
         for e in self.free:
             if e is not None:
                 e.synchronize()
+        with torch.cuda.stream(self.compute):
+            check_async_steps(self.grid)  # ImplicitSolveError if a queued step failed
         return last

@@ -4,6 +4,8 @@ Tolerances (fp64): tendencies 1e-11 relative to the field's max; one or more
 IMEX steps 1e-10 relative sup-norm per field (the north star's bound).
 """
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -340,6 +342,38 @@ def test_step_graph_nonconvergence_raises(mods):
     for _ in range(3):
         with pytest.raises(steppers.ImplicitSolveError, match="residual"):
             steppers.imex_step(s, cfg)
+
+
+def test_async_steps_match_inplace_and_report_nonconvergence(mods):
+    """swe_imex_step_async (queued graph replays, no per-call host check) gives the
+    synchronous call's states bitwise; an unconverged solve is reported by
+    check_async_steps and leaves the queued states untouched."""
+    spharm, dynamics, steppers, scenarios = mods
+    import torch
+    grid = spharm.get_grid(32)
+    cfg = steppers.StepperConfig(dt=480.0, viscosity=dynamics.ViscositySpec(2, 1e5))
+    s0 = scenarios.gaussian_bumps(grid, batch=3)
+    want = s0.copy()
+    for _ in range(3):
+        steppers.imex_steps_inplace(want, cfg, 2)
+    got = s0.copy()
+    for _ in range(3):
+        steppers.imex_steps_async(got, cfg, 2)
+    steppers.check_async_steps(grid)
+    assert torch.equal(got.data, want.data)
+    bad = dataclasses.replace(cfg, implicit_max_iter=1)
+    before = s0.data.clone()
+    with pytest.raises(steppers.ImplicitSolveError):
+        steppers.imex_steps_async(s0.copy(), bad, 1)  # first sight of the key: eager, raises
+    x = s0.copy()
+    y = s0.copy()
+    steppers.imex_steps_async(x, bad, 1)   # graph replay: queued
+    steppers.imex_steps_async(y, cfg, 1)   # queued after the failure: left untouched
+    with pytest.raises(steppers.ImplicitSolveError):
+        steppers.check_async_steps(grid)
+    torch.cuda.synchronize()
+    assert torch.equal(x.data, before) and torch.equal(y.data, before)
+    steppers.check_async_steps(grid)       # the flag was reset
 
 
 def test_step_graph_nonconvergence_keeps_input(mods):
