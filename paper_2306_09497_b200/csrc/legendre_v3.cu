@@ -278,9 +278,12 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     for (int j = 0; j < 4; ++j) acx[j][0] = acx[j][1] = 0.0;
     // the remainder path is a separate instantiation, so ordinary units keep the
     // lean register allocation of the plain 4 x 8 fragment loop
-    auto mainloop = [&](auto xt_tag, auto nj_tag) {
+    // FULL (compile time): all 4 row fragments hold pairs, so the DMMAs carry no
+    // predicate (predicated mma.sync groups cost a WARPSYNC and NOP padding each)
+    auto mainloop = [&](auto xt_tag, auto nj_tag, auto full_tag) {
       constexpr bool XT = decltype(xt_tag)::value;
       constexpr int NJ = decltype(nj_tag)::value;  // column fragments computed (8, 4, 2)
+      constexpr bool FULL = decltype(full_tag)::value;
       for (int c = 0, term = 0, cc = 0; c < nch_t * o.nterms; ++c, ++it, cc = cc + 1 == nch_t ? 0 : cc + 1, term += cc == 0) {
         const int s = it % S3_NS;
         LEGT(const long long tw = clock64();)
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
               if (kk + 1 < NKK) frag(kk + 1, q ^ 1);
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                if (i < nfr) {
+                if (FULL || i < nfr) {
 #pragma unroll
                   for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
                 }
@@ -345,10 +348,12 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
     using N8 = std::integral_constant<int, 8>;
     using N4 = std::integral_constant<int, 4>;
     using N2 = std::integral_constant<int, 2>;
-    if (xtra) mainloop(std::true_type{}, N8{});
-    else if (bcols <= 16) mainloop(std::false_type{}, N2{});
-    else if (bcols <= 32) mainloop(std::false_type{}, N4{});
-    else mainloop(std::false_type{}, N8{});
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    if (xtra) nfr == 4 ? mainloop(T_{}, N8{}, T_{}) : mainloop(T_{}, N8{}, F_{});
+    else if (bcols <= 16) mainloop(F_{}, N2{}, F_{});
+    else if (bcols <= 32) mainloop(F_{}, N4{}, F_{});
+    else nfr == 4 ? mainloop(F_{}, N8{}, T_{}) : mainloop(F_{}, N8{}, F_{});
     LEGT(const long long te = clock64();)
     if (o.layout == 0) {
       // E or O plane of [m][2][Jp][ld]
@@ -534,9 +539,10 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     // slices wch*32..) are all padding skips the stages (see leg_synth_v3)
     const bool wcols = min(V3_BN, ld - x.c0) > wch * 64;
     // the unit's F layout as a compile-time switch (interleaved rows or planes)
-    auto mainloop = [&](auto ilc, auto nj_tag) {
+    auto mainloop = [&](auto ilc, auto nj_tag, auto full_tag) {
     constexpr bool IL = decltype(ilc)::value;
     constexpr int NJ = decltype(nj_tag)::value;  // column fragments computed (8, 4, 2)
+    constexpr bool FULL = decltype(full_tag)::value;  // all A3_FR fragments hold modes
     for (int c = 0, term = 0, cc = 0; c < nch_t * o.nterms; ++c, ++it, cc = cc + 1 == nch_t ? 0 : cc + 1, term += cc == 0) {
       const int s = it % A3_NS;
       LEGT(const long long tw = clock64();)
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
             if (kk + 1 < NKK) frag(kk + 1, q ^ 1);
 #pragma unroll
             for (int i = 0; i < A3_FR; ++i)
-              if (i < nfr) {
+              if (FULL || i < nfr) {
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[q][i], b[q][j]);
               }
@@ -613,13 +619,14 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
     using N2 = std::integral_constant<int, 2>;
     const int bc = min(V3_BN, ld - x.c0);
     if (il) {
-      if (bc <= 16) mainloop(std::true_type{}, N2{});
-      else if (bc <= 32) mainloop(std::true_type{}, N4{});
-      else mainloop(std::true_type{}, N8{});
+      if (bc <= 16) mainloop(std::true_type{}, N2{}, std::false_type{});
+      else if (bc <= 32) mainloop(std::true_type{}, N4{}, std::false_type{});
+      else if (nfr == A3_FR) mainloop(std::true_type{}, N8{}, std::true_type{});
+      else mainloop(std::true_type{}, N8{}, std::false_type{});
     } else {
-      if (bc <= 16) mainloop(std::false_type{}, N2{});
-      else if (bc <= 32) mainloop(std::false_type{}, N4{});
-      else mainloop(std::false_type{}, N8{});
+      if (bc <= 16) mainloop(std::false_type{}, N2{}, std::false_type{});
+      else if (bc <= 32) mainloop(std::false_type{}, N4{}, std::false_type{});
+      else mainloop(std::false_type{}, N8{}, std::false_type{});
     }
     LEGT(const long long te = clock64();)
     const int nt = wpar ? no : ne;
