@@ -211,9 +211,10 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
     for (int s = 0; s < a.nst; ++s) m |= r_bit(a.radix[s]);
     m |= a.pfa ? RM_PFA : RM_CT;
     constexpr int R5711 = 8 | 16 | 32 | RM_PFA, R711 = 16 | 32 | RM_PFA, R7 = 16 | RM_CT;
-    if (m == R5711)
-      return g_fft_rm == 2 ? launch_lanes<FOP_NONLINEAR, 16, false, R5711 | RM_MID>(a, smem, st)
-                           : launch_lanes<FOP_NONLINEAR, 16, false, R5711>(a, smem, st);
+    if (m == R5711)  // (coprime radices: 5, 7 and 11 once each, N2 = 385)
+      return g_fft_rm == 2 && a.N2 == 385
+                 ? launch_lanes<FOP_NONLINEAR, 16, false, R5711 | RM_MID>(a, smem, st)
+                 : launch_lanes<FOP_NONLINEAR, 16, false, R5711>(a, smem, st);
     // (77 = 7 x 11 keeps the three-pass middle: the radix-7 fused middle spills and
     // the one-slice coarse step is latency-bound, 109 vs 102 us per M=51 step)
     if (m == R711) return launch_lanes<FOP_NONLINEAR, 16, false, R711>(a, smem, st);

@@ -76,10 +76,13 @@ SWE_DEV int xs(int slot, int row) { return slot * LW + (row ^ swz<LW>(slot)); }
 
 // MODE 0 DIT, 1 DIF, 2 prime-factor (no twiddles); see fft.cu.  RW rows take part
 // (RW lanes per butterfly, 32/RW butterflies per warp instruction).
-template <int R, int MODE, int RW, int LW>
-SWE_DEV void lane_stage(double2 *X, int N2, int Lp, double dir, const double2 *tw, int warp,
+// LPC, N2C > 0: digit weight and length known at compile time (the hot prime-factor
+// kernels): the butterfly index arithmetic becomes constant divisions
+template <int R, int MODE, int RW, int LW, int LPC = 0, int N2C = 0>
+SWE_DEV void lane_stage(double2 *X, int N2_, int Lp_, double dir, const double2 *tw, int warp,
                         int nw, int lane) {
   constexpr int H = (R - 1) / 2, BW = 32 / RW;
+  const int N2 = N2C ? N2C : N2_, Lp = LPC ? LPC : Lp_;
   double cr[H + 1], sr[H + 1];
   if constexpr (R != 2 && R != 4) {
 #pragma unroll
@@ -93,7 +96,8 @@ SWE_DEV void lane_stage(double2 *X, int N2, int Lp, double dir, const double2 *t
   const int row = lane & (RW - 1);
   const float inv_lp = 1.0f / (float)Lp;  // exact quotient for bf < 2^12 (N2 <= 4096)
   for (int bf = BW * warp + lane / RW; bf < nbf; bf += BW * nw) {
-    const int g = (int)(((float)bf + 0.5f) * inv_lp), k = bf - g * Lp, base = g * L + k;
+    const int g = LPC ? bf / LPC : (int)(((float)bf + 0.5f) * inv_lp), k = bf - g * Lp,
+              base = g * L + k;
     double2 v[R], y[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
@@ -255,8 +259,27 @@ SWE_DEV bool rm_pfa(const FftArgs &a) {
 // nonlinear pass can fuse them with the grid products (lane_nl_mid).  The stages of
 // a prime-factor transform commute; Lp is the stage's digit weight a.ns[s].
 // SKIP0: the caller runs stage 0 itself.
+// the R5711 | RM_MID kernels: N2 = 385 = 5 x 7 x 11 prime-factor (the radices are
+// coprime, so each appears once), stage 0 fused into lane_nl_mid; stages 1 and 2
+// (radix 7 at digit weight 5, radix 11 at 35) with compile-time index arithmetic
+constexpr int RM_385 = 8 | 16 | 32 | RM_PFA | RM_MID;
+template <int RW, int LW>
+SWE_DEV void lane_stages_385(const LCtx &c, const FftArgs &a, double dir, PhaseClock *pc, int id0) {
+  const int warp = c.tid >> 5, nw = c.nthr >> 5, lane = c.tid & 31;
+  lane_stage<7, 2, RW, LW, 5, 385>(c.X, 385, 5, dir, a.tw, warp, nw, lane);
+  __syncthreads();
+  if (pc) SWE_PHASE((*pc), id0 + 1);
+  lane_stage<11, 2, RW, LW, 35, 385>(c.X, 385, 35, dir, a.tw, warp, nw, lane);
+  __syncthreads();
+  if (pc) SWE_PHASE((*pc), id0 + 2);
+}
+
 template <int LW, bool GEN, int RM = 0, bool SKIP0 = false>
 SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c, PhaseClock *pc = nullptr) {
+  if constexpr (RM == RM_385 && SKIP0) {
+    lane_stages_385<LW, LW>(c, a, 1.0, pc, 1);
+    return;
+  }
   if (rm_pfa<RM>(a)) {
     if constexpr (!(RM & RM_CT)) {
       for (int i = 1; i <= a.nst; ++i) {
@@ -281,6 +304,10 @@ SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c, PhaseClock *pc = nullptr
 // forward transform of rows 0..RW-1 (SKIP0: stage 0 of a prime-factor length is done)
 template <int RW, int LW, bool GEN, int RM = 0, bool SKIP0 = false>
 SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c, PhaseClock *pc = nullptr) {
+  if constexpr (RM == RM_385 && SKIP0) {
+    lane_stages_385<RW, LW>(c, a, -1.0, pc, 9);
+    return;
+  }
   if (rm_pfa<RM>(a)) {
     if constexpr (!(RM & RM_CT)) {
       for (int s = SKIP0 ? 1 : 0; s < a.nst; ++s) {
