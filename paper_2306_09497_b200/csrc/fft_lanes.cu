@@ -212,7 +212,7 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
     m |= a.pfa ? RM_PFA : RM_CT;
     constexpr int R5711 = 8 | 16 | 32 | RM_PFA, R711 = 16 | 32 | RM_PFA, R7 = 16 | RM_CT;
     if (m == R5711)  // (coprime radices: 5, 7 and 11 once each, N2 = 385)
-      return g_fft_rm == 2 && a.N2 == 385
+      return g_fft_rm == 2 && a.N2 == 385 && a.M == 256  // (compiled for these)
                  ? launch_lanes<FOP_NONLINEAR, 16, false, R5711 | RM_MID>(a, smem, st)
                  : launch_lanes<FOP_NONLINEAR, 16, false, R5711>(a, smem, st);
     // (77 = 7 x 11 keeps the three-pass middle: the radix-7 fused middle spills and

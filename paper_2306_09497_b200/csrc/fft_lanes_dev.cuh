@@ -409,9 +409,10 @@ SWE_DEV double2 ld_in(const double2 *p) {
   else return __ldg(p);
 }
 
-template <int LW, int CG = 0>
+// N2C, MC > 0: length and truncation known at compile time (the N2 = 385 kernel)
+template <int LW, int CG = 0, int N2C = 0, int MC = 0>
 SWE_DEV void lane_load_eo(const FftArgs &a, const LCtx &c, int nf, int subf) {
-  const int N2 = a.N2, M = a.M, npair = N2 / 2 + 1, S = c.S;
+  const int N2 = N2C ? N2C : a.N2, M = MC ? MC : a.M, npair = N2 / 2 + 1, S = c.S;
   const size_t eo = (size_t)a.Jp * a.ld / 2;  // E -> O offset (double2)
   const size_t mstride = 2 * eo;
   const int per = npair * S, total = nf * per;
@@ -537,10 +538,10 @@ SWE_DEV double2 row_fm(const double2 *X, int row, int z1, int z2, double2 w) {
 // XN / XS hold the north / south rows (the same buffer unless split); items
 // i0, i0 + istep, ... of the (k, slice, field) range.
 // F+- of (field f, order k, slice s) handed to store(f, k, s, F+, F-)
-template <int LW, class Store>
+template <int LW, class Store, int N2C = 0, int MC = 0>
 SWE_DEV void lane_extract_to(const FftArgs &a, const LCtx &c, const double2 *XN, const double2 *XS,
                              int nf, double w01, double w23, int i0, int istep, Store store) {
-  const int M = a.M, S = c.S, N2 = a.N2, per = (M + 1) * S;
+  const int M = MC ? MC : a.M, S = c.S, N2 = N2C ? N2C : a.N2, per = (M + 1) * S;
   for (int idx = i0; idx < nf * per; idx += istep) {
     int k, s, f;
     item_ksf<false>(idx, nf, S, k, s, f);
@@ -615,18 +616,18 @@ SWE_DEV void lane_prefetch_eo(const FftArgs &a, const LCtx &c, int nf) {
 // (plus the butterfly's own).
 // Items (g, h), h fastest: 4 consecutive butterflies x 2 hemispheres of one field
 // hit 8 distinct 16-byte bank groups (xs swizzle), conflict-free.
-template <int R, int LW>
+template <int R, int LW, int N2C = 0>
 SWE_DEV void lane_nl_mid(const FftArgs &a, const LCtx &c) {
   constexpr int H = (R - 1) / 2;
   double cr[H + 1], sr[H + 1];
 #pragma unroll
   for (int e = 0; e <= H; ++e) {
-    const double2 w = __ldg(a.tw + e * (a.N2 / R));
+    const double2 w = __ldg(a.tw + e * ((N2C ? N2C : a.N2) / R));
     cr[e] = w.x;
     sr[e] = w.y;
   }
   const double ia = a.inv_acos[c.p], cs = a.coslat[c.p];
-  const int nbf = a.N2 / R;
+  const int N2 = N2C ? N2C : a.N2, nbf = N2 / R;
   for (int it = c.tid; it < 2 * nbf; it += c.nthr) {
     const int h = it & 1, base = (it >> 1) * R;
     // inverse stage-0 butterfly of field f (times 1/(a cos) when SC)
@@ -688,17 +689,18 @@ SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   const double ia = a.inv_acos[p];
   PhaseClock pc;
   lane_prefetch_eo(a, c, 7);
-  lane_load_eo<LW, CG>(a, c, 7, 5);
+  constexpr int N2C = RM == RM_385 ? 385 : 0, MC = RM == RM_385 ? 256 : 0;
+  lane_load_eo<LW, CG, N2C, MC>(a, c, 7, 5);
   __syncthreads();
   SWE_PHASE(pc, 0);
   const double w = a.wq[p] * a.inv_I, wv = a.wsin2[p] * a.inv_I * a.inv_a;
   if constexpr ((RM & RM_MID) != 0) {
     lane_ifft<LW, GEN, RM, true>(a, c, &pc);
-    lane_nl_mid<rm_radix0(RM), LW>(a, c);
+    lane_nl_mid<rm_radix0(RM), LW, N2C>(a, c);
     __syncthreads();
     SWE_PHASE(pc, 8);
     lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN, RM, true>(a, c, &pc);
-    lane_extract_to<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
+    lane_extract_to<LW, Store, N2C, MC>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
 #ifdef SWE_FFT_PHASES
     __syncthreads();
     SWE_PHASE(pc, 15);
