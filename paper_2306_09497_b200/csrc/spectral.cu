@@ -1117,22 +1117,31 @@ SWE_DEV void cf_nbrs(int r, int base, int km, int &lo, int &hi) {
     hi = li - ne + 1 < ne ? base + li - ne + 1 : -1;
   }
 }
+// MC > 0: the truncation is known at compile time (M = 256, the fine level): the
+// shared-memory array strides and the thread count become constants
+template <int MC>
 __global__ void __launch_bounds__(CF_NTMAX, 2)
-    k_cn_fused(int M, int B, const int *__restrict__ offsets, const double4 *__restrict__ cft,
+    k_cn_fused(int M_, int B, const int *__restrict__ offsets, const double4 *__restrict__ cft,
                const double *__restrict__ eps, const double *__restrict__ phibar, Ptr3C x0,
                Ptr3C x1, Ptr3C x2, double s, double alpha, Ptr3 R, int write_r, double *U0,
                double *A1, double *A2, double *B1, double *B2, const int *__restrict__ target,
                int G, unsigned long long *__restrict__ fst, double dtnu, double halfq) {
   extern __shared__ double2 fsm[];
+  const int M = MC ? MC : M_;
   const int m1 = blockIdx.y, m2 = M - m1;  // slice groups fastest: CTAs in flight cover whole rows
   const int km1 = M + 1 - m1, km2 = m2 > m1 ? M + 1 - m2 : 0, nrow = km1 + km2;
-  const int n = nrow * CF_S, NT = blockDim.x, tid = threadIdx.x;
+  // shared arrays laid out for the largest CTA (M + 2 rows, as allocated)
+  const int nmax = (M + 2) * CF_S, rmax = M + 2;
+  const int n = nrow * CF_S, tid = threadIdx.x;
+  const int NT = MC ? std::min(CF_NTMAX, (((MC + 2) * CF_S + CF_EPT - 1) / CF_EPT + 31) / 32 * 32)
+                    : (int)blockDim.x;
   // xi/delta iterates ping-pong between the A and B copies (iterate k lives in A
   // when k is even, as in global memory); the rhs xi/delta rows in Q1/Q2; Phi and
   // the rhs Phi have no stencil and stay in registers (pv, q0)
-  double2 *XA = fsm, *DA = XA + n, *XB = DA + n, *DB = XB + n, *Q1 = DB + n, *Q2 = Q1 + n;
-  double4 *rcf = reinterpret_cast<double4 *>(Q2 + n);
-  double *re = reinterpret_cast<double *>(rcf + nrow), *rbh = re + nrow;
+  double2 *XA = fsm, *DA = XA + nmax, *XB = DA + nmax, *DB = XB + nmax, *Q1 = DB + nmax,
+          *Q2 = Q1 + nmax;
+  double4 *rcf = reinterpret_cast<double4 *>(Q2 + nmax);
+  double *re = reinterpret_cast<double *>(rcf + rmax), *rbh = re + rmax;
   __shared__ unsigned long long sst[CF_KS][CF_S][6];
   __shared__ int tgt[CF_S];
   const int sl = tid % CF_S, b = blockIdx.x * CF_S + sl;
@@ -1370,14 +1379,26 @@ int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *
   const int nrow = M + 2, n = nrow * CF_S;
   const int NT = std::min(CF_NTMAX, ((n + CF_EPT - 1) / CF_EPT + 31) / 32 * 32);
   const int smem = 6 * n * (int)sizeof(double2) + nrow * (int)(sizeof(double4) + 2 * sizeof(double));
-  static int attr = 0;
-  if (smem > attr) {
-    SWE_CUDA(cudaFuncSetAttribute(k_cn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = smem;
-  }
   dim3 grid((B + CF_S - 1) / CF_S, M / 2 + 1);
-  k_cn_fused<<<grid, NT, smem, st>>>(M, B, offsets, cf, eps, phibar, x0, x1, x2, s, alpha, R,
-                                     write_r, U0, A1, A2, B1, B2, target, G, fst, dtnu, halfq);
+  if (M == 256) {
+    static int attr = 0;
+    if (smem > attr) {
+      SWE_CUDA(cudaFuncSetAttribute(k_cn_fused<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem));
+      attr = smem;
+    }
+    k_cn_fused<256><<<grid, NT, smem, st>>>(M, B, offsets, cf, eps, phibar, x0, x1, x2, s, alpha, R,
+                                            write_r, U0, A1, A2, B1, B2, target, G, fst, dtnu,
+                                            halfq);
+  } else {
+    static int attr = 0;
+    if (smem > attr) {
+      SWE_CUDA(cudaFuncSetAttribute(k_cn_fused<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = smem;
+    }
+    k_cn_fused<0><<<grid, NT, smem, st>>>(M, B, offsets, cf, eps, phibar, x0, x1, x2, s, alpha, R,
+                                          write_r, U0, A1, A2, B1, B2, target, G, fst, dtnu, halfq);
+  }
   SWE_LAUNCH_CHECK();
   return OK;
 }
