@@ -385,16 +385,23 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_synth_v3(const __grid_constant__
       // 32-byte sector, written by the two parity warps of this unit
       double2 *dst = reinterpret_cast<double2 *>(o.dst);
       const int nsl = ld >> 1;
+      // all of the unit's columns real (the usual case): one row base per fragment
+      // row and immediate offsets, no per-store column test
+      const bool fullc = x.c0 + V3_BN <= ld;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int p = pw0 + i * 8 + g;
         if (p >= tend) continue;
+        double2 *row =
+            dst + (((size_t)p * (M + 1) + x.m) * nsl + (x.c0 >> 1) + wch * 32 + t) * 2 + wpar;
+        if (fullc) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int col = x.c0 + wch * 64 + j * 8 + 2 * t;
-          if (col < ld)
-            dst[(((size_t)p * (M + 1) + x.m) * nsl + (col >> 1)) * 2 + wpar] =
-                make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);
+          for (int j = 0; j < 8; ++j) row[j * 8] = make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (x.c0 + wch * 64 + j * 8 + 2 * t < ld)
+              row[j * 8] = make_double2(acc[i][j][0], x.m ? acc[i][j][1] : 0.0);
         }
       }
       const int px = x.tile + S3_TW + g;
