@@ -217,7 +217,9 @@ int fft_lanes_launch(int op, const FftArgs &a, cudaStream_t st) {
                  : launch_lanes<FOP_NONLINEAR, 16, false, R5711>(a, smem, st);
     // (77 = 7 x 11 keeps the three-pass middle: the radix-7 fused middle spills and
     // the one-slice coarse step is latency-bound, 109 vs 102 us per M=51 step)
-    if (m == R711) return launch_lanes<FOP_NONLINEAR, 16, false, R711>(a, smem, st);
+    if (m == R711)  // (compile-time N2 = 77 / M = 51 in that kernel; else the generic one)
+      return a.N2 == 77 && a.M == 51 ? launch_lanes<FOP_NONLINEAR, 16, false, R711>(a, smem, st)
+                                     : launch_width<16, false>(op, a, smem, st);
     if (m == R7) return launch_lanes<FOP_NONLINEAR, 16, false, R7>(a, smem, st);
   }
   if (g) return lw == 16 ? launch_width<16, true>(op, a, smem, st) : launch_width<8, true>(op, a, smem, st);

@@ -274,10 +274,28 @@ SWE_DEV void lane_stages_385(const LCtx &c, const FftArgs &a, double dir, PhaseC
   if (pc) SWE_PHASE((*pc), id0 + 2);
 }
 
+// the R711 kernel (coarse M = 51): N2 = 77 = 7 x 11 prime-factor, stage 0 = radix 7
+// at digit weight 1, stage 1 = radix 11 at 7; the inverse runs stage 1 first
+constexpr int RM_77 = 16 | 32 | RM_PFA;
+template <int RW, int LW, int S0, int S1>
+SWE_DEV void lane_stages_77(const LCtx &c, const FftArgs &a, double dir) {
+  const int warp = c.tid >> 5, nw = c.nthr >> 5, lane = c.tid & 31;
+  constexpr int R0 = S0 == 0 ? 7 : 11, L0 = S0 == 0 ? 1 : 7;
+  constexpr int R1 = S1 == 0 ? 7 : 11, L1 = S1 == 0 ? 1 : 7;
+  lane_stage<R0, 2, RW, LW, L0, 77>(c.X, 77, L0, dir, a.tw, warp, nw, lane);
+  __syncthreads();
+  lane_stage<R1, 2, RW, LW, L1, 77>(c.X, 77, L1, dir, a.tw, warp, nw, lane);
+  __syncthreads();
+}
+
 template <int LW, bool GEN, int RM = 0, bool SKIP0 = false>
 SWE_DEV void lane_ifft(const FftArgs &a, const LCtx &c, PhaseClock *pc = nullptr) {
   if constexpr (RM == RM_385 && SKIP0) {
     lane_stages_385<LW, LW>(c, a, 1.0, pc, 1);
+    return;
+  }
+  if constexpr (RM == RM_77 && !SKIP0) {
+    lane_stages_77<LW, LW, 1, 0>(c, a, 1.0);
     return;
   }
   if (rm_pfa<RM>(a)) {
@@ -306,6 +324,10 @@ template <int RW, int LW, bool GEN, int RM = 0, bool SKIP0 = false>
 SWE_DEV void lane_fft(const FftArgs &a, const LCtx &c, PhaseClock *pc = nullptr) {
   if constexpr (RM == RM_385 && SKIP0) {
     lane_stages_385<RW, LW>(c, a, -1.0, pc, 9);
+    return;
+  }
+  if constexpr (RM == RM_77 && !SKIP0) {
+    lane_stages_77<RW, LW, 0, 1>(c, a, -1.0);
     return;
   }
   if (rm_pfa<RM>(a)) {
@@ -689,7 +711,8 @@ SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   const double ia = a.inv_acos[p];
   PhaseClock pc;
   lane_prefetch_eo(a, c, 7);
-  constexpr int N2C = RM == RM_385 ? 385 : 0, MC = RM == RM_385 ? 256 : 0;
+  constexpr int N2C = RM == RM_385 ? 385 : RM == RM_77 ? 77 : 0;
+  constexpr int MC = RM == RM_385 ? 256 : RM == RM_77 ? 51 : 0;
   lane_load_eo<LW, CG, N2C, MC>(a, c, 7, 5);
   __syncthreads();
   SWE_PHASE(pc, 0);
@@ -725,7 +748,7 @@ SWE_DEV void lane_nonlinear_to(const FftArgs &a, const LCtx &c, Store store) {
   __syncthreads();
   // only the 4 product fields x 2 hemispheres (S = 1)
   lane_fft<8 * lane_slices(FOP_NONLINEAR, LW), LW, GEN, RM>(a, c);
-  lane_extract_to<LW>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
+  lane_extract_to<LW, Store, N2C, MC>(a, c, c.X, c.X, 4, w, wv, c.tid, c.nthr, store);
 }
 
 template <int LW, bool GEN, int CG, int RM = 0>
