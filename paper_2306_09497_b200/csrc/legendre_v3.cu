@@ -643,6 +643,15 @@ __global__ void __launch_bounds__(V3_NT, 1) leg_anal_v3(const __grid_constant__ 
       const int tt = x.tile + (2 * i + wrq) * 8 + gr;
       if (tt >= nt) continue;
       const size_t k = (size_t)off + (wpar ? ne : 0) + tt;
+      double *row = o.dst + k * ld + x.c0;
+      if (il && x.c0 + V3_BN <= ld) {  // the usual case: immediate offsets, no column test
+        double *r0 = row + 2 * (wch * 32 + 2 * t);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<double2 *>(r0 + 2 * ((j >> 1) * 8 + (j & 1))) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+        continue;
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int col = il ? x.c0 + 2 * (wch * 32 + (j >> 1) * 8 + (j & 1) + 2 * t)
