@@ -107,19 +107,6 @@ int swe_imex_step(swe_plan *plan, double *state, const double *phibar, int batch
                   const swe_stepper_cfg *cfg, int nsteps, int *iters_out, double *resid_out,
                   void *stream);
 
-/* swe_imex_step without the per-call host check (graph replay path): enqueues
- * the layout conversion, nsteps step-graph launches and the result on `stream` and
- * returns at once, so back-to-back calls keep the device busy (the pipelined
- * host-batch API, steppers.HostPipeline).  An unconverged Coriolis solve raises a
- * per-plan device flag instead of returning SWE_ENOCONV; while it is up, queued
- * calls leave their state untouched.  Read (and optionally reset) it with
- * swe_plan_status.  Configurations without a step graph run swe_imex_step. */
-int swe_imex_step_async(swe_plan *plan, double *state, const double *phibar, int batch,
-                        const swe_stepper_cfg *cfg, int nsteps, void *stream);
-/* Synchronizes `stream` and returns in *failed whether any swe_imex_step_async call
- * since the last reset hit an unconverged solve; reset != 0 clears the flag. */
-int swe_plan_status(swe_plan *plan, int *failed, int reset, void *stream);
-
 /* truncate_pad (spharm.py:352-368) of `nfields` packed arrays between plans
  * (PrognosticState.to_truncation, dynamics.py:73-83). */
 int swe_truncate_pad(const swe_plan *src, const swe_plan *dst, const double *in, double *out,
@@ -135,10 +122,6 @@ int swe_state_stats(const swe_plan *plan, const double *state, int batch, double
  * (nullable; g[0] unused); one CUDA-graph step per point and one host check. */
 int swe_imex_sweep(swe_plan *plan, double *u, const double *g, int n, const double *phibar,
                    const swe_stepper_cfg *cfg, double *resid_out, void *stream);
-/* swe_imex_sweep without the final host check (like swe_imex_step_async: an
- * unconverged solve raises the plan's flag, read by swe_plan_status). */
-int swe_imex_sweep_async(swe_plan *plan, double *u, const double *g, int n, const double *phibar,
-                         const swe_stepper_cfg *cfg, void *stream);
 /* One SL-SI-SETTLS step (steppers.py:171-212) of every slice: state [batch][3][K]
  * advanced in place; prev [batch][3][K] is U_{n-1} (pass `state` itself for the
  * one-step variant or a cold start); the implicit solve always includes the

@@ -22,8 +22,7 @@ EXPORTS = (
     "swe_kernel_launches", "swe_last_error", "swe_profile", "swe_profile_read",
     "swe_set_option", "swe_ke_spectrum", "swe_window_maxdiff", "swe_grid_sqdiff",
     "swe_settls_step", "swe_departure_points", "swe_interpolate", "swe_imex_sweep",
-    "swe_stepper_cfg_size", "swe_synthesis_pair", "swe_grad_grid", "swe_imex_step_async",
-    "swe_plan_status", "swe_imex_sweep_async",
+    "swe_stepper_cfg_size", "swe_synthesis_pair", "swe_grad_grid",
 )
 
 
@@ -88,9 +87,6 @@ def load(path: str = LIB_PATH):
         "swe_stepper_cfg_size": (I, []),
         "swe_synthesis_pair": (I, [P, P, P, P, I, P]),
         "swe_grad_grid": (I, [P, P, P, P, I, P]),
-        "swe_imex_step_async": (I, [P, P, P, I, ctypes.POINTER(StepperCfgC), I, P]),
-        "swe_plan_status": (I, [P, ctypes.POINTER(I), I, P]),
-        "swe_imex_sweep_async": (I, [P, P, P, I, P, ctypes.POINTER(StepperCfgC), P]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

@@ -41,10 +41,7 @@ struct Work {
   double *sweep_g = nullptr;            // serial-sweep forcing, internal layout 3 x [K][2 scap]
   int scap = 0;
   int gcap = 0;
-  int *h_fail = nullptr, *d_fail = nullptr;
-  // an asynchronous call (swe_imex_step_async / swe_imex_sweep_async) may have raised
-  // d_fail since the last swe_plan_status reset: synchronous calls then keep it up
-  int async_pending = 0;  // graph mode: unconverged-solve flag (device) and its host copy
+  int *h_fail = nullptr, *d_fail = nullptr;  // graph mode: unconverged-solve flag (device) and its host copy
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
 };

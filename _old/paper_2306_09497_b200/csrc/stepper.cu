@@ -1374,9 +1374,7 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
     // one graph launch per step, one host check per call; an unconverged solve
     // (flagged on device) reruns the call on the host-driven path from the caller's
     // input so the error and residual are reported exactly as steppers.py does
-    // (a pending failure of an asynchronous call stays up for swe_plan_status; if it
-    // is up this call reruns on the host path below, which is then exact)
-    if (!pl->ws.async_pending) SWE_CUDA(cudaMemsetAsync(pl->ws.d_fail, 0, sizeof(int), r.st));
+    SWE_CUDA(cudaMemsetAsync(pl->ws.d_fail, 0, sizeof(int), r.st));
     for (int s = 0; s < nsteps; ++s) SWE_CUDA(cudaGraphLaunch(exec, r.st));
     // the result goes out before the host check (no idle gap between the graph and
     // the layout kernel) unless the device flag is up: then `state` still holds the
@@ -1399,59 +1397,8 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
   return to_boundary(s, state, batch, 3, pl->K, pl->perm, r.st);
 }
 
-int swe_imex_step_async(swe_plan *pl, double *state, const double *phibar, int batch,
-                        const swe_stepper_cfg *cfg, int nsteps, void *stream) {
-  int rc;
-  if ((rc = check_cfg(cfg))) return rc;
-  if (!phibar) {
-    set_error("phibar is NULL");
-    return E_SHAPE;
-  }
-  if ((rc = prepare(pl, batch, phibar, (cudaStream_t)stream))) return rc;
-  Run r = make_run(pl, batch, stream);
-  r.Bsel = cfg->select_batch > 0 ? cfg->select_batch : r.B;
-  cudaGraphExec_t exec = nullptr;
-  if (g_graphs && !g_prof && nsteps > 0 && (rc = step_graph(r, *cfg, &exec))) return rc;
-  const Bufs b = bufs(r);
-  SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
-  if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st))) return rc;
-  if (!exec) {
-    // no step graph yet (first sight of the configuration: step_graph captures at the
-    // second, after this eager run has set the plan's fixed-point iteration guess)
-    for (int s = 0; s < nsteps; ++s)
-      if ((rc = imex_internal(r, *cfg, nullptr, nullptr))) return rc;
-    SpecPtrsC so = {{b.U[0], b.U[1], b.U[2]}};
-    return to_boundary(so, state, batch, 3, pl->K, pl->perm, r.st);
-  }
-  for (int s = 0; s < nsteps; ++s) SWE_CUDA(cudaGraphLaunch(exec, r.st));
-  // the flag stays up once any queued step failed (no per-call reset): this and every
-  // later queued call leave their state untouched until swe_plan_status resets it
-  pl->ws.async_pending = 1;
-  SpecPtrsC so = {{b.U[0], b.U[1], b.U[2]}};
-  return to_boundary(so, state, batch, 3, pl->K, pl->perm, r.st, pl->ws.d_fail);
-}
-
-int swe_plan_status(swe_plan *pl, int *failed, int reset, void *stream) {
-  if (!pl || !failed) {
-    set_error("swe_plan_status: null argument");
-    return E_SHAPE;
-  }
-  const cudaStream_t st = (cudaStream_t)stream;
-  SWE_CUDA(cudaMemcpyAsync(pl->ws.h_fail, pl->ws.d_fail, sizeof(int), cudaMemcpyDeviceToHost, st));
-  SWE_CUDA(cudaStreamSynchronize(st));
-  *failed = *pl->ws.h_fail;
-  if (reset) {
-    SWE_CUDA(cudaMemsetAsync(pl->ws.d_fail, 0, sizeof(int), st));
-    pl->ws.async_pending = 0;
-  }
-  return OK;
-}
-
-namespace swe {
-namespace {
-// deferred: graph replays queued without the final host check (swe_imex_sweep_async)
-int imex_sweep_impl(swe_plan *pl, double *u, const double *g, int n, const double *phibar,
-                    const swe_stepper_cfg *cfg, double *resid_out, void *stream, bool deferred) {
+int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double *phibar,
+                   const swe_stepper_cfg *cfg, double *resid_out, void *stream) {
   int rc;
   if ((rc = check_cfg(cfg))) return rc;
   if (!u || !phibar || n < 0) {
@@ -1479,27 +1426,24 @@ int imex_sweep_impl(swe_plan *pl, double *u, const double *g, int n, const doubl
   }
   const size_t stride = (size_t)3 * K * 2;  // doubles per state
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
+  SpecPtrsC sc = {{b.U[0], b.U[1], b.U[2]}};
   Ptr3 U = {{b.U[0], b.U[1], b.U[2]}};
   cudaGraphExec_t exec = nullptr;
   if (g_graphs && !g_prof && (rc = step_graph(r, *cfg, &exec))) return rc;
   for (int pass = 0; pass < 2; ++pass) {
     const bool graph = pass == 0 && exec;
     if ((rc = to_internal(u, d, 1, 3, K, pl->perm, r.st))) return rc;
-    if (graph && !deferred && !w.async_pending)
-      SWE_CUDA(cudaMemsetAsync(w.d_fail, 0, sizeof(int), r.st));
+    if (graph) SWE_CUDA(cudaMemsetAsync(w.d_fail, 0, sizeof(int), r.st));
     for (int j = 1; j <= n; ++j) {
       if (graph) {
         SWE_CUDA(cudaGraphLaunch(exec, r.st));
       } else if ((rc = imex_internal(r, *cfg, nullptr, resid_out))) {
         return rc;
       }
-      if ((rc = sweep_point(K, n, j - 1, U, G, u + (size_t)j * stride, pl->perm, r.st))) return rc;
+      if (g && (rc = add_col(K, n, j - 1, U, G, r.st))) return rc;
+      if ((rc = to_boundary(sc, u + (size_t)j * stride, 1, 3, K, pl->perm, r.st))) return rc;
     }
     if (!graph) return OK;
-    if (deferred) {  // the flag is read by swe_plan_status
-      w.async_pending = 1;
-      return OK;
-    }
     SWE_CUDA(cudaMemcpyAsync(w.h_fail, w.d_fail, sizeof(int), cudaMemcpyDeviceToHost, r.st));
     SWE_CUDA(cudaStreamSynchronize(r.st));
     if (!*w.h_fail) return OK;
@@ -1507,18 +1451,6 @@ int imex_sweep_impl(swe_plan *pl, double *u, const double *g, int n, const doubl
     // which raises at the failing step with the residual like steppers.py
   }
   return OK;
-}
-}  // namespace
-}  // namespace swe
-
-int swe_imex_sweep(swe_plan *pl, double *u, const double *g, int n, const double *phibar,
-                   const swe_stepper_cfg *cfg, double *resid_out, void *stream) {
-  return imex_sweep_impl(pl, u, g, n, phibar, cfg, resid_out, stream, false);
-}
-
-int swe_imex_sweep_async(swe_plan *pl, double *u, const double *g, int n, const double *phibar,
-                         const swe_stepper_cfg *cfg, void *stream) {
-  return imex_sweep_impl(pl, u, g, n, phibar, cfg, nullptr, stream, true);
 }
 
 int swe_settls_step(swe_plan *pl, double *state, const double *prev, const double *phibar,
@@ -1629,7 +1561,7 @@ int swe_set_option(const char *key, int value) {
     g_f_il = value;
     return OK;
   }
-  if (key && strcmp(key, "fft_rm") == 0 && value >= 0 && value <= 2) {
+  if (key && strcmp(key, "fft_rm") == 0 && (value == 0 || value == 1)) {
     g_fft_rm = value;
     return OK;
   }

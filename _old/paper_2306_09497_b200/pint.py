@@ -312,22 +312,9 @@ class MgritEngine:
         kw = {}
         if getattr(self.problem, "supports_select_batch", False):
             kw["select_batch"] = x.shape[0] * self.G if sharded else 0
-        kw.update(self._deferred_kw())
         if prev is None:
             return self.problem.step_batch(level, x, **kw)
         return self.problem.step_batch(level, x, prev, **kw)
-
-    def _deferred_kw(self):
-        """Steps and sweeps queued without a host round trip where the problem
-        supports it; their errors are raised once per cycle (_check_deferred)."""
-        return {"deferred": True} if getattr(self.problem, "supports_deferred_check", False) else {}
-
-    def _check_deferred(self):
-        """Raise the problem's deferred step errors (ImplicitSolveError of a step
-        queued without a host round trip) before the iteration's results are used."""
-        f = getattr(self.problem, "check_deferred", None)
-        if f is not None:
-            f()
 
     def _exchange_halo(self, level, u):
         if self.G == 1:
@@ -420,7 +407,7 @@ class MgritEngine:
         modes = settls_boundary_policy(self.L, lv, n, self.m, self.cfg.chunk_size)
         track = self._tracks(lv)
         sweep = getattr(self.problem, "sweep_batch", None)
-        if sweep is not None and sweep(lv, u, g, **self._deferred_kw()):  # chain on the device
+        if sweep is not None and sweep(lv, u, g):   # whole chain on the device
             return
         prev = None
         for j in range(1, n + 1):
@@ -462,7 +449,7 @@ class MgritEngine:
         v[0:1] = pr.restrict_batch(0, u0)
         track = self._tracks(1) and self.L == 2
         sweep = getattr(pr, "sweep_batch", None)
-        if not track and sweep is not None and sweep(1, v, None, **self._deferred_kw()):
+        if not track and sweep is not None and sweep(1, v, None):
             # the whole serial run on the device (swe_imex_sweep: one step graph per
             # point, one host check), bitwise the per-step loop below
             return pr.prolong_batch(1, v)
@@ -501,7 +488,6 @@ class MgritEngine:
             if len(initial_cpoints) != n1 + 1:
                 raise ValueError("initial_cpoints must cover every C-point")
             guess = initial_cpoints.clone()
-        self._check_deferred()
         sync()
         trace = IterationTrace(times=times, snapshots=[SnapshotList(self.problem, guess)],
                                wall_times=[time.perf_counter() - t0], config=cfg,
@@ -532,13 +518,11 @@ class MgritEngine:
             if clock is not None:
                 clock.start()
                 self._cycle(0, u, None, cfg.cycle)
-                self._check_deferred()
                 trace.wall_times.append(clock.stop())
             else:
                 sync()
                 t0 = time.perf_counter()
                 self._cycle(0, u, None, cfg.cycle)
-                self._check_deferred()
                 sync()
                 trace.wall_times.append(time.perf_counter() - t0)
             trace.fine_steps.append(self.fine_steps - f0)
@@ -607,7 +591,6 @@ class SweProblem:
                            for lv, spec in enumerate(config.levels)]
         self.phibar = phibar
         self.step_calls = 0
-        self._pending = set()  # levels with deferred (unchecked) steps
 
     # -- batched protocol --------------------------------------------------------
     def _pb(self, n, dev):
@@ -632,41 +615,25 @@ class SweProblem:
         return torch.zeros((n, 3, g.n_modes), dtype=torch.complex128, device=f"cuda:{g.device}")
 
     supports_select_batch = True
-    supports_deferred_check = True
 
-    def check_deferred(self):
-        """ImplicitSolveError if a deferred step (step_batch(..., deferred=True))
-        did not converge (steppers.py:113-118)."""
-        from .steppers import check_async_steps
-        pending, self._pending = self._pending, set()
-        for level in sorted(pending):
-            check_async_steps(self.grids[level])
-
-    def step_batch(self, level, x, prev=None, select_batch=0, deferred=False):
+    def step_batch(self, level, x, prev=None, select_batch=0):
         """One step of every point of x; prev (SETTLS two-step history, same shape)
         or None.  For SETTLS a point's own value as its prev means no history.
-        select_batch: kernel-selection batch (steppers module docstring).
-        deferred: queue an IMEX step without a host round trip; an unconverged
-        solve is raised by check_deferred (the engine calls it once per cycle)."""
-        from .steppers import IMEX, imex_steps_async, imex_steps_inplace, settls_step_inplace
+        select_batch: kernel-selection batch (steppers module docstring)."""
+        from .steppers import IMEX, imex_steps_inplace, settls_step_inplace
         st = self.wrap(level, x.clone())
         self.step_calls += x.shape[0]
         cfg = self.level_cfgs[level]
-        if cfg.scheme == IMEX and deferred:
-            imex_steps_async(st, cfg, 1, select_batch=select_batch)
-            self._pending.add(level)
-        elif cfg.scheme == IMEX:
+        if cfg.scheme == IMEX:
             imex_steps_inplace(st, cfg, 1, select_batch=select_batch)
         else:
             settls_step_inplace(st, cfg, None if prev is None else self.wrap(level, prev),
                                 select_batch=select_batch)
         return st.data
 
-    def sweep_batch(self, level, u, g, deferred=False) -> bool:
+    def sweep_batch(self, level, u, g) -> bool:
         """u[j] = step(u[j-1]) + g[j], j = 1..n, in place on the device
-        (swe_imex_sweep); False when the level is not a plain IMEX level.
-        deferred: no host check at the end (swe_imex_sweep_async); an unconverged
-        solve is raised by check_deferred."""
+        (swe_imex_sweep); False when the level is not a plain IMEX level."""
         import ctypes
         from .spharm import _ptr, _stream
         from .steppers import IMEX, ImplicitSolveError
@@ -679,14 +646,9 @@ class SweProblem:
         pb = self._pb(1, u.device)
         c = cfg.to_c()
         resid = np.zeros(1)
-        if deferred:
-            rc = grid._lib.swe_imex_sweep_async(grid.plan, _ptr(u), None if g is None else _ptr(g),
-                                                n, _ptr(pb), ctypes.byref(c), _stream())
-            self._pending.add(level)
-        else:
-            rc = grid._lib.swe_imex_sweep(grid.plan, _ptr(u), None if g is None else _ptr(g), n,
-                                          _ptr(pb), ctypes.byref(c),
-                                          resid.ctypes.data_as(ctypes.c_void_p), _stream())
+        rc = grid._lib.swe_imex_sweep(grid.plan, _ptr(u), None if g is None else _ptr(g), n,
+                                      _ptr(pb), ctypes.byref(c),
+                                      resid.ctypes.data_as(ctypes.c_void_p), _stream())
         try:
             _lib_check(rc, "swe_imex_sweep")
         except _NoConv as exc:
