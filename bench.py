@@ -761,6 +761,9 @@ def launch_ranks(args):
 
 
 def main():
+    if os.environ.get("SWE_LIB"):  # A/B of another build of the library (tools only)
+        from paper_2306_09497_b200 import _lib as _l
+        _l.load.__defaults__ = (os.path.abspath(os.environ["SWE_LIB"]),)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

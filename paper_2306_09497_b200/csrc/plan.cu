@@ -450,6 +450,7 @@ void work_free(Work &w) {
   cudaFree(w.sweep_g);
   cudaFreeHost(w.h_fail);
   cudaFree(w.d_fail);
+  cudaFree(w.gguess);
   cudaFree(w.phi0);
   cudaFree(w.phibar);
   w = Work();
@@ -524,6 +525,11 @@ int work_reserve(swe_plan *pl, int B) {
   SWE_CUDA(cudaMallocHost(&w.h_fail, sizeof(int)));
   SWE_CUDA(cudaMalloc(&w.d_fail, sizeof(int)));
   SWE_CUDA(cudaMemset(w.d_fail, 0, sizeof(int)));  // swe_imex_step_async accumulates into it
+  SWE_CUDA(cudaMalloc(&w.gguess, sizeof(int)));
+  {
+    const int one = 1;
+    SWE_CUDA(cudaMemcpy(w.gguess, &one, sizeof(int), cudaMemcpyHostToDevice));
+  }
   SWE_CUDA(cudaMalloc(&w.sched, 2 * sizeof(unsigned long long)));
   SWE_CUDA(cudaMemset(w.sched, 0, 2 * sizeof(unsigned long long)));
   SWE_CUDA(cudaMalloc(&w.phi0, (size_t)B * sizeof(double)));

@@ -44,7 +44,10 @@ struct Work {
   int *h_fail = nullptr, *d_fail = nullptr;
   // an asynchronous call (swe_imex_step_async / swe_imex_sweep_async) may have raised
   // d_fail since the last swe_plan_status reset: synchronous calls then keep it up
-  int async_pending = 0;  // graph mode: unconverged-solve flag (device) and its host copy
+  int async_pending = 0;
+  // graph replays: the fused fixed point's iteration guess on the device (k_cn_decide
+  // updates it, so a replayed graph adapts to the states as the host path does)
+  int *gguess = nullptr;  // graph mode: unconverged-solve flag (device) and its host copy
   double *phi0 = nullptr;   // [cap] phibar*sqrt(2)*P_00: synthesis of the phi_prime shift
   double *phibar = nullptr; // [cap]
 };

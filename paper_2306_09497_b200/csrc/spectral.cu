@@ -1125,7 +1125,9 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
                const double *__restrict__ eps, const double *__restrict__ phibar, Ptr3C x0,
                Ptr3C x1, Ptr3C x2, double s, double alpha, Ptr3 R, int write_r, double *U0,
                double *A1, double *A2, double *B1, double *B2, const int *__restrict__ target,
-               int G, unsigned long long *__restrict__ fst, double dtnu, double halfq) {
+               int G, unsigned long long *__restrict__ fst, double dtnu, double halfq,
+               const int *__restrict__ Gp) {
+  if (Gp) G = max(1, min(*Gp, G));  // device-resident guess (graph replays), capped
   extern __shared__ double2 fsm[];
   const int M = MC ? MC : M_;
   const int m1 = blockIdx.y, m2 = M - m1;  // slice groups fastest: CTAs in flight cover whole rows
@@ -1375,7 +1377,7 @@ int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *
              const double *phibar, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              Ptr3 R, int write_r, double *U0, double *A1, double *A2, double *B1, double *B2,
              const int *target, int G, unsigned long long *fst, double dtnu, double halfq,
-             cudaStream_t st) {
+             cudaStream_t st, const int *Gp) {
   const int nrow = M + 2, n = nrow * CF_S;
   const int NT = std::min(CF_NTMAX, ((n + CF_EPT - 1) / CF_EPT + 31) / 32 * 32);
   const int smem = 6 * n * (int)sizeof(double2) + nrow * (int)(sizeof(double4) + 2 * sizeof(double));
@@ -1389,7 +1391,7 @@ int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *
     }
     k_cn_fused<256><<<grid, NT, smem, st>>>(M, B, offsets, cf, eps, phibar, x0, x1, x2, s, alpha, R,
                                             write_r, U0, A1, A2, B1, B2, target, G, fst, dtnu,
-                                            halfq);
+                                            halfq, Gp);
   } else {
     static int attr = 0;
     if (smem > attr) {
@@ -1397,7 +1399,8 @@ int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *
       attr = smem;
     }
     k_cn_fused<0><<<grid, NT, smem, st>>>(M, B, offsets, cf, eps, phibar, x0, x1, x2, s, alpha, R,
-                                          write_r, U0, A1, A2, B1, B2, target, G, fst, dtnu, halfq);
+                                          write_r, U0, A1, A2, B1, B2, target, G, fst, dtnu, halfq,
+                                          Gp);
   }
   SWE_LAUNCH_CHECK();
   return OK;
@@ -1423,11 +1426,13 @@ SWE_DEV bool cf_converged(const unsigned long long *q6, double tol) {
 }
 __global__ void k_cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters,
                             int *target2, int *counter, int *loop, double tol,
-                            cudaGraphConditionalHandle h, int has_h, int max_iter) {
-  __shared__ int cnt;
-  if (threadIdx.x == 0) cnt = 0;
+                            cudaGraphConditionalHandle h, int has_h, int max_iter, int *Gp) {
+  __shared__ int cnt, kmx;
+  const int Gcap = G;
+  if (Gp) G = max(1, min(*Gp, G));  // the guess the first fused pass ran with
+  if (threadIdx.x == 0) cnt = kmx = 0;
   __syncthreads();
-  int mine = 0;
+  int mine = 0, kmine = 0;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     unsigned long long *q = fst + (size_t)b * CF_KS * 6;
     int ks = 0;
@@ -1435,6 +1440,7 @@ __global__ void k_cn_decide(int B, int G, unsigned long long *fst, int *flags, i
       if (cf_converged(q + (k - 1) * 6, tol)) ks = k;
     for (int k = 0; k < G * 6; ++k) q[k] = 0ULL;
     if (ks) {
+      kmine = max(kmine, ks);
       flags[b] = 0;
       iters[b] = ks;
       target2[b] = ks < G ? ks : 0;  // recompute the final result at k*
@@ -1446,19 +1452,23 @@ __global__ void k_cn_decide(int B, int G, unsigned long long *fst, int *flags, i
     }
   }
   if (mine) atomicAdd(&cnt, mine);
+  if (kmine) atomicMax(&kmx, kmine);
   __syncthreads();
   if (threadIdx.x == 0) {
     *counter = cnt;
     *loop = G;
+    // next solve's guess: the largest first-converged iteration, or one more than
+    // this guess while slices still continue past it (as the host path's iter_guess)
+    if (Gp) *Gp = cnt ? min(Gcap, G + 1) : max(1, kmx);
     if (has_h) cudaGraphSetConditional(h, (cnt > 0 && G < max_iter) ? 1u : 0u);
   }
 }
 
 int cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters, int *target2,
               int *counter, int *loop, double tol, const cudaGraphConditionalHandle *h,
-              int max_iter, cudaStream_t st) {
+              int max_iter, cudaStream_t st, int *Gp) {
   k_cn_decide<<<1, 1024, 0, st>>>(B, G, fst, flags, iters, target2, counter, loop, tol,
-                                  h ? *h : cudaGraphConditionalHandle(0), h != nullptr, max_iter);
+                                  h ? *h : cudaGraphConditionalHandle(0), h != nullptr, max_iter, Gp);
   SWE_LAUNCH_CHECK();
   return OK;
 }

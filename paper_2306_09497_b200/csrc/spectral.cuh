@@ -88,10 +88,12 @@ int cn_fused(int M, int B, const int *offsets, const double4 *cf, const double *
              const double *phibar, Ptr3C x0, Ptr3C x1, Ptr3C x2, double s, double alpha,
              Ptr3 R, int write_r, double *U0, double *A1, double *A2, double *B1, double *B2,
              const int *target, int G, unsigned long long *fst, double dtnu, double halfq,
-             cudaStream_t st);
+             cudaStream_t st, const int *Gp = nullptr);
+// Gp (graph replays): device-resident iteration guess, read by the first fused pass
+// and k_cn_decide (capped at G) and updated by k_cn_decide for the next solve
 int cn_decide(int B, int G, unsigned long long *fst, int *flags, int *iters, int *target2,
               int *counter, int *loop, double tol, const cudaGraphConditionalHandle *h,
-              int max_iter, cudaStream_t st);
+              int max_iter, cudaStream_t st, int *Gp = nullptr);
 // serial-sweep point (B = 1): y += g[:, col] if g.p[0], then y -> dst (boundary layout)
 int sweep_point(int K, int n, int col, Ptr3 y, Ptr3C g, double *dst, const int *perm,
                 cudaStream_t st);

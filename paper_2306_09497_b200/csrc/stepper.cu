@@ -703,11 +703,16 @@ int cn_half_spec(const Run &r, const swe_stepper_cfg &cfg, const Bufs &b,
     Ptr3 R = {{b.R[0], b.R[1], b.R[2]}};
     int rc2;
     ProfScope ps(3, ((x1 ? 9.0 : 3.0) + 3.0) * 16.0 * K * B, r.st);
+    // graph replays read the guess from the device (capped at Gcap), the host path
+    // passes the plan's iter_guess
+    const int Gcap = r.graph ? std::min(cfg.implicit_max_iter, cn_fused_kmax()) : G;
     if ((rc2 = cn_fused(pl->M, B, pl->offsets, pl->cor_cf, pl->eps, w.phibar, X0, X1,
-                        X2, s, alpha, R, 0, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], nullptr, G,
-                        w.fstats, dtnu, cfg.visc_order / 2.0, r.st)) ||
-        (rc2 = cn_decide(B, G, w.fstats, w.flags, w.iters, w.target2, w.counter, w.loop,
-                         cfg.implicit_tol, h, cfg.implicit_max_iter, r.st)) ||
+                        X2, s, alpha, R, 0, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], nullptr,
+                        Gcap, w.fstats, dtnu, cfg.visc_order / 2.0, r.st,
+                        r.graph ? w.gguess : nullptr)) ||
+        (rc2 = cn_decide(B, Gcap, w.fstats, w.flags, w.iters, w.target2, w.counter, w.loop,
+                         cfg.implicit_tol, h, cfg.implicit_max_iter, r.st,
+                         r.graph ? w.gguess : nullptr)) ||
         (rc2 = cn_fused(pl->M, B, pl->offsets, pl->cor_cf, pl->eps, w.phibar, X0, X1,
                         X2, s, alpha, R, 1, dst[0], dst[1], dst[2], b.LC[0], b.LC[1], w.target2,
                         G, nullptr, dtnu, cfg.visc_order / 2.0, r.st)))
@@ -1058,6 +1063,8 @@ int step_graph(const Run &r, const swe_stepper_cfg &cfg, cudaGraphExec_t *exec) 
         rr.st = pl->cap[0];
         rr.st2 = pl->cap[1];
         rr.graph = true;
+        // seed the device-resident fixed-point guess with the host path's
+        SWE_CUDA(cudaMemcpy(pl->ws.gguess, &pl->iter_guess, sizeof(int), cudaMemcpyHostToDevice));
         g_capturing = true;
         cudaError_t e = cudaStreamBeginCapture(rr.st, cudaStreamCaptureModeRelaxed);
         int rc = e == cudaSuccess ? imex_internal(rr, cfg, nullptr, nullptr) : E_CUDA;
