@@ -444,7 +444,8 @@ def fine_cfg5(torch, slices=64, steps=5):
     g = spharm.get_grid(1024)
     s = scenarios.gaussian_bumps(g, batch=slices)
     cfg = steppers.StepperConfig(dt=2.0, viscosity=dynamics.ViscositySpec(2, 0.0))
-    steppers.imex_steps_inplace(s, cfg, 2)
+    for _ in range(2):  # the second call captures the step graph (outside the timing)
+        steppers.imex_steps_inplace(s, cfg, 1)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
