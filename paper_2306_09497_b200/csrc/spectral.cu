@@ -1117,6 +1117,12 @@ SWE_DEV void cf_nbrs(int r, int base, int km, int &lo, int &hi) {
     hi = li - ne + 1 < ne ? base + li - ne + 1 : -1;
   }
 }
+SWE_DEV bool cf_unpack(double w, int &lo, int &hi) {
+  const long long p = __double_as_longlong(w);
+  lo = (int)((p >> 20) & 0xfffff) - 1;
+  hi = (int)(p & 0xfffff) - 1;
+  return (p >> 40) != 0;
+}
 // MC > 0: the truncation is known at compile time (M = 256, the fine level): the
 // shared-memory array strides and the thread count become constants
 template <int MC>
@@ -1163,7 +1169,14 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
   auto grow = [&](int r) { return r < km1 ? off1 + r : off2 + r - km1; };
   for (int r = tid; r < nrow; r += NT) {
     const int k = grow(r);
-    rcf[r] = cft[k];
+    // the shared copy's .w (the m = 0 flag) also carries the row's stencil
+    // neighbours (no per-element neighbour registers across the iterations)
+    double4 c = cft[k];
+    int l, h;
+    if (r < km1) cf_nbrs(r, 0, km1, l, h);
+    else cf_nbrs(r, km1, km2, l, h);
+    c.w = __longlong_as_double(((long long)(c.w != 0.0) << 40) | ((long long)(l + 1) << 20) | (h + 1));
+    rcf[r] = c;
     re[r] = eps[k];
     rbh[r] = dtnu != 0.0 ? 1.0 / (1.0 + dtnu * pow(eps[k], halfq)) : 1.0;  // as k_cn_finish
   }
@@ -1174,9 +1187,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
   const bool act = mytgt != 0, fin = mytgt > 0;
   const int kout = abs(mytgt);
   const double pb = act ? phibar[b] : 0.0, apb = alpha * pb, aap = alpha * alpha * pb;
-  int lo[CF_EPT], hi[CF_EPT];
   double2 pv[CF_EPT], q0[CF_EPT];
-  double rden[CF_EPT];  // 1 / (1 + a^2 Pb eps) of each element: divisions as ddiv_r
   // ---- prologue (as k_cn_start): X staged in the B copies.  The xi/delta inputs go
   // global -> shared by cp.async (no registers, all loads of a thread in flight):
   // a single input straight into XB/DB; with the Heun terms x0 -> XA/DA, x1 ->
@@ -1185,10 +1196,7 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
 #pragma unroll
   for (int j = 0; j < CF_EPT; ++j) {
     const int e = tid + j * NT, r = e / CF_S;
-    lo[j] = hi[j] = -1;
     if (e < n && act) {
-      if (r < km1) cf_nbrs(r, 0, km1, lo[j], hi[j]);
-      else cf_nbrs(r, km1, km2, lo[j], hi[j]);
       const size_t i = (size_t)grow(r) * B + b;
       if (heun) {
         cp_async16(&XA[e], x0.p[1] + 2 * i, true);
@@ -1236,20 +1244,22 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
       const double2 ph = pv[j], xi = XB[e], de = DB[e];
       const double e_ = re[r];
       const double4 cf = rcf[r];
+      int lo, hi;
+      const bool m0 = cf_unpack(cf.w, lo, hi);
       double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
-      if (lo[j] >= 0) {
-        xl = XB[lo[j] * CF_S + sl];
-        dl = DB[lo[j] * CF_S + sl];
+      if (lo >= 0) {
+        xl = XB[lo * CF_S + sl];
+        dl = DB[lo * CF_S + sl];
       }
-      if (hi[j] >= 0) {
-        xh = XB[hi[j] * CF_S + sl];
-        dh = DB[hi[j] * CF_S + sl];
+      if (hi >= 0) {
+        xh = XB[hi * CF_S + sl];
+        dh = DB[hi * CF_S + sl];
       }
       double2 lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * xi.y),
                                 -(cf.x * dl.y + cf.y * dh.y - cf.z * xi.x));
       double2 lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * de.y,
                                 cf.x * xl.y + cf.y * xh.y + cf.z * de.x);
-      if (cf.w != 0.0) {
+      if (m0) {
         lx.y = 0.0;
         lc.y = 0.0;
       }
@@ -1267,9 +1277,9 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
         st2(R.p[2], i, r2);
       }
       const double apb_ = alpha * pb, denom = 1.0 + alpha * alpha * pb * e_;
-      rden[j] = 1.0 / denom;
-      const double2 nph = make_double2(ddiv_r(r0.x - apb_ * r2.x, denom, rden[j]),
-                                       ddiv_r(r0.y - apb_ * r2.y, denom, rden[j]));
+      const double rdn = 1.0 / denom;  // divisions as ddiv_r
+      const double2 nph = make_double2(ddiv_r(r0.x - apb_ * r2.x, denom, rdn),
+                                       ddiv_r(r0.y - apb_ * r2.y, denom, rdn));
       const double ae = alpha * e_;
       pv[j] = nph;
       XA[e] = r1;
@@ -1291,28 +1301,31 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
         const double2 rp = q0[j], r1 = Q1[e], r2 = Q2[e], o0 = pv[j];
         const double e_ = re[r];
         const double4 cf = rcf[r];
+        int lo, hi;
+        const bool m0 = cf_unpack(cf.w, lo, hi);
         const double2 x = X[e], d = D[e];
         double2 xl = make_double2(0.0, 0.0), dl = xl, xh = xl, dh = xl;
-        if (lo[j] >= 0) {
-          xl = X[lo[j] * CF_S + sl];
-          dl = D[lo[j] * CF_S + sl];
+        if (lo >= 0) {
+          xl = X[lo * CF_S + sl];
+          dl = D[lo * CF_S + sl];
         }
-        if (hi[j] >= 0) {
-          xh = X[hi[j] * CF_S + sl];
-          dh = D[hi[j] * CF_S + sl];
+        if (hi >= 0) {
+          xh = X[hi * CF_S + sl];
+          dh = D[hi * CF_S + sl];
         }
         double2 lx = make_double2(-(cf.x * dl.x + cf.y * dh.x + cf.z * x.y),
                                   -(cf.x * dl.y + cf.y * dh.y - cf.z * x.x));
         double2 lc = make_double2(cf.x * xl.x + cf.y * xh.x - cf.z * d.y,
                                   cf.x * xl.y + cf.y * xh.y + cf.z * d.x);
-        if (cf.w != 0.0) {
+        if (m0) {
           lx.y = 0.0;
           lc.y = 0.0;
         }
         const double2 rx = add2(r1, sc2(alpha, lx)), rd = add2(r2, sc2(alpha, lc));
         const double denom = 1.0 + aap * e_;
-        const double2 ph = make_double2(ddiv_r(rp.x - apb * rd.x, denom, rden[j]),
-                                        ddiv_r(rp.y - apb * rd.y, denom, rden[j]));
+        const double rdn = 1.0 / denom;  // recomputed (fewer live registers): the prologue's bits
+        const double2 ph = make_double2(ddiv_r(rp.x - apb * rd.x, denom, rdn),
+                                        ddiv_r(rp.y - apb * rd.y, denom, rdn));
         const double ae = alpha * e_;
         const double2 de = make_double2(rd.x + ae * ph.x, rd.y + ae * ph.y);
         mx[0] = max(mx[0], sqmag_bits(ph.x, ph.y));
@@ -1344,17 +1357,24 @@ __global__ void __launch_bounds__(CF_NTMAX, 2)
       }
       asm volatile("" ::: "memory");  // one element's loads in flight at a time (registers)
     }
-    // per-slice maxima: lanes of one slice differ in bits 2..4 (shuffle reduction),
-    // then lane sl + 4 q adds maximum q of slice sl: one shared atomic per warp
+    // per-slice maxima: the 8 lanes of one slice differ in bits 2..4.  Reduce-scatter
+    // over those bits (each step keeps the half of the maxima selected by the lane
+    // bit and sends the other half: 4 + 2 + 1 exchanges instead of 6 x 3), then the
+    // lane holding maximum q of slice sl adds it: one shared atomic per warp
     if (fst && it <= CF_KS) {
+      const bool b2 = lane & 4, b3 = lane & 8, b4 = lane & 16;
+      unsigned long long a4[4], a2[2];
 #pragma unroll
-      for (int q = 0; q < 6; ++q)
+      for (int i = 0; i < 4; ++i) {
+        const unsigned long long h = i + 4 < 6 ? mx[i + 4] : 0ULL;
+        a4[i] = max(b2 ? h : mx[i], __shfl_xor_sync(0xffffffffu, b2 ? mx[i] : h, 4));
+      }
 #pragma unroll
-        for (int o = CF_S; o < 32; o <<= 1) mx[q] = max(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], o));
-      const int q = lane >> 2;
-      unsigned long long v = mx[0];
-#pragma unroll
-      for (int qq = 1; qq < 6; ++qq) v = q == qq ? mx[qq] : v;
+      for (int i = 0; i < 2; ++i)
+        a2[i] = max(b3 ? a4[i + 2] : a4[i], __shfl_xor_sync(0xffffffffu, b3 ? a4[i] : a4[i + 2], 8));
+      const unsigned long long v =
+          max(b4 ? a2[1] : a2[0], __shfl_xor_sync(0xffffffffu, b4 ? a2[0] : a2[1], 16));
+      const int q = (b2 ? 4 : 0) + (b3 ? 2 : 0) + (b4 ? 1 : 0);
       if (q < 6 && v) atomicMax(&sst[it - 1][lane & 3][q], v);
     }
     __syncthreads();
