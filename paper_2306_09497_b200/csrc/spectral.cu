@@ -1452,23 +1452,32 @@ __global__ void k_cn_decide(int B, int G, unsigned long long *fst, int *flags, i
   if (Gp) G = max(1, min(*Gp, G));  // the guess the first fused pass ran with
   if (threadIdx.x == 0) cnt = kmx = 0;
   __syncthreads();
+  // a 16-lane group per slice: lane k tests iteration k + 1 (independent loads instead of
+  // one thread's dependent chain over the iterations), the first converged one by ballot
+  static_assert(CF_KS == 16, "one half-warp lane per recorded iteration");
+  const int lane = threadIdx.x & 31, k = lane & 15, sh = lane & 16;
   int mine = 0, kmine = 0;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    unsigned long long *q = fst + (size_t)b * CF_KS * 6;
-    int ks = 0;
-    for (int k = 1; k <= G && !ks; ++k)
-      if (cf_converged(q + (k - 1) * 6, tol)) ks = k;
-    for (int k = 0; k < G * 6; ++k) q[k] = 0ULL;
-    if (ks) {
-      kmine = max(kmine, ks);
-      flags[b] = 0;
-      iters[b] = ks;
-      target2[b] = ks < G ? ks : 0;  // recompute the final result at k*
-    } else {
-      flags[b] = 1;
-      iters[b] = G;
-      target2[b] = -G;  // pass 1 stored a final result: recompute the raw iterate G
-      ++mine;
+  for (int b0 = 0; b0 < B; b0 += blockDim.x / 16) {  // (uniform trip count: ballots below)
+    const int b = b0 + threadIdx.x / 16;
+    const bool live = b < B;
+    unsigned long long *q = fst + (size_t)(live ? b : 0) * CF_KS * 6;
+    const bool conv = live && k < G && cf_converged(q + k * 6, tol);
+    const unsigned m = (__ballot_sync(0xffffffffu, conv) >> sh) & 0xffffu;
+    if (live && k < G)
+      for (int f = 0; f < 6; ++f) q[k * 6 + f] = 0ULL;
+    if (live && k == 0) {
+      const int ks = m ? __ffs(m) : 0;
+      if (ks) {
+        kmine = max(kmine, ks);
+        flags[b] = 0;
+        iters[b] = ks;
+        target2[b] = ks < G ? ks : 0;  // recompute the final result at k*
+      } else {
+        flags[b] = 1;
+        iters[b] = G;
+        target2[b] = -G;  // pass 1 stored a final result: recompute the raw iterate G
+        ++mine;
+      }
     }
   }
   if (mine) atomicAdd(&cnt, mine);
@@ -1500,6 +1509,11 @@ __global__ void k_cn_finish(int K, int B, Ptr3 u, const double *b1, const double
                             const int *iters, const double *nn1a2, double dtnu, double halfq,
                             const int *counter, int *fail, const int *skip) {
   if (fail && blockIdx.x == 0 && threadIdx.x == 0 && *counter > 0) *fail = 1;
+  if (skip) {  // the common case: k_cn_fused finished every slice, nothing to do
+    int todo = 0;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) todo |= skip[b] < 0;
+    if (!__syncthreads_or(todo)) return;
+  }
   FOR_KB(K, B) {
     const int k = (int)(_i / B), b = (int)(_i - (size_t)k * B);
     if (skip && skip[b] >= 0) continue;  // finished by k_cn_fused
