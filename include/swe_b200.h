@@ -116,6 +116,15 @@ int swe_imex_step(swe_plan *plan, double *state, const double *phibar, int batch
  * swe_plan_status.  Configurations without a step graph run swe_imex_step. */
 int swe_imex_step_async(swe_plan *plan, double *state, const double *phibar, int batch,
                         const swe_stepper_cfg *cfg, int nsteps, void *stream);
+/* swe_imex_step_async out of place on strided slices: slice b is read at
+ * in + 2 * b * in_stride doubles and its result written at out + 2 * b * out_stride
+ * (strides in complex elements, >= 3 K; every slice [3][K] contiguous).  The MGRIT
+ * sweeps (pint.py:223-263) step every m-th point of the level array into its
+ * neighbour: with this entry they need no gather / scatter copies.  `out` may
+ * equal `in`; otherwise the output slices must not overlap the input slices. */
+int swe_imex_step_async_io(swe_plan *plan, const double *in, long long in_stride, double *out,
+                           long long out_stride, const double *phibar, int batch,
+                           const swe_stepper_cfg *cfg, int nsteps, void *stream);
 /* Synchronizes `stream` and returns in *failed whether any swe_imex_step_async call
  * since the last reset hit an unconverged solve; reset != 0 clears the flag. */
 int swe_plan_status(swe_plan *plan, int *failed, int reset, void *stream);

@@ -23,7 +23,7 @@ EXPORTS = (
     "swe_set_option", "swe_ke_spectrum", "swe_window_maxdiff", "swe_grid_sqdiff",
     "swe_settls_step", "swe_departure_points", "swe_interpolate", "swe_imex_sweep",
     "swe_stepper_cfg_size", "swe_synthesis_pair", "swe_grad_grid", "swe_imex_step_async",
-    "swe_plan_status", "swe_imex_sweep_async",
+    "swe_imex_step_async_io", "swe_plan_status", "swe_imex_sweep_async",
 )
 
 
@@ -89,6 +89,8 @@ def load(path: str = LIB_PATH):
         "swe_synthesis_pair": (I, [P, P, P, P, I, P]),
         "swe_grad_grid": (I, [P, P, P, P, I, P]),
         "swe_imex_step_async": (I, [P, P, P, I, ctypes.POINTER(StepperCfgC), I, P]),
+        "swe_imex_step_async_io": (I, [P, P, ctypes.c_longlong, P, ctypes.c_longlong, P, I,
+                                       ctypes.POINTER(StepperCfgC), I, P]),
         "swe_plan_status": (I, [P, ctypes.POINTER(I), I, P]),
         "swe_imex_sweep_async": (I, [P, P, P, I, P, ctypes.POINTER(StepperCfgC), P]),
     }

@@ -17,13 +17,14 @@ namespace swe {
 
 // ---- layout: boundary [B][F][K] complex <-> internal F x [K][B] complex ------
 // perm[k] = internal row of the reference's packed index k (parity-split order)
+// ss: slice stride of the boundary array in complex elements (F * K when packed)
 __global__ void k_to_internal(const double2 *__restrict__ src, SpecPtrs dst, int B, int F, int K,
-                              const int *__restrict__ perm) {
+                              const int *__restrict__ perm, size_t ss) {
   __shared__ double2 tile[32][33];
   const int f = blockIdx.z, k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int b = b0 + r, k = k0 + threadIdx.x;
-    if (b < B && k < K) tile[r][threadIdx.x] = src[((size_t)b * F + f) * K + k];
+    if (b < B && k < K) tile[r][threadIdx.x] = src[(size_t)b * ss + (size_t)f * K + k];
   }
   __syncthreads();
   double2 *d = reinterpret_cast<double2 *>(dst.p[f]);
@@ -34,7 +35,7 @@ __global__ void k_to_internal(const double2 *__restrict__ src, SpecPtrs dst, int
 }
 
 __global__ void k_to_boundary(SpecPtrsC src, double2 *__restrict__ dst, int B, int F, int K,
-                              const int *__restrict__ perm, const int *__restrict__ skip) {
+                              const int *__restrict__ perm, const int *__restrict__ skip, size_t ss) {
   if (skip && *skip) return;
   __shared__ double2 tile[32][33];
   const int f = blockIdx.z, k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
@@ -46,22 +47,24 @@ __global__ void k_to_boundary(SpecPtrsC src, double2 *__restrict__ dst, int B, i
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int b = b0 + r, k = k0 + threadIdx.x;
-    if (b < B && k < K) dst[((size_t)b * F + f) * K + k] = tile[threadIdx.x][r];
+    if (b < B && k < K) dst[(size_t)b * ss + (size_t)f * K + k] = tile[threadIdx.x][r];
   }
 }
 
 int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, const int *perm,
-                cudaStream_t st) {
+                cudaStream_t st, size_t sstride) {
   dim3 grid((K + 31) / 32, (B + 31) / 32, F), blk(32, 8);
-  k_to_internal<<<grid, blk, 0, st>>>(reinterpret_cast<const double2 *>(src), dst, B, F, K, perm);
+  k_to_internal<<<grid, blk, 0, st>>>(reinterpret_cast<const double2 *>(src), dst, B, F, K, perm,
+                                      sstride ? sstride : (size_t)F * K);
   SWE_LAUNCH_CHECK();
   return OK;
 }
 
 int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, const int *perm,
-                cudaStream_t st, const int *skip) {
+                cudaStream_t st, const int *skip, size_t sstride) {
   dim3 grid((K + 31) / 32, (B + 31) / 32, F), blk(32, 8);
-  k_to_boundary<<<grid, blk, 0, st>>>(src, reinterpret_cast<double2 *>(dst), B, F, K, perm, skip);
+  k_to_boundary<<<grid, blk, 0, st>>>(src, reinterpret_cast<double2 *>(dst), B, F, K, perm, skip,
+                                      sstride ? sstride : (size_t)F * K);
   SWE_LAUNCH_CHECK();
   return OK;
 }

@@ -20,12 +20,13 @@ struct Ptr3C {
   const double *p[3];
 };
 
+// sstride: slice stride of the boundary array in complex elements (0: packed, F * K)
 int to_internal(const double *src, const SpecPtrs &dst, int B, int F, int K, const int *perm,
-                cudaStream_t st);
+                cudaStream_t st, size_t sstride = 0);
 // skip (nullable, device): the copy is skipped when *skip != 0 (an unconverged graph
 // step leaves the caller's input in place for the host-driven rerun)
 int to_boundary(const SpecPtrsC &src, double *dst, int B, int F, int K, const int *perm,
-                cudaStream_t st, const int *skip = nullptr);
+                cudaStream_t st, const int *skip = nullptr, size_t sstride = 0);
 int lin_rhs(int K, int B, const double *const U[3], const double *lcx, const double *lcd,
             double alpha, const double *eps, const double *phibar, double *const R[3],
             cudaStream_t st);

@@ -1406,8 +1406,11 @@ int swe_imex_step(swe_plan *pl, double *state, const double *phibar, int batch,
   return to_boundary(s, state, batch, 3, pl->K, pl->perm, r.st);
 }
 
-int swe_imex_step_async(swe_plan *pl, double *state, const double *phibar, int batch,
-                        const swe_stepper_cfg *cfg, int nsteps, void *stream) {
+// the queued step of swe_imex_step_async / swe_imex_step_async_io: slices read from
+// `in` (slice stride in_stride complex elements, 0 = packed) and written to `out`
+static int step_async_io(swe_plan *pl, const double *in, size_t in_stride, double *out,
+                         size_t out_stride, const double *phibar, int batch,
+                         const swe_stepper_cfg *cfg, int nsteps, void *stream) {
   int rc;
   if ((rc = check_cfg(cfg))) return rc;
   if (!phibar) {
@@ -1421,21 +1424,43 @@ int swe_imex_step_async(swe_plan *pl, double *state, const double *phibar, int b
   if (g_graphs && !g_prof && nsteps > 0 && (rc = step_graph(r, *cfg, &exec))) return rc;
   const Bufs b = bufs(r);
   SpecPtrs d = {{b.U[0], b.U[1], b.U[2]}};
-  if ((rc = to_internal(state, d, batch, 3, pl->K, pl->perm, r.st))) return rc;
+  if ((rc = to_internal(in, d, batch, 3, pl->K, pl->perm, r.st, in_stride))) return rc;
   if (!exec) {
     // no step graph yet (first sight of the configuration: step_graph captures at the
     // second, after this eager run has set the plan's fixed-point iteration guess)
     for (int s = 0; s < nsteps; ++s)
       if ((rc = imex_internal(r, *cfg, nullptr, nullptr))) return rc;
     SpecPtrsC so = {{b.U[0], b.U[1], b.U[2]}};
-    return to_boundary(so, state, batch, 3, pl->K, pl->perm, r.st);
+    return to_boundary(so, out, batch, 3, pl->K, pl->perm, r.st, nullptr, out_stride);
   }
   for (int s = 0; s < nsteps; ++s) SWE_CUDA(cudaGraphLaunch(exec, r.st));
   // the flag stays up once any queued step failed (no per-call reset): this and every
   // later queued call leave their state untouched until swe_plan_status resets it
   pl->ws.async_pending = 1;
   SpecPtrsC so = {{b.U[0], b.U[1], b.U[2]}};
-  return to_boundary(so, state, batch, 3, pl->K, pl->perm, r.st, pl->ws.d_fail);
+  return to_boundary(so, out, batch, 3, pl->K, pl->perm, r.st, pl->ws.d_fail, out_stride);
+}
+
+int swe_imex_step_async(swe_plan *pl, double *state, const double *phibar, int batch,
+                        const swe_stepper_cfg *cfg, int nsteps, void *stream) {
+  return step_async_io(pl, state, 0, state, 0, phibar, batch, cfg, nsteps, stream);
+}
+
+int swe_imex_step_async_io(swe_plan *pl, const double *in, long long in_stride, double *out,
+                           long long out_stride, const double *phibar, int batch,
+                           const swe_stepper_cfg *cfg, int nsteps, void *stream) {
+  if (!pl || !in || !out) {
+    set_error("swe_imex_step_async_io: null argument");
+    return E_SHAPE;
+  }
+  const long long packed = 3LL * pl->K;
+  if (in_stride < packed || out_stride < packed) {
+    set_error("swe_imex_step_async_io: slice strides (%lld, %lld) below 3 K = %lld", in_stride,
+              out_stride, packed);
+    return E_SHAPE;
+  }
+  return step_async_io(pl, in, (size_t)in_stride, out, (size_t)out_stride, phibar, batch, cfg,
+                       nsteps, stream);
 }
 
 int swe_plan_status(swe_plan *pl, int *failed, int reset, void *stream) {

@@ -317,6 +317,27 @@ class MgritEngine:
             return self.problem.step_batch(level, x, **kw)
         return self.problem.step_batch(level, x, prev, **kw)
 
+    def _step_into(self, level, u, src0, dst, count) -> bool:
+        """step(u[src0 + i m]), i < count, written to u[dst + i m] (dst an int: in place
+        on strided views of the level array) or to the tensor dst, where the problem
+        supports it (no forcing on this path)."""
+        f = getattr(self.problem, "step_into", None)
+        if (f is None or not isinstance(u, torch.Tensor) or count <= 0
+                or not getattr(self.problem, "supports_deferred_check", False)):
+            return False
+        m = self.m
+        src = u[src0:src0 + (count - 1) * m + 1:m]
+        if isinstance(dst, int):
+            dst = u[dst:dst + (count - 1) * m + 1:m]
+        kw = {}
+        if getattr(self.problem, "supports_select_batch", False):
+            kw["select_batch"] = count * self.G
+        if not f(level, src, dst, **kw):
+            return False
+        if level == 0:
+            self.fine_steps += count
+        return True
+
     def _deferred_kw(self):
         """Steps and sweeps queued without a host round trip where the problem
         supports it; their errors are raised once per cycle (_check_deferred)."""
@@ -342,6 +363,15 @@ class MgritEngine:
         n = (u.shape[0] - 1) // m
         lo, hi = self._own(level, n)
         self._exchange_halo(level, u)
+        if g is None:
+            # unforced level: each F-point stepped straight into its neighbour
+            s = 1
+            while s < m and self._step_into(level, u, m * (lo - 1) + s - 1, m * (lo - 1) + s,
+                                            hi - lo + 1):
+                s += 1
+            if s == m:
+                return
+            assert s == 1  # (a problem either supports the level or does not)
         left = torch.arange(m * (lo - 1), m * hi, m, device=u.device)
         x = u[left]
         for s in range(1, m):
@@ -354,6 +384,8 @@ class MgritEngine:
         m = self.m
         n = (u.shape[0] - 1) // m
         lo, hi = self._own(level, n)
+        if g is None and self._step_into(level, u, m * lo - 1, m * lo, hi - lo + 1):
+            return
         cp = torch.arange(m * lo, m * hi + 1, m, device=u.device)
         x = self._step(level, u[cp - 1])
         if g is not None:
@@ -370,7 +402,13 @@ class MgritEngine:
     def _residual(self, level, u, g, lo, hi):
         m = self.m
         cp = torch.arange(m * lo, m * hi + 1, m, device=u.device)
-        prop = self._step(level, u[cp - 1])
+        prop = None
+        if isinstance(u, torch.Tensor):  # stepped from the strided view, no gather / clone
+            prop = torch.empty((hi - lo + 1,) + tuple(u.shape[1:]), dtype=u.dtype, device=u.device)
+            if not self._step_into(level, u, m * lo - 1, prop, hi - lo + 1):
+                prop = None
+        if prop is None:
+            prop = self._step(level, u[cp - 1])
         if g is not None:
             prop = prop + g[cp]
         return prop - u[cp]
@@ -661,6 +699,21 @@ class SweProblem:
             settls_step_inplace(st, cfg, None if prev is None else self.wrap(level, prev),
                                 select_batch=select_batch)
         return st.data
+
+    def step_into(self, level, src, dst, select_batch=0) -> bool:
+        """dst[i] = step(src[i]) for strided views of a level array (every m-th point),
+        queued like step_batch(..., deferred=True) but without the gather, clone and
+        scatter copies (swe_imex_step_async_io); False when the level is not a plain
+        IMEX level (the caller then uses step_batch)."""
+        from .steppers import IMEX, imex_step_async_io
+        cfg = self.level_cfgs[level]
+        if cfg.scheme != IMEX or src.shape[0] == 0:
+            return False
+        self.step_calls += src.shape[0]
+        imex_step_async_io(self.grids[level], src, dst, self._pb(src.shape[0], src.device), cfg, 1,
+                           select_batch=select_batch)
+        self._pending.add(level)
+        return True
 
     def sweep_batch(self, level, u, g, deferred=False) -> bool:
         """u[j] = step(u[j-1]) + g[j], j = 1..n, in place on the device

@@ -131,6 +131,37 @@ def imex_steps_async(state: PrognosticState, cfg: StepperConfig, nsteps: int = 1
     return state
 
 
+def imex_step_async_io(grid: SphereGrid, src: torch.Tensor, dst: torch.Tensor,
+                       phibar: torch.Tensor, cfg: StepperConfig, nsteps: int = 1,
+                       select_batch: int = 0):
+    """imex_steps_async out of place on strided slices (swe_imex_step_async_io):
+    dst[b] = nsteps IMEX steps of src[b].  src / dst are [batch, 3, K] complex128
+    views whose slices are contiguous but may be any distance apart (every m-th
+    point of an MGRIT level array), so a sweep needs no gather / scatter copy."""
+    if cfg.scheme != IMEX:
+        raise ValueError("imex_step_async_io needs scheme='imex'")
+    K = grid.n_modes
+    for t in (src, dst):
+        if (t.dtype != torch.complex128 or t.dim() != 3 or tuple(t.shape[1:]) != (3, K)
+                or t.stride(2) != 1 or t.stride(1) != K or not t.is_cuda):
+            raise ValueError(f"state views must be cuda complex128 [batch, 3, {K}] with "
+                             "contiguous slices")
+    B = src.shape[0]
+    if dst.shape[0] != B or phibar.numel() != B:
+        raise ValueError("src, dst and phibar must hold the same number of slices")
+    ss = src.stride(0) if B > 1 else 3 * K
+    ds = dst.stride(0) if B > 1 else 3 * K
+    if ss < 3 * K or ds < 3 * K:
+        raise ValueError("slices of a state view must not overlap")
+    c = cfg.to_c(select_batch)
+    rc = grid._lib.swe_imex_step_async_io(grid.plan, _ptr(src), ss, _ptr(dst), ds, _ptr(phibar),
+                                          int(B), ctypes.byref(c), int(nsteps), _stream())
+    try:
+        _lib.check(rc, "swe_imex_step_async_io")
+    except _lib.NoConvergence as exc:
+        raise ImplicitSolveError(str(exc)) from None
+
+
 def check_async_steps(grid: SphereGrid, reset: bool = True):
     """Wait for the queued imex_steps_async calls of `grid`'s plan and raise
     ImplicitSolveError if any of them hit an unconverged solve (steppers.py:113-118)."""
