@@ -322,10 +322,21 @@ class MgritEngine:
         on strided views of the level array) or to the tensor dst, where the problem
         supports it (no forcing on this path)."""
         f = getattr(self.problem, "step_into", None)
-        if (f is None or not isinstance(u, torch.Tensor) or count <= 0
+        if (f is None or count <= 0
                 or not getattr(self.problem, "supports_deferred_check", False)):
             return False
         m = self.m
+        if isinstance(u, LevelWindow):  # a rank's block of the level: local rows
+            last = (count - 1) * m - u.base
+            if (src0 < u.base or src0 + last >= u.data.shape[0]
+                    or (isinstance(dst, int) and (dst < u.base or dst + last >= u.data.shape[0]))):
+                return False
+            src0 -= u.base
+            if isinstance(dst, int):
+                dst -= u.base
+            u = u.data
+        if not isinstance(u, torch.Tensor):
+            return False
         src = u[src0:src0 + (count - 1) * m + 1:m]
         if isinstance(dst, int):
             dst = u[dst:dst + (count - 1) * m + 1:m]
@@ -403,8 +414,9 @@ class MgritEngine:
         m = self.m
         cp = torch.arange(m * lo, m * hi + 1, m, device=u.device)
         prop = None
-        if isinstance(u, torch.Tensor):  # stepped from the strided view, no gather / clone
-            prop = torch.empty((hi - lo + 1,) + tuple(u.shape[1:]), dtype=u.dtype, device=u.device)
+        if isinstance(u, (torch.Tensor, LevelWindow)):  # from the strided view, no gather / clone
+            ref = u.data if isinstance(u, LevelWindow) else u
+            prop = torch.empty((hi - lo + 1,) + tuple(ref.shape[1:]), dtype=ref.dtype, device=ref.device)
             if not self._step_into(level, u, m * lo - 1, prop, hi - lo + 1):
                 prop = None
         if prop is None:

@@ -194,14 +194,37 @@ def _free_port():
     return p
 
 
+class StridedScalarProblem(BatchedScalarProblem):
+    """BatchedScalarProblem with the optional strided in-place step protocol
+    (SweProblem.step_into: dst[i] = step(src[i]) on views of the level array)."""
+
+    supports_deferred_check = True
+
+    def __init__(self, factors):
+        super().__init__(factors)
+        self.into_calls = 0
+
+    def check_deferred(self):
+        pass
+
+    def step_batch(self, level, x, deferred=False):
+        return super().step_batch(level, x)
+
+    def step_into(self, level, src, dst):
+        assert src.shape == dst.shape and src.data_ptr() != dst.data_ptr()
+        self.into_calls += 1
+        dst.copy_(super().step_batch(level, src))
+        return True
+
+
 def _rank_main(rank, world, port, name, factors, c, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        prob = BatchedScalarProblem(factors)
+        prob = (StridedScalarProblem if name.startswith("strided_") else BatchedScalarProblem)(factors)
         tr = pint.mgrit_run(prob, engine_cfg(c), 1.0 + 0.0j, comm=pint.Comm())
         snaps = np.stack([s.tensor.numpy() for s in tr.snapshots])
-        out[rank] = (snaps, prob.step_calls)
+        out[rank] = (snaps, prob.step_calls, getattr(prob, "into_calls", None))
     finally:
         dist.destroy_process_group()
 
@@ -222,6 +245,34 @@ def test_two_rank_gloo_bitwise(name, factors, c):
         assert p.exitcode == 0
     for r in range(2):
         assert np.array_equal(out[r][0], ref), (name, r)
+
+
+@pytest.mark.parametrize("name,factors,c", configs())
+def test_strided_step_protocol_bitwise(name, factors, c):
+    """A problem offering step_into has its unforced sweeps stepped on strided views
+    of the level array (full array at one rank, LevelWindow blocks at two): same
+    trace and step count as the gather / step_batch / scatter path."""
+    plain = BatchedScalarProblem(factors)
+    single = pint.mgrit_run(plain, engine_cfg(c), 1.0 + 0.0j)
+    ref = np.stack([s.tensor.numpy() for s in single.snapshots])
+    prob = StridedScalarProblem(factors)
+    tr = pint.mgrit_run(prob, engine_cfg(c), 1.0 + 0.0j)
+    assert np.array_equal(np.stack([s.tensor.numpy() for s in tr.snapshots]), ref)
+    assert prob.into_calls > 0 and prob.step_calls == plain.step_calls
+    assert tr.fine_steps == single.fine_steps
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, "strided_" + name, factors, c, out))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    for r in range(2):
+        assert np.array_equal(out[r][0], ref), (name, r)
+        assert out[r][2] > 0, "the rank's LevelWindow sweeps did not take the strided path"
 
 
 def test_stepper_config_implicit_solver():
